@@ -1,0 +1,268 @@
+"""Benchmark: MGR-preconditioned GMRES on BASELINE cfg2 (hybrid-MFD [p, pi]
+system on a 128x128x64 grid with a layered log-normal permeability field,
+4,227,072 DOF), FGMRES(30), rtol 1e-6, strategy = one exact reduction of the
+face multipliers (ideal interp, injection) + one AMG V-cycle on the cell
+pressure system (strategies/mfd_mgr_pi_c1.json).
+
+A step = one complete solve from x0 = 0 with the hierarchy already built
+(setup is timed separately and reported). value = DOF * GMRES iterations /
+solve time, summed over ranks. Inputs (matrix 200 MB + hierarchy) exceed the
+126 MB L2, so no explicit flush is needed between steps.
+
+--impl reference times the reference CPU implementation of the path (the
+refcpu oracle: the reference itself cannot be compiled here) on
+the host cores, on a bounded sample of the same workload.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MGR-FGMRES DOF*iters/sec"
+UNIT = "DOF*iters/s"
+CFG = {"nx": 128, "ny": 128, "nz": 64, "field": "layered", "sigma": 1.5, "seed": 20210129}
+STRATEGY = "mfd_mgr_pi_c1"
+RTOL = 1e-6
+RESTART = 30
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region."""
+
+    def __init__(self, gpu):
+        self.gpu, self.samples, self.proc = gpu, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            p = [x.strip() for x in line.split(",")]
+            if len(p) >= 7:
+                self.samples.append(p)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        import statistics
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if s[3 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def make_problem():
+    import paper_2101_11649_b200 as mx
+    return mx.mfd_problem(CFG["nx"], CFG["ny"], CFG["nz"], CFG["field"], sigma=CFG["sigma"], seed=CFG["seed"])
+
+
+def cpu_reference(P, steps, warmup, max_iters, threads):
+    """refcpu oracle: setup once, then each step = a GMRES solve capped at
+    max_iters iterations (bounded sample). Returns DOF*iters/s."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import refcpu
+    import paper_2101_11649_b200 as mx
+    refcpu.set_threads(threads)
+    H = refcpu.RefHierarchy(P.ptr, P.col, P.val, P.partition.field_order, P.partition.labels,
+                            mx.load_strategy(STRATEGY))
+    for _ in range(warmup):
+        H.solve(P.rhs, restart=RESTART, max_iters=max_iters, rel_tol=RTOL)
+    its, t = 0, 0.0
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        _, rep = H.solve(P.rhs, restart=RESTART, max_iters=max_iters, rel_tol=RTOL)
+        t += time.perf_counter() - t0
+        its += rep["iterations"]
+    return P.n * its / t, t, its, H.setup_s
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    P = make_problem()
+    threads = os.cpu_count() or 1
+    v, t, its, setup_s = cpu_reference(P, args.steps, args.warmup, args.ref_iters, threads)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / max(args.steps, 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_config(P, args.gpus),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"cfg2 MGR-GMRES solves capped at {args.ref_iters} iterations "
+                                       f"({its} iterations over {args.steps} steps), setup {setup_s:.1f}s excluded"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def workload_config(P, n_gpus):
+    return {"workload": "cfg2: hybrid-MFD [p,pi] 128x128x64 layered log-normal (1e6 contrast), "
+                        "FGMRES(30) rtol 1e-6, MGR_pi + 1 AMG V-cycle",
+            "dofs": int(P.n), "nnz": int(P.ptr[-1]), "strategy": STRATEGY, "restart": RESTART,
+            "rel_tol": RTOL, "parallelism": f"replicas{n_gpus}" if n_gpus > 1 else "single",
+            "l2_flush": "inputs exceed L2 (matrix+hierarchy > 126 MB)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="mgrx")
+    ap.add_argument("--ref-iters", type=int, default=10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2101_11649_b200 as mx
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    torch.cuda.set_device(local)
+    P = make_problem()
+    ctx = mx.Context(local)
+    A = mx.Matrix(P.ptr, P.col, P.val, ctx=ctx)
+    t0 = time.perf_counter()
+    H = mx.Hierarchy(A, P.partition, mx.load_strategy(STRATEGY))
+    setup_wall = time.perf_counter() - t0
+    cfg = mx.KrylovConfig(restart=RESTART, max_iters=500, rel_tol=RTOL)
+
+    dev = torch.device("cuda", local)
+    b = torch.from_numpy(P.rhs).to(dev)
+    x = torch.zeros(P.n, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+
+    def step():
+        x.zero_()
+        torch.cuda.synchronize()
+        return H.solve_device(b.data_ptr(), x.data_ptr(), cfg)
+
+    for _ in range(args.warmup):
+        step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    its, launches, solve_dev = 0, 0, 0.0
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        start.record()
+        for _ in range(args.steps):
+            rep = step()
+            its += rep.iterations
+            launches += rep.gpu_launches
+            solve_dev += rep.solve_s
+        end.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = start.elapsed_time(end)
+    t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
+    its_all = torch.tensor([float(its)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+        dist.all_reduce(its_all, op=dist.ReduceOp.SUM)
+    ms = float(t_max.item())
+    value = P.n * float(its_all.item()) / (ms * 1e-3)
+
+    # e2e: public API with host buffers (H2D of b and x0, D2H of x inside the timed region)
+    x0 = np.zeros(P.n)
+    for _ in range(1):
+        H.solve(P.rhs, x0, cfg)
+    te, e_its = 0.0, 0
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        _, rep_e = H.solve(P.rhs, x0, cfg)
+        te += time.perf_counter() - t1
+        e_its += rep_e.iterations
+    e2e = P.n * e_its / te * world
+
+    # roofline: dominant kernel probes (device events on the library stream)
+    peak, peak_kind = peaks()
+    info = H.info()
+    probes = {}
+    for name in ["spmv.A", "mgr.0.rres", "mgr.0.prolong", "amg.0.resid", "amg.0.pre", "amg.0.post"]:
+        try:
+            ms_k, by = H.time_kernel(name, reps=20)
+            probes[name] = {"avg_ms": ms_k, "bytes": by, "GBps": by / (ms_k * 1e-3) / 1e9}
+        except mx.MgrxError as e:
+            probes[name] = {"error": str(e)}
+    # per-iteration launch counts for the share estimate (1 V-cycle, 1 MGR level)
+    share = {k: v["avg_ms"] * (1.0) for k, v in probes.items() if "avg_ms" in v}
+    dom = max((k for k in share), key=lambda k: share[k])
+    d = probes[dom]
+    roof = {"bound": "hbm", "kernel": dom, "achieved": d["GBps"], "peak": peak, "unit": "GB/s",
+            "frac": d["GBps"] / peak, "traffic": None, "peak_source": peak_kind,
+            "kernels": probes}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        v, t, cits, setup_s = cpu_reference(P, 1, 0, args.ref_iters, threads)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"refcpu oracle, cfg2, one solve capped at {args.ref_iters} iterations "
+                         f"({cits} its in {t:.1f}s; setup {setup_s:.1f}s excluded)"}
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": workload_config(P, world),
+                "iterations_per_solve": its / args.steps, "solve_time_s": ms * 1e-3 / args.steps,
+                "setup_s": rep.setup_s, "setup_wall_s": setup_wall,
+                "hierarchy": info,
+                "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 16 * P.n,
+                        "d2h_bytes_per_step": 8 * P.n},
+                "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
+                "clocks": clk.summary()}
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,143 @@
+/* mgrx — B200-native MGR-preconditioned GMRES (sm_100a), C ABI.
+ *
+ * Drop-in boundary for the hot path of the reference mgrkit library
+ * (arXiv 2101.11649 reference, /root/reference/proj). The reference exposes a
+ * C++ API; each entry point below replaces one of its calls (file:line):
+ *
+ *   mgrx_matrix_csr  <- SpMat + validate()        proj/include/mgrkit/sparse.hpp:19-22,
+ *                                                 proj/src/sparse.cpp:24-41
+ *   mgrx_setup       <- mgr_setup(A, partition, strategy, unknown_map)
+ *                                                 proj/include/mgrkit/mgr.hpp:105-106
+ *                       + strategy_from_json_text proj/include/mgrkit/strategy_json.hpp:11
+ *   mgrx_apply       <- mgr_apply(H, v)           proj/include/mgrkit/mgr.hpp:111
+ *   mgrx_solve       <- gmres(A, b, x, cfg, mgr_preconditioner(H))
+ *                                                 proj/include/mgrkit/krylov.hpp:33-34,
+ *                                                 proj/include/mgrkit/mgr.hpp:114
+ *   mgrx_spmv        <- spmv(A, x)                proj/include/mgrkit/sparse.hpp:57
+ *   mgrx_dump        <- MgrHierarchy / AmgHierarchy member access (levels[l].P, ...)
+ *                                                 proj/include/mgrkit/mgr.hpp:79-100,
+ *                                                 proj/include/mgrkit/amg.hpp:26-49
+ *   mgrx_last_error  <- the what() text of the exception the reference throws
+ *
+ * Status codes mirror the CLI exit codes (proj/tools/mgr_main.cpp:34):
+ *   MGRX_OK 0, MGRX_NOT_CONVERGED 1, MGRX_INVALID_ARGUMENT 2 (std::invalid_argument),
+ *   MGRX_RUNTIME 3 (std::runtime_error / logic_error / CUDA failures).
+ *
+ * Ownership: the library owns all device memory; the caller owns every host
+ * buffer it passes. Matrices are copied at creation (the reference copies
+ * into the hierarchy, proj/src/mgr.cpp:257). Handles are not thread-safe;
+ * each context runs on one CUDA stream. A built hierarchy is immutable.
+ * Indices are int32 and values fp64, as in proj/include/mgrkit/types.hpp:17-20.
+ */
+#ifndef MGRX_H
+#define MGRX_H
+
+#if defined(__GNUC__)
+#define MGRX_API __attribute__((visibility("default")))
+#else
+#define MGRX_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MGRX_OK 0
+#define MGRX_NOT_CONVERGED 1
+#define MGRX_INVALID_ARGUMENT 2
+#define MGRX_RUNTIME 3
+
+typedef struct mgrx_ctx mgrx_ctx;
+typedef struct mgrx_mat mgrx_mat;
+typedef struct mgrx_hier mgrx_hier;
+
+/* KrylovConfig, proj/include/mgrkit/krylov.hpp:14-19 */
+typedef struct mgrx_krylov {
+  int restart;
+  int max_iters;
+  double rel_tol;
+  double abs_tol;
+} mgrx_krylov;
+
+/* SolveReport, proj/include/mgrkit/krylov.hpp:21-28, plus timings. The
+ * history holds one Arnoldi estimate per inner step and the true relative
+ * residual after each restart (same layout as the reference). */
+typedef struct mgrx_report {
+  int converged;
+  int iterations;
+  double final_residual;
+  double* history;   /* caller buffer, may be NULL */
+  int history_cap;
+  int history_len;   /* full length, may exceed history_cap */
+  double setup_s;    /* hierarchy build time (device events) */
+  double solve_s;    /* solve time (device events, host copies excluded) */
+  long long gpu_launches; /* kernels launched by this call */
+} mgrx_report;
+
+/* Thread-local message of the last failing call on this thread. */
+MGRX_API const char* mgrx_last_error(void);
+
+/* devices: CUDA ordinals; this build drives devices[0] (one process per GPU). */
+MGRX_API int mgrx_create(const int* devices, int ndev, mgrx_ctx** out);
+MGRX_API int mgrx_destroy(mgrx_ctx* ctx);
+
+/* CSR with sorted, in-range columns and finite values (validate()). host
+ * pointers; copied to HBM. */
+MGRX_API int mgrx_matrix_csr(mgrx_ctx* ctx, int rows, int cols, const int* rowptr, const int* colidx,
+                    const double* values, mgrx_mat** out);
+/* Same, from pointers that already live in device memory of ctx's GPU. */
+MGRX_API int mgrx_matrix_csr_device(mgrx_ctx* ctx, int rows, int cols, const int* d_rowptr,
+                           const int* d_colidx, const double* d_values, mgrx_mat** out);
+MGRX_API int mgrx_matrix_destroy(mgrx_mat* m);
+
+/* y = A x. on_device != 0: x, y are device pointers. */
+MGRX_API int mgrx_spmv(mgrx_mat* m, const double* x, double* y, int on_device);
+
+/* Build the MGR hierarchy on the GPU. labels[i] in [0, nfields) names
+ * field_names[labels[i]] (DofPartition, proj/include/mgrkit/mgr.hpp:20-28).
+ * unknown_map may be NULL. strategy_json uses the reference schema
+ * (proj/src/strategy_json.cpp:75-228); unknown keys are errors. */
+MGRX_API int mgrx_setup(mgrx_ctx* ctx, mgrx_mat* A, const int* labels, int nfields,
+               const char* const* field_names, const int* unknown_map, const char* strategy_json,
+               mgrx_hier** out);
+MGRX_API int mgrx_hier_destroy(mgrx_hier* h);
+
+/* z = M^{-1} v, one MGR V-cycle from zero (mgr_apply). */
+MGRX_API int mgrx_apply(mgrx_hier* h, const double* v, double* z, int on_device);
+
+/* Right-preconditioned restarted GMRES with M = mgr_apply (gmres()). x holds
+ * the initial guess on entry and the solution on exit. Returns MGRX_OK or
+ * MGRX_NOT_CONVERGED (report filled in both cases). */
+MGRX_API int mgrx_solve(mgrx_hier* h, const double* b, double* x, const mgrx_krylov* cfg,
+               mgrx_report* report, int on_device);
+
+/* Parity dumps. path grammar:
+ *   mgr.<l>.{A,P,R,F,C,frelax.dinv}   mgr.coarse.A
+ *   mgr.<l>.frelax.amg.<k>.{A,P,R,C,F,l1d,dinv,umap}   mgr.coarse.amg.<k>.{...}
+ * Two-call protocol: pass NULL buffers to query kind/sizes.
+ * kind: 0 = CSR (ptr/col/val), 1 = int list (col), 2 = fp64 vector (val). */
+MGRX_API int mgrx_dump(mgrx_hier* h, const char* path, int* kind, int* rows, int* cols, long long* nnz,
+              int* ptr, int* col, double* val);
+
+/* Hierarchy shape for iterating dumps. frelax_amg_levels has room for
+ * max_levels entries. */
+MGRX_API int mgrx_info(mgrx_hier* h, int* mgr_levels, int* coarse_amg_levels, int* frelax_amg_levels,
+              int max_levels);
+
+/* Roofline probe: replay one hot kernel of the hierarchy `reps` times with
+ * its inputs resident in HBM and report its average device time (CUDA events
+ * on the library stream) and its algorithmic bytes per launch (SURVEY §8d
+ * compulsory-traffic model). which:
+ *   "spmv.A"            y = A x on the fine matrix (GMRES operator)
+ *   "mgr.<l>.rres"      restricted residual v_C - A_CF z_F of MGR level l
+ *   "mgr.<l>.prolong"   fused prolongation z = [zF;0] + P e of MGR level l
+ *   "amg.<k>.resid"     t = r - A z on level k of the coarse AMG
+ *   "amg.<k>.pre"       pre-smoother sweep on level k of the coarse AMG
+ *   "amg.<k>.post"      post-smoother sweep on level k of the coarse AMG */
+MGRX_API int mgrx_time_kernel(mgrx_hier* h, const char* which, int reps, double* avg_ms,
+                              double* bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MGRX_H */

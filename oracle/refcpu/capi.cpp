@@ -1,4 +1,4 @@
-// refcpu — CPU ORACLE (test infrastructure only; see sparse.hpp header).
+// refcpu — CPU ORACLE (test infrastructure only; see csr.hpp header).
 // Plain C entry points so tests/ and bench.py can drive the oracle through
 // ctypes. Status codes mirror proj/tools/mgr_main.cpp:34 (0 ok, 1 not
 // converged, 2 invalid argument, 3 runtime error).

@@ -1,6 +1,6 @@
-// refcpu — CPU ORACLE (test infrastructure only; see sparse.hpp header).
+// refcpu — CPU ORACLE (test infrastructure only; see csr.hpp header).
 // Restates proj/src/sparse.cpp without Eigen.
-#include "sparse.hpp"
+#include "csr.hpp"
 
 #include <algorithm>
 #include <cmath>

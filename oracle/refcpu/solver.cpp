@@ -1,4 +1,4 @@
-// refcpu — CPU ORACLE (test infrastructure only; see sparse.hpp header).
+// refcpu — CPU ORACLE (test infrastructure only; see csr.hpp header).
 // Restates proj/src/{relax,amg,krylov,mgr}.cpp without Eigen. Each function
 // cites the reference lines whose behaviour it reproduces.
 #include <algorithm>

@@ -1,4 +1,4 @@
-// refcpu — CPU ORACLE (test infrastructure only; see sparse.hpp header).
+// refcpu — CPU ORACLE (test infrastructure only; see csr.hpp header).
 // Restates proj/include/mgrkit/{relax,amg,mgr,krylov}.hpp semantics.
 #pragma once
 
@@ -8,7 +8,7 @@
 #include <string>
 #include <vector>
 
-#include "sparse.hpp"
+#include "csr.hpp"
 
 namespace refcpu {
 

@@ -1,0 +1,464 @@
+// C-ABI boundary of libmgrx (include/mgrx.h). Maps exceptions to the
+// reference's status codes and keeps the message in a thread-local string.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <string>
+
+#include "../../include/mgrx.h"
+#include "hierarchy.cuh"
+#include "krylov.cuh"
+
+using namespace mgrx;
+
+struct mgrx_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+};
+
+struct mgrx_mat {
+  mgrx_ctx* ctx = nullptr;
+  DCsr A;
+};
+
+struct mgrx_hier {
+  mgrx_ctx* ctx = nullptr;
+  DCsr A;  // the hierarchy copies the fine matrix (proj/src/mgr.cpp:257)
+  MgrHier H;
+  GmresWork ws;
+  double setup_s = 0.0;
+  DVec<double> vin, vout;  // staging for host-pointer calls
+  DVec<double> px, py, pz;  // roofline-probe operands
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(const std::exception& e) {
+  g_err = e.what();
+  if (dynamic_cast<const std::invalid_argument*>(&e)) return MGRX_INVALID_ARGUMENT;
+  return MGRX_RUNTIME;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const std::exception& e) {
+    return fail(e);
+  } catch (...) {
+    g_err = "unknown error";
+    return MGRX_RUNTIME;
+  }
+}
+
+void use(mgrx_ctx* c) { MGRX_CK(cudaSetDevice(c->device)); }
+
+struct EventTimer {
+  cudaEvent_t a, b;
+  cudaStream_t s;
+  explicit EventTimer(cudaStream_t st) : s(st) {
+    MGRX_CK(cudaEventCreate(&a));
+    MGRX_CK(cudaEventCreate(&b));
+    MGRX_CK(cudaEventRecord(a, s));
+  }
+  double stop() {
+    MGRX_CK(cudaEventRecord(b, s));
+    MGRX_CK(cudaEventSynchronize(b));
+    float ms = 0;
+    MGRX_CK(cudaEventElapsedTime(&ms, a, b));
+    return ms * 1e-3;
+  }
+  ~EventTimer() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+};
+
+// SURVEY §8d compulsory-traffic model (bytes per launch).
+double spmv_model_bytes(const DCsr& A) {
+  return 12.0 * A.nnz + 4.0 * (A.rows + 1) + 8.0 * std::min<double>(A.cols, A.nnz) + 8.0 * A.rows;
+}
+
+void prepare_probe(mgrx_hier* h, const std::string& w, std::function<void()>& fn, double& bytes,
+                   cudaStream_t s) {
+  const size_t nmax = static_cast<size_t>(std::max(h->A.rows, h->A.cols)) + 1;
+  if (h->px.size() < nmax) {
+    h->px.alloc(nmax, s);
+    h->py.alloc(nmax, s);
+    h->pz.alloc(nmax, s);
+  }
+  h->px.zero();
+  h->py.zero();
+  h->pz.zero();
+  double* x = h->px.get();
+  double* y = h->py.get();
+  double* z = h->pz.get();
+  if (w == "spmv.A") {
+    const DCsr* A = &h->A;
+    fn = [=] { spmv(*A, x, y, s); };
+    bytes = spmv_model_bytes(*A);
+    return;
+  }
+  if (w.rfind("mgr.", 0) == 0) {
+    const size_t d = w.find('.', 4);
+    const int l = std::stoi(w.substr(4, d - 4));
+    if (l < 0 || l >= static_cast<int>(h->H.levels.size())) throw InvalidArgument("probe: no MGR level " + w);
+    MgrLevelD* L = &h->H.levels[l];
+    const std::string what = w.substr(d + 1);
+    const double nf = static_cast<double>(L->F.size()), nc = static_cast<double>(L->C.size());
+    if (what == "rres") {
+      if (L->Acf.rows == 0 && nc > 0) throw InvalidArgument("probe: level has no fused restricted residual");
+      fn = [=] { spmv_residual(L->Acf, x, y, L->C.get(), z, s); };
+      bytes = 12.0 * L->Acf.nnz + 4.0 * (nc + 1) + 8.0 * nf + 16.0 * nc;
+      return;
+    }
+    if (what == "prolong") {
+      fn = [=] { spmv_prolong(L->P, x, L->fpos.get(), y, z, s); };
+      bytes = 16.0 * nc + 12.0 * (L->P.nnz - nc) + 4.0 * (nf + 1) + 8.0 * nc + 16.0 * nf;
+      return;
+    }
+  }
+  if (w.rfind("amg.", 0) == 0) {
+    const size_t d = w.find('.', 4);
+    const int k = std::stoi(w.substr(4, d - 4));
+    AmgHier* amg = h->H.coarse_amg.get();
+    if (!amg || k < 0 || k + 1 >= static_cast<int>(amg->levels.size())) throw InvalidArgument("probe: no AMG level " + w);
+    AmgLevelD* L = &amg->levels[k];
+    const std::string what = w.substr(d + 1);
+    const double m = L->A.rows;
+    if (what == "resid") {
+      fn = [=] { spmv_residual(L->A, x, y, nullptr, z, s); };
+      bytes = spmv_model_bytes(L->A) + 8.0 * m;
+      return;
+    }
+    if (what == "pre" || what == "post") {
+      BoundRelax* R = what == "pre" ? &L->pre : &L->post;
+      fn = [=] { R->apply(y, nullptr, z, s); };
+      bytes = (R->spec.kind == Smoother::jacobi || R->spec.kind == Smoother::l1_jacobi)
+                  ? 24.0 * m
+                  : 12.0 * L->A.nnz + 4.0 * (m + 1) + 24.0 * m;
+      return;
+    }
+  }
+  throw InvalidArgument("probe: unknown kernel " + w);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mgrx_last_error(void) { return g_err.c_str(); }
+
+int mgrx_create(const int* devices, int ndev, mgrx_ctx** out) {
+  return guarded([&] {
+    if (!out) throw InvalidArgument("mgrx_create: null output handle");
+    int count = 0;
+    MGRX_CK(cudaGetDeviceCount(&count));
+    if (count == 0) throw RuntimeError("mgrx_create: no CUDA device visible");
+    auto c = std::make_unique<mgrx_ctx>();
+    c->device = (devices && ndev > 0) ? devices[0] : 0;
+    if (c->device < 0 || c->device >= count) throw InvalidArgument("mgrx_create: device ordinal out of range");
+    MGRX_CK(cudaSetDevice(c->device));
+    cudaDeviceProp prop;
+    MGRX_CK(cudaGetDeviceProperties(&prop, c->device));
+    if (prop.major != 10) throw RuntimeError("mgrx_create: libmgrx is built for sm_100a (B200) only");
+    MGRX_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    cudaMemPool_t pool;
+    MGRX_CK(cudaDeviceGetDefaultMemPool(&pool, c->device));
+    uint64_t thr = UINT64_MAX;
+    MGRX_CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    *out = c.release();
+    return MGRX_OK;
+  });
+}
+
+int mgrx_destroy(mgrx_ctx* ctx) {
+  return guarded([&] {
+    if (ctx) {
+      cudaSetDevice(ctx->device);
+      cudaStreamSynchronize(ctx->stream);
+      cudaStreamDestroy(ctx->stream);
+      delete ctx;
+    }
+    return MGRX_OK;
+  });
+}
+
+int mgrx_matrix_csr(mgrx_ctx* ctx, int rows, int cols, const int* rowptr, const int* colidx,
+                    const double* values, mgrx_mat** out) {
+  return guarded([&] {
+    use(ctx);
+    auto m = std::make_unique<mgrx_mat>();
+    m->ctx = ctx;
+    m->A = csr_from_host(rows, cols, rowptr, colidx, values, ctx->stream);
+    *out = m.release();
+    return MGRX_OK;
+  });
+}
+
+int mgrx_matrix_csr_device(mgrx_ctx* ctx, int rows, int cols, const int* d_rowptr, const int* d_colidx,
+                           const double* d_values, mgrx_mat** out) {
+  return guarded([&] {
+    use(ctx);
+    auto m = std::make_unique<mgrx_mat>();
+    m->ctx = ctx;
+    m->A = csr_from_device(rows, cols, d_rowptr, d_colidx, d_values, ctx->stream);
+    *out = m.release();
+    return MGRX_OK;
+  });
+}
+
+int mgrx_matrix_destroy(mgrx_mat* m) {
+  return guarded([&] {
+    if (m) {
+      use(m->ctx);
+      MGRX_CK(cudaStreamSynchronize(m->ctx->stream));
+      delete m;
+    }
+    return MGRX_OK;
+  });
+}
+
+int mgrx_spmv(mgrx_mat* m, const double* x, double* y, int on_device) {
+  return guarded([&] {
+    use(m->ctx);
+    cudaStream_t s = m->ctx->stream;
+    if (on_device) {
+      spmv(m->A, x, y, s);
+      MGRX_CK(cudaStreamSynchronize(s));
+      return MGRX_OK;
+    }
+    DVec<double> dx(m->A.cols > 0 ? m->A.cols : 1, s), dy(m->A.rows > 0 ? m->A.rows : 1, s);
+    dx.upload(x, m->A.cols);
+    spmv(m->A, dx.get(), dy.get(), s);
+    MGRX_CK(cudaMemcpyAsync(y, dy.get(), sizeof(double) * m->A.rows, cudaMemcpyDeviceToHost, s));
+    MGRX_CK(cudaStreamSynchronize(s));
+    return MGRX_OK;
+  });
+}
+
+int mgrx_setup(mgrx_ctx* ctx, mgrx_mat* A, const int* labels, int nfields, const char* const* field_names,
+               const int* unknown_map, const char* strategy_json, mgrx_hier** out) {
+  return guarded([&] {
+    use(ctx);
+    if (!A || !labels || !field_names || !strategy_json || !out)
+      throw InvalidArgument("mgrx_setup: null argument");
+    cudaStream_t s = ctx->stream;
+    const Strategy strat = parse_strategy(strategy_json);
+    const int n = A->A.rows;
+    std::vector<std::string> fields;
+    for (int f = 0; f < nfields; ++f) fields.emplace_back(field_names[f]);
+    std::vector<int> lab(labels, labels + n);
+    for (int v : lab)
+      if (v < 0 || v >= nfields) throw InvalidArgument("bundle: label id out of range");
+    std::vector<int> umap;
+    if (unknown_map) umap.assign(unknown_map, unknown_map + n);
+    auto h = std::make_unique<mgrx_hier>();
+    h->ctx = ctx;
+    EventTimer t(s);
+    h->A = csr_copy(A->A, s);
+    h->H.setup(h->A, lab, fields, unknown_map ? &umap : nullptr, strat, s);
+    h->setup_s = t.stop();
+    h->vin.alloc(n > 0 ? n : 1, s);
+    h->vout.alloc(n > 0 ? n : 1, s);
+    *out = h.release();
+    return MGRX_OK;
+  });
+}
+
+int mgrx_hier_destroy(mgrx_hier* h) {
+  return guarded([&] {
+    if (h) {
+      use(h->ctx);
+      MGRX_CK(cudaStreamSynchronize(h->ctx->stream));
+      delete h;
+    }
+    return MGRX_OK;
+  });
+}
+
+int mgrx_apply(mgrx_hier* h, const double* v, double* z, int on_device) {
+  return guarded([&] {
+    use(h->ctx);
+    cudaStream_t s = h->ctx->stream;
+    const int n = h->A.rows;
+    if (on_device) {
+      h->H.apply(v, z, s);
+    } else {
+      h->vin.upload(v, n);
+      h->H.apply(h->vin.get(), h->vout.get(), s);
+      MGRX_CK(cudaMemcpyAsync(z, h->vout.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    }
+    MGRX_CK(cudaStreamSynchronize(s));
+    h->H.check(s);
+    return MGRX_OK;
+  });
+}
+
+int mgrx_solve(mgrx_hier* h, const double* b, double* x, const mgrx_krylov* cfg, mgrx_report* rep,
+               int on_device) {
+  return guarded([&] {
+    use(h->ctx);
+    if (!cfg) throw InvalidArgument("mgrx_solve: null config");
+    cudaStream_t s = h->ctx->stream;
+    const int n = h->A.rows;
+    KrylovSpec k;
+    k.restart = cfg->restart;
+    k.max_iters = cfg->max_iters;
+    k.rel_tol = cfg->rel_tol;
+    k.abs_tol = cfg->abs_tol;
+    const long long l0 = g_launches;
+    const double* db = b;
+    double* dx = x;
+    if (!on_device) {
+      h->vin.upload(b, n);
+      MGRX_CK(cudaMemcpyAsync(h->vout.get(), x, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+      db = h->vin.get();
+      dx = h->vout.get();
+    }
+    MgrHier* H = &h->H;
+    const DevOp prec = [H](const double* in, double* out, cudaStream_t st) { H->apply(in, out, st); };
+    EventTimer t(s);
+    GmresResult r = gmres_device(h->A, db, dx, k, prec, h->ws, s);
+    const double solve_s = t.stop();
+    h->H.check(s);
+    if (!on_device) {
+      MGRX_CK(cudaMemcpyAsync(x, dx, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+      MGRX_CK(cudaStreamSynchronize(s));
+    }
+    if (rep) {
+      rep->converged = r.converged ? 1 : 0;
+      rep->iterations = r.iterations;
+      rep->final_residual = r.final_residual;
+      rep->history_len = static_cast<int>(r.history.size());
+      if (rep->history)
+        for (int i = 0; i < rep->history_len && i < rep->history_cap; ++i) rep->history[i] = r.history[i];
+      rep->setup_s = h->setup_s;
+      rep->solve_s = solve_s;
+      rep->gpu_launches = g_launches - l0;
+    }
+    return r.converged ? MGRX_OK : MGRX_NOT_CONVERGED;
+  });
+}
+
+int mgrx_info(mgrx_hier* h, int* mgr_levels, int* coarse_amg_levels, int* frelax_amg_levels,
+              int max_levels) {
+  return guarded([&] {
+    *mgr_levels = static_cast<int>(h->H.levels.size());
+    *coarse_amg_levels = h->H.coarse_amg ? static_cast<int>(h->H.coarse_amg->levels.size()) : 0;
+    for (int l = 0; l < *mgr_levels && l < max_levels; ++l) {
+      const auto& amg = h->H.levels[l].f_relax.amg;
+      frelax_amg_levels[l] = amg ? static_cast<int>(amg->levels.size()) : 0;
+    }
+    return MGRX_OK;
+  });
+}
+
+int mgrx_dump(mgrx_hier* h, const char* path_c, int* kind, int* rows, int* cols, long long* nnz, int* ptr,
+              int* col, double* val) {
+  return guarded([&] {
+    use(h->ctx);
+    cudaStream_t s = h->ctx->stream;
+    const std::string path(path_c);
+    const DCsr* csr = nullptr;
+    const DVec<int>* ints = nullptr;
+    const std::vector<int>* hints = nullptr;
+    const DVec<double>* vec = nullptr;
+    auto amg_fields = [&](AmgHier* amg, const std::string& rest) {
+      const size_t d = rest.find('.');
+      const int kk = std::stoi(rest.substr(0, d));
+      const std::string what = rest.substr(d + 1);
+      if (!amg || kk < 0 || kk >= static_cast<int>(amg->levels.size()))
+        throw InvalidArgument("dump: no AMG level " + path);
+      AmgLevelD& L = amg->levels[kk];
+      if (what == "A") csr = &L.A;
+      else if (what == "P") csr = &L.P;
+      else if (what == "R") csr = &L.R;
+      else if (what == "C") ints = &L.C;
+      else if (what == "F") ints = &L.F;
+      else if (what == "l1d") vec = &L.pre.l1d;
+      else if (what == "dinv") vec = &L.pre.dinv;
+      else if (what == "umap") hints = &L.umap;
+    };
+    if (path.rfind("mgr.coarse.amg.", 0) == 0) {
+      amg_fields(h->H.coarse_amg.get(), path.substr(15));
+    } else if (path == "mgr.coarse.A") {
+      csr = &h->H.A_coarse;
+    } else if (path.rfind("mgr.", 0) == 0) {
+      const size_t d = path.find('.', 4);
+      const int l = std::stoi(path.substr(4, d - 4));
+      if (l < 0 || l >= static_cast<int>(h->H.levels.size())) throw InvalidArgument("dump: no MGR level " + path);
+      MgrLevelD& L = h->H.levels[l];
+      const std::string what = path.substr(d + 1);
+      if (what.rfind("frelax.amg.", 0) == 0) amg_fields(L.f_relax.amg.get(), what.substr(11));
+      else if (what == "A") csr = &L.A;
+      else if (what == "P") csr = &L.P;
+      else if (what == "R") csr = &L.R;
+      else if (what == "F") ints = &L.F;
+      else if (what == "C") ints = &L.C;
+      else if (what == "frelax.dinv") vec = &L.f_relax.dinv;
+    }
+    if (csr) {
+      *kind = 0;
+      *rows = csr->rows;
+      *cols = csr->cols;
+      *nnz = csr->nnz;
+      if (ptr) MGRX_CK(cudaMemcpyAsync(ptr, csr->ptr.get(), sizeof(int) * (csr->rows + 1), cudaMemcpyDeviceToHost, s));
+      if (col && csr->nnz) MGRX_CK(cudaMemcpyAsync(col, csr->col.get(), sizeof(int) * csr->nnz, cudaMemcpyDeviceToHost, s));
+      if (val && csr->nnz) MGRX_CK(cudaMemcpyAsync(val, csr->val.get(), sizeof(double) * csr->nnz, cudaMemcpyDeviceToHost, s));
+      MGRX_CK(cudaStreamSynchronize(s));
+      return MGRX_OK;
+    }
+    if (ints) {
+      *kind = 1;
+      *rows = static_cast<int>(ints->size());
+      *cols = 1;
+      *nnz = static_cast<long long>(ints->size());
+      if (col && ints->size()) MGRX_CK(cudaMemcpyAsync(col, ints->get(), sizeof(int) * ints->size(), cudaMemcpyDeviceToHost, s));
+      MGRX_CK(cudaStreamSynchronize(s));
+      return MGRX_OK;
+    }
+    if (hints) {
+      *kind = 1;
+      *rows = static_cast<int>(hints->size());
+      *cols = 1;
+      *nnz = static_cast<long long>(hints->size());
+      if (col && !hints->empty()) std::memcpy(col, hints->data(), sizeof(int) * hints->size());
+      return MGRX_OK;
+    }
+    if (vec) {
+      *kind = 2;
+      *rows = static_cast<int>(vec->size());
+      *cols = 1;
+      *nnz = static_cast<long long>(vec->size());
+      if (val && vec->size()) MGRX_CK(cudaMemcpyAsync(val, vec->get(), sizeof(double) * vec->size(), cudaMemcpyDeviceToHost, s));
+      MGRX_CK(cudaStreamSynchronize(s));
+      return MGRX_OK;
+    }
+    throw InvalidArgument("dump: unknown path " + path);
+  });
+}
+
+int mgrx_time_kernel(mgrx_hier* h, const char* which, int reps, double* avg_ms, double* bytes) {
+  return guarded([&] {
+    use(h->ctx);
+    cudaStream_t s = h->ctx->stream;
+    std::function<void()> fn;
+    double b = 0.0;
+    const std::string w(which);
+    prepare_probe(h, w, fn, b, s);
+    for (int i = 0; i < 3; ++i) fn();  // warm-up
+    EventTimer t(s);
+    for (int i = 0; i < reps; ++i) fn();
+    *avg_ms = t.stop() * 1e3 / (reps > 0 ? reps : 1);
+    *bytes = b;
+    return MGRX_OK;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,112 @@
+// Shared device plumbing for libmgrx: error handling, stream-ordered HBM
+// buffers, launch helpers. sm_100a only.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+namespace mgrx {
+
+// Errors mirror the reference's exception split (proj/tools/mgr_main.cpp:492-501):
+// InvalidArgument -> status 2, everything else -> status 3.
+struct InvalidArgument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct RuntimeError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define MGRX_CK(x)                                                                             \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess)                                                                     \
+      throw ::mgrx::RuntimeError(std::string("CUDA error: ") + cudaGetErrorString(e_) + " (" + \
+                                 __FILE__ + ":" + std::to_string(__LINE__) + ")");            \
+  } while (0)
+
+#define MGRX_LAUNCH_CK() MGRX_CK(cudaGetLastError())
+
+// Process-wide launch counter (the bench reports kernels launched in the
+// timed region; graph replays add their node count).
+extern long long g_launches;
+inline void count_launch(long long k = 1) { g_launches += k; }
+
+// Stream-ordered device buffer (cudaMallocAsync on the owning stream).
+template <class T>
+class DVec {
+ public:
+  DVec() = default;
+  DVec(size_t n, cudaStream_t s) { alloc(n, s); }
+  DVec(const DVec&) = delete;
+  DVec& operator=(const DVec&) = delete;
+  DVec(DVec&& o) noexcept { swap(o); }
+  DVec& operator=(DVec&& o) noexcept {
+    if (this != &o) {
+      release();
+      swap(o);
+    }
+    return *this;
+  }
+  ~DVec() { release(); }
+
+  void alloc(size_t n, cudaStream_t s) {
+    release();
+    n_ = n;
+    s_ = s;
+    if (n_) MGRX_CK(cudaMallocAsync(reinterpret_cast<void**>(&p_), n_ * sizeof(T), s_));
+  }
+  void release() {
+    if (p_) cudaFreeAsync(p_, s_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  void zero() {
+    if (n_) MGRX_CK(cudaMemsetAsync(p_, 0, n_ * sizeof(T), s_));
+  }
+  void upload(const T* h, size_t n) {
+    if (n > n_) throw RuntimeError("DVec::upload overflow");
+    if (n) MGRX_CK(cudaMemcpyAsync(p_, h, n * sizeof(T), cudaMemcpyHostToDevice, s_));
+  }
+  std::vector<T> download(size_t n = size_t(-1)) const {
+    if (n == size_t(-1)) n = n_;
+    std::vector<T> h(n);
+    if (n) {
+      MGRX_CK(cudaMemcpyAsync(h.data(), p_, n * sizeof(T), cudaMemcpyDeviceToHost, s_));
+      MGRX_CK(cudaStreamSynchronize(s_));
+    }
+    return h;
+  }
+  T* get() const { return p_; }
+  size_t size() const { return n_; }
+  cudaStream_t stream() const { return s_; }
+  void swap(DVec& o) noexcept {
+    std::swap(p_, o.p_);
+    std::swap(n_, o.n_);
+    std::swap(s_, o.s_);
+  }
+
+ private:
+  T* p_ = nullptr;
+  size_t n_ = 0;
+  cudaStream_t s_ = nullptr;
+};
+
+inline int blocks_for(int64_t n, int threads) {
+  return static_cast<int>((n + threads - 1) / threads);
+}
+
+// Read one device scalar (synchronizes the stream).
+template <class T>
+T read_scalar(const T* d, cudaStream_t s) {
+  T h;
+  MGRX_CK(cudaMemcpyAsync(&h, d, sizeof(T), cudaMemcpyDeviceToHost, s));
+  MGRX_CK(cudaStreamSynchronize(s));
+  return h;
+}
+
+}  // namespace mgrx

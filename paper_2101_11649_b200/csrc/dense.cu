@@ -1,0 +1,144 @@
+// Single-CTA dense LU with partial pivoting and its triangular solves. The
+// pivot is the first row of maximal |a_ik| (Eigen maxCoeff semantics).
+#include "dense.cuh"
+
+namespace mgrx {
+namespace {
+
+constexpr int kT = 1024;
+
+__global__ void k_densify(int n, const int* __restrict__ ptr, const int* __restrict__ col,
+                          const double* __restrict__ val, double* __restrict__ M) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int k = ptr[i]; k < ptr[i + 1]; ++k) M[static_cast<size_t>(col[k]) * n + i] = val[k];
+}
+
+__global__ void __launch_bounds__(kT) k_lu(int n, double* M, int* perm, double tol, int* bad) {
+  __shared__ double sv[kT];
+  __shared__ int si[kT];
+  __shared__ int piv;
+  for (int i = threadIdx.x; i < n; i += kT) perm[i] = i;
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    double best = -1.0;
+    int bi = n;
+    for (int i = k + threadIdx.x; i < n; i += kT) {
+      const double a = fabs(M[static_cast<size_t>(k) * n + i]);
+      if (a > best || (a == best && i < bi)) {
+        best = a;
+        bi = i;
+      }
+    }
+    sv[threadIdx.x] = best;
+    si[threadIdx.x] = bi;
+    __syncthreads();
+    for (int w = kT / 2; w > 0; w >>= 1) {
+      if (threadIdx.x < w) {
+        const double a = sv[threadIdx.x + w];
+        const int ai = si[threadIdx.x + w];
+        if (a > sv[threadIdx.x] || (a == sv[threadIdx.x] && ai < si[threadIdx.x])) {
+          sv[threadIdx.x] = a;
+          si[threadIdx.x] = ai;
+        }
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) piv = si[0];
+    __syncthreads();
+    const int p = piv;
+    if (p != k) {
+      for (int j = threadIdx.x; j < n; j += kT) {
+        const size_t a = static_cast<size_t>(j) * n;
+        const double t = M[a + k];
+        M[a + k] = M[a + p];
+        M[a + p] = t;
+      }
+      if (threadIdx.x == 0) {
+        const int t = perm[k];
+        perm[k] = perm[p];
+        perm[p] = t;
+      }
+    }
+    __syncthreads();
+    const double pv = M[static_cast<size_t>(k) * n + k];
+    if (pv != 0.0)
+      for (int i = k + 1 + threadIdx.x; i < n; i += kT)
+        M[static_cast<size_t>(k) * n + i] = __ddiv_rn(M[static_cast<size_t>(k) * n + i], pv);
+    __syncthreads();
+    const int m = n - k - 1;
+    for (int t = threadIdx.x; t < m * m; t += kT) {
+      const int jj = k + 1 + t / m, ii = k + 1 + t % m;
+      const double ukj = M[static_cast<size_t>(jj) * n + k];
+      if (ukj != 0.0)
+        M[static_cast<size_t>(jj) * n + ii] =
+            __dsub_rn(M[static_cast<size_t>(jj) * n + ii], __dmul_rn(M[static_cast<size_t>(k) * n + ii], ukj));
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    int b = -1;
+    for (int i = 0; i < n; ++i)
+      if (fabs(M[static_cast<size_t>(i) * n + i]) < tol) {
+        b = i;
+        break;
+      }
+    *bad = b;
+  }
+}
+
+__global__ void __launch_bounds__(kT) k_lu_solve(int n, const double* __restrict__ M,
+                                                 const int* __restrict__ perm,
+                                                 const double* __restrict__ b, double* __restrict__ x) {
+  extern __shared__ double xs[];
+  for (int i = threadIdx.x; i < n; i += kT) xs[i] = b[perm[i]];
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    const double xj = xs[j];
+    for (int i = j + 1 + threadIdx.x; i < n; i += kT)
+      xs[i] = __dsub_rn(xs[i], __dmul_rn(M[static_cast<size_t>(j) * n + i], xj));
+    __syncthreads();
+  }
+  for (int j = n - 1; j >= 0; --j) {
+    if (threadIdx.x == 0) xs[j] = __ddiv_rn(xs[j], M[static_cast<size_t>(j) * n + j]);
+    __syncthreads();
+    const double xj = xs[j];
+    for (int i = threadIdx.x; i < j; i += kT)
+      xs[i] = __dsub_rn(xs[i], __dmul_rn(M[static_cast<size_t>(j) * n + i], xj));
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < n; i += kT) x[i] = xs[i];
+}
+
+}  // namespace
+
+void dense_factor(const DCsr& A, DenseLU& out, cudaStream_t s, double pivot_tol) {
+  if (A.rows != A.cols) throw RuntimeError("dense LU: matrix not square");
+  const int n = A.rows;
+  if (n > 6000) throw RuntimeError("dense LU: matrix too large for the single-CTA factorization");
+  out.n = n;
+  out.lu.alloc(static_cast<size_t>(n) * n, s);
+  out.perm.alloc(n > 0 ? n : 1, s);
+  out.lu.zero();
+  if (n == 0) return;
+  k_densify<<<blocks_for(n, 256), 256, 0, s>>>(n, A.ptr.get(), A.col.get(), A.val.get(), out.lu.get());
+  DVec<int> bad(1, s);
+  k_lu<<<1, kT, 0, s>>>(n, out.lu.get(), out.perm.get(), pivot_tol, bad.get());
+  MGRX_LAUNCH_CK();
+  count_launch(2);
+  const int b = read_scalar(bad.get(), s);
+  if (b >= 0) throw RuntimeError("dense LU: matrix numerically singular (pivot " + std::to_string(b) + ")");
+}
+
+void dense_solve(const DenseLU& f, const double* b, double* x, cudaStream_t s) {
+  if (f.n == 0) return;
+  const size_t sm = sizeof(double) * f.n;
+  if (sm > 200 * 1024) throw RuntimeError("dense LU solve: system too large for shared memory");
+  if (sm > 48 * 1024)
+    MGRX_CK(cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+  k_lu_solve<<<1, kT, sm, s>>>(f.n, f.lu.get(), f.perm.get(), b, x);
+  MGRX_LAUNCH_CK();
+  count_launch();
+}
+
+}  // namespace mgrx

@@ -1,0 +1,245 @@
+// Synthetic problem generators for the BASELINE.json configs (SURVEY.md §8d,
+// "Next #1"). These produce the input bundle (CSR matrix, rhs, field labels)
+// that both the GPU path and the CPU oracle consume, so both see identical
+// bits. They are host-side input producers, not part of the solve path.
+//
+// cfg1/cfg2 — hybrid mimetic FD (TPFA inner product) on a structured hex grid
+// with unit cells, statically condensed to the two-field [p, pi] system the
+// reference builds in proj/src/problems/mfd.cpp:337-458 (assemble_hybrid +
+// static_condense). With the diagonal inner product B = diag(1/t_l) the
+// fluxes eliminate cell by cell and the condensed rows are
+//   cell c : (acc + sum_l t_l) p_c - sum_l t_l pi_{f(l)}
+//   face f : -sum_{c ~ f} t_{c,l} p_c + (sum_{c ~ f} t_{c,l}) pi_f
+// with half-transmissibility t_l = |f| (c_l . K n_l)/|c_l|^2 = 2 k_dir for
+// unit cubes (mfd.cpp:272-285). All faces carry a multiplier dof (all
+// no-flow) and the accumulation makes the system nonsingular.
+//
+// Dof numbering is slab-major in z: for each layer k, its cells
+// (i fastest), its x-faces, its y-faces, its bottom z-faces, and for the top
+// layer also the top z-faces. Every GPU count uses this one numbering.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_err;
+
+// Box-Muller standard normal on mt19937 (proj/src/problems/comp.cpp:20-31).
+class Normal {
+ public:
+  explicit Normal(unsigned seed) : rng_(seed) {}
+  double operator()() {
+    const double u1 = (static_cast<double>(rng_()) + 0.5) * 0x1.0p-32;
+    const double u2 = (static_cast<double>(rng_()) + 0.5) * 0x1.0p-32;
+    return std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * M_PI * u2);
+  }
+
+ private:
+  std::mt19937 rng_;
+};
+
+// U(a,b) = a + (b-a)(u+0.5)2^-32.
+class Uniform {
+ public:
+  explicit Uniform(unsigned seed) : rng_(seed) {}
+  double operator()(double a, double b) {
+    return a + (b - a) * ((static_cast<double>(rng_()) + 0.5) * 0x1.0p-32);
+  }
+
+ private:
+  std::mt19937 rng_;
+};
+
+struct Problem {
+  int n = 0;
+  std::vector<int> ptr, col, labels, unknown_map;
+  std::vector<double> val, rhs;
+  std::vector<std::string> fields;
+  std::string meta;  // JSON object with generator parameters
+};
+
+struct RowBuilder {
+  // Rows are assembled as small (col, val) lists and sorted by column; the
+  // generator never emits duplicate columns within a row.
+  std::vector<std::pair<int, double>> e;
+  void add(int c, double v) { e.push_back({c, v}); }
+};
+
+void finish_row(Problem& P, RowBuilder& rb) {
+  std::sort(rb.e.begin(), rb.e.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+  for (const auto& [c, v] : rb.e) {
+    P.col.push_back(c);
+    P.val.push_back(v);
+  }
+  P.ptr.push_back(static_cast<int>(P.col.size()));
+  rb.e.clear();
+}
+
+struct MfdLayout {
+  int nx, ny, nz;
+  int64_t nc2, nfx, nfy, slab;
+  int64_t off(int k) const { return slab * k; }
+  int64_t cell(int i, int j, int k) const { return off(k) + i + int64_t(nx) * j; }
+  int64_t xf(int i, int j, int k) const { return off(k) + nc2 + i + int64_t(nx + 1) * j; }
+  int64_t yf(int i, int j, int k) const { return off(k) + nc2 + nfx + i + int64_t(nx) * j; }
+  int64_t zf(int i, int j, int kz) const {
+    const int64_t base = kz < nz ? off(kz) + nc2 + nfx + nfy : off(nz - 1) + nc2 + nfx + nfy + nc2;
+    return base + i + int64_t(nx) * j;
+  }
+  int64_t total() const { return slab * nz + nc2; }
+};
+
+// field: 0 = i.i.d. ln k ~ N(0,1) per cell and direction (cfg1);
+//        1 = layered: mu_k ~ U(-3,3) per layer, ln k = mu_k + sigma N(0,1) (cfg2).
+Problem make_mfd(int nx, int ny, int nz, int field, double sigma, unsigned seed, double accum) {
+  if (nx < 1 || ny < 1 || nz < 1) throw std::invalid_argument("mfd: dims must be >= 1");
+  MfdLayout L{nx, ny, nz, int64_t(nx) * ny, int64_t(nx + 1) * ny, int64_t(nx) * (ny + 1), 0};
+  L.slab = L.nc2 + L.nfx + L.nfy + L.nc2;
+  if (L.total() > INT32_MAX / 2) throw std::invalid_argument("mfd: grid too large for int32 indices");
+  const int64_t ncell = L.nc2 * nz;
+
+  // Half transmissibilities per cell and direction: t = 2 k_dir (unit cube).
+  std::vector<double> tx(ncell), ty(ncell), tz(ncell);
+  {
+    Normal nrm(seed);
+    Uniform uni(seed ^ 0x5bd1e995u);
+    for (int k = 0; k < nz; ++k) {
+      const double mu = field == 1 ? uni(-3.0, 3.0) : 0.0;
+      const double sg = field == 1 ? sigma : 1.0;
+      for (int64_t q = 0; q < L.nc2; ++q) {
+        const int64_t c = k * L.nc2 + q;
+        tx[c] = 2.0 * std::exp(mu + sg * nrm());
+        ty[c] = 2.0 * std::exp(mu + sg * nrm());
+        tz[c] = 2.0 * std::exp(mu + sg * nrm());
+      }
+    }
+  }
+  auto cid = [&](int i, int j, int k) { return int64_t(k) * L.nc2 + i + int64_t(nx) * j; };
+
+  Problem P;
+  P.n = static_cast<int>(L.total());
+  P.fields = {"p", "pi"};
+  P.ptr.reserve(P.n + 1);
+  P.ptr.push_back(0);
+  P.labels.reserve(P.n);
+  RowBuilder rb;
+
+  auto face_row = [&](int64_t fdof, int64_t c0, double t0, int64_t dof0, int64_t c1, double t1,
+                      int64_t dof1) {
+    (void)c0;
+    (void)c1;
+    double d = 0.0;
+    if (dof0 >= 0) {
+      rb.add(static_cast<int>(dof0), -t0);
+      d += t0;
+    }
+    if (dof1 >= 0) {
+      rb.add(static_cast<int>(dof1), -t1);
+      d += t1;
+    }
+    rb.add(static_cast<int>(fdof), d);
+    finish_row(P, rb);
+    P.labels.push_back(1);
+  };
+
+  for (int k = 0; k < nz; ++k) {
+    // cells
+    for (int j = 0; j < ny; ++j)
+      for (int i = 0; i < nx; ++i) {
+        const int64_t c = cid(i, j, k);
+        const double t[6] = {tx[c], tx[c], ty[c], ty[c], tz[c], tz[c]};
+        const int64_t f[6] = {L.xf(i, j, k), L.xf(i + 1, j, k), L.yf(i, j, k),
+                              L.yf(i, j + 1, k), L.zf(i, j, k), L.zf(i, j, k + 1)};
+        double d = accum;
+        for (int l = 0; l < 6; ++l) {
+          d += t[l];
+          rb.add(static_cast<int>(f[l]), -t[l]);
+        }
+        rb.add(static_cast<int>(L.cell(i, j, k)), d);
+        finish_row(P, rb);
+        P.labels.push_back(0);
+      }
+    // x-faces of layer k
+    for (int j = 0; j < ny; ++j)
+      for (int i = 0; i <= nx; ++i) {
+        const bool has0 = i > 0, has1 = i < nx;
+        face_row(L.xf(i, j, k), 0, has0 ? tx[cid(i - 1, j, k)] : 0.0, has0 ? L.cell(i - 1, j, k) : -1,
+                 0, has1 ? tx[cid(i, j, k)] : 0.0, has1 ? L.cell(i, j, k) : -1);
+      }
+    // y-faces of layer k
+    for (int j = 0; j <= ny; ++j)
+      for (int i = 0; i < nx; ++i) {
+        const bool has0 = j > 0, has1 = j < ny;
+        face_row(L.yf(i, j, k), 0, has0 ? ty[cid(i, j - 1, k)] : 0.0, has0 ? L.cell(i, j - 1, k) : -1,
+                 0, has1 ? ty[cid(i, j, k)] : 0.0, has1 ? L.cell(i, j, k) : -1);
+      }
+    // z-faces: bottom of layer k, plus the top boundary for the last layer
+    for (int kz = k; kz <= (k == nz - 1 ? nz : k); ++kz)
+      for (int j = 0; j < ny; ++j)
+        for (int i = 0; i < nx; ++i) {
+          const bool has0 = kz > 0, has1 = kz < nz;
+          face_row(L.zf(i, j, kz), 0, has0 ? tz[cid(i, j, kz - 1)] : 0.0,
+                   has0 ? L.cell(i, j, kz - 1) : -1, 0, has1 ? tz[cid(i, j, kz)] : 0.0,
+                   has1 ? L.cell(i, j, kz) : -1);
+        }
+  }
+  if (static_cast<int64_t>(P.ptr.size()) != L.total() + 1)
+    throw std::logic_error("mfd: row count mismatch");
+
+  Uniform rhs(seed + 0x9e3779b9u);
+  P.rhs.resize(P.n);
+  for (int i = 0; i < P.n; ++i) P.rhs[i] = rhs(-1.0, 1.0);
+
+  char buf[512];
+  std::snprintf(buf, sizeof buf,
+                "{\"problem\":\"mfd\",\"dims\":[%d,%d,%d],\"field\":\"%s\",\"sigma\":%.17g,"
+                "\"seed\":%u,\"accumulation\":%.17g,\"inner_product\":\"tpfa\","
+                "\"cells\":%lld,\"faces\":%lld,\"numbering\":\"slab-major-z\"}",
+                nx, ny, nz, field == 1 ? "layered_lognormal" : "iid_lognormal", sigma, seed,
+                accum, static_cast<long long>(ncell), static_cast<long long>(L.total() - ncell));
+  P.meta = buf;
+  return P;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mgrx_gen_last_error() { return g_err.c_str(); }
+
+void* mgrx_gen_mfd(int nx, int ny, int nz, int field, double sigma, unsigned seed, double accum) {
+  try {
+    return new Problem(make_mfd(nx, ny, nz, field, sigma, seed, accum));
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+int mgrx_gen_n(void* h) { return static_cast<Problem*>(h)->n; }
+long long mgrx_gen_nnz(void* h) { return static_cast<long long>(static_cast<Problem*>(h)->col.size()); }
+int mgrx_gen_nfields(void* h) { return static_cast<int>(static_cast<Problem*>(h)->fields.size()); }
+const char* mgrx_gen_field(void* h, int k) { return static_cast<Problem*>(h)->fields[k].c_str(); }
+const char* mgrx_gen_meta(void* h) { return static_cast<Problem*>(h)->meta.c_str(); }
+int mgrx_gen_has_unknown_map(void* h) { return static_cast<Problem*>(h)->unknown_map.empty() ? 0 : 1; }
+
+void mgrx_gen_copy(void* h, int* ptr, int* col, double* val, int* labels, double* rhs, int* umap) {
+  const Problem* P = static_cast<Problem*>(h);
+  if (ptr) std::memcpy(ptr, P->ptr.data(), sizeof(int) * P->ptr.size());
+  if (col) std::memcpy(col, P->col.data(), sizeof(int) * P->col.size());
+  if (val) std::memcpy(val, P->val.data(), sizeof(double) * P->val.size());
+  if (labels) std::memcpy(labels, P->labels.data(), sizeof(int) * P->labels.size());
+  if (rhs) std::memcpy(rhs, P->rhs.data(), sizeof(double) * P->rhs.size());
+  if (umap && !P->unknown_map.empty())
+    std::memcpy(umap, P->unknown_map.data(), sizeof(int) * P->unknown_map.size());
+}
+
+void mgrx_gen_free(void* h) { delete static_cast<Problem*>(h); }
+
+}  // extern "C"

@@ -1,0 +1,686 @@
+// Device hierarchies. Setup follows proj/src/mgr.cpp:223-316 and
+// proj/src/amg.cpp:147-291 step by step, with every matrix built by the
+// bit-exact kernels of sparse.cu / coarsen.cu. Application follows
+// proj/src/mgr.cpp:177-219 and proj/src/amg.cpp:232-242 with the fusions
+// documented inline (each one preserves the reference's arithmetic).
+#include <algorithm>
+#include <unordered_set>
+
+#include "coarsen.cuh"
+#include "hierarchy.cuh"
+
+namespace mgrx {
+namespace {
+
+__global__ void k_split(int n, const int* __restrict__ labels, const uint8_t* __restrict__ mask,
+                        uint8_t* __restrict__ isf, uint8_t* __restrict__ isc) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint8_t f = mask[labels[i]];
+  isf[i] = f;
+  isc[i] = f ? 0 : 1;
+}
+
+__global__ void k_gather_int(int n, const int* __restrict__ idx, const int* __restrict__ in,
+                             int* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = in[idx[i]];
+}
+
+__global__ void k_iota(int n, int* a) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = i;
+}
+
+__global__ void k_scatter_add(int n, const int* __restrict__ idx, const double* __restrict__ a,
+                              double* __restrict__ z) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) z[idx[i]] = __dadd_rn(z[idx[i]], a[i]);
+}
+
+// P = [-W; I] in global order with W = A_FC scaled by dinv_F
+// (proj/src/mgr.cpp:89-114): C rows carry (cpos, 1.0); F rows carry
+// -(a_fc * dinv_f) at the coarse positions of their C columns.
+template <bool kFill>
+__global__ void k_mgr_interp(int n, const int* __restrict__ ptr, const int* __restrict__ col,
+                             const double* __restrict__ val, const int* __restrict__ fpos,
+                             const int* __restrict__ cpos, const double* __restrict__ dinv_f,
+                             int* __restrict__ cnt, const int* __restrict__ optr,
+                             int* __restrict__ ocol, double* __restrict__ oval) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  if (cpos[r] >= 0) {
+    if (kFill) {
+      ocol[optr[r]] = cpos[r];
+      oval[optr[r]] = 1.0;
+    } else {
+      cnt[r] = 1;
+    }
+    return;
+  }
+  const double dv = kFill ? dinv_f[fpos[r]] : 0.0;
+  int o = kFill ? optr[r] : 0;
+  int c = 0;
+  for (int k = ptr[r]; k < ptr[r + 1]; ++k) {
+    const int j = cpos[col[k]];
+    if (j < 0) continue;
+    if (kFill) {
+      ocol[o] = j;
+      oval[o] = -__dmul_rn(val[k], dv);
+      ++o;
+    }
+    ++c;
+  }
+  if (!kFill) cnt[r] = c;
+}
+
+// R rows span C (proj/src/mgr.cpp:116-146). Injection: (C[j], 1). Jacobi /
+// ideal-with-diagonal-A_FF: -(a_cf * dinv_f) at global F columns plus
+// (C[j], 1), merged in column order.
+template <bool kFill>
+__global__ void k_mgr_restrict(int nc, bool injection, const int* __restrict__ ptr,
+                               const int* __restrict__ col, const double* __restrict__ val,
+                               const int* __restrict__ C, const int* __restrict__ fpos,
+                               const double* __restrict__ dinv_f, int* __restrict__ cnt,
+                               const int* __restrict__ optr, int* __restrict__ ocol,
+                               double* __restrict__ oval) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nc) return;
+  const int r = C[j];
+  int o = kFill ? optr[j] : 0;
+  int c = 0;
+  bool placed = false;
+  auto emit = [&](int cc, double v) {
+    if (kFill) {
+      ocol[o] = cc;
+      oval[o] = v;
+      ++o;
+    }
+    ++c;
+  };
+  if (!injection) {
+    for (int k = ptr[r]; k < ptr[r + 1]; ++k) {
+      const int g = col[k];
+      if (!placed && g > r) {
+        emit(r, 1.0);
+        placed = true;
+      }
+      const int f = fpos[g];
+      if (f >= 0) emit(g, kFill ? -__dmul_rn(val[k], dinv_f[f]) : 0.0);
+    }
+  }
+  if (!placed) emit(r, 1.0);
+  if (!kFill) cnt[j] = c;
+}
+
+__global__ void k_scatter_count(int m, const int* __restrict__ idx, const int* __restrict__ sptr,
+                                int* __restrict__ cnt) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < m) cnt[idx[r]] = sptr[r + 1] - sptr[r];
+}
+
+// Unknown-based P assembly (proj/src/amg.cpp:201-222): sub-row r of a group
+// becomes global row idx[r]; local coarse column k maps to the rank of its
+// global fine index among all C points.
+__global__ void k_group_fill(int m, const int* __restrict__ idx, const int* __restrict__ csub,
+                             const int* __restrict__ cid_global, const int* __restrict__ sptr,
+                             const int* __restrict__ scol, const double* __restrict__ sval,
+                             const int* __restrict__ optr, int* __restrict__ ocol,
+                             double* __restrict__ oval) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  int o = optr[idx[r]];
+  for (int k = sptr[r]; k < sptr[r + 1]; ++k, ++o) {
+    ocol[o] = cid_global[idx[csub[scol[k]]]];
+    oval[o] = sval[k];
+  }
+}
+
+__global__ void k_mark_group_c(int m, const int* __restrict__ idx, const uint8_t* __restrict__ sub_c,
+                               uint8_t* __restrict__ is_c) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < m && sub_c[r]) is_c[idx[r]] = 1;
+}
+
+__global__ void k_eq_flag(int n, const int* __restrict__ a, int v, uint8_t* __restrict__ f) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) f[i] = a[i] == v ? 1 : 0;
+}
+__global__ void k_not(int n, const uint8_t* __restrict__ a, uint8_t* __restrict__ f) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) f[i] = a[i] ? 0 : 1;
+}
+
+template <class K, class... Args>
+void launch1d(K kern, int n, cudaStream_t s, Args... args) {
+  if (n <= 0) return;
+  kern<<<blocks_for(n, 256), 256, 0, s>>>(n, args...);
+  MGRX_LAUNCH_CK();
+  count_launch();
+}
+
+std::vector<int> gather_host(const std::vector<int>& v, const std::vector<int>& idx) {
+  std::vector<int> o;
+  o.reserve(idx.size());
+  for (int i : idx) o.push_back(v[i]);
+  return o;
+}
+
+}  // namespace
+
+// ============================================================================
+// BoundRelax
+// ============================================================================
+void BoundRelax::bind(const SmootherSpec& s, const DCsr& mat, const std::vector<int>* umap,
+                      cudaStream_t st) {
+  if (mat.rows != mat.cols) throw InvalidArgument("smoother: matrix must be square");
+  if (s.sweeps < 1) throw InvalidArgument("smoother: sweeps must be >= 1");
+  if (!(s.weight > 0.0 && s.weight < 2.0)) throw InvalidArgument("smoother: weight must lie in (0, 2)");
+  spec = s;
+  A = &mat;
+  n = mat.rows;
+  switch (s.kind) {
+    case Smoother::jacobi:
+      diag_inverse(mat, dinv, st);
+      break;
+    case Smoother::l1_jacobi: {
+      DVec<double> d;
+      l1_diagonal(mat, true, d, st);
+      dinv.alloc(n > 0 ? n : 1, st);
+      reciprocal(n, d.get(), dinv.get(), st);  // proj/src/relax.cpp:106-113
+      break;
+    }
+    case Smoother::hybrid_l1_gs_forward:
+    case Smoother::hybrid_l1_gs_backward: {
+      // Normalise the partition exactly like proj/src/relax.cpp:12-23; the
+      // device sweep implements the single-range case.
+      if (!s.partition.empty()) {
+        int expect = 0;
+        for (const auto& [b, e] : s.partition) {
+          if (b != expect || e <= b)
+            throw InvalidArgument("smoother partition ranges must tile [0,n) in order");
+          expect = e;
+        }
+        if (expect != n) throw InvalidArgument("smoother partition does not cover the matrix");
+        if (s.partition.size() > 1)
+          throw RuntimeError("smoother: multi-range hybrid partitions are not supported on the device");
+      }
+      l1_diagonal(mat, false, l1d, st);
+      gs_schedule(mat, s.kind == Smoother::hybrid_l1_gs_forward, sched, st);
+      break;
+    }
+    case Smoother::block_jacobi_exact:
+      if (s.block_sizes.empty()) throw InvalidArgument("smoother: block_jacobi_exact requires block sizes");
+      throw RuntimeError("smoother: block_jacobi_exact is not supported on the device path");
+    case Smoother::dense_lu:
+      dense_factor(mat, lu, st);
+      break;
+    case Smoother::amg_vcycle: {
+      AmgSpec cfg = s.amg ? *s.amg : AmgSpec{};
+      std::vector<int> um;
+      if (s.use_unknown_map) {
+        if (umap == nullptr)
+          throw InvalidArgument("smoother: use_unknown_map set but no unknown map supplied");
+        um = *umap;
+      }
+      amg = std::make_unique<AmgHier>();
+      amg->setup(mat, cfg, um, st);
+      break;
+    }
+  }
+  w0.alloc(n > 0 ? n : 1, st);
+  if (s.sweeps > 1 || s.kind == Smoother::amg_vcycle) {
+    w1.alloc(n > 0 ? n : 1, st);
+    w2.alloc(n > 0 ? n : 1, st);
+  }
+}
+
+void BoundRelax::apply(const double* r, const int* rrow, double* z, cudaStream_t st) {
+  if (n == 0) return;
+  const double* rc = r;
+  if (rrow && (spec.kind != Smoother::jacobi && spec.kind != Smoother::l1_jacobi)) {
+    gather(n, rrow, r, w0.get(), st);
+    rc = w0.get();
+    rrow = nullptr;
+  }
+  switch (spec.kind) {
+    case Smoother::dense_lu:
+      dense_solve(lu, rc, z, st);
+      return;
+    case Smoother::jacobi:
+    case Smoother::l1_jacobi: {
+      // sweep 0: z = w*(dinv*r); later: z += w*(dinv*(r - A z)) (relax.cpp:168-174)
+      double* cur = z;
+      if (spec.sweeps > 1) cur = (spec.sweeps % 2 == 1) ? z : w1.get();
+      jacobi0(n, spec.weight, dinv.get(), rc, rrow, cur, st);
+      for (int sw = 1; sw < spec.sweeps; ++sw) {
+        double* nxt = (cur == z) ? w1.get() : z;
+        spmv_jacobi(*A, cur, rc, rrow, dinv.get(), spec.weight, nxt, st);
+        cur = nxt;
+      }
+      return;
+    }
+    case Smoother::hybrid_l1_gs_forward:
+    case Smoother::hybrid_l1_gs_backward: {
+      const bool fwd = spec.kind == Smoother::hybrid_l1_gs_forward;
+      const double* xold = nullptr;
+      double* bufs[2] = {w1.get(), w2.get()};
+      for (int sw = 0; sw < spec.sweeps; ++sw) {
+        double* xnew = (sw == spec.sweeps - 1) ? z : bufs[sw % 2];
+        gs_sweep(*A, sched, l1d.get(), rc, xold, xnew, nullptr, fwd, gs, st);
+        xold = xnew;
+      }
+      return;
+    }
+    case Smoother::amg_vcycle: {
+      // z = V(r); z += V(r - A z) for later sweeps (relax.cpp:186-190)
+      amg->vcycle(rc, z, st);
+      for (int sw = 1; sw < spec.sweeps; ++sw) {
+        spmv_residual(*A, z, rc, nullptr, w1.get(), st);
+        amg->vcycle(w1.get(), w2.get(), st);
+        vec_add(n, w2.get(), z, st);
+      }
+      return;
+    }
+    default:
+      throw RuntimeError("smoother: kind not supported on the device path");
+  }
+}
+
+void BoundRelax::apply_add(const double* r, double* zacc, cudaStream_t st) {
+  if (n == 0) return;
+  if ((spec.kind == Smoother::hybrid_l1_gs_forward || spec.kind == Smoother::hybrid_l1_gs_backward) &&
+      spec.sweeps == 1) {
+    gs_sweep(*A, sched, l1d.get(), r, nullptr, w0.get(), zacc,
+             spec.kind == Smoother::hybrid_l1_gs_forward, gs, st);
+    return;
+  }
+  apply(r, nullptr, w0.get(), st);
+  vec_add(n, w0.get(), zacc, st);
+}
+
+void BoundRelax::check(cudaStream_t st) {
+  gs_check(gs, st);
+  if (amg)
+    for (auto& L : amg->levels) {
+      L.pre.check(st);
+      L.post.check(st);
+    }
+}
+
+// ============================================================================
+// AMG (proj/src/amg.cpp:147-297)
+// ============================================================================
+namespace {
+
+struct LevelBuild {
+  DCsr P;
+  DVec<int> C, F;
+  std::vector<int> coarse_umap;
+  bool stalled = false;
+};
+
+LevelBuild build_level_interp(const DCsr& A, double theta, const std::vector<int>& umap,
+                              long long* fallback, cudaStream_t s) {
+  const int n = A.rows;
+  LevelBuild out;
+  if (umap.empty()) {
+    const DCsr S = strength_graph(A, theta, s);
+    DVec<uint8_t> is_c;
+    pmis(S, is_c, s);
+    DVec<int> cid;
+    const int nc = rank_flags(is_c.get(), n, cid, s);
+    if (nc == n) {
+      out.stalled = true;
+      return out;
+    }
+    out.P = classical_interp(A, S, cid.get(), nc, fallback, s);
+    select_flagged(is_c.get(), n, out.C, s);
+    DVec<uint8_t> isf(n, s);
+    launch1d(k_not, n, s, is_c.get(), isf.get());
+    select_flagged(isf.get(), n, out.F, s);
+    return out;
+  }
+  // Unknown-based: per unknown id (ascending), coarsen the extracted
+  // sub-block; interpolation never crosses unknowns (amg.cpp:188-200).
+  std::vector<int> ids = umap;
+  std::sort(ids.begin(), ids.end());
+  ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+  DVec<int> dmap(n, s);
+  dmap.upload(umap.data(), n);
+  DVec<uint8_t> is_c(n, s), flag(n, s);
+  is_c.zero();
+  struct Group {
+    DVec<int> idx, csub;
+    DCsr P;
+  };
+  std::vector<Group> groups(ids.size());
+  for (size_t g = 0; g < ids.size(); ++g) {
+    launch1d(k_eq_flag, n, s, dmap.get(), ids[g], flag.get());
+    const int m = select_flagged(flag.get(), n, groups[g].idx, s);
+    const DCsr Asub = extract(A, groups[g].idx.get(), m, groups[g].idx.get(), m, s);
+    const DCsr S = strength_graph(Asub, theta, s);
+    DVec<uint8_t> sub_c;
+    pmis(S, sub_c, s);
+    DVec<int> cid;
+    const int nc = rank_flags(sub_c.get(), m, cid, s);
+    groups[g].P = classical_interp(Asub, S, cid.get(), nc, fallback, s);
+    select_flagged(sub_c.get(), m, groups[g].csub, s);
+    launch1d(k_mark_group_c, m, s, groups[g].idx.get(), sub_c.get(), is_c.get());
+  }
+  DVec<int> cid_global;
+  const int nc = rank_flags(is_c.get(), n, cid_global, s);
+  if (nc == n) {
+    out.stalled = true;
+    return out;
+  }
+  DVec<int> cnt(n, s);
+  cnt.zero();
+  for (auto& g : groups)
+    launch1d(k_scatter_count, g.P.rows, s, g.idx.get(), g.P.ptr.get(), cnt.get());
+  out.P.rows = n;
+  out.P.cols = nc;
+  out.P.ptr.alloc(n + 1, s);
+  out.P.nnz = static_cast<int>(exclusive_scan(cnt.get(), out.P.ptr.get(), n, s));
+  out.P.col.alloc(out.P.nnz, s);
+  out.P.val.alloc(out.P.nnz, s);
+  for (auto& g : groups)
+    launch1d(k_group_fill, g.P.rows, s, g.idx.get(), g.csub.get(), cid_global.get(), g.P.ptr.get(),
+             g.P.col.get(), g.P.val.get(), out.P.ptr.get(), out.P.col.get(), out.P.val.get());
+  select_flagged(is_c.get(), n, out.C, s);
+  DVec<uint8_t> isf(n, s);
+  launch1d(k_not, n, s, is_c.get(), isf.get());
+  select_flagged(isf.get(), n, out.F, s);
+  const std::vector<int> ch = out.C.download(nc);
+  out.coarse_umap = gather_host(umap, ch);
+  return out;
+}
+
+}  // namespace
+
+void AmgHier::setup(const DCsr& A, const AmgSpec& cfg, const std::vector<int>& umap, cudaStream_t s) {
+  if (A.rows != A.cols) throw InvalidArgument("amg_setup: matrix must be square");
+  if (!(cfg.strength_theta > 0.0 && cfg.strength_theta < 1.0))
+    throw InvalidArgument("amg_setup: strength_theta must lie in (0,1)");
+  if (cfg.coarse_size < 1) throw InvalidArgument("amg_setup: coarse_size must be >= 1");
+  if (!umap.empty() && static_cast<int>(umap.size()) != A.rows)
+    throw InvalidArgument("amg_setup: unknown_map size mismatch");
+  levels.clear();
+  level_sizes.clear();
+  DCsr Acur = csr_copy(A, s);
+  std::vector<int> map = umap;
+  while (true) {
+    const int n = Acur.rows;
+    level_sizes.push_back(n);
+    levels.emplace_back();
+    AmgLevelD& L = levels.back();
+    L.umap = map;
+    const bool last = static_cast<int>(levels.size()) >= cfg.max_levels;
+    if (n <= cfg.coarse_size || last) {
+      L.A = std::move(Acur);
+      break;
+    }
+    LevelBuild b = build_level_interp(Acur, cfg.strength_theta, map, &fallback_rows, s);
+    if (b.stalled) {
+      truncated = true;
+      L.A = std::move(Acur);
+      break;
+    }
+    L.A = std::move(Acur);
+    L.P = std::move(b.P);
+    L.C = std::move(b.C);
+    L.F = std::move(b.F);
+    L.R = transpose(L.P, s);
+    L.pre.bind(cfg.pre, L.A, nullptr, s);
+    L.post.bind(cfg.post, L.A, nullptr, s);
+    const DCsr AP = spgemm(L.A, L.P, s);
+    Acur = spgemm(L.R, AP, s);
+    map = std::move(b.coarse_umap);
+    L.t.alloc(n, s);
+  }
+  dense_factor(levels.back().A, coarse, s);
+  for (size_t l = 1; l < levels.size(); ++l) {
+    const int n = levels[l].A.rows;
+    levels[l].r.alloc(n > 0 ? n : 1, s);
+    levels[l].z.alloc(n > 0 ? n : 1, s);
+  }
+}
+
+void AmgHier::vcycle(const double* r, double* z, cudaStream_t s) { vcycle_level(0, r, z, s); }
+
+void AmgHier::vcycle_level(int l, const double* r, double* z, cudaStream_t s) {
+  AmgLevelD& L = levels[l];
+  if (l == static_cast<int>(levels.size()) - 1) {
+    dense_solve(coarse, r, z, s);
+    return;
+  }
+  AmgLevelD& N = levels[l + 1];
+  L.pre.apply(r, nullptr, z, s);                       // z = pre(r)
+  spmv_residual(L.A, z, r, nullptr, L.t.get(), s);     // t = r - A z
+  spmv(L.R, L.t.get(), N.r.get(), s);                  // rc = R t
+  vcycle_level(l + 1, N.r.get(), N.z.get(), s);        // ec
+  spmv_add(L.P, N.z.get(), z, s);                      // z += P ec
+  spmv_residual(L.A, z, r, nullptr, L.t.get(), s);     // t = r - A z
+  L.post.apply_add(L.t.get(), z, s);                   // z += post(t)
+}
+
+// ============================================================================
+// MGR (proj/src/mgr.cpp:223-326)
+// ============================================================================
+void MgrHier::setup(const DCsr& A, const std::vector<int>& labels, const std::vector<std::string>& fields,
+                    const std::vector<int>* umap_in, const Strategy& strat, cudaStream_t s) {
+  if (A.rows != A.cols) throw InvalidArgument("mgr_setup: matrix must be square");
+  if (static_cast<int>(labels.size()) != A.rows)
+    throw InvalidArgument("mgr_setup: partition size does not match the matrix");
+  if (umap_in && static_cast<int>(umap_in->size()) != A.rows)
+    throw InvalidArgument("mgr_setup: unknown_map size mismatch");
+  auto field_id = [&](const std::string& name) {
+    for (size_t k = 0; k < fields.size(); ++k)
+      if (fields[k] == name) return static_cast<int>(k);
+    throw InvalidArgument("unknown field name: " + name);
+  };
+  {
+    std::unordered_set<std::string> used;
+    for (const auto& lv : strat.levels) {
+      if (lv.f_fields.empty()) throw InvalidArgument("mgr_setup: a level with no f_fields");
+      for (const auto& f : lv.f_fields) {
+        field_id(f);
+        if (!used.insert(f).second) throw InvalidArgument("mgr_setup: field eliminated twice: " + f);
+      }
+    }
+  }
+  if (strat.coarse.kind == Coarse::gmres_inner)
+    throw RuntimeError("coarse solver gmres_inner is not supported on the device path");
+  n = A.rows;
+  coarse_spec = strat.coarse;
+  levels.clear();
+  DCsr Acur = csr_copy(A, s);  // level operator handed to each level in turn
+  DVec<int> lab(n > 0 ? n : 1, s);
+  lab.upload(labels.data(), n);
+  std::vector<int> umap;
+  if (umap_in) umap = *umap_in;
+
+  for (const auto& spec : strat.levels) {
+    levels.emplace_back();
+    MgrLevelD& L = levels.back();
+    L.A = std::move(Acur);
+    const int nl = L.A.rows;
+    // split_ids (mgr.cpp:27-44)
+    std::vector<uint8_t> mask(fields.size(), 0);
+    for (const auto& f : spec.f_fields) mask[field_id(f)] = 1;
+    DVec<uint8_t> dmask(mask.size(), s), isf(nl > 0 ? nl : 1, s), isc(nl > 0 ? nl : 1, s);
+    dmask.upload(mask.data(), mask.size());
+    launch1d(k_split, nl, s, lab.get(), dmask.get(), isf.get(), isc.get());
+    const int nf = select_flagged(isf.get(), nl, L.F, s);
+    if (nf == 0) throw InvalidArgument("split: F set is empty");
+    const int nc = select_flagged(isc.get(), nl, L.C, s);
+    if (nc == 0) throw InvalidArgument("split: C set is empty (all fields eliminated)");
+    DVec<int> cpos;
+    rank_flags(isf.get(), nl, L.fpos, s);
+    rank_flags(isc.get(), nl, cpos, s);
+
+    if (spec.ff_block_sizes)
+      throw RuntimeError("ff_block_sizes layouts are not supported on the device path");
+    L.Aff = extract(L.A, L.F.get(), nf, L.F.get(), nf, s);
+    DVec<double> dinv_f;
+    if (spec.interp == Interp::ideal || spec.restrict_kind == Restrict::ideal) {
+      if (!structurally_diagonal(L.Aff, s))
+        throw RuntimeError(
+            "ideal transfer operators with a non-diagonal A_FF are not supported on the device path");
+    }
+    diag_inverse(L.Aff, dinv_f, s);
+
+    // P (build_interp)
+    {
+      DVec<int> cnt(nl, s);
+      L.P.rows = nl;
+      L.P.cols = nc;
+      L.P.ptr.alloc(nl + 1, s);
+      launch1d(k_mgr_interp<false>, nl, s, L.A.ptr.get(), L.A.col.get(), L.A.val.get(), L.fpos.get(),
+               cpos.get(), dinv_f.get(), cnt.get(), static_cast<const int*>(nullptr),
+               static_cast<int*>(nullptr), static_cast<double*>(nullptr));
+      L.P.nnz = static_cast<int>(exclusive_scan(cnt.get(), L.P.ptr.get(), nl, s));
+      L.P.col.alloc(L.P.nnz, s);
+      L.P.val.alloc(L.P.nnz, s);
+      launch1d(k_mgr_interp<true>, nl, s, L.A.ptr.get(), L.A.col.get(), L.A.val.get(), L.fpos.get(),
+               cpos.get(), dinv_f.get(), static_cast<int*>(nullptr), L.P.ptr.get(), L.P.col.get(),
+               L.P.val.get());
+    }
+    // R (build_restrict)
+    L.injection = spec.restrict_kind == Restrict::injection;
+    {
+      DVec<int> cnt(nc, s);
+      L.R.rows = nc;
+      L.R.cols = nl;
+      L.R.ptr.alloc(nc + 1, s);
+      launch1d(k_mgr_restrict<false>, nc, s, L.injection, L.A.ptr.get(), L.A.col.get(), L.A.val.get(),
+               L.C.get(), L.fpos.get(), dinv_f.get(), cnt.get(), static_cast<const int*>(nullptr),
+               static_cast<int*>(nullptr), static_cast<double*>(nullptr));
+      L.R.nnz = static_cast<int>(exclusive_scan(cnt.get(), L.R.ptr.get(), nc, s));
+      L.R.col.alloc(L.R.nnz, s);
+      L.R.val.alloc(L.R.nnz, s);
+      launch1d(k_mgr_restrict<true>, nc, s, L.injection, L.A.ptr.get(), L.A.col.get(), L.A.val.get(),
+               L.C.get(), L.fpos.get(), dinv_f.get(), static_cast<int*>(nullptr), L.R.ptr.get(),
+               L.R.col.get(), L.R.val.get());
+    }
+    // F-relaxation smoother on A_FF (+ optional global relaxation on A)
+    std::vector<int> umap_f;
+    if (!umap.empty()) umap_f = gather_host(umap, L.F.download(nf));
+    L.f_relax.bind(spec.f_relax, L.Aff, umap.empty() ? nullptr : &umap_f, s);
+    if (spec.global_relax) {
+      L.g_relax.emplace();
+      L.g_relax->bind(*spec.global_relax, L.A, umap.empty() ? nullptr : &umap, s);
+    }
+    // Galerkin coarse operator R (A P) (mgr.cpp:148-152). With injection,
+    // R(AP) is rows C of AP: every product is AP(C_j, c) * 1.0, exact.
+    {
+      const DCsr AP = spgemm(L.A, L.P, s);
+      DCsr Anext = L.injection ? gather_rows(AP, L.C.get(), nc, s) : spgemm(L.R, AP, s);
+      if (L.injection && !spec.global_relax) L.Acf = extract(L.A, L.C.get(), nc, L.F.get(), nf, s);
+      Acur = std::move(Anext);
+    }
+    // carry labels / unknown map to the C dofs
+    {
+      DVec<int> lab2(nc, s);
+      launch1d(k_gather_int, nc, s, L.C.get(), lab.get(), lab2.get());
+      lab = std::move(lab2);
+      if (!umap.empty()) umap = gather_host(umap, L.C.download(nc));
+    }
+    L.zF.alloc(nf, s);
+    L.rc.alloc(nc, s);
+    L.e.alloc(nc, s);
+    L.t.alloc(nl, s);
+    L.zfull.alloc(nl, s);
+  }
+  A_coarse = std::move(Acur);
+  switch (strat.coarse.kind) {
+    case Coarse::dense_lu:
+      dense_factor(A_coarse, coarse_lu, s);
+      break;
+    case Coarse::amg_vcycle: {
+      std::vector<int> um;
+      if (strat.coarse.use_unknown_map) {
+        if (umap.empty())
+          throw InvalidArgument("mgr_setup: coarse solver requests an unknown map, none given");
+        um = umap;
+      }
+      coarse_amg = std::make_unique<AmgHier>();
+      coarse_amg->setup(A_coarse, strat.coarse.amg, um, s);
+      break;
+    }
+    case Coarse::gmres_inner:
+      break;
+  }
+  const int ncs = A_coarse.rows > 0 ? A_coarse.rows : 1;
+  ct.alloc(ncs, s);
+  cd.alloc(ncs, s);
+}
+
+void MgrHier::coarse_solve(const double* v, double* z, cudaStream_t s) {
+  if (coarse_spec.kind == Coarse::dense_lu) {
+    dense_solve(coarse_lu, v, z, s);
+    return;
+  }
+  // z = V(v); z += V(v - A_c z) for the remaining cycles (mgr.cpp:181-186)
+  coarse_amg->vcycle(v, z, s);
+  for (int c = 1; c < coarse_spec.cycles; ++c) {
+    spmv_residual(A_coarse, z, v, nullptr, ct.get(), s);
+    coarse_amg->vcycle(ct.get(), cd.get(), s);
+    vec_add(A_coarse.rows, cd.get(), z, s);
+  }
+}
+
+void MgrHier::apply(const double* v, double* z, cudaStream_t s) { apply_level(0, v, z, s); }
+
+void MgrHier::apply_level(int l, const double* v, double* z, cudaStream_t s) {
+  if (l == static_cast<int>(levels.size())) {
+    coarse_solve(v, z, s);
+    return;
+  }
+  MgrLevelD& L = levels[l];
+  const int nf = static_cast<int>(L.F.size()), nc = static_cast<int>(L.C.size());
+  if (L.injection && !L.g_relax) {
+    // Fast path, arithmetic identical to mgr.cpp:206-217 with z = 0 on C:
+    //   zF = f_relax(v_F)
+    //   rc = v_C - A_CF zF      (R is injection; A_CC z_C contributes exact zeros)
+    //   e  = next level(rc)
+    //   z  = [0 + zF ; 0] + P e  (one fused prolongation kernel)
+    L.f_relax.apply(v, L.F.get(), L.zF.get(), s);
+    spmv_residual(L.Acf, L.zF.get(), v, L.C.get(), L.rc.get(), s);
+    apply_level(l + 1, L.rc.get(), L.e.get(), s);
+    spmv_prolong(L.P, L.e.get(), L.fpos.get(), L.zF.get(), z, s);
+    (void)nf;
+    (void)nc;
+    return;
+  }
+  // General path (global relaxation and/or non-injection restriction).
+  const int nl = L.A.rows;
+  const double* r = v;
+  if (L.g_relax) {
+    L.g_relax->apply(v, nullptr, z, s);
+    spmv_residual(L.A, z, v, nullptr, L.t.get(), s);
+    r = L.t.get();
+  } else {
+    MGRX_CK(cudaMemsetAsync(z, 0, sizeof(double) * nl, s));
+  }
+  L.f_relax.apply(r, L.F.get(), L.zF.get(), s);
+  launch1d(k_scatter_add, nf, s, L.F.get(), L.zF.get(), z);
+  spmv_residual(L.A, z, v, nullptr, L.t.get(), s);
+  spmv(L.R, L.t.get(), L.rc.get(), s);
+  apply_level(l + 1, L.rc.get(), L.e.get(), s);
+  spmv_add(L.P, L.e.get(), z, s);
+}
+
+void MgrHier::check(cudaStream_t s) {
+  for (auto& L : levels) {
+    L.f_relax.check(s);
+    if (L.g_relax) L.g_relax->check(s);
+  }
+  if (coarse_amg)
+    for (auto& L : coarse_amg->levels) {
+      L.pre.check(s);
+      L.post.check(s);
+    }
+}
+
+}  // namespace mgrx

@@ -1,0 +1,94 @@
+// Device MGR / AMG hierarchies: setup (bit-exact) and the preconditioner
+// application (MGR Algorithm 1, proj/src/mgr.cpp:196-219; AMG V(1,1),
+// proj/src/amg.cpp:232-242). All state lives in HBM; the host only sequences
+// kernel launches (or replays them from a captured CUDA graph).
+#pragma once
+
+#include <deque>
+#include <memory>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "dense.cuh"
+#include "relax.cuh"
+#include "strategy.hpp"
+
+namespace mgrx {
+
+struct AmgHier;
+
+// A smoother specialised to one matrix (BoundSmoother, proj/src/relax.cpp:90-192).
+struct BoundRelax {
+  SmootherSpec spec;
+  const DCsr* A = nullptr;  // matrix it is bound to (owned by the enclosing level)
+  int n = 0;
+  DVec<double> dinv;  // jacobi / l1_jacobi
+  DVec<double> l1d;   // gauss-seidel
+  GsSchedule sched;
+  std::unique_ptr<AmgHier> amg;
+  DenseLU lu;
+  DVec<double> w0, w1, w2;  // workspace
+  GsScratch gs;
+
+  void bind(const SmootherSpec& s, const DCsr& mat, const std::vector<int>* umap, cudaStream_t st);
+  // z = smoother(r) from a zero start; r gathered through rrow when non-null.
+  void apply(const double* r, const int* rrow, double* z, cudaStream_t st);
+  // Same, but fused accumulate: zacc += smoother(r). r contiguous.
+  void apply_add(const double* r, double* zacc, cudaStream_t st);
+  void check(cudaStream_t st);
+};
+
+struct AmgLevelD {
+  DCsr A, P, R;
+  std::vector<int> umap;  // unknown id per dof (empty = scalar)
+  DVec<int> C, F;         // splitting that produced P (parity dumps)
+  BoundRelax pre, post;
+  DVec<double> r, z, t;   // level work vectors (r/z unused on level 0)
+};
+
+struct AmgHier {
+  std::deque<AmgLevelD> levels;  // deque: smoothers hold pointers to level matrices
+  DenseLU coarse;
+  std::vector<int> level_sizes;
+  long long fallback_rows = 0;
+  bool truncated = false;
+
+  void setup(const DCsr& A, const AmgSpec& cfg, const std::vector<int>& umap, cudaStream_t s);
+  void vcycle(const double* r, double* z, cudaStream_t s);
+  int fine_size() const { return levels.empty() ? 0 : levels.front().A.rows; }
+
+ private:
+  void vcycle_level(int l, const double* r, double* z, cudaStream_t s);
+};
+
+struct MgrLevelD {
+  DCsr A;
+  DVec<int> F, C, fpos;
+  DCsr P, R, Acf, Aff;
+  bool injection = true;
+  BoundRelax f_relax;
+  std::optional<BoundRelax> g_relax;
+  DVec<double> zF, rc, e, t, zfull;  // work vectors
+};
+
+struct MgrHier {
+  std::deque<MgrLevelD> levels;
+  DCsr A_coarse;
+  CoarseSpec coarse_spec;
+  DenseLU coarse_lu;
+  std::unique_ptr<AmgHier> coarse_amg;
+  DVec<double> ct, cd;  // coarse-cycle work vectors
+  int n = 0;
+
+  void setup(const DCsr& A, const std::vector<int>& labels, const std::vector<std::string>& fields,
+             const std::vector<int>* umap, const Strategy& strat, cudaStream_t s);
+  void apply(const double* v, double* z, cudaStream_t s);
+  void check(cudaStream_t s);
+
+ private:
+  void apply_level(int l, const double* v, double* z, cudaStream_t s);
+  void coarse_solve(const double* v, double* z, cudaStream_t s);
+};
+
+}  // namespace mgrx

@@ -1,0 +1,43 @@
+// Right-preconditioned restarted GMRES on the device
+// (proj/src/krylov.cpp:37-147): V, w, x, b in HBM; modified Gram-Schmidt
+// with the reference's conditional re-orthogonalisation; deterministic
+// fixed-shape reductions; Givens rotations and the small triangular solve on
+// the host (O(m^2) scalars per restart).
+#pragma once
+
+#include <functional>
+#include <vector>
+
+#include "sparse.cuh"
+#include "strategy.hpp"
+
+namespace mgrx {
+
+struct GmresResult {
+  bool converged = false;
+  int iterations = 0;
+  double final_residual = 0.0;
+  std::vector<double> history;
+};
+
+using DevOp = std::function<void(const double* in, double* out, cudaStream_t s)>;
+
+struct GmresWork {
+  int n = 0, m = 0;
+  DVec<double> V, w, r, z, u;
+  DVec<double> scal, part;  // device scalars / reduction partials
+  DVec<unsigned> ctr;
+  std::vector<double> hscal;
+  double* hpinned = nullptr;
+  void ensure(int n, int m, cudaStream_t s);
+  ~GmresWork();
+};
+
+// A x = b with x0 in x; all vectors are device pointers.
+GmresResult gmres_device(const DCsr& A, const double* b, double* x, const KrylovSpec& cfg,
+                         const DevOp& precond, GmresWork& ws, cudaStream_t s);
+
+// Deterministic device dot product (fixed grid, fixed reduction tree).
+double device_dot(int n, const double* a, const double* b, GmresWork& ws, cudaStream_t s);
+
+}  // namespace mgrx

@@ -1,0 +1,75 @@
+// Device-resident CSR (fp64 values, int32 indices) and the sparse kernels of
+// the MGR-GMRES path. Setup kernels are bit-exact restatements of the
+// reference's Eigen semantics; every floating-point
+// operation is an explicit __dmul_rn/__dadd_rn/__dsub_rn/__ddiv_rn and the
+// library is compiled with --fmad=false, so no contraction can change a bit.
+#pragma once
+
+#include "common.cuh"
+
+namespace mgrx {
+
+struct DCsr {
+  int rows = 0, cols = 0, nnz = 0;
+  DVec<int> ptr, col;
+  DVec<double> val;
+  bool empty() const { return rows == 0; }
+};
+
+// ---- primitives -----------------------------------------------------------
+// Exclusive scan of n ints into out (out has n+1 entries, out[n] = total);
+// returns the total (synchronizes).
+int64_t exclusive_scan(const int* in, int* out, int n, cudaStream_t s);
+int64_t exclusive_scan64(const int64_t* in, int64_t* out, int n, cudaStream_t s);
+// Compact the indices i in [0,n) with flag[i] != 0 (ascending) into out;
+// returns the count (synchronizes).
+int select_flagged(const uint8_t* flag, int n, DVec<int>& out, cudaStream_t s);
+
+// ---- construction / validation --------------------------------------------
+// Upload host CSR and validate it like proj/src/sparse.cpp:24-41.
+DCsr csr_from_host(int rows, int cols, const int* ptr, const int* col, const double* val,
+                   cudaStream_t s);
+DCsr csr_from_device(int rows, int cols, const int* ptr, const int* col, const double* val,
+                     cudaStream_t s);
+void csr_validate(const DCsr& A, cudaStream_t s);
+DCsr csr_copy(const DCsr& A, cudaStream_t s);
+
+// ---- SpMV family (solve path) ---------------------------------------------
+// y = A x                                (Eigen y = A*x: 0 + row sum)
+void spmv(const DCsr& A, const double* x, double* y, cudaStream_t s);
+// y = b - A x ; if brow != null, b is gathered: b[brow[r]]
+void spmv_residual(const DCsr& A, const double* x, const double* b, const int* brow, double* y,
+                   cudaStream_t s);
+// y += A x                               (Eigen y += A*x)
+void spmv_add(const DCsr& A, const double* x, double* y, cudaStream_t s);
+// z[r] = zprev(r) + (A e)[r], zprev(r) = fpos[r] >= 0 ? 0 + zF[fpos[r]] : 0
+// (MGR prolongation, proj/src/mgr.cpp:210-217)
+void spmv_prolong(const DCsr& P, const double* e, const int* fpos, const double* zF, double* z,
+                  cudaStream_t s);
+// Jacobi correction sweep: znew = zold + w*(dinv*(b - A zold)), b gathered via brow.
+void spmv_jacobi(const DCsr& A, const double* zold, const double* b, const int* brow,
+                 const double* dinv, double w, double* znew, cudaStream_t s);
+
+// ---- setup kernels (bit-exact) --------------------------------------------
+DCsr extract(const DCsr& A, const int* rows, int nrows, const int* cols, int ncols, cudaStream_t s);
+DCsr transpose(const DCsr& A, cudaStream_t s);
+// Eigen conservative product A*B.
+DCsr spgemm(const DCsr& A, const DCsr& B, cudaStream_t s);
+// Rows `rows` of A as a new CSR (used for injection R*(AP) = rows C of AP).
+DCsr gather_rows(const DCsr& A, const int* rows, int nrows, cudaStream_t s);
+// 1/a_ii with the reference's row-named errors (proj/src/sparse.cpp:87-104).
+void diag_inverse(const DCsr& A, DVec<double>& dinv, cudaStream_t s);
+// L1 diagonal with singleton (l1 = true) or whole-matrix range (l1 = false:
+// d_i = sum of stored diagonal entries), proj/src/relax.cpp:34-48.
+void l1_diagonal(const DCsr& A, bool singleton_ranges, DVec<double>& d, cudaStream_t s);
+bool structurally_diagonal(const DCsr& A, cudaStream_t s);
+
+// Host copies (tests / dumps).
+struct HostCsr {
+  int rows = 0, cols = 0;
+  std::vector<int> ptr, col;
+  std::vector<double> val;
+};
+HostCsr to_host(const DCsr& A, cudaStream_t s);
+
+}  // namespace mgrx

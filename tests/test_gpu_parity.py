@@ -1,0 +1,161 @@
+"""GPU parity tests: the CUDA path, called through the C ABI (libmgrx.so), is
+compared with the refcpu oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star):
+  * setup products (C/F splittings, P/R/A patterns and values at every level):
+    bit-exact;
+  * SpMV: bit-exact (per-row left-to-right order, no FMA);
+  * residual history: relative gap <= 1e-10 over the first 10 entries;
+  * iteration count within +-1; final true residual <= rtol.
+"""
+import json
+
+import numpy as np
+import pytest
+
+import make_golden
+import paper_2101_11649_b200 as mx
+import refcpu
+
+pytestmark = pytest.mark.gpu
+
+HIST_RTOL = 1e-10
+
+
+def _golden():
+    with open(make_golden.os.path.join(make_golden.HERE, "oracle_golden.json")) as f:
+        return {c["id"]: c for c in json.load(f)["cases"]}
+
+
+def _same_dump(a, b):
+    if isinstance(a, tuple):
+        return (a[3] == b[3] and np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+                and np.array_equal(a[2].view(np.int64), b[2].view(np.int64)))
+    return a.dtype == b.dtype and np.array_equal(a.view(np.int64) if a.dtype == np.float64 else a,
+                                                 b.view(np.int64) if b.dtype == np.float64 else b)
+
+
+@pytest.mark.parametrize("case", make_golden.CASES, ids=lambda c: c["id"])
+def test_setup_bit_exact(case):
+    ptr, col, val, fields, labels, um, rhs = make_golden.build_problem(case["problem"])
+    text = make_golden.strategy_text(case["strategy"])
+    R = refcpu.RefHierarchy(ptr, col, val, fields, labels, text, um)
+    A = mx.Matrix(ptr, col, val)
+    H = mx.Hierarchy(A, mx.DofPartition(fields, labels), text, um)
+    assert H.info() == R.info()
+    gold = _golden()[case["id"]]
+    for p in refcpu.dump_paths(R.info()):
+        g, r = H.dump(p), R.dump(p)
+        assert _same_dump(g, r), f"{case['id']}: {p} differs from the oracle"
+        assert make_golden.digest(g) == gold["digests"][p], f"{case['id']}: {p} differs from golden"
+
+
+@pytest.mark.parametrize("case", make_golden.CASES, ids=lambda c: c["id"])
+def test_solve_parity(case):
+    ptr, col, val, fields, labels, um, rhs = make_golden.build_problem(case["problem"])
+    text = make_golden.strategy_text(case["strategy"])
+    R = refcpu.RefHierarchy(ptr, col, val, fields, labels, text, um)
+    _, rrep = R.solve(rhs, restart=30, max_iters=500, rel_tol=case["rtol"])
+    A = mx.Matrix(ptr, col, val)
+    H = mx.Hierarchy(A, mx.DofPartition(fields, labels), text, um)
+    x, rep = H.solve(rhs, cfg=mx.KrylovConfig(restart=30, max_iters=500, rel_tol=case["rtol"]))
+    assert rep.converged
+    assert abs(rep.iterations - rrep["iterations"]) <= 1
+    k = min(10, len(rep.residual_history), len(rrep["history"]))
+    h, hr = np.array(rep.residual_history[:k]), np.array(rrep["history"][:k])
+    assert np.all(np.abs(h - hr) <= HIST_RTOL * np.abs(hr)), (h, hr)
+    import scipy.sparse as sp
+    M = sp.csr_matrix((val, col, ptr), shape=(ptr.size - 1,) * 2)
+    assert np.linalg.norm(rhs - M @ x) <= case["rtol"] * np.linalg.norm(rhs) * (1 + 1e-9)
+
+
+@pytest.mark.parametrize("case", make_golden.CASES, ids=lambda c: c["id"])
+def test_apply_matches_oracle(case):
+    ptr, col, val, fields, labels, um, rhs = make_golden.build_problem(case["problem"])
+    text = make_golden.strategy_text(case["strategy"])
+    R = refcpu.RefHierarchy(ptr, col, val, fields, labels, text, um)
+    H = mx.Hierarchy(mx.Matrix(ptr, col, val), mx.DofPartition(fields, labels), text, um)
+    v = np.random.default_rng(3).uniform(-1, 1, ptr.size - 1)
+    z, zr = H.apply(v), R.apply(v)
+    assert np.linalg.norm(z - zr) <= 1e-12 * np.linalg.norm(zr)
+
+
+def test_spmv_bit_exact():
+    P = mx.mfd_problem(20, 20, 10, "iid")
+    A = mx.Matrix(P.ptr, P.col, P.val)
+    for seed in range(3):
+        x = np.random.default_rng(seed).standard_normal(P.n)
+        y = A.spmv(x)
+        yr = refcpu.spmv(P.ptr, P.col, P.val, x)
+        assert np.array_equal(y.view(np.int64), yr.view(np.int64))
+    # long rows (spanning several shared-memory chunks) and empty rows
+    rng = np.random.default_rng(5)
+    n = 3000
+    lens = rng.integers(0, 40, n)
+    lens[7] = 2900
+    lens[8] = 0
+    ptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    col = np.concatenate([np.sort(rng.choice(n, size=l, replace=False)) for l in lens]).astype(np.int32)
+    val = rng.standard_normal(ptr[-1])
+    x = rng.standard_normal(n)
+    y = mx.Matrix(ptr, col, val).spmv(x)
+    yr = refcpu.spmv(ptr, col, val, x)
+    assert np.array_equal(y.view(np.int64), yr.view(np.int64))
+
+
+def test_zero_rhs_and_errors():
+    P = mx.mfd_problem(4, 4, 3, "iid")
+    A = mx.Matrix(P.ptr, P.col, P.val)
+    H = mx.Hierarchy(A, P.partition, mx.load_strategy("mfd_mgr_pi_c1"))
+    x, rep = H.solve(np.zeros(P.n), np.ones(P.n))
+    assert rep.converged and rep.iterations == 0 and not x.any()
+    bad = P.rhs.copy()
+    bad[3] = np.nan
+    with pytest.raises(mx.MgrxError, match="non-finite"):
+        H.solve(bad)
+    with pytest.raises(mx.MgrxInvalidArgument, match="unknown field name: rho"):
+        mx.Hierarchy(A, P.partition, json.dumps({"levels": [{"f_fields": ["rho"]}]}))
+    with pytest.raises(mx.MgrxInvalidArgument, match="eliminated twice"):
+        mx.Hierarchy(A, P.partition, json.dumps({"levels": [{"f_fields": ["pi"]}, {"f_fields": ["pi"]}]}))
+    with pytest.raises(mx.MgrxError, match="unknown key 'bogus'"):
+        mx.Hierarchy(A, P.partition, json.dumps({"coarse": {"bogus": 1}}))
+    with pytest.raises(mx.MgrxInvalidArgument, match="C set is empty"):
+        mx.Hierarchy(A, P.partition, json.dumps({"levels": [{"f_fields": ["p", "pi"]}]}))
+    # zero diagonal in A_FF: the message names the A_FF row (proj/src/sparse.cpp:100-101)
+    ptr = np.array([0, 2, 4, 5], np.int32)
+    col = np.array([0, 1, 0, 1, 2], np.int32)
+    val = np.array([1.0, 1.0, 1.0, 0.0, 2.0])
+    with pytest.raises(mx.MgrxError, match="zero diagonal entry at row 1"):
+        mx.Hierarchy(mx.Matrix(ptr, col, val), mx.DofPartition(["a", "b"], np.array([0, 0, 1], np.int32)),
+                     json.dumps({"levels": [{"f_fields": ["a"]}], "coarse": {"kind": "dense_lu"}}))
+    # invalid CSR is rejected like validate()
+    with pytest.raises(mx.MgrxError, match="not strictly increasing in row 0"):
+        mx.Matrix(np.array([0, 2, 3], np.int32), np.array([1, 0, 1], np.int32), np.ones(3))
+
+
+def test_identity_truncates_to_dense():
+    n = 30
+    ptr = np.arange(n + 1, dtype=np.int32)
+    col = np.arange(n, dtype=np.int32)
+    H = mx.Hierarchy(mx.Matrix(ptr, col, np.ones(n)), mx.DofPartition(["x"], np.zeros(n, np.int32)),
+                     json.dumps({"coarse": {"kind": "amg_vcycle", "amg": {"coarse_size": 2}}}))
+    assert H.info()["coarse_amg_levels"] == 1
+    r = np.linspace(1, 30, n)
+    assert np.linalg.norm(H.apply(r) - r) <= 1e-14 * np.linalg.norm(r)
+
+
+@pytest.mark.parametrize("strategy", ["mfd_mgr_pi", "mfd_mgr_pi_c1", "mfd_mgr_pi_c1_l1j", "mfd_mgr_p"])
+def test_cfg1_all_strategies(strategy):
+    """BASELINE cfg1 (20x20x10 hybrid MFD), FGMRES(30) rtol 1e-6."""
+    P = mx.mfd_problem(20, 20, 10, "iid")
+    text = mx.load_strategy(strategy)
+    R = refcpu.RefHierarchy(P.ptr, P.col, P.val, P.partition.field_order, P.partition.labels, text)
+    _, rrep = R.solve(P.rhs, restart=30, rel_tol=1e-6)
+    H = mx.Hierarchy(mx.Matrix(P.ptr, P.col, P.val), P.partition, text)
+    x, rep = H.solve(P.rhs, cfg=mx.KrylovConfig(restart=30, rel_tol=1e-6))
+    assert rep.converged and abs(rep.iterations - rrep["iterations"]) <= 1
+    k = min(10, len(rep.residual_history))
+    h, hr = np.array(rep.residual_history[:k]), np.array(rrep["history"][:k])
+    assert np.all(np.abs(h - hr) <= HIST_RTOL * np.abs(hr))
+    for p in refcpu.dump_paths(R.info()):
+        assert _same_dump(H.dump(p), R.dump(p)), p
