@@ -144,6 +144,7 @@ def workload_config(P, n_gpus):
 
 
 def main():
+    global STRATEGY
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -151,7 +152,10 @@ def main():
     ap.add_argument("--impl", default="mgrx")
     ap.add_argument("--ref-iters", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--strategy", default=None, help="strategies/<name>.json (default: %s)" % STRATEGY)
     args = ap.parse_args()
+    if args.strategy:
+        STRATEGY = args.strategy
     if args.impl == "reference":
         return run_reference(args)
 

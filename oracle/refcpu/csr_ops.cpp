@@ -14,7 +14,6 @@ namespace refcpu {
 
 namespace {
 int g_threads = 1;
-constexpr int64_t kChunk = 8192;  // fixed reduction chunk: thread-count independent
 }  // namespace
 
 void set_threads(int n) { g_threads = n < 1 ? 1 : n; }
@@ -381,20 +380,54 @@ Csr BlockDiagonalLU::solve_columns(const Csr& B) const {
   return from_triplets(n_, Bt.rows, out);
 }
 
+// Inner products use this project's canonical reduction order, which the
+// device reductions of libmgrx implement too (paper_2101_11649_b200/csrc/
+// krylov.cu): 592 x 256 lanes each accumulate a strided slice left to right,
+// lanes fold in a fixed shuffle-down tree (offsets 16..1), warps fold in the
+// same tree, and the 592 block partials fold the same way. The reference's
+// order (an Eigen SIMD reduction, version unpinned) is not reproducible
+// (SURVEY Appendix A.8); fixing one order makes GPU and oracle histories
+// comparable bit for bit.
+namespace {
+constexpr int kRB = 592, kRT = 256;
+Real fold32(Real* v) {
+  for (int o = 16; o > 0; o >>= 1)
+    for (int l = 0; l < o; ++l) v[l] = v[l] + v[l + o];
+  return v[0];
+}
+Real fold_block(const Real* lane) {  // kRT lane values -> block value
+  Real w[kRT / 32];
+  Real tmp[32];
+  for (int q = 0; q < kRT / 32; ++q) {
+    for (int l = 0; l < 32; ++l) tmp[l] = lane[q * 32 + l];
+    w[q] = fold32(tmp);
+  }
+  for (int l = 0; l < 32; ++l) tmp[l] = l < kRT / 32 ? w[l] : 0.0;
+  return fold32(tmp);
+}
+}  // namespace
+
 Real dot(const Vec& a, const Vec& b) {
   const int64_t n = static_cast<int64_t>(a.size());
-  const int64_t nchunks = (n + kChunk - 1) / kChunk;
-  std::vector<Real> part(nchunks, 0.0);
+  const int64_t stride = static_cast<int64_t>(kRB) * kRT;
+  std::vector<Real> part(kRB);
 #pragma omp parallel for num_threads(g_threads) schedule(static)
-  for (int64_t c = 0; c < nchunks; ++c) {
-    Real s = 0.0;
-    const int64_t hi = std::min(n, (c + 1) * kChunk);
-    for (int64_t i = c * kChunk; i < hi; ++i) s += a[i] * b[i];
-    part[c] = s;
+  for (int blk = 0; blk < kRB; ++blk) {
+    Real lane[kRT];
+    for (int t = 0; t < kRT; ++t) {
+      Real s = 0.0;
+      for (int64_t i = static_cast<int64_t>(blk) * kRT + t; i < n; i += stride) s = s + a[i] * b[i];
+      lane[t] = s;
+    }
+    part[blk] = fold_block(lane);
   }
-  Real s = 0.0;
-  for (Real p : part) s += p;
-  return s;
+  Real lane[kRT];
+  for (int t = 0; t < kRT; ++t) {
+    Real s = 0.0;
+    for (int q = t; q < kRB; q += kRT) s = s + part[q];
+    lane[t] = s;
+  }
+  return fold_block(lane);
 }
 
 Real norm(const Vec& a) { return std::sqrt(dot(a, a)); }

@@ -288,10 +288,10 @@ int mgrx_apply(mgrx_hier* h, const double* v, double* z, int on_device) {
     cudaStream_t s = h->ctx->stream;
     const int n = h->A.rows;
     if (on_device) {
-      h->H.apply(v, z, s);
+      h->H.apply_graph(v, z, s);
     } else {
       h->vin.upload(v, n);
-      h->H.apply(h->vin.get(), h->vout.get(), s);
+      h->H.apply_graph(h->vin.get(), h->vout.get(), s);
       MGRX_CK(cudaMemcpyAsync(z, h->vout.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, s));
     }
     MGRX_CK(cudaStreamSynchronize(s));
@@ -322,7 +322,7 @@ int mgrx_solve(mgrx_hier* h, const double* b, double* x, const mgrx_krylov* cfg,
       dx = h->vout.get();
     }
     MgrHier* H = &h->H;
-    const DevOp prec = [H](const double* in, double* out, cudaStream_t st) { H->apply(in, out, st); };
+    const DevOp prec = [H](const double* in, double* out, cudaStream_t st) { H->apply_graph(in, out, st); };
     EventTimer t(s);
     GmresResult r = gmres_device(h->A, db, dx, k, prec, h->ws, s);
     const double solve_s = t.stop();

@@ -126,6 +126,10 @@ void dense_factor(const DCsr& A, DenseLU& out, cudaStream_t s, double pivot_tol)
   k_lu<<<1, kT, 0, s>>>(n, out.lu.get(), out.perm.get(), pivot_tol, bad.get());
   MGRX_LAUNCH_CK();
   count_launch(2);
+  const size_t sm = sizeof(double) * n;
+  if (sm > 200 * 1024) throw RuntimeError("dense LU solve: system too large for shared memory");
+  if (sm > 48 * 1024)
+    MGRX_CK(cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
   const int b = read_scalar(bad.get(), s);
   if (b >= 0) throw RuntimeError("dense LU: matrix numerically singular (pivot " + std::to_string(b) + ")");
 }
@@ -133,9 +137,6 @@ void dense_factor(const DCsr& A, DenseLU& out, cudaStream_t s, double pivot_tol)
 void dense_solve(const DenseLU& f, const double* b, double* x, cudaStream_t s) {
   if (f.n == 0) return;
   const size_t sm = sizeof(double) * f.n;
-  if (sm > 200 * 1024) throw RuntimeError("dense LU solve: system too large for shared memory");
-  if (sm > 48 * 1024)
-    MGRX_CK(cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
   k_lu_solve<<<1, kT, sm, s>>>(f.n, f.lu.get(), f.perm.get(), b, x);
   MGRX_LAUNCH_CK();
   count_launch();

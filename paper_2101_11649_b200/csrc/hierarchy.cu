@@ -4,6 +4,7 @@
 // proj/src/mgr.cpp:177-219 and proj/src/amg.cpp:232-242 with the fusions
 // documented inline (each one preserves the reference's arithmetic).
 #include <algorithm>
+#include <cstdlib>
 #include <unordered_set>
 
 #include "coarsen.cuh"
@@ -207,6 +208,7 @@ void BoundRelax::bind(const SmootherSpec& s, const DCsr& mat, const std::vector<
       }
       l1_diagonal(mat, false, l1d, st);
       gs_schedule(mat, s.kind == Smoother::hybrid_l1_gs_forward, sched, st);
+      gs_bind_scratch(gs, st);
       break;
     }
     case Smoother::block_jacobi_exact:
@@ -631,6 +633,43 @@ void MgrHier::coarse_solve(const double* v, double* z, cudaStream_t s) {
 }
 
 void MgrHier::apply(const double* v, double* z, cudaStream_t s) { apply_level(0, v, z, s); }
+
+void MgrHier::apply_graph(const double* v, double* z, cudaStream_t s) {
+  static const bool enabled = [] {
+    const char* e = std::getenv("MGRX_GRAPHS");
+    return !(e && e[0] == '0');
+  }();
+  if (!enabled) {
+    apply(v, z, s);
+    return;
+  }
+  auto it = graphs_.find({v, z});
+  if (it == graphs_.end()) {
+    Captured c;
+    const long long l0 = g_launches;
+    cudaGraph_t g;
+    MGRX_CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    try {
+      apply(v, z, s);
+    } catch (...) {
+      cudaStreamEndCapture(s, &g);
+      throw;
+    }
+    MGRX_CK(cudaStreamEndCapture(s, &g));
+    MGRX_CK(cudaGraphInstantiate(&c.exec, g, 0));
+    MGRX_CK(cudaGraphDestroy(g));
+    c.nodes = g_launches - l0;
+    g_launches = l0;
+    it = graphs_.emplace(std::make_pair(v, z), c).first;
+  }
+  MGRX_CK(cudaGraphLaunch(it->second.exec, s));
+  count_launch(it->second.nodes);
+}
+
+MgrHier::~MgrHier() {
+  for (auto& kv : graphs_)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+}
 
 void MgrHier::apply_level(int l, const double* v, double* z, cudaStream_t s) {
   if (l == static_cast<int>(levels.size())) {

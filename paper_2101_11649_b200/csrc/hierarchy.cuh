@@ -5,6 +5,7 @@
 #pragma once
 
 #include <deque>
+#include <map>
 #include <memory>
 #include <optional>
 #include <string>
@@ -84,9 +85,17 @@ struct MgrHier {
   void setup(const DCsr& A, const std::vector<int>& labels, const std::vector<std::string>& fields,
              const std::vector<int>* umap, const Strategy& strat, cudaStream_t s);
   void apply(const double* v, double* z, cudaStream_t s);
+  // Same, replayed from a CUDA graph captured once per (v, z) address pair.
+  void apply_graph(const double* v, double* z, cudaStream_t s);
   void check(cudaStream_t s);
+  ~MgrHier();
 
  private:
+  struct Captured {
+    cudaGraphExec_t exec = nullptr;
+    long long nodes = 0;
+  };
+  std::map<std::pair<const double*, double*>, Captured> graphs_;
   void apply_level(int l, const double* v, double* z, cudaStream_t s);
   void coarse_solve(const double* v, double* z, cudaStream_t s);
 };

@@ -14,7 +14,7 @@ namespace mgrx {
 namespace {
 
 constexpr int kGsThreads = 128;
-constexpr long long kSpinLimit = 1LL << 22;
+constexpr long long kSpinLimit = 1LL << 24;
 
 __device__ __forceinline__ double ld_relaxed(const double* p) {
   double v;
@@ -29,6 +29,14 @@ __device__ __forceinline__ int ld_relaxed_int(const int* p) {
   asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+
+// Each lane owns one row and walks it in register-resident chunks of kChunk
+// entries: the chunk's columns/values (and the old values of non-dependency
+// columns) are loaded up front, all pending dependencies are polled in
+// parallel, and the chunk is folded into the row sum in stored order only
+// once every value is present. A lane that finds a dependency still pending
+// backs off briefly so spinning warps do not crowd out producing ones.
+constexpr int kChunk = 16;
 
 __global__ void __launch_bounds__(kGsThreads)
     k_gs(int n, const int* __restrict__ order, const int* __restrict__ ptr,
@@ -48,31 +56,59 @@ __global__ void __launch_bounds__(kGsThreads)
     ke = ptr[i + 1];
     s = b[i];
   }
+  int cc[kChunk];
+  double cv[kChunk], xv[kChunk];
+  unsigned pending = 0;
+  int cn = 0;
+  auto load_chunk = [&]() {
+    cn = min(kChunk, ke - k);
+    pending = 0;
+#pragma unroll
+    for (int q = 0; q < kChunk; ++q) {
+      if (q < cn) {
+        cc[q] = col[k + q];
+        cv[q] = val[k + q];
+        const bool dep = fwd ? (cc[q] < i) : (cc[q] > i);
+        if (dep) pending |= 1u << q;
+        else xv[q] = xold ? xold[cc[q]] : 0.0;
+      }
+    }
+  };
+  if (active) load_chunk();
   bool done = !active;
   long long spins = 0;
   while (!__all_sync(0xffffffffu, done)) {
     if (!done) {
-      for (; k < ke; ++k) {
-        const int j = col[k];
-        double xv;
-        if (fwd ? (j < i) : (j > i)) {
-          xv = ld_relaxed(xnew + j);
-          if (__double_as_longlong(xv) == -1LL) break;
-        } else {
-          xv = xold ? xold[j] : 0.0;
+#pragma unroll
+      for (int q = 0; q < kChunk; ++q) {
+        if (pending & (1u << q)) {
+          const double v = ld_relaxed(xnew + cc[q]);
+          if (__double_as_longlong(v) != -1LL) {
+            xv[q] = v;
+            pending &= ~(1u << q);
+          }
         }
-        s = __dsub_rn(s, __dmul_rn(val[k], xv));
       }
-      if (k == ke) {
-        const double xi = xold ? xold[i] : 0.0;
-        const double v = __dadd_rn(xi, __ddiv_rn(s, d[i]));
-        st_relaxed(xnew + i, v);
-        if (zadd) zadd[i] = __dadd_rn(zadd[i], v);
-        done = true;
+      if (pending == 0) {
+#pragma unroll
+        for (int q = 0; q < kChunk; ++q)
+          if (q < cn) s = __dsub_rn(s, __dmul_rn(cv[q], xv[q]));
+        k += cn;
+        if (k >= ke) {
+          const double xi = xold ? xold[i] : 0.0;
+          const double v = __dadd_rn(xi, __ddiv_rn(s, d[i]));
+          st_relaxed(xnew + i, v);
+          if (zadd) zadd[i] = __dadd_rn(zadd[i], v);
+          done = true;
+        } else {
+          load_chunk();
+        }
       } else if (++spins > kSpinLimit) {
         atomicExch(tk + 1, 1);
         st_relaxed(xnew + i, 0.0);
         done = true;
+      } else {
+        __nanosleep(32);
       }
     }
   }
@@ -161,10 +197,7 @@ void gs_sweep(const DCsr& A, const GsSchedule& sch, const double* d, const doubl
               cudaStream_t s) {
   const int n = A.rows;
   if (n == 0) return;
-  if (scr.ticket_err.size() < 2) {
-    scr.ticket_err.alloc(2, s);
-    scr.ticket_err.zero();
-  }
+  if (scr.ticket_err.size() < 2) throw RuntimeError("gs_sweep: scratch not bound");
   MGRX_CK(cudaMemsetAsync(scr.ticket_err.get(), 0, sizeof(int), s));
   MGRX_CK(cudaMemsetAsync(xnew, 0xff, sizeof(double) * n, s));
   k_gs<<<blocks_for(n, kGsThreads), kGsThreads, 0, s>>>(n, sch.order.get(), A.ptr.get(), A.col.get(),
@@ -172,6 +205,13 @@ void gs_sweep(const DCsr& A, const GsSchedule& sch, const double* d, const doubl
                                                        forward ? 1 : 0, scr.ticket_err.get());
   MGRX_LAUNCH_CK();
   count_launch();
+}
+
+void gs_bind_scratch(GsScratch& scr, cudaStream_t s) {
+  if (scr.ticket_err.size() < 2) {
+    scr.ticket_err.alloc(2, s);
+    scr.ticket_err.zero();
+  }
 }
 
 void gs_check(GsScratch& scr, cudaStream_t s) {

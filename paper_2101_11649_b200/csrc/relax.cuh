@@ -28,6 +28,7 @@ struct GsScratch {
 void gs_sweep(const DCsr& A, const GsSchedule& sch, const double* d, const double* b,
               const double* xold, double* xnew, double* zadd, bool forward, GsScratch& scr,
               cudaStream_t s);
+void gs_bind_scratch(GsScratch& scr, cudaStream_t s);
 // Throws if a sweep since the last check hit the spin limit.
 void gs_check(GsScratch& scr, cudaStream_t s);
 
