@@ -230,7 +230,10 @@ def main():
     peak, peak_kind = peaks()
     info = H.info()
     probes = {}
-    for name in ["spmv.A", "mgr.0.rres", "mgr.0.prolong", "amg.0.resid", "amg.0.pre", "amg.0.post"]:
+    names = ["spmv.A", "mgr.0.rres", "mgr.0.prolong"]
+    for k in range(max(info["coarse_amg_levels"] - 1, 0)):
+        names += [f"amg.{k}.resid", f"amg.{k}.pre", f"amg.{k}.post"]
+    for name in names:
         try:
             ms_k, by = H.time_kernel(name, reps=20)
             probes[name] = {"avg_ms": ms_k, "bytes": by, "GBps": by / (ms_k * 1e-3) / 1e9}

@@ -139,9 +139,10 @@ void prepare_probe(mgrx_hier* h, const std::string& w, std::function<void()>& fn
     if (what == "pre" || what == "post") {
       BoundRelax* R = what == "pre" ? &L->pre : &L->post;
       fn = [=] { R->apply(y, nullptr, z, s); };
+      const double sweep_more = spmv_model_bytes(L->A) + 16.0 * m;  // later sweeps: SpMV + 16m
       bytes = (R->spec.kind == Smoother::jacobi || R->spec.kind == Smoother::l1_jacobi)
-                  ? 24.0 * m
-                  : 12.0 * L->A.nnz + 4.0 * (m + 1) + 24.0 * m;
+                  ? 24.0 * m + (R->spec.sweeps - 1) * sweep_more
+                  : R->spec.sweeps * (12.0 * L->A.nnz + 4.0 * (m + 1) + 24.0 * m);
       return;
     }
   }

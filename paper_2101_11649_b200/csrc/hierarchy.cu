@@ -4,6 +4,7 @@
 // proj/src/mgr.cpp:177-219 and proj/src/amg.cpp:232-242 with the fusions
 // documented inline (each one preserves the reference's arithmetic).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <unordered_set>
 
@@ -207,7 +208,7 @@ void BoundRelax::bind(const SmootherSpec& s, const DCsr& mat, const std::vector<
           throw RuntimeError("smoother: multi-range hybrid partitions are not supported on the device");
       }
       l1_diagonal(mat, false, l1d, st);
-      gs_schedule(mat, s.kind == Smoother::hybrid_l1_gs_forward, sched, st);
+      gs_schedule(mat, s.kind == Smoother::hybrid_l1_gs_forward, l1d.get(), s.sweeps > 1, sched, st);
       gs_bind_scratch(gs, st);
       break;
     }
@@ -441,6 +442,13 @@ void AmgHier::setup(const DCsr& A, const AmgSpec& cfg, const std::vector<int>& u
     L.t.alloc(n, s);
   }
   dense_factor(levels.back().A, coarse, s);
+  if (const char* v = std::getenv("MGRX_VERBOSE"); v && v[0] == '1') {
+    for (size_t l = 0; l < levels.size(); ++l) {
+      const AmgLevelD& L = levels[l];
+      std::fprintf(stderr, "[mgrx] amg level %zu: n=%d nnz=%d gs_depth=%d/%d\n", l, L.A.rows, L.A.nnz,
+                   L.pre.sched.levels, L.post.sched.levels);
+    }
+  }
   for (size_t l = 1; l < levels.size(); ++l) {
     const int n = levels[l].A.rows;
     levels[l].r.alloc(n > 0 ? n : 1, s);

@@ -6,7 +6,12 @@
 // produce, and a finished row publishes its 64-bit result with one relaxed
 // gpu-scope store. Every row performs exactly the reference's operations in
 // the reference's order, so the result is bitwise equal to the CPU loop.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
 
 #include "relax.cuh"
 
@@ -14,7 +19,11 @@ namespace mgrx {
 namespace {
 
 constexpr int kGsThreads = 128;
+constexpr int kGsCap = 4096;  // sweep-CSR entries staged in shared memory per CTA
+constexpr size_t kGsSmem = kGsCap * (2 * sizeof(double) + sizeof(int));
+constexpr int kPoll = 8;       // entries polled per lane per round
 constexpr long long kSpinLimit = 1LL << 24;
+constexpr int kDepBit = 1 << 31;
 
 __device__ __forceinline__ double ld_relaxed(const double* p) {
   double v;
@@ -29,89 +38,284 @@ __device__ __forceinline__ int ld_relaxed_int(const int* p) {
   asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ bool pending_value(double v) { return __double_as_longlong(v) == -1LL; }
 
-// Each lane owns one row and walks it in register-resident chunks of kChunk
-// entries: the chunk's columns/values (and the old values of non-dependency
-// columns) are loaded up front, all pending dependencies are polled in
-// parallel, and the chunk is folded into the row sum in stored order only
-// once every value is present. A lane that finds a dependency still pending
-// backs off briefly so spinning warps do not crowd out producing ones.
-constexpr int kChunk = 16;
-
+// Sync-free sweep kernel. A team of kT lanes owns one row (kT = 1, 4 or 8,
+// chosen from the average dependency count). The CTA takes kGsThreads/kT
+// consecutive sweep positions per ticket and stages their sweep-CSR entries
+// in shared memory, next to one value slot per entry. In every round the team
+// lanes poll all still-missing dependency values of the row in parallel and
+// park them in the slots; the team leader folds the slots into the row sum in
+// stored order for as far as they are filled. So when the last dependency
+// lands, everything else is already on chip and the row finishes at once.
+// kFull: entries carry a dependency flag; other columns read the old iterate.
+// Persistent CTAs: the grid keeps only a few dependency levels in flight, so
+// polling does not starve the rows that produce values.
+template <int kT, bool kFull>
 __global__ void __launch_bounds__(kGsThreads)
-    k_gs(int n, const int* __restrict__ order, const int* __restrict__ ptr,
-         const int* __restrict__ col, const double* __restrict__ val, const double* __restrict__ d,
+    k_gs(int n, const int* __restrict__ order, const int* __restrict__ sptr,
+         const int* __restrict__ scol, const double* __restrict__ sval, const double* __restrict__ sd,
          const double* __restrict__ b, const double* __restrict__ xold, double* xnew, double* zadd,
-         int fwd, int* tk) {
+         int* tk) {
+  extern __shared__ double smem[];
+  double* cval = smem;                     // kGsCap entry values
+  double* cx = smem + kGsCap;              // kGsCap parked x values
+  int* ccol = reinterpret_cast<int*>(smem + 2 * kGsCap);
   __shared__ int base;
-  if (threadIdx.x == 0) base = atomicAdd(tk, kGsThreads);
-  __syncthreads();
-  const int pos = base + threadIdx.x;
-  const bool active = pos < n;
-  int i = 0, k = 0, ke = 0;
-  double s = 0.0;
-  if (active) {
-    i = order[pos];
-    k = ptr[i];
-    ke = ptr[i + 1];
-    s = b[i];
-  }
-  int cc[kChunk];
-  double cv[kChunk], xv[kChunk];
-  unsigned pending = 0;
-  int cn = 0;
-  auto load_chunk = [&]() {
-    cn = min(kChunk, ke - k);
-    pending = 0;
-#pragma unroll
-    for (int q = 0; q < kChunk; ++q) {
-      if (q < cn) {
-        cc[q] = col[k + q];
-        cv[q] = val[k + q];
-        const bool dep = fwd ? (cc[q] < i) : (cc[q] > i);
-        if (dep) pending |= 1u << q;
-        else xv[q] = xold ? xold[cc[q]] : 0.0;
+  constexpr int kRowsPerCta = kGsThreads / kT;
+  const int lane = threadIdx.x & 31;
+  const int u = lane % kT;                 // lane within team
+  const int leader = lane - u;
+  const unsigned team_mask = (kT == 32 ? 0xffffffffu : ((1u << kT) - 1u)) << leader;
+  while (true) {
+    if (threadIdx.x == 0) base = atomicAdd(tk, kRowsPerCta);
+    __syncthreads();
+    const int p0 = base;
+    if (p0 >= n) return;
+    const int pend = min(p0 + kRowsPerCta, n);
+    const int e0 = sptr[p0], e1 = sptr[pend];
+    const bool staged = (e1 - e0) <= kGsCap;
+    if (staged)
+      for (int q = e0 + threadIdx.x; q < e1; q += kGsThreads) {
+        int c = scol[q];
+        ccol[q - e0] = c;
+        cval[q - e0] = sval[q];
+        double v = __longlong_as_double(-1LL);
+        if (kFull && !(c & kDepBit)) v = xold[c];
+        cx[q - e0] = v;
       }
+    __syncthreads();
+    const int p = p0 + threadIdx.x / kT;
+    const bool active = p < n;
+    int i = 0, k = 0, ke = 0;
+    double s = 0.0;
+    if (active) {
+      i = order[p];
+      k = sptr[p];
+      ke = sptr[p + 1];
+      if (u == 0) s = b[i];
     }
-  };
-  if (active) load_chunk();
-  bool done = !active;
-  long long spins = 0;
-  while (!__all_sync(0xffffffffu, done)) {
-    if (!done) {
+    bool done = !active;
+    long long spins = 0;
+    while (!__all_sync(0xffffffffu, done)) {
+      if (!done) {
+        if (staged) {
+          // poll the missing dependencies of the row's next kPoll*kT entries
+          // (team-strided): all loads are issued before any is consumed, so a
+          // round costs one L2 round trip however many values are missing
+          bool need[kPoll];
+          int ce[kPoll];
+          double pv[kPoll];
 #pragma unroll
-      for (int q = 0; q < kChunk; ++q) {
-        if (pending & (1u << q)) {
-          const double v = ld_relaxed(xnew + cc[q]);
-          if (__double_as_longlong(v) != -1LL) {
-            xv[q] = v;
-            pending &= ~(1u << q);
+          for (int t = 0; t < kPoll; ++t) {
+            const int e = k + u + t * kT;
+            need[t] = e < ke && pending_value(cx[e - e0]);
+            int c = need[t] ? ccol[e - e0] : 0;
+            if (kFull) c &= ~kDepBit;
+            ce[t] = c;
+          }
+#pragma unroll
+          for (int t = 0; t < kPoll; ++t)
+            if (need[t]) pv[t] = ld_relaxed(xnew + ce[t]);
+#pragma unroll
+          for (int t = 0; t < kPoll; ++t)
+            if (need[t] && !pending_value(pv[t])) cx[k + u + t * kT - e0] = pv[t];
+          __syncwarp(team_mask);
+          int k2 = k;
+          if (u == 0) {
+            while (k2 < ke && !pending_value(cx[k2 - e0])) {
+              s = __dsub_rn(s, __dmul_rn(cval[k2 - e0], cx[k2 - e0]));
+              ++k2;
+            }
+          }
+          k2 = __shfl_sync(team_mask, k2, leader);
+          const bool progressed = k2 > k;
+          k = k2;
+          if (k >= ke) {
+            if (u == 0) {
+              const double xi = kFull ? xold[i] : 0.0;
+              const double v = __dadd_rn(xi, __ddiv_rn(s, sd[p]));
+              st_relaxed(xnew + i, v);
+              if (zadd) zadd[i] = __dadd_rn(zadd[i], v);
+            }
+            done = true;
+          } else if (!progressed) {
+            if (++spins > kSpinLimit) {
+              if (u == 0) {
+                atomicExch(tk + 1, 1);
+                st_relaxed(xnew + i, 0.0);
+              }
+              done = true;
+            } else {
+              __nanosleep(20);
+            }
+          }
+        } else {
+          // unstaged fallback (huge rows): leader walks the row from global memory
+          bool prog = false;
+          if (u == 0) {
+            while (k < ke) {
+              int c = scol[k];
+              double xv;
+              if (kFull && !(c & kDepBit)) {
+                xv = xold[c];
+              } else {
+                if (kFull) c &= ~kDepBit;
+                xv = ld_relaxed(xnew + c);
+                if (pending_value(xv)) break;
+              }
+              s = __dsub_rn(s, __dmul_rn(sval[k], xv));
+              ++k;
+              prog = true;
+            }
+          }
+          k = __shfl_sync(team_mask, k, leader);
+          prog = __shfl_sync(team_mask, prog, leader);
+          if (k >= ke) {
+            if (u == 0) {
+              const double xi = kFull ? xold[i] : 0.0;
+              const double v = __dadd_rn(xi, __ddiv_rn(s, sd[p]));
+              st_relaxed(xnew + i, v);
+              if (zadd) zadd[i] = __dadd_rn(zadd[i], v);
+            }
+            done = true;
+          } else if (!prog) {
+            if (++spins > kSpinLimit) {
+              if (u == 0) {
+                atomicExch(tk + 1, 1);
+                st_relaxed(xnew + i, 0.0);
+              }
+              done = true;
+            } else {
+              __nanosleep(20);
+            }
           }
         }
       }
-      if (pending == 0) {
-#pragma unroll
-        for (int q = 0; q < kChunk; ++q)
-          if (q < cn) s = __dsub_rn(s, __dmul_rn(cv[q], xv[q]));
-        k += cn;
-        if (k >= ke) {
-          const double xi = xold ? xold[i] : 0.0;
-          const double v = __dadd_rn(xi, __ddiv_rn(s, d[i]));
-          st_relaxed(xnew + i, v);
-          if (zadd) zadd[i] = __dadd_rn(zadd[i], v);
-          done = true;
-        } else {
-          load_chunk();
-        }
-      } else if (++spins > kSpinLimit) {
-        atomicExch(tk + 1, 1);
-        st_relaxed(xnew + i, 0.0);
-        done = true;
-      } else {
-        __nanosleep(32);
-      }
+    }
+    __syncthreads();
+  }
+}
+
+// Level-synchronous sweep inside one thread-block cluster: all CTAs of the
+// cluster walk the dependency levels in lockstep; rows of a level are
+// independent, so each thread computes whole rows (same arithmetic, same
+// order), publishes x_i to L2 (st.cg), and a cluster barrier (release /
+// acquire) separates levels. Reads of new values bypass L1 (ld.cg), so no SM
+// sees a stale line. Latency hiding: a thread's row for level L+1 (indices,
+// rhs, diagonal and up to kLvChunk entries) is loaded into registers before
+// the barrier that ends level L, and all its dependency values are then
+// requested at once, so a level costs about one L2 round trip plus the
+// barrier instead of a chain of dependent loads.
+constexpr int kLvThreads = 512;
+constexpr int kLvChunk = 8;
+constexpr int kLvMaxLevels = 8192;
+
+template <bool kFull, bool kCluster>
+__global__ void __launch_bounds__(kLvThreads)
+    k_gs_lv(int nlev, const int* __restrict__ lptr, const int* __restrict__ order,
+            const int* __restrict__ sptr, const int* __restrict__ scol, const double* __restrict__ sval,
+            const double* __restrict__ sd, const double* __restrict__ b, const double* __restrict__ xold,
+            double* xnew, double* zadd) {
+  namespace cg = cooperative_groups;
+  __shared__ int slp[kLvMaxLevels + 1];
+  int nthr = blockDim.x, tid = threadIdx.x;
+  if (kCluster) {
+    cg::cluster_group cl = cg::this_cluster();
+    nthr = static_cast<int>(cl.num_blocks()) * blockDim.x;
+    tid = static_cast<int>(cl.block_rank()) * blockDim.x + threadIdx.x;
+  }
+  const bool lp_smem = nlev <= kLvMaxLevels;
+  if (lp_smem)
+    for (int q = threadIdx.x; q <= nlev; q += blockDim.x) slp[q] = lptr[q];
+  __syncthreads();
+#define LP(q) (lp_smem ? slp[(q)] : lptr[(q)])
+  // register-resident prefetched row
+  int ri = 0, rk0 = 0, rk1 = 0, rp = 0;
+  double rb = 0.0, rd = 1.0;
+  int rc[kLvChunk];
+  double ra[kLvChunk];
+  bool have = false;
+#define LV_FETCH(P)                                                    \
+  {                                                                    \
+    rp = (P);                                                          \
+    ri = order[rp];                                                    \
+    rk0 = sptr[rp];                                                    \
+    rk1 = sptr[rp + 1];                                                \
+    rb = b[ri];                                                        \
+    rd = sd[rp];                                                       \
+    const int m_ = rk1 - rk0;                                          \
+    _Pragma("unroll") for (int q = 0; q < kLvChunk; ++q) if (q < m_) { \
+      rc[q] = scol[rk0 + q];                                           \
+      ra[q] = sval[rk0 + q];                                           \
+    }                                                                  \
+  }
+#define LV_XLOAD(C, OUT)                   \
+  {                                        \
+    int c_ = (C);                          \
+    if (kFull && !(c_ & kDepBit)) {        \
+      OUT = xold[c_];                      \
+    } else {                               \
+      if (kFull) c_ &= ~kDepBit;           \
+      OUT = __ldcg(xnew + c_);             \
+    }                                      \
+  }
+#define LV_ROW()                                                                  \
+  {                                                                               \
+    double s_ = rb;                                                               \
+    const int m_ = rk1 - rk0;                                                     \
+    double xv_[kLvChunk];                                                         \
+    _Pragma("unroll") for (int q = 0; q < kLvChunk; ++q) if (q < m_)              \
+        LV_XLOAD(rc[q], xv_[q]);                                                  \
+    _Pragma("unroll") for (int q = 0; q < kLvChunk; ++q) if (q < m_)              \
+        s_ = __dsub_rn(s_, __dmul_rn(ra[q], xv_[q]));                             \
+    for (int k0 = rk0 + kLvChunk; k0 < rk1; k0 += kLvChunk) {                     \
+      const int mm_ = min(kLvChunk, rk1 - k0);                                    \
+      _Pragma("unroll") for (int q = 0; q < kLvChunk; ++q) if (q < mm_) {         \
+        rc[q] = scol[k0 + q];                                                     \
+        ra[q] = sval[k0 + q];                                                     \
+      }                                                                           \
+      _Pragma("unroll") for (int q = 0; q < kLvChunk; ++q) if (q < mm_)           \
+          LV_XLOAD(rc[q], xv_[q]);                                                \
+      _Pragma("unroll") for (int q = 0; q < kLvChunk; ++q) if (q < mm_)           \
+          s_ = __dsub_rn(s_, __dmul_rn(ra[q], xv_[q]));                           \
+    }                                                                             \
+    const double v_ = __dadd_rn(kFull ? xold[ri] : 0.0, __ddiv_rn(s_, rd));       \
+    __stcg(xnew + ri, v_);                                                        \
+    if (zadd) zadd[ri] = __dadd_rn(zadd[ri], v_);                                 \
+  }
+  {
+    const int p = LP(0) + tid;
+    if (p < LP(1)) {
+      LV_FETCH(p);
+      have = true;
     }
   }
+  for (int L = 0; L < nlev; ++L) {
+    const int e = LP(L + 1);
+    if (have) LV_ROW();
+    for (int p = LP(L) + tid + nthr; p < e; p += nthr) {
+      LV_FETCH(p);
+      LV_ROW();
+    }
+    have = false;
+    if (L + 1 < nlev) {
+      const int p = e + tid;
+      if (p < LP(L + 2)) {
+        LV_FETCH(p);
+        have = true;
+      }
+    }
+    if (kCluster) {
+      cg::this_cluster().sync();
+    } else {
+      __syncthreads();
+    }
+  }
+#undef LP
+#undef LV_FETCH
+#undef LV_XLOAD
+#undef LV_ROW
 }
 
 // Dependency levels by monotone in-place relaxation: lev[i] = 1 + max over
@@ -137,6 +341,36 @@ __global__ void k_iota(int n, int* a) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = i;
 }
+// Sweep CSR construction (positions p in sweep order).
+__global__ void k_sweep_count(int n, const int* __restrict__ order, const int* __restrict__ ptr,
+                              const int* __restrict__ col, int fwd, int full, int* __restrict__ cnt) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int i = order[p];
+  int c = 0;
+  for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
+    const int j = col[k];
+    c += (full || (fwd ? j < i : j > i)) ? 1 : 0;
+  }
+  cnt[p] = c;
+}
+__global__ void k_sweep_fill(int n, const int* __restrict__ order, const int* __restrict__ ptr,
+                             const int* __restrict__ col, const double* __restrict__ val, int fwd,
+                             int full, const int* __restrict__ sptr, int* __restrict__ scol,
+                             double* __restrict__ sval) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int i = order[p];
+  int o = sptr[p];
+  for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
+    const int j = col[k];
+    const bool dep = fwd ? j < i : j > i;
+    if (!full && !dep) continue;
+    scol[o] = (full && dep) ? (j | kDepBit) : j;
+    sval[o] = val[k];
+    ++o;
+  }
+}
 __global__ void k_jacobi0(int n, double w, const double* __restrict__ dinv,
                           const double* __restrict__ r, const int* __restrict__ rrow,
                           double* __restrict__ z) {
@@ -154,18 +388,38 @@ __global__ void k_gather(int n, const int* __restrict__ idx, const double* __res
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) y[i] = x[idx[i]];
 }
-
 __global__ void k_recip(int n, const double* __restrict__ d, double* __restrict__ y) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) y[i] = __ddiv_rn(1.0, d[i]);
 }
 
+void build_sweep_csr(const DCsr& A, const GsSchedule& sch, bool forward, bool full, DVec<int>& sptr,
+                     DVec<int>& scol, DVec<double>& sval, cudaStream_t s) {
+  const int n = A.rows;
+  DVec<int> cnt(n, s);
+  sptr.alloc(n + 1, s);
+  const int nb = blocks_for(n, 256);
+  k_sweep_count<<<nb, 256, 0, s>>>(n, sch.order.get(), A.ptr.get(), A.col.get(), forward ? 1 : 0,
+                                   full ? 1 : 0, cnt.get());
+  MGRX_LAUNCH_CK();
+  count_launch();
+  const int nnz = static_cast<int>(exclusive_scan(cnt.get(), sptr.get(), n, s));
+  scol.alloc(nnz > 0 ? nnz : 1, s);
+  sval.alloc(nnz > 0 ? nnz : 1, s);
+  k_sweep_fill<<<nb, 256, 0, s>>>(n, sch.order.get(), A.ptr.get(), A.col.get(), A.val.get(),
+                                  forward ? 1 : 0, full ? 1 : 0, sptr.get(), scol.get(), sval.get());
+  MGRX_LAUNCH_CK();
+  count_launch();
+}
+
 }  // namespace
 
-void gs_schedule(const DCsr& A, bool forward, GsSchedule& out, cudaStream_t s) {
+void gs_schedule(const DCsr& A, bool forward, const double* d, bool full, GsSchedule& out,
+                 cudaStream_t s) {
   const int n = A.rows;
   out.order.alloc(n > 0 ? n : 1, s);
   out.levels = 0;
+  out.level_ptr.assign(1, 0);
   if (n == 0) return;
   DVec<int> lev(n, s), flag(1, s);
   lev.zero();
@@ -189,25 +443,130 @@ void gs_schedule(const DCsr& A, bool forward, GsSchedule& out, cudaStream_t s) {
   MGRX_CK(cub::DeviceRadixSort::SortPairs(t.get(), tmp, lev.get(), lev_sorted.get(), idx.get(),
                                           out.order.get(), n, 0, 31, s));
   count_launch(4);
-  out.levels = read_scalar(lev_sorted.get() + (n - 1), s) + 1;
+  const std::vector<int> ls = lev_sorted.download(n);
+  out.levels = ls.back() + 1;
+  out.level_ptr.assign(out.levels + 1, 0);
+  for (int p = 0; p < n; ++p) ++out.level_ptr[ls[p] + 1];
+  for (int l = 0; l < out.levels; ++l) out.level_ptr[l + 1] += out.level_ptr[l];
+
+  build_sweep_csr(A, out, forward, false, out.dptr, out.dcol, out.dval, s);
+  out.has_full = full;
+  if (full) build_sweep_csr(A, out, forward, true, out.fptr, out.fcol, out.fval, s);
+  out.sd.alloc(n, s);
+  gather(n, out.order.get(), d, out.sd.get(), s);
+  int dep_nnz = 0;
+  MGRX_CK(cudaMemcpyAsync(&dep_nnz, out.dptr.get() + n, sizeof(int), cudaMemcpyDeviceToHost, s));
+  MGRX_CK(cudaStreamSynchronize(s));
+  const double avg = full ? (2.0 * dep_nnz) / n : static_cast<double>(dep_nnz) / n;
+  out.team = avg <= 6.0 ? 1 : (avg <= 24.0 ? 4 : 8);
+  out.dlptr.alloc(out.levels + 1, s);
+  out.dlptr.upload(out.level_ptr.data(), out.levels + 1);
+  // Sweep mode: MGRX_GS_MODE=lv selects the level-synchronous cluster
+  // kernel; default is the sync-free kernel. Cluster size from the
+  // average level width (about 1 row per thread).
+  static const int mode = [] {
+    const char* e = std::getenv("MGRX_GS_MODE");
+    return (e && e[0] == 'l') ? 1 : 0;
+  }();
+  if (mode == 1) {
+    const double width = static_cast<double>(n) / out.levels;
+    out.cluster = std::max(1, std::min(16, static_cast<int>(std::ceil(width / kLvThreads))));
+  } else {
+    out.cluster = 0;
+  }
 }
 
 void gs_sweep(const DCsr& A, const GsSchedule& sch, const double* d, const double* b,
               const double* xold, double* xnew, double* zadd, bool forward, GsScratch& scr,
               cudaStream_t s) {
+  (void)d;
+  (void)forward;
   const int n = A.rows;
   if (n == 0) return;
   if (scr.ticket_err.size() < 2) throw RuntimeError("gs_sweep: scratch not bound");
+  const bool full_sweep = xold != nullptr;
+  if (full_sweep && !sch.has_full) throw RuntimeError("gs_sweep: schedule built without the full sweep CSR");
+  if (sch.cluster > 0) {
+    // level-synchronous cluster sweep
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(sch.cluster);
+    cfg.blockDim = dim3(kLvThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = sch.cluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const int* sp = full_sweep ? sch.fptr.get() : sch.dptr.get();
+    const int* sc = full_sweep ? sch.fcol.get() : sch.dcol.get();
+    const double* sv = full_sweep ? sch.fval.get() : sch.dval.get();
+    const bool clus = sch.cluster > 1;
+    if (!clus) cfg.numAttrs = 0;
+    if (full_sweep && clus)
+      MGRX_CK(cudaLaunchKernelEx(&cfg, k_gs_lv<true, true>, sch.levels, sch.dlptr.get(), sch.order.get(), sp,
+                                 sc, sv, sch.sd.get(), b, xold, xnew, zadd));
+    else if (full_sweep)
+      MGRX_CK(cudaLaunchKernelEx(&cfg, k_gs_lv<true, false>, sch.levels, sch.dlptr.get(), sch.order.get(), sp,
+                                 sc, sv, sch.sd.get(), b, xold, xnew, zadd));
+    else if (clus)
+      MGRX_CK(cudaLaunchKernelEx(&cfg, k_gs_lv<false, true>, sch.levels, sch.dlptr.get(), sch.order.get(), sp,
+                                 sc, sv, sch.sd.get(), b, xold, xnew, zadd));
+    else
+      MGRX_CK(cudaLaunchKernelEx(&cfg, k_gs_lv<false, false>, sch.levels, sch.dlptr.get(), sch.order.get(), sp,
+                                 sc, sv, sch.sd.get(), b, xold, xnew, zadd));
+    count_launch();
+    return;
+  }
   MGRX_CK(cudaMemsetAsync(scr.ticket_err.get(), 0, sizeof(int), s));
   MGRX_CK(cudaMemsetAsync(xnew, 0xff, sizeof(double) * n, s));
-  k_gs<<<blocks_for(n, kGsThreads), kGsThreads, 0, s>>>(n, sch.order.get(), A.ptr.get(), A.col.get(),
-                                                       A.val.get(), d, b, xold, xnew, zadd,
-                                                       forward ? 1 : 0, scr.ticket_err.get());
+  // Team size from the average dependency count; grid: enough CTAs to keep
+  // ~kFlight dependency levels of rows in flight.
+  static const int kFlight = [] {
+    const char* e = std::getenv("MGRX_GS_FLIGHT");
+    return e ? std::max(1, std::atoi(e)) : 6;
+  }();
+  const bool full = full_sweep;
+  const int T = sch.team;
+  const double per_level = static_cast<double>(n) / std::max(sch.levels, 1);
+  const int rows_per_cta = kGsThreads / T;
+  const int grid = std::max(1, std::min(blocks_for(n, rows_per_cta),
+                                        static_cast<int>(kFlight * per_level / rows_per_cta) + 1));
+  const int* sp = full ? sch.fptr.get() : sch.dptr.get();
+  const int* sc = full ? sch.fcol.get() : sch.dcol.get();
+  const double* sv = full ? sch.fval.get() : sch.dval.get();
+  int* tk = scr.ticket_err.get();
+#define MGRX_GS_LAUNCH(TT, FF)                                                                    \
+  k_gs<TT, FF><<<grid, kGsThreads, kGsSmem, s>>>(n, sch.order.get(), sp, sc, sv, sch.sd.get(), b, \
+                                                 xold, xnew, zadd, tk)
+  if (T == 1) {
+    if (full) MGRX_GS_LAUNCH(1, true); else MGRX_GS_LAUNCH(1, false);
+  } else if (T == 4) {
+    if (full) MGRX_GS_LAUNCH(4, true); else MGRX_GS_LAUNCH(4, false);
+  } else {
+    if (full) MGRX_GS_LAUNCH(8, true); else MGRX_GS_LAUNCH(8, false);
+  }
+#undef MGRX_GS_LAUNCH
   MGRX_LAUNCH_CK();
   count_launch();
 }
 
 void gs_bind_scratch(GsScratch& scr, cudaStream_t s) {
+  static const bool attrs = [] {
+    MGRX_CK(cudaFuncSetAttribute(k_gs_lv<false, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    MGRX_CK(cudaFuncSetAttribute(k_gs_lv<true, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    const int sm = static_cast<int>(kGsSmem);
+    MGRX_CK(cudaFuncSetAttribute(k_gs<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    MGRX_CK(cudaFuncSetAttribute(k_gs<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    MGRX_CK(cudaFuncSetAttribute(k_gs<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    MGRX_CK(cudaFuncSetAttribute(k_gs<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    MGRX_CK(cudaFuncSetAttribute(k_gs<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    MGRX_CK(cudaFuncSetAttribute(k_gs<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    return true;
+  }();
+  (void)attrs;
   if (scr.ticket_err.size() < 2) {
     scr.ticket_err.alloc(2, s);
     scr.ticket_err.zero();
@@ -242,13 +601,11 @@ void gather(int n, const int* idx, const double* x, double* y, cudaStream_t s) {
   count_launch();
 }
 
-}  // namespace mgrx
-
-namespace mgrx {
 void reciprocal(int n, const double* d, double* y, cudaStream_t s) {
   if (n == 0) return;
   k_recip<<<blocks_for(n, 256), 256, 0, s>>>(n, d, y);
   MGRX_LAUNCH_CK();
   count_launch();
 }
+
 }  // namespace mgrx

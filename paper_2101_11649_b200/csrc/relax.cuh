@@ -9,11 +9,31 @@ namespace mgrx {
 // Rows in dependency-level order for one sweep direction: every row's
 // dependencies (columns j < i forward, j > i backward) sit at earlier
 // positions, which is what makes the sync-free sweep deadlock-free.
+//
+// The schedule also stores the sweep in "sweep CSR" form: rows permuted to
+// sweep order, so a CTA's rows are one contiguous block of entries that it
+// stages in shared memory with coalesced loads.
+//   dep  : only the dependency entries (columns visited earlier in the
+//          sweep). A sweep from zero needs nothing else: every other term is
+//          a_ij * 0, which leaves the partial sum (and so x_i) unchanged.
+//   full : every stored entry, dependency entries flagged by bit 31 of the
+//          column (multi-sweep smoothers, whose old iterate is nonzero).
 struct GsSchedule {
-  DVec<int> order;
+  DVec<int> order;                 // sweep position -> row
+  std::vector<int> level_ptr;      // host: positions of each dependency level
   int levels = 0;
+  DVec<int> dptr, dcol;            // dep-only sweep CSR
+  DVec<double> dval;
+  DVec<int> fptr, fcol;            // full sweep CSR (only when sweeps > 1)
+  DVec<double> fval;
+  DVec<double> sd;                 // d in sweep order
+  bool has_full = false;
+  int team = 1;                    // lanes per row in the sync-free kernel
+  int cluster = 0;                 // >0: level-synchronous sweep in one cluster of this size
+  DVec<int> dlptr;                 // device copy of level_ptr
 };
-void gs_schedule(const DCsr& A, bool forward, GsSchedule& out, cudaStream_t s);
+void gs_schedule(const DCsr& A, bool forward, const double* d, bool full, GsSchedule& out,
+                 cudaStream_t s);
 
 // Scratch for a GS sweep (ticket counter + error flag).
 struct GsScratch {

@@ -2,6 +2,7 @@
 // kernels (extract, transpose, conservative SpGEMM, diagonal helpers).
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <cstdio>
 
 #include "sparse.cuh"
@@ -241,6 +242,36 @@ __global__ void __launch_bounds__(kRows) k_spmv(int rows, const int* __restrict_
   if (r < rows) epi(r, sum);
 }
 
+// Warp-per-row variant for small or long-row matrices (coarse AMG levels):
+// lanes form 32 products at a time, lane 0 folds them left to right, so the
+// arithmetic is the same sequential row sum; rows are independent warps,
+// which keeps enough loads in flight when the matrix has few rows.
+constexpr int kWarps = 8;
+
+template <class Epi>
+__global__ void __launch_bounds__(kWarps * 32) k_spmv_wpr(int rows, const int* __restrict__ ptr,
+                                                          const int* __restrict__ col,
+                                                          const double* __restrict__ val,
+                                                          const double* __restrict__ x, Epi epi) {
+  __shared__ double prod[kWarps][32];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  for (int r = blockIdx.x * kWarps + w; r < rows; r += gridDim.x * kWarps) {
+    const int lo = __ldg(ptr + r), hi = __ldg(ptr + r + 1);
+    double sum = 0.0;
+    for (int c0 = lo; c0 < hi; c0 += 32) {
+      const int q = c0 + l;
+      prod[w][l] = q < hi ? __dmul_rn(__ldg(val + q), __ldg(x + __ldg(col + q))) : 0.0;
+      __syncwarp();
+      if (l == 0) {
+        const int m = min(32, hi - c0);
+        for (int t = 0; t < m; ++t) sum = __dadd_rn(sum, prod[w][t]);
+      }
+      __syncwarp();
+    }
+    if (l == 0) epi(r, sum);
+  }
+}
+
 struct EpiStore {
   double* y;
   __device__ void operator()(int r, double s) const { y[r] = __dadd_rn(0.0, s); }
@@ -285,6 +316,14 @@ struct EpiJacobi {
 template <class Epi>
 void launch_spmv(const DCsr& A, const double* x, Epi epi, cudaStream_t s) {
   if (A.rows == 0) return;
+  const bool small = A.rows <= 65536 || A.nnz > 24LL * A.rows;
+  if (small) {
+    const int grid = std::min(blocks_for(A.rows, kWarps), 148 * 8);
+    k_spmv_wpr<<<grid, kWarps * 32, 0, s>>>(A.rows, A.ptr.get(), A.col.get(), A.val.get(), x, epi);
+    MGRX_LAUNCH_CK();
+    count_launch();
+    return;
+  }
   k_spmv<<<blocks_for(A.rows, kRows), kRows, 0, s>>>(A.rows, A.ptr.get(), A.col.get(), A.val.get(),
                                                       x, epi);
   MGRX_LAUNCH_CK();
