@@ -193,7 +193,10 @@ def main():
     torch.cuda.synchronize()
     its, launches, solve_dev = 0, 0, 0.0
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    prof = bool(os.environ.get("MGRX_PROFILE_TIMED"))
     with Clocks(local) as clk:
+        if prof:
+            torch.cuda.profiler.start()
         start.record()
         for _ in range(args.steps):
             rep = step()
@@ -202,6 +205,8 @@ def main():
             solve_dev += rep.solve_s
         end.record()
         torch.cuda.synchronize()
+        if prof:
+            torch.cuda.profiler.stop()
     if world > 1:
         dist.barrier()
     ms = start.elapsed_time(end)
