@@ -26,9 +26,24 @@ sys.path.insert(0, ROOT)
 
 METRIC = "MGR-FGMRES DOF*iters/sec"
 UNIT = "DOF*iters/s"
-CFG = {"nx": 128, "ny": 128, "nz": 64, "field": "layered", "sigma": 1.5, "seed": 20210129}
-STRATEGY = "mfd_mgr_pi_c1"
-RTOL = 1e-6
+# Workloads (BASELINE.json configs). cfg2 is the headline (the metric's
+# config, single GPU); the others are available for measurements and parity.
+CONFIGS = {
+    "cfg1": {"kind": "mfd", "dims": (20, 20, 10), "field": "iid", "seed": 20210128,
+             "strategy": "mfd_mgr_pi_c1", "rtol": 1e-6,
+             "desc": "cfg1: hybrid-MFD [p,pi] 20x20x10 iid log-normal, FGMRES(30) rtol 1e-6, MGR_pi + 1 AMG V-cycle"},
+    "cfg2": {"kind": "mfd", "dims": (128, 128, 64), "field": "layered", "seed": 20210129,
+             "strategy": "mfd_mgr_pi_c1", "rtol": 1e-6,
+             "desc": "cfg2: hybrid-MFD [p,pi] 128x128x64 layered log-normal (1e6 contrast), "
+                     "FGMRES(30) rtol 1e-6, MGR_pi + 1 AMG V-cycle"},
+    "cfg3": {"kind": "comp", "dims": (100, 100, 50), "wells": 8, "seed": 20210130,
+             "strategy": "comp_mgr", "rtol": 1e-5,
+             "desc": "cfg3: compositional p+3 densities 100x100x50 (4x4 blocks) + 8 wells x 50 elements x 5 dofs, "
+                     "FGMRES(30) rtol 1e-5, MGR rho3 -> rho1,rho2 -> p(AMG) -> wells(dense LU)"},
+}
+CONFIG = "cfg2"
+STRATEGY = CONFIGS[CONFIG]["strategy"]
+RTOL = CONFIGS[CONFIG]["rtol"]
 RESTART = 30
 
 
@@ -94,7 +109,10 @@ def peaks():
 
 def make_problem():
     import paper_2101_11649_b200 as mx
-    return mx.mfd_problem(CFG["nx"], CFG["ny"], CFG["nz"], CFG["field"], sigma=CFG["sigma"], seed=CFG["seed"])
+    c = CONFIGS[CONFIG]
+    if c["kind"] == "mfd":
+        return mx.mfd_problem(*c["dims"], c["field"], sigma=1.5, seed=c["seed"])
+    return mx.comp_problem(*c["dims"], wells=c["wells"], seed=c["seed"])
 
 
 def cpu_reference(P, steps, warmup, max_iters, threads):
@@ -136,16 +154,16 @@ def run_reference(args):
 
 
 def workload_config(P, n_gpus):
-    return {"workload": "cfg2: hybrid-MFD [p,pi] 128x128x64 layered log-normal (1e6 contrast), "
-                        "FGMRES(30) rtol 1e-6, MGR_pi + 1 AMG V-cycle",
+    return {"workload": CONFIGS[CONFIG]["desc"],
             "dofs": int(P.n), "nnz": int(P.ptr[-1]), "strategy": STRATEGY, "restart": RESTART,
             "rel_tol": RTOL, "parallelism": f"replicas{n_gpus}" if n_gpus > 1 else "single",
             "l2_flush": "inputs exceed L2 (matrix+hierarchy > 126 MB)"}
 
 
 def main():
-    global STRATEGY
+    global STRATEGY, CONFIG, RTOL
     ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
@@ -154,6 +172,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--strategy", default=None, help="strategies/<name>.json (default: %s)" % STRATEGY)
     args = ap.parse_args()
+    CONFIG = args.config
+    STRATEGY = CONFIGS[CONFIG]["strategy"]
+    RTOL = CONFIGS[CONFIG]["rtol"]
     if args.strategy:
         STRATEGY = args.strategy
     if args.impl == "reference":

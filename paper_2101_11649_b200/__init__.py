@@ -357,6 +357,8 @@ def _genlib() -> C.CDLL:
         G = C.CDLL(_GEN_PATH)
         G.mgrx_gen_mfd.restype = C.c_void_p
         G.mgrx_gen_mfd.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint, C.c_double]
+        G.mgrx_gen_comp.restype = C.c_void_p
+        G.mgrx_gen_comp.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint]
         for f in ("mgrx_gen_n", "mgrx_gen_nfields", "mgrx_gen_has_unknown_map"):
             getattr(G, f).argtypes = [C.c_void_p]
         G.mgrx_gen_nnz.argtypes = [C.c_void_p]
@@ -415,6 +417,13 @@ def mfd_problem(nx: int, ny: int, nz: int, field: str = "iid", sigma: float = 1.
     cfg2: 128x128x64 layered)."""
     kind = {"iid": 0, "layered": 1}[field]
     return _take(_genlib().mgrx_gen_mfd(nx, ny, nz, kind, sigma, seed, accumulation))
+
+
+def comp_problem(nx: int, ny: int, nz: int, wells: int = 8, sigma_t: float = 2.0,
+                 seed: int = 20210130) -> Problem:
+    """Compositional [p, rho1, rho2, rho3] + wells (BASELINE cfg3: 100x100x50,
+    8 wells; cfg5: weak-scaled)."""
+    return _take(_genlib().mgrx_gen_comp(nx, ny, nz, wells, sigma_t, seed))
 
 
 STRATEGY_DIR = os.path.join(os.path.dirname(_HERE), "strategies")

@@ -207,9 +207,206 @@ Problem make_mfd(int nx, int ny, int nz, int field, double sigma, unsigned seed,
   return P;
 }
 
+// ---------------------------------------------------------------------------
+// cfg3/cfg5 — compositional multiphase Jacobian with wells, restating the
+// structure of proj/src/problems/comp.cpp:59-233 with the BASELINE knobs
+// (SURVEY D5, D6, D9): 4 unknowns per cell (p, rho1, rho2, rho3) stored
+// cell-interleaved (the 4x4 block layout), a 7-point pressure M-matrix with
+// ln T ~ N(0, sigma_T^2) per face, density blocks that are mass-diagonal
+// plus first-order upwind advection (per-face ratio U(0.1, 0.9) of the mass
+// diagonal split over the 6 faces, so rows stay diagonally dominant), cross-
+// field couplings on the own cell only, and rho3 as the strictly
+// cell-diagonal volume constraint. Vertical wells: one element per layer,
+// 5 dofs per element (p, rho1, rho2, rho3, rate), chained along the well,
+// coupled to the perforated cells, with a rate-control row (stored zero
+// diagonal) on the top element like the reference's control rows.
+// Numbering is slab-major: each z-layer's cells, then (after all layers)
+// the well block; the well field is never eliminated before the coarse grid.
+Problem make_comp(int nx, int ny, int nz, int wells, double sigma_t, unsigned seed) {
+  if (nx < 2 || ny < 2 || nz < 2) throw std::invalid_argument("comp: grid dims must be at least 2 each");
+  if (wells < 0) throw std::invalid_argument("comp: negative well count");
+  const int64_t N = int64_t(nx) * ny * nz;
+  const int64_t Wd = int64_t(wells) * nz * 5;
+  if (4 * N + Wd > INT32_MAX / 2) throw std::invalid_argument("comp: grid too large for int32 indices");
+  const double acc = 1e-2, mass = 1.0, coupling = 0.1, gamma = 0.5;
+  auto cid = [&](int i, int j, int k) { return int64_t(i) + int64_t(nx) * (j + int64_t(ny) * k); };
+  auto dof = [&](int64_t c, int f) { return 4 * c + f; };
+  const int64_t ow = 4 * N;
+  auto wdof = [&](int w, int e, int f) { return ow + (int64_t(w) * nz + e) * 5 + f; };
+
+  // face transmissibilities (x, y, z faces to the +neighbour) and upwind data
+  Normal nrm(seed);
+  Uniform uni(seed ^ 0x27d4eb2du);
+  std::vector<double> Tf(3 * N, 0.0), rf(3 * N, 0.0);
+  std::vector<signed char> upw(3 * N, 0);  // +1: cell c is upwind of its +neighbour
+  for (int k = 0; k < nz; ++k)
+    for (int j = 0; j < ny; ++j)
+      for (int i = 0; i < nx; ++i) {
+        const int64_t c = cid(i, j, k);
+        for (int d = 0; d < 3; ++d) {
+          const bool has = (d == 0 && i + 1 < nx) || (d == 1 && j + 1 < ny) || (d == 2 && k + 1 < nz);
+          if (!has) continue;
+          Tf[3 * c + d] = std::exp(sigma_t * nrm());
+          rf[3 * c + d] = uni(0.1, 0.9);
+          // smooth analytic head h = cos(0.3 i) + sin(0.2 j) + 0.1 k drives the upwinding
+          const double h0 = std::cos(0.3 * i) + std::sin(0.2 * j) + 0.1 * k;
+          const double h1 = std::cos(0.3 * (i + (d == 0))) + std::sin(0.2 * (j + (d == 1))) + 0.1 * (k + (d == 2));
+          upw[3 * c + d] = h0 >= h1 ? 1 : -1;
+        }
+      }
+  auto nbr = [&](int i, int j, int k, int d, int sgn) -> int64_t {
+    const int ii = i + (d == 0) * sgn, jj = j + (d == 1) * sgn, kk = k + (d == 2) * sgn;
+    if (ii < 0 || jj < 0 || kk < 0 || ii >= nx || jj >= ny || kk >= nz) return -1;
+    return cid(ii, jj, kk);
+  };
+  // well columns on the areal diagonal (proj/src/problems/comp.cpp:49-56)
+  std::vector<std::pair<int, int>> wcol(wells);
+  for (int w = 0; w < wells; ++w) {
+    const int ix = std::min(int((w + 1) * int64_t(nx) / (wells + 1)), nx - 1);
+    const int iy = std::min(int((w + 1) * int64_t(ny) / (wells + 1)), ny - 1);
+    wcol[w] = {ix, iy};
+  }
+  auto perf_well = [&](int i, int j) {
+    for (int w = 0; w < wells; ++w)
+      if (wcol[w].first == i && wcol[w].second == j) return w;
+    return -1;
+  };
+
+  Problem P;
+  P.n = static_cast<int>(4 * N + Wd);
+  P.fields = {"p", "rho1", "rho2", "rho3", "well"};
+  if (wells == 0) P.fields.pop_back();
+  P.ptr.reserve(P.n + 1);
+  P.ptr.push_back(0);
+  P.labels.reserve(P.n);
+  RowBuilder rb;
+  const double gp = gamma, g1 = 0.1 * gamma;
+  for (int k = 0; k < nz; ++k)
+    for (int j = 0; j < ny; ++j)
+      for (int i = 0; i < nx; ++i) {
+        const int64_t c = cid(i, j, k);
+        const int pw = k >= 1 ? perf_well(i, j) : -1;  // layer 0 faces the control element
+        // --- pressure row
+        {
+          double d = acc;
+          for (int dd = 0; dd < 3; ++dd)
+            for (int sgn : {-1, 1}) {
+              const int64_t m = nbr(i, j, k, dd, sgn);
+              if (m < 0) continue;
+              const double T = sgn > 0 ? Tf[3 * c + dd] : Tf[3 * m + dd];
+              d += T;
+              rb.add(static_cast<int>(dof(m, 0)), -T);
+            }
+          rb.add(static_cast<int>(dof(c, 1)), coupling * acc);
+          rb.add(static_cast<int>(dof(c, 2)), 0.5 * coupling * acc);
+          rb.add(static_cast<int>(dof(c, 3)), 0.25 * coupling * acc);
+          if (pw >= 0) {
+            d += gp;
+            rb.add(static_cast<int>(wdof(pw, k, 0)), -gp);
+          }
+          rb.add(static_cast<int>(dof(c, 0)), d);
+          finish_row(P, rb);
+          P.labels.push_back(0);
+        }
+        // --- density rows rho1, rho2 (upwind advection within the field)
+        for (int f = 1; f <= 2; ++f) {
+          double d = mass;
+          for (int dd = 0; dd < 3; ++dd)
+            for (int sgn : {-1, 1}) {
+              const int64_t m = nbr(i, j, k, dd, sgn);
+              if (m < 0) continue;
+              const int64_t fc = sgn > 0 ? c : m;  // face owner (minus side)
+              const double a = rf[3 * fc + dd] * mass / 6.0;
+              const bool c_upwind = (sgn > 0) ? (upw[3 * fc + dd] > 0) : (upw[3 * fc + dd] < 0);
+              if (c_upwind) d += a;                                   // outflow on the diagonal
+              else rb.add(static_cast<int>(dof(m, f)), -a);          // inflow from the upwind cell
+            }
+          rb.add(static_cast<int>(dof(c, 0)), (f == 1 ? -1.0 : -0.5) * coupling * mass);
+          if (f == 1) rb.add(static_cast<int>(dof(c, 2)), 0.5 * coupling * mass);
+          else rb.add(static_cast<int>(dof(c, 1)), 0.25 * coupling * mass);
+          if (pw >= 0) {
+            d += (f == 1 ? g1 : 0.5 * g1);
+            rb.add(static_cast<int>(wdof(pw, k, f)), -(f == 1 ? g1 : 0.5 * g1));
+          }
+          rb.add(static_cast<int>(dof(c, f)), d);
+          finish_row(P, rb);
+          P.labels.push_back(f);
+        }
+        // --- volume constraint rho3: strictly cell-diagonal
+        rb.add(static_cast<int>(dof(c, 0)), 0.2);
+        rb.add(static_cast<int>(dof(c, 1)), 0.3);
+        rb.add(static_cast<int>(dof(c, 2)), 0.3);
+        rb.add(static_cast<int>(dof(c, 3)), 1.0);
+        finish_row(P, rb);
+        P.labels.push_back(3);
+      }
+  // --- wells: chained elements, rate control on the top element
+  for (int w = 0; w < wells; ++w) {
+    const auto [ix, iy] = wcol[w];
+    for (int e = 0; e < nz; ++e) {
+      const int64_t c = cid(ix, iy, e);
+      // pressure
+      if (e == 0) {
+        rb.add(static_cast<int>(wdof(w, 0, 0)), 0.0);  // stored zero diagonal (control row)
+        rb.add(static_cast<int>(wdof(w, 0, 4)), 1.0);
+        if (nz > 1) rb.add(static_cast<int>(wdof(w, 1, 4)), 0.25);
+      } else {
+        rb.add(static_cast<int>(wdof(w, e, 0)), 4.0 + gp);
+        rb.add(static_cast<int>(wdof(w, e - 1, 0)), -1.0);
+        if (e + 1 < nz) rb.add(static_cast<int>(wdof(w, e + 1, 0)), -1.0);
+        rb.add(static_cast<int>(wdof(w, e, 4)), 1.0);
+        rb.add(static_cast<int>(wdof(w, e - 1, 4)), -1.0);
+        rb.add(static_cast<int>(dof(c, 0)), -gp);
+      }
+      finish_row(P, rb);
+      P.labels.push_back(4);
+      // densities
+      for (int f = 1; f <= 3; ++f) {
+        const double g = f == 1 ? g1 : (f == 2 ? 0.5 * g1 : 0.0);
+        rb.add(static_cast<int>(wdof(w, e, f)), 3.0 + g);
+        if (e > 0) rb.add(static_cast<int>(wdof(w, e - 1, f)), -0.75);
+        if (e + 1 < nz) rb.add(static_cast<int>(wdof(w, e + 1, f)), -0.75);
+        rb.add(static_cast<int>(wdof(w, e, 0)), 0.3);
+        if (g > 0.0 && e > 0) rb.add(static_cast<int>(dof(c, f)), -g);
+        finish_row(P, rb);
+        P.labels.push_back(4);
+      }
+      // rate
+      rb.add(static_cast<int>(wdof(w, e, 4)), 2.0);
+      if (e > 0) rb.add(static_cast<int>(wdof(w, e - 1, 4)), -0.4);
+      if (e + 1 < nz) rb.add(static_cast<int>(wdof(w, e + 1, 4)), -0.4);
+      rb.add(static_cast<int>(wdof(w, e, 0)), 1.0);
+      if (e + 1 < nz) rb.add(static_cast<int>(wdof(w, e + 1, 0)), -1.0);
+      finish_row(P, rb);
+      P.labels.push_back(4);
+    }
+  }
+  if (static_cast<int64_t>(P.ptr.size()) != P.n + 1) throw std::logic_error("comp: row count mismatch");
+  Uniform rhs(seed + 0x9e3779b9u);
+  P.rhs.resize(P.n);
+  for (int i = 0; i < P.n; ++i) P.rhs[i] = rhs(-1.0, 1.0);
+  char buf[512];
+  std::snprintf(buf, sizeof buf,
+                "{\"problem\":\"comp\",\"dims\":[%d,%d,%d],\"wells\":%d,\"well_elements\":%d,"
+                "\"dofs_per_cell\":4,\"dofs_per_well_element\":5,\"sigma_lnT\":%.17g,\"seed\":%u,"
+                "\"layout\":\"cell-interleaved 4x4 blocks, wells last\"}",
+                nx, ny, nz, wells, nz, sigma_t, seed);
+  P.meta = buf;
+  return P;
+}
+
 }  // namespace
 
 extern "C" {
+
+void* mgrx_gen_comp(int nx, int ny, int nz, int wells, double sigma_t, unsigned seed) {
+  try {
+    return new Problem(make_comp(nx, ny, nz, wells, sigma_t, seed));
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
 
 const char* mgrx_gen_last_error() { return g_err.c_str(); }
 

@@ -100,6 +100,9 @@ def build_problem(spec):
     if kind == "mfd":
         P = mx.mfd_problem(*spec["dims"], spec.get("field", "iid"), seed=spec.get("seed", 20210128))
         return P.ptr, P.col, P.val, P.partition.field_order, P.partition.labels, None, P.rhs
+    if kind == "comp":
+        P = mx.comp_problem(*spec["dims"], wells=spec.get("wells", 2), seed=spec.get("seed", 20210130))
+        return P.ptr, P.col, P.val, P.partition.field_order, P.partition.labels, None, P.rhs
     rng = np.random.default_rng(spec.get("seed", 7))
     if kind == "laplace2d":
         ptr, col, val = rows_to_csr(laplace2d(*spec["dims"]))
@@ -145,6 +148,10 @@ CASES = [
      "rtol": 1e-8},
     {"id": "sdd200_global_relax", "problem": {"kind": "sdd2", "n": 200}, "strategy": GLOBAL_RELAX,
      "rtol": 1e-9},
+    {"id": "comp_10x10x5_w2", "problem": {"kind": "comp", "dims": [10, 10, 5], "wells": 2},
+     "strategy": "comp_mgr", "rtol": 1e-5},
+    {"id": "comp_24x20x12_w3", "problem": {"kind": "comp", "dims": [24, 20, 12], "wells": 3},
+     "strategy": "comp_mgr", "rtol": 1e-5},
     {"id": "sdd400_restrict_jacobi", "problem": {"kind": "sdd2", "n": 400}, "strategy": TWO_FIELD_RJAC,
      "rtol": 1e-9},
 ]
