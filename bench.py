@@ -40,6 +40,9 @@ CONFIGS = {
              "strategy": "comp_mgr", "rtol": 1e-5,
              "desc": "cfg3: compositional p+3 densities 100x100x50 (4x4 blocks) + 8 wells x 50 elements x 5 dofs, "
                      "FGMRES(30) rtol 1e-5, MGR rho3 -> rho1,rho2 -> p(AMG) -> wells(dense LU)"},
+    "cfg4": {"kind": "frac", "m": 64, "seed": 20210131, "strategy": "frac_mgr_u", "rtol": 1e-6,
+             "desc": "cfg4: 3-D Q1 elasticity 64^3 nodes (81 nnz/row) + mid-plane fracture lubrication, "
+                     "FGMRES(30) rtol 1e-6, MGR_u with unknown-based AMG on A_uu, AMG coarse on p"},
 }
 CONFIG = "cfg2"
 STRATEGY = CONFIGS[CONFIG]["strategy"]
@@ -112,6 +115,8 @@ def make_problem():
     c = CONFIGS[CONFIG]
     if c["kind"] == "mfd":
         return mx.mfd_problem(*c["dims"], c["field"], sigma=1.5, seed=c["seed"])
+    if c["kind"] == "frac":
+        return mx.frac_problem(c["m"], seed=c["seed"])
     return mx.comp_problem(*c["dims"], wells=c["wells"], seed=c["seed"])
 
 
@@ -123,7 +128,7 @@ def cpu_reference(P, steps, warmup, max_iters, threads):
     import paper_2101_11649_b200 as mx
     refcpu.set_threads(threads)
     H = refcpu.RefHierarchy(P.ptr, P.col, P.val, P.partition.field_order, P.partition.labels,
-                            mx.load_strategy(STRATEGY))
+                            mx.load_strategy(STRATEGY), P.unknown_map)
     for _ in range(warmup):
         H.solve(P.rhs, restart=RESTART, max_iters=max_iters, rel_tol=RTOL)
     its, t = 0, 0.0
@@ -193,7 +198,7 @@ def main():
     ctx = mx.Context(local)
     A = mx.Matrix(P.ptr, P.col, P.val, ctx=ctx)
     t0 = time.perf_counter()
-    H = mx.Hierarchy(A, P.partition, mx.load_strategy(STRATEGY))
+    H = mx.Hierarchy(A, P.partition, mx.load_strategy(STRATEGY), P.unknown_map)
     setup_wall = time.perf_counter() - t0
     cfg = mx.KrylovConfig(restart=RESTART, max_iters=500, rel_tol=RTOL)
 

@@ -359,6 +359,8 @@ def _genlib() -> C.CDLL:
         G.mgrx_gen_mfd.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint, C.c_double]
         G.mgrx_gen_comp.restype = C.c_void_p
         G.mgrx_gen_comp.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint]
+        G.mgrx_gen_frac.restype = C.c_void_p
+        G.mgrx_gen_frac.argtypes = [C.c_int, C.c_double, C.c_uint]
         for f in ("mgrx_gen_n", "mgrx_gen_nfields", "mgrx_gen_has_unknown_map"):
             getattr(G, f).argtypes = [C.c_void_p]
         G.mgrx_gen_nnz.argtypes = [C.c_void_p]
@@ -426,7 +428,13 @@ def comp_problem(nx: int, ny: int, nz: int, wells: int = 8, sigma_t: float = 2.0
     return _take(_genlib().mgrx_gen_comp(nx, ny, nz, wells, sigma_t, seed))
 
 
-STRATEGY_DIR = os.path.join(os.path.dirname(_HERE), "strategies")
+def frac_problem(nodes_per_side: int = 64, sigma_e: float = 0.5, seed: int = 20210131) -> Problem:
+    """3-D Q1 elasticity + planar-fracture lubrication, fields {u, p} with a
+    displacement-component unknown map (BASELINE cfg4: 64^3 nodes)."""
+    return _take(_genlib().mgrx_gen_frac(nodes_per_side, sigma_e, seed))
+
+
+STRATEGY_DIR =os.path.join(os.path.dirname(_HERE), "strategies")
 
 
 def load_strategy(name: str) -> str:

@@ -395,9 +395,243 @@ Problem make_comp(int nx, int ny, int nz, int wells, double sigma_t, unsigned se
   return P;
 }
 
+// ---------------------------------------------------------------------------
+// cfg4 — hydraulic fracturing: 3-D Q1 hex elasticity coupled to lubrication
+// flow on a planar fracture, the 3-D restatement of proj/src/problems/
+// frac.cpp:75-168 (2-D Q4 there). Unit cube, m^3 nodes (m per
+// side), bottom (k = 0) and top (k = m-1) node planes fixed and eliminated.
+// The fracture is the mid node plane km = m/2 over all (m-1)^2 face
+// elements: interior plane nodes are duplicated (elements above use the
+// copies), perimeter nodes are shared tips. Nondimensional units: E per
+// element log-normal with median 1 (<-> 10 GPa) and sigma_lnE 0.5, nu 0.25.
+// Fracture element e: pressure dof with storage c_s h^2, cubic-law
+// transmissibility between neighbours T = harmonic((w/w_ref)^3 / 12),
+// w ~ U(1e-4, 1e-3) m, w_ref = 1e-3. Coupling: the element pressure loads its
+// face corners equally and oppositely (-/+ h^2/4 on u_z of top copy /
+// original), the pressure row takes the transposed jump rate (rate/dt).
+// Dofs: u node-interleaved (x, y, z) in slab-major node order (each node
+// plane's originals, then for km its copies), then the fracture pressures;
+// unknown_map = displacement component (0 on p), fields {u, p}.
+void q1_stiffness(double h, double nu, double Ke[24][24]) {
+  // isotropic D for E = 1
+  const double lam = nu / ((1.0 + nu) * (1.0 - 2.0 * nu)), mu = 0.5 / (1.0 + nu);
+  double D[6][6] = {};
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) D[a][b] = lam + (a == b ? 2.0 * mu : 0.0);
+  for (int a = 3; a < 6; ++a) D[a][a] = mu;
+  const int sgn[8][3] = {{-1, -1, -1}, {1, -1, -1}, {1, 1, -1}, {-1, 1, -1},
+                         {-1, -1, 1},  {1, -1, 1},  {1, 1, 1},  {-1, 1, 1}};
+  for (int a = 0; a < 24; ++a)
+    for (int b = 0; b < 24; ++b) Ke[a][b] = 0.0;
+  const double g = 1.0 / std::sqrt(3.0);
+  const double jdet = (h / 2) * (h / 2) * (h / 2), dinv = 2.0 / h;
+  for (int qx = -1; qx <= 1; qx += 2)
+    for (int qy = -1; qy <= 1; qy += 2)
+      for (int qz = -1; qz <= 1; qz += 2) {
+        const double xi[3] = {qx * g, qy * g, qz * g};
+        double dN[8][3];
+        for (int a = 0; a < 8; ++a)
+          for (int d = 0; d < 3; ++d) {
+            double v = 0.125 * sgn[a][d];
+            for (int e = 0; e < 3; ++e)
+              if (e != d) v *= 1.0 + sgn[a][e] * xi[e];
+            dN[a][d] = v * dinv;
+          }
+        double B[6][24] = {};
+        for (int a = 0; a < 8; ++a) {
+          B[0][3 * a] = dN[a][0];
+          B[1][3 * a + 1] = dN[a][1];
+          B[2][3 * a + 2] = dN[a][2];
+          B[3][3 * a] = dN[a][1];
+          B[3][3 * a + 1] = dN[a][0];
+          B[4][3 * a + 1] = dN[a][2];
+          B[4][3 * a + 2] = dN[a][1];
+          B[5][3 * a] = dN[a][2];
+          B[5][3 * a + 2] = dN[a][0];
+        }
+        for (int a = 0; a < 24; ++a)
+          for (int b = 0; b < 24; ++b) {
+            double s = 0.0;
+            for (int r = 0; r < 6; ++r)
+              for (int c = 0; c < 6; ++c) s += B[r][a] * D[r][c] * B[c][b];
+            Ke[a][b] += s * jdet;
+          }
+      }
+  for (int a = 0; a < 24; ++a)  // exact symmetry
+    for (int b = a + 1; b < 24; ++b) Ke[a][b] = Ke[b][a] = 0.5 * (Ke[a][b] + Ke[b][a]);
+}
+
+Problem make_frac(int m, double sigma_e, unsigned seed) {
+  if (m < 4 || m % 2 != 0) throw std::invalid_argument("frac: nodes per side must be even and >= 4");
+  const int ne = m - 1, km = m / 2;
+  const double h = 1.0 / ne, nu = 0.25;
+  const int64_t nplane = int64_t(m) * m;
+  auto nid = [&](int i, int j, int k) { return int64_t(i) + int64_t(m) * (j + int64_t(m) * k); };
+  const int64_t nn = nplane * m;
+  auto interior = [&](int i, int j) { return i > 0 && i < m - 1 && j > 0 && j < m - 1; };
+  // node numbering (free nodes only): planes 1..m-2; plane km followed by copies
+  std::vector<int64_t> nodeid(nn + nplane, -1);  // [0,nn): originals, [nn, nn+nplane): copies
+  int64_t nf = 0;
+  for (int k = 1; k < m - 1; ++k) {
+    for (int j = 0; j < m; ++j)
+      for (int i = 0; i < m; ++i) nodeid[nid(i, j, k)] = nf++;
+    if (k == km)
+      for (int j = 0; j < m; ++j)
+        for (int i = 0; i < m; ++i)
+          if (interior(i, j)) nodeid[nn + i + int64_t(m) * j] = nf++;
+  }
+  const int64_t nu_dofs = 3 * nf, np = int64_t(ne) * ne;
+  if (nu_dofs + np > INT32_MAX / 2) throw std::invalid_argument("frac: too large for int32 indices");
+
+  double Ke[24][24];
+  q1_stiffness(h, nu, Ke);
+  Normal nrm(seed);
+  Uniform uni(seed ^ 0x85ebca6bu);
+  std::vector<double> E(int64_t(ne) * ne * ne);
+  for (auto& e : E) e = std::exp(sigma_e * nrm());
+  std::vector<double> w(np);
+  for (auto& x : w) x = uni(1e-4, 1e-3);
+
+  // node-block accumulation: per free node a small list of (col node, 3x3)
+  struct Blk {
+    int64_t col;
+    double v[9];
+  };
+  std::vector<std::vector<Blk>> rows(nf);
+  auto add_block = [&](int64_t r, int64_t c, const double* v9, double scale) {
+    auto& R = rows[r];
+    for (auto& b : R)
+      if (b.col == c) {
+        for (int q = 0; q < 9; ++q) b.v[q] += scale * v9[q];
+        return;
+      }
+    Blk b;
+    b.col = c;
+    for (int q = 0; q < 9; ++q) b.v[q] = scale * v9[q];
+    R.push_back(b);
+  };
+  const int off[8][3] = {{0, 0, 0}, {1, 0, 0}, {1, 1, 0}, {0, 1, 0}, {0, 0, 1}, {1, 0, 1}, {1, 1, 1}, {0, 1, 1}};
+  for (int ez = 0; ez < ne; ++ez)
+    for (int ey = 0; ey < ne; ++ey)
+      for (int ex = 0; ex < ne; ++ex) {
+        int64_t nd[8];
+        for (int a = 0; a < 8; ++a) {
+          const int i = ex + off[a][0], j = ey + off[a][1], k = ez + off[a][2];
+          int64_t g = nodeid[nid(i, j, k)];
+          if (k == km && ez == km && interior(i, j)) g = nodeid[nn + i + int64_t(m) * j];  // copy above
+          nd[a] = g;
+        }
+        const double Ee = E[ex + int64_t(ne) * (ey + int64_t(ne) * ez)];
+        for (int a = 0; a < 8; ++a) {
+          if (nd[a] < 0) continue;
+          for (int b2 = 0; b2 < 8; ++b2) {
+            if (nd[b2] < 0) continue;
+            double v9[9];
+            for (int r = 0; r < 3; ++r)
+              for (int c = 0; c < 3; ++c) v9[3 * r + c] = Ke[3 * a + r][3 * b2 + c];
+            add_block(nd[a], nd[b2], v9, Ee);
+          }
+        }
+      }
+  // fracture coupling lists: for every u_z dof, (p index, coefficient)
+  std::vector<std::vector<std::pair<int64_t, double>>> up(nf);
+  const double load = h * h / 4.0;
+  auto fe = [&](int i, int j) { return int64_t(i) + int64_t(ne) * j; };
+  for (int j = 0; j < ne; ++j)
+    for (int i = 0; i < ne; ++i)
+      for (int a = 0; a < 4; ++a) {
+        const int ii = i + (a == 1 || a == 2), jj = j + (a >= 2);
+        if (!interior(ii, jj)) continue;  // shared tip: no jump
+        const int64_t top = nodeid[nn + ii + int64_t(m) * jj], bot = nodeid[nid(ii, jj, km)];
+        up[top].push_back({fe(i, j), -load});
+        up[bot].push_back({fe(i, j), load});
+      }
+
+  Problem P;
+  P.n = static_cast<int>(nu_dofs + np);
+  P.fields = {"u", "p"};
+  P.ptr.reserve(P.n + 1);
+  P.ptr.push_back(0);
+  P.labels.reserve(P.n);
+  P.unknown_map.reserve(P.n);
+  RowBuilder rb;
+  for (int64_t r = 0; r < nf; ++r)
+    for (int cr = 0; cr < 3; ++cr) {
+      for (const auto& b : rows[r])
+        for (int cc = 0; cc < 3; ++cc) rb.add(static_cast<int>(3 * b.col + cc), b.v[3 * cr + cc]);
+      if (cr == 2)
+        for (const auto& [pe, v] : up[r]) {
+          bool merged = false;
+          for (auto& e : rb.e)
+            if (e.first == static_cast<int>(nu_dofs + pe)) {
+              e.second += v;
+              merged = true;
+            }
+          if (!merged) rb.add(static_cast<int>(nu_dofs + pe), v);
+        }
+      finish_row(P, rb);
+      P.labels.push_back(0);
+      P.unknown_map.push_back(cr);
+    }
+  // pressure rows: storage + cubic-law flow + transposed jump rate
+  std::vector<std::vector<std::pair<int64_t, double>>> pu(np);
+  for (int64_t r = 0; r < nf; ++r)
+    for (const auto& [pe, v] : up[r]) pu[pe].push_back({3 * r + 2, -v});  // rate/dt with dt = 1
+  const double cs = 1e-2 * h * h;
+  for (int j = 0; j < ne; ++j)
+    for (int i = 0; i < ne; ++i) {
+      const int64_t e = fe(i, j);
+      auto kk = [&](int64_t q) { const double r = w[q] / 1e-3; return r * r * r / 12.0; };
+      double d = cs;
+      const int nbi[4] = {i - 1, i + 1, i, i};
+      const int nbj[4] = {j, j, j - 1, j + 1};
+      for (int q = 0; q < 4; ++q) {
+        if (nbi[q] < 0 || nbj[q] < 0 || nbi[q] >= ne || nbj[q] >= ne) continue;
+        const int64_t o = fe(nbi[q], nbj[q]);
+        const double T = 2.0 * kk(e) * kk(o) / (kk(e) + kk(o));
+        d += T;
+        rb.add(static_cast<int>(nu_dofs + o), -T);
+      }
+      rb.add(static_cast<int>(nu_dofs + e), d);
+      for (const auto& [c, v] : pu[e]) {
+        bool merged = false;
+        for (auto& x : rb.e)
+          if (x.first == static_cast<int>(c)) {
+            x.second += v;
+            merged = true;
+          }
+        if (!merged) rb.add(static_cast<int>(c), v);
+      }
+      finish_row(P, rb);
+      P.labels.push_back(1);
+      P.unknown_map.push_back(0);
+    }
+  Uniform rhs(seed + 0x9e3779b9u);
+  P.rhs.resize(P.n);
+  for (int i = 0; i < P.n; ++i) P.rhs[i] = rhs(-1.0, 1.0);
+  char buf[512];
+  std::snprintf(buf, sizeof buf,
+                "{\"problem\":\"frac\",\"nodes_per_side\":%d,\"elements\":%lld,\"fracture_elements\":%lld,"
+                "\"u_dofs\":%lld,\"sigma_lnE\":%.17g,\"nu\":0.25,\"seed\":%u,"
+                "\"units\":\"nondimensional, E median 1 <-> 10 GPa\",\"bc\":\"bottom and top node planes fixed\"}",
+                m, static_cast<long long>(ne) * ne * ne, static_cast<long long>(np),
+                static_cast<long long>(nu_dofs), sigma_e, seed);
+  P.meta = buf;
+  return P;
+}
+
 }  // namespace
 
 extern "C" {
+
+void* mgrx_gen_frac(int m, double sigma_e, unsigned seed) {
+  try {
+    return new Problem(make_frac(m, sigma_e, seed));
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
 
 void* mgrx_gen_comp(int nx, int ny, int nz, int wells, double sigma_t, unsigned seed) {
   try {

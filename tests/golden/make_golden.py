@@ -100,6 +100,9 @@ def build_problem(spec):
     if kind == "mfd":
         P = mx.mfd_problem(*spec["dims"], spec.get("field", "iid"), seed=spec.get("seed", 20210128))
         return P.ptr, P.col, P.val, P.partition.field_order, P.partition.labels, None, P.rhs
+    if kind == "frac":
+        P = mx.frac_problem(spec["m"], seed=spec.get("seed", 20210131))
+        return P.ptr, P.col, P.val, P.partition.field_order, P.partition.labels, P.unknown_map, P.rhs
     if kind == "comp":
         P = mx.comp_problem(*spec["dims"], wells=spec.get("wells", 2), seed=spec.get("seed", 20210130))
         return P.ptr, P.col, P.val, P.partition.field_order, P.partition.labels, None, P.rhs
@@ -152,6 +155,8 @@ CASES = [
      "strategy": "comp_mgr", "rtol": 1e-5},
     {"id": "comp_24x20x12_w3", "problem": {"kind": "comp", "dims": [24, 20, 12], "wells": 3},
      "strategy": "comp_mgr", "rtol": 1e-5},
+    {"id": "frac_m6_mgr_u", "problem": {"kind": "frac", "m": 6}, "strategy": "frac_mgr_u", "rtol": 1e-6},
+    {"id": "frac_m10_mgr_u", "problem": {"kind": "frac", "m": 10}, "strategy": "frac_mgr_u", "rtol": 1e-6},
     {"id": "sdd400_restrict_jacobi", "problem": {"kind": "sdd2", "n": 400}, "strategy": TWO_FIELD_RJAC,
      "rtol": 1e-9},
 ]
