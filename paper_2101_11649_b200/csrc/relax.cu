@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 #include "relax.cuh"
@@ -40,6 +41,16 @@ __device__ __forceinline__ int ld_relaxed_int(const int* p) {
 }
 __device__ __forceinline__ bool pending_value(double v) { return __double_as_longlong(v) == -1LL; }
 
+// Optional sweep trace (MGRX_GS_TRACE=<dir>): per row, the %globaltimer when
+// its lane started on it and when it published x_i. Diagnostic only.
+__device__ unsigned long long* g_trace_start = nullptr;
+__device__ unsigned long long* g_trace_pub = nullptr;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 // Sync-free sweep kernel. A team of kT lanes owns one row (kT = 1, 4 or 8,
 // chosen from the average dependency count). The CTA takes kGsThreads/kT
 // consecutive sweep positions per ticket and stages their sweep-CSR entries
@@ -56,7 +67,7 @@ __global__ void __launch_bounds__(kGsThreads)
     k_gs(int n, const int* __restrict__ order, const int* __restrict__ sptr,
          const int* __restrict__ scol, const double* __restrict__ sval, const double* __restrict__ sd,
          const double* __restrict__ b, const double* __restrict__ xold, double* xnew, double* zadd,
-         int* tk) {
+         int* tk, unsigned sleep_ns, int pub_mode) {
   extern __shared__ double smem[];
   double* cval = smem;                     // kGsCap entry values
   double* cx = smem + kGsCap;              // kGsCap parked x values
@@ -94,6 +105,7 @@ __global__ void __launch_bounds__(kGsThreads)
       k = sptr[p];
       ke = sptr[p + 1];
       if (u == 0) s = b[i];
+      if (g_trace_start && u == 0) g_trace_start[i] = gtimer();
     }
     bool done = !active;
     long long spins = 0;
@@ -135,7 +147,14 @@ __global__ void __launch_bounds__(kGsThreads)
             if (u == 0) {
               const double xi = kFull ? xold[i] : 0.0;
               const double v = __dadd_rn(xi, __ddiv_rn(s, sd[p]));
-              st_relaxed(xnew + i, v);
+              if (pub_mode == 2) {
+                atomicExch(reinterpret_cast<unsigned long long*>(xnew + i),
+                           static_cast<unsigned long long>(__double_as_longlong(v)));
+              } else {
+                st_relaxed(xnew + i, v);
+                if (pub_mode == 1) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+              }
+              if (g_trace_pub) g_trace_pub[i] = gtimer();
               if (zadd) zadd[i] = __dadd_rn(zadd[i], v);
             }
             done = true;
@@ -146,8 +165,8 @@ __global__ void __launch_bounds__(kGsThreads)
                 st_relaxed(xnew + i, 0.0);
               }
               done = true;
-            } else {
-              __nanosleep(20);
+            } else if (sleep_ns > 0) {
+              __nanosleep(sleep_ns);
             }
           }
         } else {
@@ -414,6 +433,49 @@ void build_sweep_csr(const DCsr& A, const GsSchedule& sch, bool forward, bool fu
 
 }  // namespace
 
+// Diagnostic sweep trace (MGRX_GS_TRACE=<dir>): the first sweep of each
+// schedule is run with %globaltimer stamps and written out with its order
+// and dependency CSR for offline critical-path analysis.
+struct Trace {
+  DVec<unsigned long long> t0, t1;
+  bool on = false;
+};
+void trace_begin(Trace& tr, const GsSchedule& sch, int n, cudaStream_t s) {
+  static std::vector<const void*> seen;
+  for (const void* k : seen)
+    if (k == static_cast<const void*>(&sch)) return;
+  seen.push_back(&sch);
+  tr.on = true;
+  tr.t0.alloc(n, s);
+  tr.t1.alloc(n, s);
+  unsigned long long* p0 = tr.t0.get();
+  unsigned long long* p1 = tr.t1.get();
+  MGRX_CK(cudaMemcpyToSymbolAsync(g_trace_start, &p0, sizeof(p0), 0, cudaMemcpyHostToDevice, s));
+  MGRX_CK(cudaMemcpyToSymbolAsync(g_trace_pub, &p1, sizeof(p1), 0, cudaMemcpyHostToDevice, s));
+}
+void trace_end(Trace& tr, const char* dir, const GsSchedule& sch, int n, cudaStream_t s) {
+  if (!tr.on) return;
+  std::vector<unsigned long long> a = tr.t0.download(n), b = tr.t1.download(n);
+  std::vector<int> ord = sch.order.download(n), dp = sch.dptr.download(n + 1);
+  std::vector<int> dc = sch.dcol.download(dp[n] > 0 ? dp[n] : 1);
+  unsigned long long* nul = nullptr;
+  MGRX_CK(cudaMemcpyToSymbolAsync(g_trace_start, &nul, sizeof(nul), 0, cudaMemcpyHostToDevice, s));
+  MGRX_CK(cudaMemcpyToSymbolAsync(g_trace_pub, &nul, sizeof(nul), 0, cudaMemcpyHostToDevice, s));
+  MGRX_CK(cudaStreamSynchronize(s));
+  char path[512];
+  std::snprintf(path, sizeof path, "%s/gs_n%d_lv%d_%p.bin", dir, n, sch.levels, static_cast<const void*>(&sch));
+  if (FILE* f = std::fopen(path, "wb")) {
+    int hdr[3] = {n, sch.levels, dp[n]};
+    std::fwrite(hdr, sizeof(int), 3, f);
+    std::fwrite(ord.data(), sizeof(int), n, f);
+    std::fwrite(dp.data(), sizeof(int), n + 1, f);
+    std::fwrite(dc.data(), sizeof(int), dp[n], f);
+    std::fwrite(a.data(), sizeof(unsigned long long), n, f);
+    std::fwrite(b.data(), sizeof(unsigned long long), n, f);
+    std::fclose(f);
+  }
+}
+
 void gs_schedule(const DCsr& A, bool forward, const double* d, bool full, GsSchedule& out,
                  cudaStream_t s) {
   const int n = A.rows;
@@ -538,9 +600,20 @@ void gs_sweep(const DCsr& A, const GsSchedule& sch, const double* d, const doubl
   const int* sc = full ? sch.fcol.get() : sch.dcol.get();
   const double* sv = full ? sch.fval.get() : sch.dval.get();
   int* tk = scr.ticket_err.get();
+  static const unsigned kSleep = [] {
+    const char* e = std::getenv("MGRX_GS_SLEEP");
+    return e ? static_cast<unsigned>(std::atoi(e)) : 20u;
+  }();
+  static const int kPub = [] {
+    const char* e = std::getenv("MGRX_GS_PUB");
+    return e ? std::atoi(e) : 0;
+  }();
+  const char* trace_dir = std::getenv("MGRX_GS_TRACE");
+  Trace tr;
+  if (trace_dir && !full) trace_begin(tr, sch, n, s);
 #define MGRX_GS_LAUNCH(TT, FF)                                                                    \
   k_gs<TT, FF><<<grid, kGsThreads, kGsSmem, s>>>(n, sch.order.get(), sp, sc, sv, sch.sd.get(), b, \
-                                                 xold, xnew, zadd, tk)
+                                                 xold, xnew, zadd, tk, kSleep, kPub)
   if (T == 1) {
     if (full) MGRX_GS_LAUNCH(1, true); else MGRX_GS_LAUNCH(1, false);
   } else if (T == 4) {
@@ -549,6 +622,7 @@ void gs_sweep(const DCsr& A, const GsSchedule& sch, const double* d, const doubl
     if (full) MGRX_GS_LAUNCH(8, true); else MGRX_GS_LAUNCH(8, false);
   }
 #undef MGRX_GS_LAUNCH
+  if (trace_dir) trace_end(tr, trace_dir, sch, n, s);
   MGRX_LAUNCH_CK();
   count_launch();
 }
