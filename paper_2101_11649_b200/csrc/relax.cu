@@ -337,6 +337,130 @@ __global__ void __launch_bounds__(kLvThreads)
 #undef LV_ROW
 }
 
+// Pipelined single-CTA level sweep. The sweep is cut into "steps": runs of
+// consecutive sweep positions inside one dependency level that fit a shared
+// memory buffer (kPipeRows rows, kPipeEnt entries). One 1024-thread CTA walks
+// the steps; while it computes step s it prefetches step s+1 (row ids, rhs in
+// sweep order, diagonal, dependency columns/values) with cp.async into the
+// other buffer, so a step costs the L2 round trip of its x values plus a
+// barrier. Rows in a step are independent; values are published with st.cg
+// and read with ld.cg, ordered by __syncthreads inside the CTA.
+constexpr int kPipeThreads = 1024;
+constexpr int kPipeRows = 1536;
+constexpr int kPipeEnt = 5120;
+struct PipeBuf {
+  double sd[kPipeRows];
+  double bp[kPipeRows];
+  double val[kPipeEnt];
+  int ord[kPipeRows];
+  int ptr[kPipeRows + 1];
+  int col[kPipeEnt];
+};
+constexpr size_t kPipeSmem = 2 * sizeof(PipeBuf);
+constexpr int kPipeMaxSteps = 2048;
+
+__device__ __forceinline__ void cpa4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src));
+}
+__device__ __forceinline__ void cpa8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src));
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;"); }
+__device__ __forceinline__ void cpa_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+template <bool kFull>
+__global__ void __launch_bounds__(kPipeThreads)
+    k_gs_pipe(int nsteps, const int* __restrict__ steps, const int* __restrict__ order,
+              const int* __restrict__ sptr, const int* __restrict__ scol, const double* __restrict__ sval,
+              const double* __restrict__ sd, const double* __restrict__ bp, const double* __restrict__ xold,
+              double* xnew, double* zadd) {
+  extern __shared__ __align__(16) unsigned char pipe_raw[];
+  PipeBuf* buf = reinterpret_cast<PipeBuf*>(pipe_raw);
+  const int tid = threadIdx.x;
+  // step boundaries (positions and entry offsets) staged once, so issuing a
+  // prefetch never waits on a global load
+  __shared__ int stp[kPipeMaxSteps + 1], ste[kPipeMaxSteps + 1];
+  const bool st_smem = nsteps <= kPipeMaxSteps;
+  if (st_smem)
+    for (int q = tid; q <= nsteps; q += kPipeThreads) {
+      stp[q] = steps[q];
+      ste[q] = steps[nsteps + 1 + q];
+    }
+  __syncthreads();
+  auto SP = [&](int q) { return st_smem ? stp[q] : steps[q]; };
+  auto SE = [&](int q) { return st_smem ? ste[q] : steps[nsteps + 1 + q]; };
+  auto issue = [&](int st, PipeBuf& B) {
+    const int p0 = SP(st), p1 = SP(st + 1);
+    const int nr = p1 - p0;
+    const int e0 = SE(st), e1 = SE(st + 1);
+    for (int q = tid; q < nr; q += kPipeThreads) {
+      cpa4(&B.ord[q], order + p0 + q);
+      cpa8(&B.sd[q], sd + p0 + q);
+      cpa8(&B.bp[q], bp + p0 + q);
+    }
+    for (int q = tid; q <= nr; q += kPipeThreads) cpa4(&B.ptr[q], sptr + p0 + q);
+    for (int q = tid; q < e1 - e0; q += kPipeThreads) {
+      cpa4(&B.col[q], scol + e0 + q);
+      cpa8(&B.val[q], sval + e0 + q);
+    }
+    cpa_commit();
+  };
+  issue(0, buf[0]);
+  for (int st = 0; st < nsteps; ++st) {
+    PipeBuf& B = buf[st & 1];
+    if (st + 1 < nsteps) issue(st + 1, buf[(st + 1) & 1]);
+    else cpa_commit();  // keep the group count uniform for wait_group 1
+    cpa_wait1();
+    __syncthreads();
+    const int nr = SP(st + 1) - SP(st);
+    const int e0 = B.ptr[0];
+    for (int q = tid; q < nr; q += kPipeThreads) {
+      const int i = B.ord[q];
+      double s = B.bp[q];
+      const int k1 = B.ptr[q + 1] - e0;
+      for (int k = B.ptr[q] - e0; k < k1; ++k) {
+        int c = B.col[k];
+        double x;
+        if (kFull && !(c & kDepBit)) {
+          x = xold[c];
+        } else {
+          if (kFull) c &= ~kDepBit;
+          x = __ldcg(xnew + c);
+        }
+        s = __dsub_rn(s, __dmul_rn(B.val[k], x));
+      }
+      const double v = __dadd_rn(kFull ? xold[i] : 0.0, __ddiv_rn(s, B.sd[q]));
+      __stcg(xnew + i, v);
+      if (zadd) zadd[i] = __dadd_rn(zadd[i], v);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_gather_d(int n, const int* __restrict__ idx, const double* __restrict__ x,
+                           double* __restrict__ y) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = x[idx[i]];
+}
+
+std::vector<int> pipe_steps(const std::vector<int>& level_ptr, const std::vector<int>& sptr) {
+  std::vector<int> st{0};
+  for (size_t L = 0; L + 1 < level_ptr.size(); ++L) {
+    int p = level_ptr[L];
+    const int pe = level_ptr[L + 1];
+    while (p < pe) {
+      int q = p;
+      while (q < pe && q - p < kPipeRows && sptr[q + 1] - sptr[p] <= kPipeEnt) ++q;
+      if (q == p) ++q;  // a single row longer than the buffer is never produced by the generators
+      st.push_back(q);
+      p = q;
+    }
+  }
+  return st;
+}
+
 // Dependency levels by monotone in-place relaxation: lev[i] = 1 + max over
 // dependencies; converges to the longest-path level.
 __global__ void k_levels(int n, const int* __restrict__ ptr, const int* __restrict__ col, int fwd,
@@ -526,15 +650,52 @@ void gs_schedule(const DCsr& A, bool forward, const double* d, bool full, GsSche
   // Sweep mode: MGRX_GS_MODE=lv selects the level-synchronous cluster
   // kernel; default is the sync-free kernel. Cluster size from the
   // average level width (about 1 row per thread).
+  // 0 sync-free (default, fastest measured at cfg2: 2-3 us per dependency
+  // hop), 1 level-synchronous cluster (MGRX_GS_MODE=lv), 2 pipelined single
+  // CTA (MGRX_GS_MODE=pipe); both alternatives measured 2-4x slower.
   static const int mode = [] {
     const char* e = std::getenv("MGRX_GS_MODE");
-    return (e && e[0] == 'l') ? 1 : 0;
+    if (e && e[0] == 'l') return 1;
+    if (e && e[0] == 'p') return 2;
+    return 0;
   }();
   if (mode == 1) {
     const double width = static_cast<double>(n) / out.levels;
     out.cluster = std::max(1, std::min(16, static_cast<int>(std::ceil(width / kLvThreads))));
   } else {
     out.cluster = 0;
+  }
+  out.pipe = 0;
+  if (mode == 2) {
+    const std::vector<int> dp = out.dptr.download(n + 1);
+    bool ok = true;
+    for (int q = 0; q < n && ok; ++q) ok = dp[q + 1] - dp[q] <= kPipeEnt;
+    std::vector<int> fp;
+    if (ok && full) {
+      fp = out.fptr.download(n + 1);
+      for (int q = 0; q < n && ok; ++q) ok = fp[q + 1] - fp[q] <= kPipeEnt;
+    }
+    if (ok) {
+      auto with_offsets = [](const std::vector<int>& st, const std::vector<int>& ptr) {
+        std::vector<int> v(st);
+        for (int q : st) v.push_back(ptr[q]);
+        return v;
+      };
+      const std::vector<int> st = pipe_steps(out.level_ptr, dp);
+      out.ndsteps = static_cast<int>(st.size()) - 1;
+      const std::vector<int> stv = with_offsets(st, dp);
+      out.dsteps.alloc(stv.size(), s);
+      out.dsteps.upload(stv.data(), stv.size());
+      if (full) {
+        const std::vector<int> st2 = pipe_steps(out.level_ptr, fp);
+        out.nfsteps = static_cast<int>(st2.size()) - 1;
+        const std::vector<int> stv2 = with_offsets(st2, fp);
+        out.fsteps.alloc(stv2.size(), s);
+        out.fsteps.upload(stv2.data(), stv2.size());
+      }
+      out.bp.alloc(n, s);
+      out.pipe = 1;
+    }
   }
 }
 
@@ -548,6 +709,21 @@ void gs_sweep(const DCsr& A, const GsSchedule& sch, const double* d, const doubl
   if (scr.ticket_err.size() < 2) throw RuntimeError("gs_sweep: scratch not bound");
   const bool full_sweep = xold != nullptr;
   if (full_sweep && !sch.has_full) throw RuntimeError("gs_sweep: schedule built without the full sweep CSR");
+  if (sch.pipe) {
+    k_gather_d<<<blocks_for(n, 256), 256, 0, s>>>(n, sch.order.get(), b, const_cast<double*>(sch.bp.get()));
+    const int* sp = full_sweep ? sch.fptr.get() : sch.dptr.get();
+    const int* sc = full_sweep ? sch.fcol.get() : sch.dcol.get();
+    const double* sv = full_sweep ? sch.fval.get() : sch.dval.get();
+    if (full_sweep)
+      k_gs_pipe<true><<<1, kPipeThreads, kPipeSmem, s>>>(sch.nfsteps, sch.fsteps.get(), sch.order.get(), sp, sc,
+                                                         sv, sch.sd.get(), sch.bp.get(), xold, xnew, zadd);
+    else
+      k_gs_pipe<false><<<1, kPipeThreads, kPipeSmem, s>>>(sch.ndsteps, sch.dsteps.get(), sch.order.get(), sp, sc,
+                                                          sv, sch.sd.get(), sch.bp.get(), xold, xnew, zadd);
+    MGRX_LAUNCH_CK();
+    count_launch(2);
+    return;
+  }
   if (sch.cluster > 0) {
     // level-synchronous cluster sweep
     cudaLaunchConfig_t cfg = {};
@@ -629,6 +805,8 @@ void gs_sweep(const DCsr& A, const GsSchedule& sch, const double* d, const doubl
 
 void gs_bind_scratch(GsScratch& scr, cudaStream_t s) {
   static const bool attrs = [] {
+    MGRX_CK(cudaFuncSetAttribute(k_gs_pipe<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kPipeSmem)));
+    MGRX_CK(cudaFuncSetAttribute(k_gs_pipe<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kPipeSmem)));
     MGRX_CK(cudaFuncSetAttribute(k_gs_lv<false, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     MGRX_CK(cudaFuncSetAttribute(k_gs_lv<true, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     const int sm = static_cast<int>(kGsSmem);

@@ -31,6 +31,10 @@ struct GsSchedule {
   int team = 1;                    // lanes per row in the sync-free kernel
   int cluster = 0;                 // >0: level-synchronous sweep in one cluster of this size
   DVec<int> dlptr;                 // device copy of level_ptr
+  int pipe = 0;                    // 1: pipelined single-CTA level sweep
+  DVec<int> dsteps, fsteps;        // step boundaries (positions) for the pipelined sweep
+  int ndsteps = 0, nfsteps = 0;
+  DVec<double> bp;                 // rhs gathered into sweep order (pipelined sweep)
 };
 void gs_schedule(const DCsr& A, bool forward, const double* d, bool full, GsSchedule& out,
                  cudaStream_t s);
