@@ -173,3 +173,24 @@ def test_cfg1_all_strategies(strategy):
     assert ok, detail
     for p in refcpu.dump_paths(R.info()):
         assert _same_dump(H.dump(p), R.dump(p)), p
+
+
+def test_sharded_path_device_backend_single_rank():
+    """dist.py on the GPU backend (libmgrx slab SpMV), world size 1: the
+    sharded V-cycle reproduces the library's own apply."""
+    from paper_2101_11649_b200 import dist as D
+    P = mx.mfd_problem(8, 6, 5, "iid")
+    text = mx.load_strategy("mfd_mgr_pi_c1_l1j")
+    H = mx.Hierarchy(mx.Matrix(P.ptr, P.col, P.val), P.partition, text)
+    comm = D.Comm()
+    be = D.DeviceBackend(mx.default_context())
+    rr = [(0, P.n)]
+    M = D.DistMgr(comm, be, H.dump, H.info(), json.loads(text), rr)
+    v = np.random.default_rng(4).uniform(-1, 1, P.n)
+    z = M.apply(be.vec(v)).cpu().numpy()
+    zr = H.apply(v)
+    assert np.linalg.norm(z - zr) <= 1e-12 * np.linalg.norm(zr)
+    A = D.DistOperator(comm, be, (P.ptr, P.col, P.val), rr, rr)
+    x, rep = D.gmres(comm, be, A, M.apply, be.vec(P.rhs), be.zeros(P.n), restart=30, rel_tol=1e-6)
+    _, rep2 = H.solve(P.rhs, cfg=mx.KrylovConfig(restart=30, rel_tol=1e-6))
+    assert rep["converged"] and abs(rep["iterations"] - rep2.iterations) <= 1
