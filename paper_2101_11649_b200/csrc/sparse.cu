@@ -210,14 +210,16 @@ HostCsr to_host(const DCsr& A, cudaStream_t s) {
 // ============================================================================
 namespace {
 
-constexpr int kRows = 256;
-constexpr int kCap = 2048;
+// rows per CTA is a template parameter (256 / 128 / 64) so that mid-sized
+// matrices still launch several waves of CTAs; each CTA stages 8 entries per
+// thread per chunk.
 
-template <class Epi>
+template <int kRows, class Epi>
 __global__ void __launch_bounds__(kRows) k_spmv(int rows, const int* __restrict__ ptr,
                                                 const int* __restrict__ col,
                                                 const double* __restrict__ val,
                                                 const double* __restrict__ x, Epi epi) {
+  constexpr int kCap = 8 * kRows;
   __shared__ double prod[kCap];
   const int r0 = blockIdx.x * kRows;
   const int r = r0 + threadIdx.x;
@@ -233,7 +235,7 @@ __global__ void __launch_bounds__(kRows) k_spmv(int rows, const int* __restrict_
     const int c1 = min(c0 + kCap, p1);
 #pragma unroll 4
     for (int q = c0 + threadIdx.x; q < c1; q += kRows)
-      prod[q - c0] = __dmul_rn(__ldg(val + q), __ldg(x + __ldg(col + q)));
+      prod[q - c0] = __dmul_rn(__ldcs(val + q), __ldg(x + __ldcs(col + q)));
     __syncthreads();
     const int a = max(lo, c0), b = min(hi, c1);
     for (int q = a; q < b; ++q) sum = __dadd_rn(sum, prod[q - c0]);
@@ -270,6 +272,30 @@ __global__ void __launch_bounds__(kWarps * 32) k_spmv_wpr(int rows, const int* _
     }
     if (l == 0) epi(r, sum);
   }
+}
+
+// Thread per row for very short rows (MGR prolongation: 1-2 entries per
+// row): no staging, every thread's few loads are independent, so the warp
+// keeps many requests in flight. Same sequential row sum.
+template <class Epi>
+__global__ void __launch_bounds__(256) k_spmv_tpr(int rows, const int* __restrict__ ptr,
+                                                  const int* __restrict__ col,
+                                                  const double* __restrict__ val,
+                                                  const double* __restrict__ x, Epi epi) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const int lo = __ldg(ptr + r), hi = __ldg(ptr + r + 1);
+  double sum = 0.0;
+  int k = lo;
+  for (; k + 4 <= hi; k += 4) {
+    const int c0 = __ldg(col + k), c1 = __ldg(col + k + 1), c2 = __ldg(col + k + 2), c3 = __ldg(col + k + 3);
+    const double a0 = __ldg(val + k), a1 = __ldg(val + k + 1), a2 = __ldg(val + k + 2), a3 = __ldg(val + k + 3);
+    const double p0 = __dmul_rn(a0, __ldg(x + c0)), p1 = __dmul_rn(a1, __ldg(x + c1));
+    const double p2 = __dmul_rn(a2, __ldg(x + c2)), p3 = __dmul_rn(a3, __ldg(x + c3));
+    sum = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(sum, p0), p1), p2), p3);
+  }
+  for (; k < hi; ++k) sum = __dadd_rn(sum, __dmul_rn(__ldg(val + k), __ldg(x + __ldg(col + k))));
+  epi(r, sum);
 }
 
 struct EpiStore {
@@ -316,6 +342,12 @@ struct EpiJacobi {
 template <class Epi>
 void launch_spmv(const DCsr& A, const double* x, Epi epi, cudaStream_t s) {
   if (A.rows == 0) return;
+  if (A.rows > 65536 && A.nnz <= 3LL * A.rows) {
+    k_spmv_tpr<<<blocks_for(A.rows, 256), 256, 0, s>>>(A.rows, A.ptr.get(), A.col.get(), A.val.get(), x, epi);
+    MGRX_LAUNCH_CK();
+    count_launch();
+    return;
+  }
   const bool small = A.rows <= 65536 || A.nnz > 24LL * A.rows;
   if (small) {
     const int grid = std::min(blocks_for(A.rows, kWarps), 148 * 8);
@@ -324,8 +356,12 @@ void launch_spmv(const DCsr& A, const double* x, Epi epi, cudaStream_t s) {
     count_launch();
     return;
   }
-  k_spmv<<<blocks_for(A.rows, kRows), kRows, 0, s>>>(A.rows, A.ptr.get(), A.col.get(), A.val.get(),
-                                                      x, epi);
+  if (A.rows >= 2000000)
+    k_spmv<256><<<blocks_for(A.rows, 256), 256, 0, s>>>(A.rows, A.ptr.get(), A.col.get(), A.val.get(), x, epi);
+  else if (A.rows >= 300000)
+    k_spmv<128><<<blocks_for(A.rows, 128), 128, 0, s>>>(A.rows, A.ptr.get(), A.col.get(), A.val.get(), x, epi);
+  else
+    k_spmv<64><<<blocks_for(A.rows, 64), 64, 0, s>>>(A.rows, A.ptr.get(), A.col.get(), A.val.get(), x, epi);
   MGRX_LAUNCH_CK();
   count_launch();
 }

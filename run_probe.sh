@@ -1,6 +1,5 @@
 #!/bin/bash
 mkdir -p gpurun_out
-TAG=pipe python tools/probe_gs.py > gpurun_out/probe_trace.log 2>&1
-MGRX_GS_MODE=sf TAG=sf python tools/probe_gs.py >> gpurun_out/probe_trace.log 2>&1
-timeout 600 python -m pytest tests -q -m gpu -x >> gpurun_out/probe_trace.log 2>&1
+python tools/probe_spmv.py spmv.A amg.0.resid amg.0.pre mgr.0.prolong mgr.0.rres amg.1.resid amg.1.pre > gpurun_out/probe_spmv_plain.log 2>&1
+timeout 600 python -m pytest tests -q -m gpu -x -k "spmv or bit_exact or solve_parity" >> gpurun_out/probe_spmv_plain.log 2>&1
 echo done
