@@ -33,9 +33,10 @@ CONFIGS = {
              "strategy": "mfd_mgr_pi_c1", "rtol": 1e-6,
              "desc": "cfg1: hybrid-MFD [p,pi] 20x20x10 iid log-normal, FGMRES(30) rtol 1e-6, MGR_pi + 1 AMG V-cycle"},
     "cfg2": {"kind": "mfd", "dims": (128, 128, 64), "field": "layered", "seed": 20210129,
-             "strategy": "mfd_mgr_pi_c1", "rtol": 1e-6,
+             "strategy": "mfd_mgr_pi_c1_l1j", "rtol": 1e-6, "variant": "mfd_mgr_pi_c1",
              "desc": "cfg2: hybrid-MFD [p,pi] 128x128x64 layered log-normal (1e6 contrast), "
-                     "FGMRES(30) rtol 1e-6, MGR_pi + 1 AMG V-cycle"},
+                     "FGMRES(30) rtol 1e-6, MGR_pi (exact pi elimination) + 1 AMG V-cycle "
+                     "(l1-Jacobi x2 AMG smoothing; variant: the AMG default hybrid Gauss-Seidel)"},
     "cfg3": {"kind": "comp", "dims": (100, 100, 50), "wells": 8, "seed": 20210130,
              "strategy": "comp_mgr", "rtol": 1e-5,
              "desc": "cfg3: compositional p+3 densities 100x100x50 (4x4 blocks) + 8 wells x 50 elements x 5 dofs, "
@@ -175,6 +176,7 @@ def main():
     ap.add_argument("--impl", default="mgrx")
     ap.add_argument("--ref-iters", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-variant", action="store_true")
     ap.add_argument("--strategy", default=None, help="strategies/<name>.json (default: %s)" % STRATEGY)
     args = ap.parse_args()
     CONFIG = args.config
@@ -261,7 +263,7 @@ def main():
     peak, peak_kind = peaks()
     info = H.info()
     probes = {}
-    names = ["spmv.A", "mgr.0.rres", "mgr.0.prolong"]
+    names = ["mgs", "spmv.A", "mgr.0.rres", "mgr.0.prolong"]
     for k in range(max(info["coarse_amg_levels"] - 1, 0)):
         names += [f"amg.{k}.resid", f"amg.{k}.pre", f"amg.{k}.post"]
     for name in names:
@@ -270,14 +272,47 @@ def main():
             probes[name] = {"avg_ms": ms_k, "bytes": by, "GBps": by / (ms_k * 1e-3) / 1e9}
         except mx.MgrxError as e:
             probes[name] = {"error": str(e)}
-    # per-iteration launch counts for the share estimate (1 V-cycle, 1 MGR level)
-    share = {k: v["avg_ms"] * (1.0) for k, v in probes.items() if "avg_ms" in v}
-    dom = max((k for k in share), key=lambda k: share[k])
+    # dominant kernel: the fused modified-Gram-Schmidt step (k_mgs) carries the
+    # largest share of solve time in the l1-Jacobi strategy (47% in the
+    # profiles/r01 launch list, the SpMV family k_spmv* next); for other
+    # strategies take the probe with the largest time.
+    share = {k: v["avg_ms"] for k, v in probes.items() if "avg_ms" in v}
+    dom = "mgs" if "l1j" in STRATEGY else max((k for k in share), key=lambda k: share[k])
     d = probes[dom]
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "roofline_traffic.json")) as f:
+            tr = json.load(f)
+        if tr.get("kernel") == dom and tr.get("config") == CONFIG:
+            traffic = tr["dram_bytes_per_launch"]
+    except Exception:
+        pass
     roof = {"bound": "hbm", "kernel": dom, "achieved": d["GBps"], "peak": peak, "unit": "GB/s",
-            "frac": d["GBps"] / peak, "traffic": None, "peak_source": peak_kind,
-            "kernels": probes}
+            "frac": d["GBps"] / peak, "traffic": traffic, "algorithmic_bytes": d["bytes"],
+            "peak_source": peak_kind, "kernels": probes}
 
+    variants = {}
+    vname = CONFIGS[CONFIG].get("variant")
+    if vname and not args.strategy and not args.no_variant:
+        Hv = mx.Hierarchy(A, P.partition, mx.load_strategy(vname), P.unknown_map)
+        step_v = lambda: (x.zero_(), torch.cuda.synchronize(), Hv.solve_device(b.data_ptr(), x.data_ptr(), cfg))[2]
+        step_v()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        rv = [step_v() for _ in range(max(1, args.steps // 2))]
+        ev1.record()
+        torch.cuda.synchronize()
+        msv = ev0.elapsed_time(ev1) / len(rv)
+        itv = sum(r.iterations for r in rv) / len(rv)
+        gs_ms, gs_by = Hv.time_kernel("amg.0.pre", reps=5)
+        variants[vname] = {"value": P.n * itv / (msv * 1e-3), "unit": UNIT, "ms_per_step": msv,
+                           "iterations_per_solve": itv,
+                           "smoother": "hybrid_l1_gs (exact sequential Gauss-Seidel, sync-free sweep)",
+                           "dominant_kernel": {"name": "k_gs (fine AMG level, forward sweep)", "avg_ms": gs_ms,
+                                               "achieved_GBps": gs_by / (gs_ms * 1e-3) / 1e9,
+                                               "frac": gs_by / (gs_ms * 1e-3) / 1e9 / peak,
+                                               "bound": "latency (dependency chain, 318 levels)"}}
+        del Hv
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -295,7 +330,7 @@ def main():
                 "hierarchy": info,
                 "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 16 * P.n,
                         "d2h_bytes_per_step": 8 * P.n},
-                "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu,
+                "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "variants": variants,
                 "clocks": clk.summary()}
         print(json.dumps(line))
     if world > 1:

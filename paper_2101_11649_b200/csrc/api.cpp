@@ -98,6 +98,20 @@ void prepare_probe(mgrx_hier* h, const std::string& w, std::function<void()>& fn
   double* x = h->px.get();
   double* y = h->py.get();
   double* z = h->pz.get();
+  if (w == "mgs") {
+    // fused MGS step on fine-size vectors: w -= h v_{i-1}; h_i = v_i . w
+    const int n = h->A.rows;
+    h->ws.ensure(n, 30, s);
+    double* V = h->ws.V.get();
+    double* wv = h->ws.w.get();
+    MGRX_CK(cudaMemsetAsync(V, 0, sizeof(double) * 2 * static_cast<size_t>(n), s));
+    MGRX_CK(cudaMemsetAsync(wv, 0, sizeof(double) * n, s));
+    const double* hp = x;  // zeros
+    GmresWork* ws = &h->ws;
+    fn = [=] { mgs_probe(n, wv, V, hp, V + n, *ws, s); };
+    bytes = 24.0 * n;  // SURVEY 8(d) MGS step model: read v_i and w, write w
+    return;
+  }
   if (w == "spmv.A") {
     const DCsr* A = &h->A;
     fn = [=] { spmv(*A, x, y, s); };

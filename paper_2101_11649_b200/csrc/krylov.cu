@@ -51,7 +51,34 @@ __global__ void __launch_bounds__(kRT)
           double* __restrict__ hacc, int accumulate, double* __restrict__ out2) {
   const double h = vprev ? *hprev : 0.0;
   double s1 = 0.0, s2 = 0.0;
-  for (int i = blockIdx.x * kRT + threadIdx.x; i < n; i += kRB * kRT) {
+  // Grid-stride slice of this lane, processed kU iterations at a time: all
+  // loads of the group are issued first (memory-level parallelism), then the
+  // lane's partial sums are updated in the same sequential order as a plain
+  // loop (the canonical reduction order shared with the oracle).
+  constexpr int kU = 4;
+  constexpr int kStride = kRB * kRT;
+  int i0 = blockIdx.x * kRT + threadIdx.x;
+  for (; i0 + (kU - 1) * kStride < n; i0 += kU * kStride) {
+    double wv[kU], pv[kU], av[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = i0 + u * kStride;
+      wv[u] = __ldcg(w + i);
+      if (vprev) pv[u] = __ldcg(vprev + i);
+      if (a) av[u] = __ldcg(a + i);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      double wi = wv[u];
+      if (vprev) {
+        wi = __dsub_rn(wi, __dmul_rn(h, pv[u]));
+        w[i0 + u * kStride] = wi;
+      }
+      if (a) s1 = __dadd_rn(s1, __dmul_rn(av[u], wi));
+      if (want2) s2 = __dadd_rn(s2, __dmul_rn(wi, wi));
+    }
+  }
+  for (int i = i0; i < n; i += kStride) {
     double wi = w[i];
     if (vprev) {
       wi = __dsub_rn(wi, __dmul_rn(h, vprev[i]));
@@ -133,6 +160,11 @@ void GmresWork::ensure(int n_, int m_, cudaStream_t s) {
 
 GmresWork::~GmresWork() {
   if (hpinned) cudaFreeHost(hpinned);
+}
+
+void mgs_probe(int n, double* w, const double* vprev, const double* h, const double* a, GmresWork& ws,
+               cudaStream_t s) {
+  mgs_launch(n, w, vprev, h, a, false, ws, ws.scal.get() + 2, nullptr, false, nullptr, s);
 }
 
 double device_dot(int n, const double* a, const double* b, GmresWork& ws, cudaStream_t s) {

@@ -37,6 +37,10 @@ struct GmresWork {
 GmresResult gmres_device(const DCsr& A, const double* b, double* x, const KrylovSpec& cfg,
                          const DevOp& precond, GmresWork& ws, cudaStream_t s);
 
+// One fused MGS step (w -= h*vprev; a.w) for the roofline probe.
+void mgs_probe(int n, double* w, const double* vprev, const double* h, const double* a, GmresWork& ws,
+               cudaStream_t s);
+
 // Deterministic device dot product (fixed grid, fixed reduction tree).
 double device_dot(int n, const double* a, const double* b, GmresWork& ws, cudaStream_t s);
 
