@@ -22,7 +22,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libmgrx.so")
+_LIB_PATH = os.environ.get("MGRX_LIB") or os.path.join(_HERE, "libmgrx.so")
 _GEN_PATH = os.path.join(_HERE, "libmgrx_problems.so")
 
 OK, NOT_CONVERGED, INVALID_ARGUMENT, RUNTIME = 0, 1, 2, 3

@@ -22,7 +22,10 @@ namespace {
 constexpr int kGsThreads = 128;
 constexpr int kGsCap = 4096;  // sweep-CSR entries staged in shared memory per CTA
 constexpr size_t kGsSmem = kGsCap * (2 * sizeof(double) + sizeof(int));
-constexpr int kPoll = 8;       // entries polled per lane per round
+#ifndef MGRX_KPOLL
+#define MGRX_KPOLL 8
+#endif
+constexpr int kPoll = MGRX_KPOLL;  // entries polled per lane per round
 constexpr long long kSpinLimit = 1LL << 24;
 constexpr int kDepBit = 1 << 31;
 

@@ -194,3 +194,54 @@ def test_sharded_path_device_backend_single_rank():
     x, rep = D.gmres(comm, be, A, M.apply, be.vec(P.rhs), be.zeros(P.n), restart=30, rel_tol=1e-6)
     _, rep2 = H.solve(P.rhs, cfg=mx.KrylovConfig(restart=30, rel_tol=1e-6))
     assert rep["converged"] and abs(rep["iterations"] - rep2.iterations) <= 1
+
+
+@pytest.mark.parametrize("mode", ["lv", "pipe"])
+def test_alternative_gs_sweeps_are_bit_exact(mode):
+    """The level-synchronous cluster sweep and the pipelined single-CTA sweep
+    (MGRX_GS_MODE, read once per process) reproduce the oracle bitwise."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
+        "import paper_2101_11649_b200 as mx, refcpu;"
+        "P = mx.mfd_problem(20, 20, 10, 'iid'); t = mx.load_strategy('mfd_mgr_p');"
+        "H = mx.Hierarchy(mx.Matrix(P.ptr, P.col, P.val), P.partition, t);"
+        "R = refcpu.RefHierarchy(P.ptr, P.col, P.val, P.partition.field_order, P.partition.labels, t);"
+        "v = np.random.default_rng(1).uniform(-1, 1, P.n);"
+        "assert np.array_equal(H.apply(v).view(np.int64), R.apply(v).view(np.int64));"
+        "x, rep = H.solve(P.rhs, cfg=mx.KrylovConfig(restart=30, rel_tol=1e-6));"
+        "_, rr = R.solve(P.rhs, restart=30, rel_tol=1e-6);"
+        "assert rep.iterations == rr['iterations'] and rep.residual_history == rr['history'];"
+        "print('ok')")
+    root = make_golden.ROOT
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                         env={**__import__("os").environ, "MGRX_GS_MODE": mode}, timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+def test_edge_cases():
+    # 1x1 system, coarse dense LU only
+    H = mx.Hierarchy(mx.Matrix(np.array([0, 1], np.int32), np.array([0], np.int32), np.array([4.0])),
+                     mx.DofPartition(["x"], np.zeros(1, np.int32)), json.dumps({"coarse": {"kind": "dense_lu"}}))
+    x, rep = H.solve(np.array([2.0]), cfg=mx.KrylovConfig(rel_tol=1e-12))
+    assert rep.converged and x[0] == 0.5
+    # a row without a stored diagonal in A_FF: "missing diagonal entry at row k"
+    ptr = np.array([0, 1, 3, 4], np.int32)
+    col = np.array([1, 0, 1, 2], np.int32)
+    with pytest.raises(mx.MgrxError, match="missing diagonal entry at row 0"):
+        mx.Hierarchy(mx.Matrix(ptr, col, np.ones(4)), mx.DofPartition(["a", "b"], np.array([0, 0, 1], np.int32)),
+                     json.dumps({"levels": [{"f_fields": ["a"]}], "coarse": {"kind": "dense_lu"}}))
+    # validation errors of the CSR boundary (proj/src/sparse.cpp:24-41)
+    with pytest.raises(mx.MgrxError, match="column index out of range in row 1"):
+        mx.Matrix(np.array([0, 1, 2], np.int32), np.array([0, 5], np.int32), np.ones(2))
+    with pytest.raises(mx.MgrxError, match="non-finite value stored in row 0"):
+        mx.Matrix(np.array([0, 1, 2], np.int32), np.array([0, 1], np.int32), np.array([np.inf, 1.0]))
+    # rectangular SpMV with empty rows
+    M = mx.Matrix(np.array([0, 0, 2, 2], np.int32), np.array([1, 4], np.int32), np.array([2.0, 3.0]), shape=(3, 5))
+    y = M.spmv(np.arange(5, dtype=np.float64))
+    assert list(y) == [0.0, 14.0, 0.0]
+    # singular coarse matrix -> dense LU pivot error
+    with pytest.raises(mx.MgrxError, match="numerically singular"):
+        mx.Hierarchy(mx.Matrix(np.array([0, 1, 2], np.int32), np.array([0, 1], np.int32), np.array([1.0, 0.0])),
+                     mx.DofPartition(["x"], np.zeros(2, np.int32)), json.dumps({"coarse": {"kind": "dense_lu"}}))
