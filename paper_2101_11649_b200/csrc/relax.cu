@@ -448,14 +448,102 @@ __global__ void k_gather_d(int n, const int* __restrict__ idx, const double* __r
   if (i < n) y[i] = x[idx[i]];
 }
 
-std::vector<int> pipe_steps(const std::vector<int>& level_ptr, const std::vector<int>& sptr) {
+// Small-level variant: the whole iterate x lives in shared memory (n <=
+// kSmallN), so a dependency level costs shared-memory latency plus one
+// barrier — no L2 round trip on the critical path. Row data streams through
+// two cp.async buffers exactly as in k_gs_pipe. This is what the coarse AMG
+// levels use (their dependency chains are long: 343 / 160 / 59 levels at cfg2).
+constexpr int kSmallN = 12288;
+constexpr int kSmallRows = 512;
+constexpr int kSmallEnt = 2048;
+struct SmallBuf {
+  double sd[kSmallRows];
+  double bp[kSmallRows];
+  double val[kSmallEnt];
+  int ord[kSmallRows];
+  int ptr[kSmallRows + 1];
+  int col[kSmallEnt];
+};
+constexpr size_t kSmallSmem = 2 * sizeof(SmallBuf) + kSmallN * sizeof(double);
+
+template <bool kFull>
+__global__ void __launch_bounds__(kPipeThreads)
+    k_gs_small(int nsteps, const int* __restrict__ steps, const int* __restrict__ order,
+               const int* __restrict__ sptr, const int* __restrict__ scol, const double* __restrict__ sval,
+               const double* __restrict__ sd, const double* __restrict__ bp, const double* __restrict__ xold,
+               double* xnew, double* zadd) {
+  extern __shared__ __align__(16) unsigned char small_raw[];
+  SmallBuf* buf = reinterpret_cast<SmallBuf*>(small_raw);
+  double* xs = reinterpret_cast<double*>(small_raw + 2 * sizeof(SmallBuf));
+  const int tid = threadIdx.x;
+  __shared__ int stp[kPipeMaxSteps + 1], ste[kPipeMaxSteps + 1];
+  const bool st_smem = nsteps <= kPipeMaxSteps;
+  if (st_smem)
+    for (int q = tid; q <= nsteps; q += kPipeThreads) {
+      stp[q] = steps[q];
+      ste[q] = steps[nsteps + 1 + q];
+    }
+  __syncthreads();
+  auto SP = [&](int q) { return st_smem ? stp[q] : steps[q]; };
+  auto SE = [&](int q) { return st_smem ? ste[q] : steps[nsteps + 1 + q]; };
+  auto issue = [&](int st, SmallBuf& B) {
+    const int p0 = SP(st), p1 = SP(st + 1);
+    const int nr = p1 - p0;
+    const int e0 = SE(st), e1 = SE(st + 1);
+    for (int q = tid; q < nr; q += kPipeThreads) {
+      cpa4(&B.ord[q], order + p0 + q);
+      cpa8(&B.sd[q], sd + p0 + q);
+      cpa8(&B.bp[q], bp + p0 + q);
+    }
+    for (int q = tid; q <= nr; q += kPipeThreads) cpa4(&B.ptr[q], sptr + p0 + q);
+    for (int q = tid; q < e1 - e0; q += kPipeThreads) {
+      cpa4(&B.col[q], scol + e0 + q);
+      cpa8(&B.val[q], sval + e0 + q);
+    }
+    cpa_commit();
+  };
+  issue(0, buf[0]);
+  for (int st = 0; st < nsteps; ++st) {
+    SmallBuf& B = buf[st & 1];
+    if (st + 1 < nsteps) issue(st + 1, buf[(st + 1) & 1]);
+    else cpa_commit();
+    cpa_wait1();
+    __syncthreads();
+    const int nr = SP(st + 1) - SP(st);
+    const int e0 = B.ptr[0];
+    for (int q = tid; q < nr; q += kPipeThreads) {
+      const int i = B.ord[q];
+      double s = B.bp[q];
+      const int k1 = B.ptr[q + 1] - e0;
+      for (int k = B.ptr[q] - e0; k < k1; ++k) {
+        int c = B.col[k];
+        double x;
+        if (kFull && !(c & kDepBit)) {
+          x = xold[c];
+        } else {
+          if (kFull) c &= ~kDepBit;
+          x = xs[c];
+        }
+        s = __dsub_rn(s, __dmul_rn(B.val[k], x));
+      }
+      const double v = __dadd_rn(kFull ? xold[i] : 0.0, __ddiv_rn(s, B.sd[q]));
+      xs[i] = v;
+      xnew[i] = v;
+      if (zadd) zadd[i] = __dadd_rn(zadd[i], v);
+    }
+    __syncthreads();
+  }
+}
+
+std::vector<int> pipe_steps(const std::vector<int>& level_ptr, const std::vector<int>& sptr,
+                            int rows_cap = kPipeRows, int ent_cap = kPipeEnt) {
   std::vector<int> st{0};
   for (size_t L = 0; L + 1 < level_ptr.size(); ++L) {
     int p = level_ptr[L];
     const int pe = level_ptr[L + 1];
     while (p < pe) {
       int q = p;
-      while (q < pe && q - p < kPipeRows && sptr[q + 1] - sptr[p] <= kPipeEnt) ++q;
+      while (q < pe && q - p < rows_cap && sptr[q + 1] - sptr[p] <= ent_cap) ++q;
       if (q == p) ++q;  // a single row longer than the buffer is never produced by the generators
       st.push_back(q);
       p = q;
@@ -669,6 +757,38 @@ void gs_schedule(const DCsr& A, bool forward, const double* d, bool full, GsSche
     out.cluster = 0;
   }
   out.pipe = 0;
+  out.small = 0;
+  if (n <= kSmallN && mode == 0) {
+    const std::vector<int> dp = out.dptr.download(n + 1);
+    bool ok = true;
+    for (int q = 0; q < n && ok; ++q) ok = dp[q + 1] - dp[q] <= kSmallEnt;
+    std::vector<int> fp;
+    if (ok && full) {
+      fp = out.fptr.download(n + 1);
+      for (int q = 0; q < n && ok; ++q) ok = fp[q + 1] - fp[q] <= kSmallEnt;
+    }
+    if (ok) {
+      auto with_offsets = [](const std::vector<int>& st, const std::vector<int>& ptr) {
+        std::vector<int> v(st);
+        for (int q : st) v.push_back(ptr[q]);
+        return v;
+      };
+      const std::vector<int> st = pipe_steps(out.level_ptr, dp, kSmallRows, kSmallEnt);
+      out.ndsteps = static_cast<int>(st.size()) - 1;
+      const std::vector<int> stv = with_offsets(st, dp);
+      out.dsteps.alloc(stv.size(), s);
+      out.dsteps.upload(stv.data(), stv.size());
+      if (full) {
+        const std::vector<int> st2 = pipe_steps(out.level_ptr, fp, kSmallRows, kSmallEnt);
+        out.nfsteps = static_cast<int>(st2.size()) - 1;
+        const std::vector<int> stv2 = with_offsets(st2, fp);
+        out.fsteps.alloc(stv2.size(), s);
+        out.fsteps.upload(stv2.data(), stv2.size());
+      }
+      out.bp.alloc(n, s);
+      out.small = 1;
+    }
+  }
   if (mode == 2) {
     const std::vector<int> dp = out.dptr.download(n + 1);
     bool ok = true;
@@ -712,6 +832,21 @@ void gs_sweep(const DCsr& A, const GsSchedule& sch, const double* d, const doubl
   if (scr.ticket_err.size() < 2) throw RuntimeError("gs_sweep: scratch not bound");
   const bool full_sweep = xold != nullptr;
   if (full_sweep && !sch.has_full) throw RuntimeError("gs_sweep: schedule built without the full sweep CSR");
+  if (sch.small) {
+    k_gather_d<<<blocks_for(n, 256), 256, 0, s>>>(n, sch.order.get(), b, const_cast<double*>(sch.bp.get()));
+    const int* sp = full_sweep ? sch.fptr.get() : sch.dptr.get();
+    const int* sc = full_sweep ? sch.fcol.get() : sch.dcol.get();
+    const double* sv = full_sweep ? sch.fval.get() : sch.dval.get();
+    if (full_sweep)
+      k_gs_small<true><<<1, kPipeThreads, kSmallSmem, s>>>(sch.nfsteps, sch.fsteps.get(), sch.order.get(), sp, sc,
+                                                           sv, sch.sd.get(), sch.bp.get(), xold, xnew, zadd);
+    else
+      k_gs_small<false><<<1, kPipeThreads, kSmallSmem, s>>>(sch.ndsteps, sch.dsteps.get(), sch.order.get(), sp,
+                                                            sc, sv, sch.sd.get(), sch.bp.get(), xold, xnew, zadd);
+    MGRX_LAUNCH_CK();
+    count_launch(2);
+    return;
+  }
   if (sch.pipe) {
     k_gather_d<<<blocks_for(n, 256), 256, 0, s>>>(n, sch.order.get(), b, const_cast<double*>(sch.bp.get()));
     const int* sp = full_sweep ? sch.fptr.get() : sch.dptr.get();
@@ -808,6 +943,8 @@ void gs_sweep(const DCsr& A, const GsSchedule& sch, const double* d, const doubl
 
 void gs_bind_scratch(GsScratch& scr, cudaStream_t s) {
   static const bool attrs = [] {
+    MGRX_CK(cudaFuncSetAttribute(k_gs_small<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmallSmem)));
+    MGRX_CK(cudaFuncSetAttribute(k_gs_small<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmallSmem)));
     MGRX_CK(cudaFuncSetAttribute(k_gs_pipe<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kPipeSmem)));
     MGRX_CK(cudaFuncSetAttribute(k_gs_pipe<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kPipeSmem)));
     MGRX_CK(cudaFuncSetAttribute(k_gs_lv<false, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));

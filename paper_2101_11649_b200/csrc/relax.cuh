@@ -32,6 +32,7 @@ struct GsSchedule {
   int cluster = 0;                 // >0: level-synchronous sweep in one cluster of this size
   DVec<int> dlptr;                 // device copy of level_ptr
   int pipe = 0;                    // 1: pipelined single-CTA level sweep
+  int small = 0;                   // 1: single-CTA sweep with x in shared memory (n <= 12288)
   DVec<int> dsteps, fsteps;        // step boundaries (positions) for the pipelined sweep
   int ndsteps = 0, nfsteps = 0;
   DVec<double> bp;                 // rhs gathered into sweep order (pipelined sweep)

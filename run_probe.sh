@@ -1,5 +1,5 @@
 #!/bin/bash
 mkdir -p gpurun_out
-TAG=kpoll8 python tools/probe_gs.py > gpurun_out/probe_trace.log 2>&1
-for kp in 1 2; do MGRX_LIB=paper_2101_11649_b200/build/libmgrx_kpoll$kp.so TAG=kpoll$kp python tools/probe_gs.py >> gpurun_out/probe_trace.log 2>&1; done
+TAG=small python tools/probe_gs.py > gpurun_out/probe_trace.log 2>&1
+timeout 600 python -m pytest tests -q -m gpu -x -k "bit_exact or solve_parity or apply or cfg1 or alternative or edge" >> gpurun_out/probe_trace.log 2>&1
 echo done
