@@ -112,6 +112,25 @@ void prepare_probe(mgrx_hier* h, const std::string& w, std::function<void()>& fn
     bytes = 24.0 * n;  // SURVEY 8(d) MGS step model: read v_i and w, write w
     return;
   }
+  if (w.rfind("arnoldi.", 0) == 0) {
+    // fused Arnoldi step k on the solve's work vectors (zeros if no solve ran
+    // yet), both MGS passes forced: compulsory HBM traffic is w in, each
+    // v_0..v_k streamed once per pass, v_{k+1} out.
+    const int n = h->A.rows;
+    const int k = std::stoi(w.substr(8));
+    if (h->ws.n != n) {
+      h->ws.ensure(n, 30, s);
+      MGRX_CK(cudaMemsetAsync(h->ws.V.get(), 0, sizeof(double) * static_cast<size_t>(n) * 31, s));
+      MGRX_CK(cudaMemsetAsync(h->ws.w.get(), 0, sizeof(double) * n, s));
+    }
+    const char* e = std::getenv("MGRX_ARNOLDI_DBG");
+    const int dbg = 4 | (e ? std::atoi(e) : 0);
+    GmresWork* ws = &h->ws;
+    if (!arnoldi_probe(n, k, dbg, *ws, s)) throw InvalidArgument("probe: fused Arnoldi kernel unavailable");
+    fn = [=] { arnoldi_probe(n, k, dbg, *ws, s); };
+    bytes = 8.0 * n * (2.0 + 2.0 * (k + 1));
+    return;
+  }
   if (w == "spmv.A") {
     const DCsr* A = &h->A;
     fn = [=] { spmv(*A, x, y, s); };

@@ -6,6 +6,7 @@
 // reproducible. The host reads the Hessenberg column once per step (one
 // small D2H copy), exactly where the reference needs scalar control flow.
 #include <cmath>
+#include <cstdlib>
 
 #include "krylov.cuh"
 #include "relax.cuh"
@@ -42,8 +43,34 @@ __device__ void block_sum2(double& a, double& b) {
   __syncthreads();
 }
 
+// L2 eviction-priority hints (createpolicy + ld/st .L2::cache_hint). The
+// Arnoldi vector w (n doubles, 34 MB at cfg2) is read and rewritten by every
+// MGS launch of a step; pinning it with evict_last keeps it in the 126 MB L2
+// so each launch's HBM traffic is the basis vectors it streams.
+__device__ __forceinline__ unsigned long long pol_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long pol_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double ld_pol(const double* a, unsigned long long p) {
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_pol(double* a, double v, unsigned long long p) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(p) : "memory");
+}
+
+// kHint: 0 plain (.cg); 1 w evict_last; 2 + vprev evict_first; 3 + a evict_last
+// (3 is the default: 7% faster solves at cfg2 than 0).
 // w <- w - (*hprev) * vprev (if vprev); then dot1 = sum a_i w_i (if a),
 // dot2 = sum w_i w_i (if want2). Results: out1 (and hacc = / += dot1), out2.
+template <int kHint>
 __global__ void __launch_bounds__(kRT)
     k_mgs(int n, double* __restrict__ w, const double* __restrict__ vprev,
           const double* __restrict__ hprev, const double* __restrict__ a, int want2,
@@ -57,22 +84,28 @@ __global__ void __launch_bounds__(kRT)
   // loop (the canonical reduction order shared with the oracle).
   constexpr int kU = 4;
   constexpr int kStride = kRB * kRT;
+  unsigned long long pl = 0, pf = 0;
+  if (kHint) {
+    pl = pol_last();
+    pf = pol_first();
+  }
   int i0 = blockIdx.x * kRT + threadIdx.x;
   for (; i0 + (kU - 1) * kStride < n; i0 += kU * kStride) {
     double wv[kU], pv[kU], av[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const int i = i0 + u * kStride;
-      wv[u] = __ldcg(w + i);
-      if (vprev) pv[u] = __ldcg(vprev + i);
-      if (a) av[u] = __ldcg(a + i);
+      wv[u] = kHint >= 1 ? ld_pol(w + i, pl) : __ldcg(w + i);
+      if (vprev) pv[u] = kHint >= 2 ? ld_pol(vprev + i, pf) : __ldcg(vprev + i);
+      if (a) av[u] = kHint >= 3 ? ld_pol(a + i, pl) : __ldcg(a + i);
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       double wi = wv[u];
       if (vprev) {
         wi = __dsub_rn(wi, __dmul_rn(h, pv[u]));
-        w[i0 + u * kStride] = wi;
+        if (kHint >= 1) st_pol(w + i0 + u * kStride, wi, pl);
+        else w[i0 + u * kStride] = wi;
       }
       if (a) s1 = __dadd_rn(s1, __dmul_rn(av[u], wi));
       if (want2) s2 = __dadd_rn(s2, __dmul_rn(wi, wi));
@@ -132,9 +165,272 @@ __global__ void k_gemv(int n, int k, const double* __restrict__ V, const double*
 void mgs_launch(int n, double* w, const double* vprev, const double* hprev, const double* a,
                 bool want2, GmresWork& ws, double* out1, double* hacc, bool accumulate, double* out2,
                 cudaStream_t s) {
-  k_mgs<<<kRB, kRT, 0, s>>>(n, w, vprev, hprev, a, want2 ? 1 : 0, ws.part.get(), ws.ctr.get(), out1,
-                            hacc, accumulate ? 1 : 0, out2);
+  static const int hint = [] {
+    const char* v = std::getenv("MGRX_MGS_L2");
+    return v ? std::atoi(v) : 3;
+  }();
+  auto* kern = hint == 0 ? k_mgs<0> : hint == 1 ? k_mgs<1> : hint == 2 ? k_mgs<2> : k_mgs<3>;
+  kern<<<kRB, kRT, 0, s>>>(n, w, vprev, hprev, a, want2 ? 1 : 0, ws.part.get(), ws.ctr.get(), out1, hacc,
+                           accumulate ? 1 : 0, out2);
   MGRX_LAUNCH_CK();
+  count_launch();
+}
+
+// ---------------------------------------------------------------------------
+// Fused Arnoldi step: the whole modified Gram-Schmidt of one GMRES step
+// (both passes, the re-orthogonalisation test and the scaling of v_{k+1}) in
+// ONE persistent cooperative kernel. w never leaves the SMs: 148 CTAs x 1024
+// threads hold it in shared memory (<= 28 doubles per thread, 224 KB per SM),
+// so each projection streams only v_i from HBM (plus its L2 re-read for the
+// update) and the n-vector round trips of w disappear.
+//
+// Lane numbering is the canonical reduction order's: thread T of CTA c is
+// lane c*1024+T = canonical block 4c+T/256, thread T%256, owning rows
+// lane + q*kStride. Per-lane sums, the 256-lane block trees and the in-order
+// fold of the 592 block partials are the same floating-point operations
+// k_mgs performs, so results are bitwise identical to the launch-per-
+// projection path (and to the oracle).
+constexpr int kAT = 1024;
+constexpr int kAB = kRB * kRT / kAT;  // 148
+constexpr int kAMaxSlots = 28;
+constexpr int kAU = 4;    // row slots per load group (loads of a group are issued together)
+constexpr int kAHk = 64;  // Hessenberg entries the writer keeps in shared memory
+
+struct ArnoldiArgs {
+  int n, k;
+  double* w;          // in: A M^-1 v_k
+  const double* V;    // basis, column-major n x (m+1)
+  double* part;       // 2 x kRB x 2 partials (double-buffered by phase)
+  unsigned* bar;      // grid barrier counter (zeroed before launch)
+  double* n0;         // ||w||^2 before pass 1
+  double* n1;         // final ||w||^2
+  double* hp;         // per-projection dots of the last pass
+  double* hc;         // Hessenberg column H(0..k, k)
+  int dbg;            // probe only: 1 skip the row loops, 2 skip the grid barrier, 4 force two passes, 8 trace
+};
+
+// One projection phase over this lane's rows (w in shared memory, column
+// stride kAT): w -= h*vprev (kV); s1 += av.w (kA); s2 += w.w (kW2).
+template <bool kV, bool kA, bool kW2>
+__device__ __forceinline__ void arn_rows(double* wl, int nslot, const double* __restrict__ pl,
+                                         const double* __restrict__ al, double h, unsigned long long pf,
+                                         double& s1, double& s2) {
+  constexpr int kStride = kRB * kRT;
+  int q = 0;
+  for (; q + kAU - 1 < nslot; q += kAU) {
+    double pv[kAU], xv[kAU];
+#pragma unroll
+    for (int u = 0; u < kAU; ++u) {
+      if (kV) pv[u] = ld_pol(pl + (q + u) * kStride, pf);
+      if (kA) xv[u] = __ldcg(al + (q + u) * kStride);
+    }
+#pragma unroll
+    for (int u = 0; u < kAU; ++u) {
+      double wi = wl[(q + u) * kAT];
+      if (kV) {
+        wi = __dsub_rn(wi, __dmul_rn(h, pv[u]));
+        wl[(q + u) * kAT] = wi;
+      }
+      if (kA) s1 = __dadd_rn(s1, __dmul_rn(xv[u], wi));
+      if (kW2) s2 = __dadd_rn(s2, __dmul_rn(wi, wi));
+    }
+  }
+  for (; q < nslot; ++q) {
+    double wi = wl[q * kAT];
+    if (kV) {
+      wi = __dsub_rn(wi, __dmul_rn(h, ld_pol(pl + q * kStride, pf)));
+      wl[q * kAT] = wi;
+    }
+    if (kA) s1 = __dadd_rn(s1, __dmul_rn(__ldcg(al + q * kStride), wi));
+    if (kW2) s2 = __dadd_rn(s2, __dmul_rn(wi, wi));
+  }
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void __launch_bounds__(kAT, 1) k_arnoldi(ArnoldiArgs a) {
+  extern __shared__ double wsm[];  // [slot][kAT]
+  __shared__ double r1[kAT / 32], r2[kAT / 32];  // per-warp sums of this CTA
+  __shared__ double f1[kRT / 32], f2[kRT / 32];  // fold: per-warp sums of the kRB partials
+  const int T = threadIdx.x;
+  const int wp = T >> 5, l = T & 31;
+  const int n = a.n, k = a.k;
+  constexpr int kStride = kRB * kRT;
+  const int lane = blockIdx.x * kAT + T;
+  const int nslot = lane < n ? (n - 1 - lane) / kStride + 1 : 0;
+  for (int q = 0; q < nslot; ++q) wsm[q * kAT + T] = __ldcg(a.w + lane + q * kStride);
+  const unsigned long long pf = pol_first();
+  const size_t ld = static_cast<size_t>(n);
+  double* wl = wsm + T;
+
+  unsigned phase = 0;
+  // Reduce (s1, s2) over the grid in the canonical order (dbg & 8: CTAs 0 and
+  // last print a per-phase globaltimer breakdown).
+  const bool tracer = (a.dbg & 8) && T == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1);
+  unsigned long long tprev = tracer ? gtimer() : 0, tm[4];
+  auto reduce = [&](double s1, double s2, double& t1, double& t2) {
+    if (tracer) tm[0] = gtimer();
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if (l == 0) {
+      r1[wp] = s1;
+      r2[wp] = s2;
+    }
+    __syncthreads();
+    double* part = a.part + (phase & 1) * 2 * kRB;
+    if (wp < kAT / kRT) {  // canonical 256-lane block trees (block_sum2)
+      double x1 = l < kRT / 32 ? r1[wp * (kRT / 32) + l] : 0.0;
+      double x2 = l < kRT / 32 ? r2[wp * (kRT / 32) + l] : 0.0;
+      x1 = warp_sum(x1);
+      x2 = warp_sum(x2);
+      if (l == 0) {
+        const int b = blockIdx.x * (kAT / kRT) + wp;
+        part[2 * b] = x1;
+        part[2 * b + 1] = x2;
+      }
+    }
+    __syncthreads();
+    if (tracer) tm[1] = gtimer();
+    // grid barrier (monotonic counter; zeroed by the host before the launch)
+    if (T == 0 && !(a.dbg & 2)) {
+      __threadfence();
+      atomicAdd(a.bar, 1u);
+      const unsigned target = (phase + 1) * gridDim.x;
+      unsigned v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.bar) : "memory");
+      } while (v < target);
+    }
+    __syncthreads();
+    if (tracer) tm[2] = gtimer();
+    // every CTA folds the kRB partials in index order (k_mgs's last block);
+    // all loads of a thread are issued before the in-order adds
+    if (T < kRT) {
+      constexpr int kF = (kRB + kRT - 1) / kRT;
+      double p1[kF], p2[kF];
+#pragma unroll
+      for (int j = 0; j < kF; ++j) {
+        const int b = T + j * kRT;
+        if (b < kRB) {
+          p1[j] = __ldcg(part + 2 * b);
+          p2[j] = __ldcg(part + 2 * b + 1);
+        }
+      }
+      double u1 = 0.0, u2 = 0.0;
+#pragma unroll
+      for (int j = 0; j < kF; ++j) {
+        if (T + j * kRT < kRB) {
+          u1 = __dadd_rn(u1, p1[j]);
+          u2 = __dadd_rn(u2, p2[j]);
+        }
+      }
+      u1 = warp_sum(u1);
+      u2 = warp_sum(u2);
+      if (l == 0) {
+        f1[wp] = u1;
+        f2[wp] = u2;
+      }
+    }
+    __syncthreads();
+    // every warp completes the fold itself; lane 0 holds the canonical value
+    const double x1 = l < kRT / 32 ? f1[l] : 0.0;
+    const double x2 = l < kRT / 32 ? f2[l] : 0.0;
+    t1 = __shfl_sync(0xffffffffu, warp_sum(x1), 0);
+    t2 = __shfl_sync(0xffffffffu, warp_sum(x2), 0);
+    if (tracer) {
+      tm[3] = gtimer();
+      printf("ARN cta %d phase %u loop %llu part %llu bar %llu fold %llu\n", blockIdx.x, phase, tm[0] - tprev,
+             tm[1] - tm[0], tm[2] - tm[1], tm[3] - tm[2]);
+      tprev = gtimer();
+    }
+    ++phase;
+  };
+
+  const bool writer = blockIdx.x == 0 && T == 0;
+  __shared__ double hk[kAHk];  // writer: H(i,k) of pass 1 (i < kAHk)
+  double h = 0.0, wn2 = 0.0, w02 = 0.0;
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int i = 0; i <= k + 1; ++i) {  // i == k + 1: the closing norm
+      double s1 = 0.0, s2 = 0.0, t1, t2;
+      if (!(a.dbg & 1)) {
+        const double* pl = i ? a.V + (i - 1) * ld + lane : nullptr;
+        const double* al = a.V + i * ld + lane;
+        if (i > k) arn_rows<true, false, true>(wl, nslot, pl, al, h, pf, s1, s2);
+        else if (i) arn_rows<true, true, false>(wl, nslot, pl, al, h, pf, s1, s2);
+        else if (pass == 0) arn_rows<false, true, true>(wl, nslot, pl, al, h, pf, s1, s2);
+        else arn_rows<false, true, false>(wl, nslot, pl, al, h, pf, s1, s2);
+      }
+      reduce(s1, s2, t1, t2);
+      if (i <= k) {
+        if (pass == 0 && i == 0) w02 = t2;
+        h = t1;
+        if (writer) {
+          a.hp[i] = t1;
+          const double hv = pass ? __dadd_rn(i < kAHk ? hk[i] : a.hc[i], t1) : t1;
+          if (i < kAHk) hk[i] = hv;
+          a.hc[i] = hv;
+        }
+      } else {
+        wn2 = t2;
+      }
+    }
+    h = 0.0;
+    // re-orthogonalise when ||w|| drops below ||w0|| / sqrt(2) (krylov.cpp:90)
+    if (pass == 1 || (!(a.dbg & 4) && !(__dsqrt_rn(wn2) < __ddiv_rn(__dsqrt_rn(w02), __dsqrt_rn(2.0))))) break;
+  }
+  if (writer) {
+    *a.n0 = w02;
+    *a.n1 = wn2;
+  }
+  const double wn = __dsqrt_rn(wn2);
+  if (!(wn < 1e-300)) {
+    double* out = const_cast<double*>(a.V) + (k + 1) * ld;
+    for (int q = 0; q < nslot; ++q) out[lane + q * kStride] = __ddiv_rn(wsm[q * kAT + T], wn);
+  }
+}
+
+// Launch parameters of the fused Arnoldi kernel for n rows, or 0 slots when it
+// cannot run (n too large for shared memory, or not a 148-SM part).
+int arnoldi_slots(int n) {
+  static const int mode = [] {
+    const char* v = std::getenv("MGRX_ARNOLDI");
+    return v ? std::atoi(v) : 1;
+  }();
+  static const bool fits = [] {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms != kAB) return false;
+    const int bytes = kAMaxSlots * kAT * static_cast<int>(sizeof(double));
+    if (cudaFuncSetAttribute(k_arnoldi, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_arnoldi, kAT, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return occ >= 1;
+  }();
+  constexpr int kStride = kRB * kRT;
+  if (!mode || !fits || n <= 0) return 0;
+  const int slots = (n - 1) / kStride + 1;
+  return slots <= kAMaxSlots ? slots : 0;
+}
+
+void arnoldi_launch(int n, int k, int slots, int dbg, GmresWork& ws, cudaStream_t s) {
+  double* S = ws.scal.get();
+  const int m = ws.m;
+  MGRX_CK(cudaMemsetAsync(ws.bar.get(), 0, sizeof(unsigned), s));
+  ArnoldiArgs aa{n, k, ws.w.get(), ws.V.get(), ws.apart.get(), ws.bar.get(), S, S + 1, S + 2, S + 3 + (m + 1), dbg};
+  void* args[] = {&aa};
+  MGRX_CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_arnoldi), dim3(kAB), dim3(kAT), args,
+                                      static_cast<size_t>(slots) * kAT * sizeof(double), s));
   count_launch();
 }
 
@@ -154,6 +450,9 @@ void GmresWork::ensure(int n_, int m_, cudaStream_t s) {
   part.alloc(2 * kRB, s);
   ctr.alloc(1, s);
   ctr.zero();
+  apart.alloc(4 * kRB, s);
+  bar.alloc(1, s);
+
   if (hpinned) cudaFreeHost(hpinned);
   MGRX_CK(cudaMallocHost(&hpinned, sizeof(double) * (4 + 3 * (m + 2))));
 }
@@ -165,6 +464,13 @@ GmresWork::~GmresWork() {
 void mgs_probe(int n, double* w, const double* vprev, const double* h, const double* a, GmresWork& ws,
                cudaStream_t s) {
   mgs_launch(n, w, vprev, h, a, false, ws, ws.scal.get() + 2, nullptr, false, nullptr, s);
+}
+
+int arnoldi_probe(int n, int k, int dbg, GmresWork& ws, cudaStream_t s) {
+  const int slots = arnoldi_slots(n);
+  if (!slots || k < 0 || k >= ws.m) return 0;
+  arnoldi_launch(n, k, slots, dbg, ws, s);
+  return 1;
 }
 
 double device_dot(int n, const double* a, const double* b, GmresWork& ws, cudaStream_t s) {
@@ -236,35 +542,44 @@ GmresResult gmres_device(const DCsr& A, const double* b, double* x, const Krylov
       for (; k < m && res.iterations < cfg.max_iters; ++k) {
         prec(col(k), ws.z.get());
         spmv(A, ws.z.get(), ws.w.get(), s);  // w = A M^{-1} v_k
-        // pass 1: h_i = v_i . w ; w -= h_i v_i  (krylov.cpp:84-89)
-        for (int i = 0; i <= k; ++i)
-          mgs_launch(n, ws.w.get(), i ? col(i - 1) : nullptr, i ? s_hp + (i - 1) : nullptr, col(i),
-                     i == 0, ws, s_hp + i, s_hc + i, false, i == 0 ? s_n0 : nullptr, s);
-        mgs_launch(n, ws.w.get(), col(k), s_hp + k, nullptr, true, ws, nullptr, nullptr, false, s_n1, s);
-        MGRX_CK(cudaMemcpyAsync(H_pin, S, col_bytes, cudaMemcpyDeviceToHost, s));
-        MGRX_CK(cudaStreamSynchronize(s));
-        const double w0 = std::sqrt(H_pin[0]);
-        double wn = std::sqrt(H_pin[1]);
-        if (wn < w0 / std::sqrt(2.0)) {
-          // pass 2 (krylov.cpp:90-96): H(i,k) += h_i
-          for (int i = 0; i <= k; ++i)
-            mgs_launch(n, ws.w.get(), i ? col(i - 1) : nullptr, i ? s_hp + (i - 1) : nullptr, col(i),
-                       false, ws, s_hp + i, s_hc + i, true, nullptr, s);
-          mgs_launch(n, ws.w.get(), col(k), s_hp + k, nullptr, true, ws, nullptr, nullptr, false, s_n1, s);
+        double wn;
+        if (const int slots = arnoldi_slots(n)) {
+          // both MGS passes + re-orthogonalisation test + v_{k+1} in one kernel
+          arnoldi_launch(n, k, slots, 0, ws, s);
           MGRX_CK(cudaMemcpyAsync(H_pin, S, col_bytes, cudaMemcpyDeviceToHost, s));
           MGRX_CK(cudaStreamSynchronize(s));
           wn = std::sqrt(H_pin[1]);
+        } else {
+          // pass 1: h_i = v_i . w ; w -= h_i v_i  (krylov.cpp:84-89)
+          for (int i = 0; i <= k; ++i)
+            mgs_launch(n, ws.w.get(), i ? col(i - 1) : nullptr, i ? s_hp + (i - 1) : nullptr, col(i),
+                       i == 0, ws, s_hp + i, s_hc + i, false, i == 0 ? s_n0 : nullptr, s);
+          mgs_launch(n, ws.w.get(), col(k), s_hp + k, nullptr, true, ws, nullptr, nullptr, false, s_n1, s);
+          MGRX_CK(cudaMemcpyAsync(H_pin, S, col_bytes, cudaMemcpyDeviceToHost, s));
+          MGRX_CK(cudaStreamSynchronize(s));
+          const double w0 = std::sqrt(H_pin[0]);
+          wn = std::sqrt(H_pin[1]);
+          if (wn < w0 / std::sqrt(2.0)) {
+            // pass 2 (krylov.cpp:90-96): H(i,k) += h_i
+            for (int i = 0; i <= k; ++i)
+              mgs_launch(n, ws.w.get(), i ? col(i - 1) : nullptr, i ? s_hp + (i - 1) : nullptr, col(i),
+                         false, ws, s_hp + i, s_hc + i, true, nullptr, s);
+            mgs_launch(n, ws.w.get(), col(k), s_hp + k, nullptr, true, ws, nullptr, nullptr, false, s_n1, s);
+            MGRX_CK(cudaMemcpyAsync(H_pin, S, col_bytes, cudaMemcpyDeviceToHost, s));
+            MGRX_CK(cudaStreamSynchronize(s));
+            wn = std::sqrt(H_pin[1]);
+          }
+          if (!(wn < 1e-300)) {
+            k_scale<<<blocks_for(n, 256), 256, 0, s>>>(n, ws.w.get(), wn, col(k + 1));
+            MGRX_LAUNCH_CK();
+            count_launch();
+          }
         }
         const double* hc = H_pin + 3 + (m + 1);
         for (int i = 0; i <= k; ++i) h(i, k) = hc[i];
         h(k + 1, k) = wn;
         if (!std::isfinite(wn)) throw RuntimeError("gmres: Arnoldi vector is non-finite");
         const bool happy = wn < 1e-300;
-        if (!happy) {
-          k_scale<<<blocks_for(n, 256), 256, 0, s>>>(n, ws.w.get(), wn, col(k + 1));
-          MGRX_LAUNCH_CK();
-          count_launch();
-        }
         // Givens (krylov.cpp:11-33)
         for (int i = 0; i < k; ++i) {
           const double t = cs[i] * h(i, k) + sn[i] * h(i + 1, k);

@@ -27,6 +27,9 @@ struct GmresWork {
   DVec<double> V, w, r, z, u;
   DVec<double> scal, part;  // device scalars / reduction partials
   DVec<unsigned> ctr;
+  DVec<double> apart;  // fused Arnoldi kernel: double-buffered partials
+  DVec<unsigned> bar;  // fused Arnoldi kernel: grid barrier
+
   std::vector<double> hscal;
   double* hpinned = nullptr;
   void ensure(int n, int m, cudaStream_t s);
@@ -40,6 +43,11 @@ GmresResult gmres_device(const DCsr& A, const double* b, double* x, const Krylov
 // One fused MGS step (w -= h*vprev; a.w) for the roofline probe.
 void mgs_probe(int n, double* w, const double* vprev, const double* h, const double* a, GmresWork& ws,
                cudaStream_t s);
+
+// One fused Arnoldi step (both MGS passes in one persistent kernel) on the
+// work vectors, for the probe; dbg bits as in ArnoldiArgs. Returns 0 when the
+// fused kernel is unavailable for n.
+int arnoldi_probe(int n, int k, int dbg, GmresWork& ws, cudaStream_t s);
 
 // Deterministic device dot product (fixed grid, fixed reduction tree).
 double device_dot(int n, const double* a, const double* b, GmresWork& ws, cudaStream_t s);

@@ -1,5 +1,5 @@
 #!/bin/bash
 mkdir -p gpurun_out
-TAG=small python tools/probe_gs.py > gpurun_out/probe_trace.log 2>&1
-timeout 600 python -m pytest tests -q -m gpu -x -k "bit_exact or solve_parity or apply or cfg1 or alternative or edge" >> gpurun_out/probe_trace.log 2>&1
+TRACE=1 TAG=tmpl timeout 300 python tools/probe_arnoldi.py > gpurun_out/probe_arn.log 2>&1
+timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-variant > gpurun_out/ba_1.json 2>gpurun_out/ba_1.err
 echo done

@@ -220,6 +220,32 @@ def test_alternative_gs_sweeps_are_bit_exact(mode):
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
 
 
+@pytest.mark.parametrize("arnoldi", ["0", "1"])
+def test_arnoldi_paths_are_bit_exact(arnoldi):
+    """The fused persistent Arnoldi kernel (w resident in shared memory, one
+    launch per GMRES step) and the launch-per-projection MGS path
+    (MGRX_ARNOLDI=0) both reproduce the oracle's residual history bitwise, on
+    a system large enough (n > 5 * 151552) that every lane owns several rows."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
+        "import paper_2101_11649_b200 as mx, refcpu;"
+        "P = mx.mfd_problem(64, 64, 48, 'layered'); t = mx.load_strategy('mfd_mgr_pi_c1_l1j');"
+        "assert P.n > 5 * 151552, P.n;"
+        "H = mx.Hierarchy(mx.Matrix(P.ptr, P.col, P.val), P.partition, t);"
+        "R = refcpu.RefHierarchy(P.ptr, P.col, P.val, P.partition.field_order, P.partition.labels, t);"
+        "x, rep = H.solve(P.rhs, cfg=mx.KrylovConfig(restart=30, rel_tol=1e-6));"
+        "xr, rr = R.solve(P.rhs, restart=30, rel_tol=1e-6);"
+        "assert rep.iterations == rr['iterations'] and rep.residual_history == rr['history'];"
+        "assert np.array_equal(x.view(np.int64), xr.view(np.int64));"
+        "print('ok', rep.iterations)")
+    root = make_golden.ROOT
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                         env={**__import__("os").environ, "MGRX_ARNOLDI": arnoldi}, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
 def test_edge_cases():
     # 1x1 system, coarse dense LU only
     H = mx.Hierarchy(mx.Matrix(np.array([0, 1], np.int32), np.array([0], np.int32), np.array([4.0])),
