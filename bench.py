@@ -263,7 +263,7 @@ def main():
     peak, peak_kind = peaks()
     info = H.info()
     probes = {}
-    names = ["mgs", "spmv.A", "mgr.0.rres", "mgr.0.prolong"]
+    names = ["arnoldi.15", "mgs", "spmv.A", "mgr.0.rres", "mgr.0.prolong"]
     for k in range(max(info["coarse_amg_levels"] - 1, 0)):
         names += [f"amg.{k}.resid", f"amg.{k}.pre", f"amg.{k}.post"]
     for name in names:
@@ -272,12 +272,17 @@ def main():
             probes[name] = {"avg_ms": ms_k, "bytes": by, "GBps": by / (ms_k * 1e-3) / 1e9}
         except mx.MgrxError as e:
             probes[name] = {"error": str(e)}
-    # dominant kernel: the fused modified-Gram-Schmidt step (k_mgs) carries the
-    # largest share of solve time in the l1-Jacobi strategy (47% in the
-    # profiles/r01 launch list, the SpMV family k_spmv* next); for other
-    # strategies take the probe with the largest time.
+    # dominant kernel: the fused Arnoldi step (k_arnoldi: both MGS passes of one
+    # GMRES step in one persistent launch) carries the largest share of solve
+    # time in the l1-Jacobi strategy (~37% in the profiles/r01 launch list, the
+    # SpMV family k_spmv* next); arnoldi.15 is the step at the mean Krylov
+    # index of a 30-step restart cycle. For other strategies take the probe
+    # with the largest time.
     share = {k: v["avg_ms"] for k, v in probes.items() if "avg_ms" in v}
-    dom = "mgs" if "l1j" in STRATEGY else max((k for k in share), key=lambda k: share[k])
+    if "l1j" in STRATEGY:
+        dom = "arnoldi.15" if "avg_ms" in probes.get("arnoldi.15", {}) else "mgs"
+    else:
+        dom = max((k for k in share), key=lambda k: share[k])
     d = probes[dom]
     traffic = None
     try:

@@ -110,6 +110,63 @@ __global__ void __launch_bounds__(kT) k_lu_solve(int n, const double* __restrict
   for (int i = threadIdx.x; i < n; i += kT) x[i] = xs[i];
 }
 
+// Small systems (n <= 160, the usual coarsest AMG level): one warp, the
+// factors staged in shared memory, lane l owning x_{l+32r} in registers, and
+// the same update order as k_lu_solve (so results are bitwise identical) with
+// warp shuffles in place of block barriers.
+constexpr int kWarpLuMax = 160;
+constexpr int kWarpLuR = (kWarpLuMax + 31) / 32;
+
+__global__ void __launch_bounds__(32) k_lu_solve_warp(int n, const double* __restrict__ M,
+                                                      const int* __restrict__ perm, const double* __restrict__ b,
+                                                      double* __restrict__ x) {
+  extern __shared__ double Ms[];
+  const int l = threadIdx.x;
+  for (int e = l; e < n * n; e += 32) Ms[e] = M[e];
+  double xr[kWarpLuR];
+#pragma unroll
+  for (int r = 0; r < kWarpLuR; ++r) {
+    const int i = l + 32 * r;
+    xr[r] = i < n ? b[perm[i]] : 0.0;
+  }
+  __syncwarp();
+  // j = 32*jr + jl; x_j lives in register jr of lane jl (static index)
+#pragma unroll
+  for (int jr = 0; jr < kWarpLuR; ++jr) {
+    for (int jl = 0; jl < 32; ++jl) {
+      const int j = 32 * jr + jl;
+      if (j >= n) break;
+      const double xj = __shfl_sync(0xffffffffu, xr[jr], jl);
+      const double* Mj = Ms + j * n;
+#pragma unroll
+      for (int r = 0; r < kWarpLuR; ++r) {
+        const int i = l + 32 * r;
+        if (i > j && i < n) xr[r] = __dsub_rn(xr[r], __dmul_rn(Mj[i], xj));
+      }
+    }
+  }
+#pragma unroll
+  for (int jr = kWarpLuR - 1; jr >= 0; --jr) {
+    for (int jl = 31; jl >= 0; --jl) {
+      const int j = 32 * jr + jl;
+      if (j >= n) continue;
+      const double* Mj = Ms + j * n;
+      if (l == jl) xr[jr] = __ddiv_rn(xr[jr], Mj[j]);
+      const double xj = __shfl_sync(0xffffffffu, xr[jr], jl);
+#pragma unroll
+      for (int r = 0; r < kWarpLuR; ++r) {
+        const int i = l + 32 * r;
+        if (i < j) xr[r] = __dsub_rn(xr[r], __dmul_rn(Mj[i], xj));
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < kWarpLuR; ++r) {
+    const int i = l + 32 * r;
+    if (i < n) x[i] = xr[r];
+  }
+}
+
 }  // namespace
 
 void dense_factor(const DCsr& A, DenseLU& out, cudaStream_t s, double pivot_tol) {
@@ -126,6 +183,11 @@ void dense_factor(const DCsr& A, DenseLU& out, cudaStream_t s, double pivot_tol)
   k_lu<<<1, kT, 0, s>>>(n, out.lu.get(), out.perm.get(), pivot_tol, bad.get());
   MGRX_LAUNCH_CK();
   count_launch(2);
+  if (n <= kWarpLuMax) {
+    const int smw = static_cast<int>(sizeof(double) * n * n);
+    if (smw > 48 * 1024)
+      MGRX_CK(cudaFuncSetAttribute(k_lu_solve_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, smw));
+  }
   const size_t sm = sizeof(double) * n;
   if (sm > 200 * 1024) throw RuntimeError("dense LU solve: system too large for shared memory");
   if (sm > 48 * 1024)
@@ -136,6 +198,12 @@ void dense_factor(const DCsr& A, DenseLU& out, cudaStream_t s, double pivot_tol)
 
 void dense_solve(const DenseLU& f, const double* b, double* x, cudaStream_t s) {
   if (f.n == 0) return;
+  if (f.n <= kWarpLuMax) {
+    k_lu_solve_warp<<<1, 32, sizeof(double) * f.n * f.n, s>>>(f.n, f.lu.get(), f.perm.get(), b, x);
+    MGRX_LAUNCH_CK();
+    count_launch();
+    return;
+  }
   const size_t sm = sizeof(double) * f.n;
   k_lu_solve<<<1, kT, sm, s>>>(f.n, f.lu.get(), f.perm.get(), b, x);
   MGRX_LAUNCH_CK();

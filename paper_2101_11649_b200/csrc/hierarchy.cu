@@ -251,18 +251,9 @@ void BoundRelax::apply(const double* r, const int* rrow, double* z, cudaStream_t
       dense_solve(lu, rc, z, st);
       return;
     case Smoother::jacobi:
-    case Smoother::l1_jacobi: {
-      // sweep 0: z = w*(dinv*r); later: z += w*(dinv*(r - A z)) (relax.cpp:168-174)
-      double* cur = z;
-      if (spec.sweeps > 1) cur = (spec.sweeps % 2 == 1) ? z : w1.get();
-      jacobi0(n, spec.weight, dinv.get(), rc, rrow, cur, st);
-      for (int sw = 1; sw < spec.sweeps; ++sw) {
-        double* nxt = (cur == z) ? w1.get() : z;
-        spmv_jacobi(*A, cur, rc, rrow, dinv.get(), spec.weight, nxt, st);
-        cur = nxt;
-      }
+    case Smoother::l1_jacobi:
+      jacobi_sweeps(rc, rrow, z, nullptr, st);
       return;
-    }
     case Smoother::hybrid_l1_gs_forward:
     case Smoother::hybrid_l1_gs_backward: {
       const bool fwd = spec.kind == Smoother::hybrid_l1_gs_forward;
@@ -290,8 +281,42 @@ void BoundRelax::apply(const double* r, const int* rrow, double* z, cudaStream_t
   }
 }
 
+constexpr int kFoldSweep0MaxRows = 65536;
+
+// sweep 0: z = w*(dinv*r); later: z += w*(dinv*(r - A z)) (relax.cpp:168-174).
+// Sweep 0 is folded into sweep 1 (its iterate is formed on the fly from r),
+// and with zacc the last sweep adds its result into zacc (apply_add).
+void BoundRelax::jacobi_sweeps(const double* rc, const int* rrow, double* z, double* zacc, cudaStream_t st) {
+  if (spec.sweeps <= 1) {
+    double* out = zacc ? w0.get() : z;
+    jacobi0(n, spec.weight, dinv.get(), rc, rrow, out, st);
+    if (zacc) vec_add(n, out, zacc, st);
+    return;
+  }
+  // Folding sweep 0 doubles the gathers per nonzero (dinv and r instead of
+  // z): a win only where launch latency dominates (measured at cfg2: levels of
+  // <= 64K rows faster, the 1M / 366K-row levels 15-20% slower).
+  const double* cur = nullptr;
+  double* bufs[2] = {w1.get(), w2.get()};
+  if (n > kFoldSweep0MaxRows) {
+    jacobi0(n, spec.weight, dinv.get(), rc, rrow, w2.get(), st);
+    cur = w2.get();
+    bufs[1] = w0.get();  // w2 holds sweep 0; w0 is free (no gather when jacobi)
+  }
+  for (int sw = 1; sw < spec.sweeps; ++sw) {
+    const bool last = sw == spec.sweeps - 1;
+    double* nxt = last ? (zacc ? nullptr : z) : bufs[sw % 2];
+    spmv_jacobi_ex(*A, cur, rc, rrow, dinv.get(), spec.weight, nxt, last ? zacc : nullptr, st);
+    cur = nxt;
+  }
+}
+
 void BoundRelax::apply_add(const double* r, double* zacc, cudaStream_t st) {
   if (n == 0) return;
+  if (spec.kind == Smoother::jacobi || spec.kind == Smoother::l1_jacobi) {
+    jacobi_sweeps(r, nullptr, nullptr, zacc, st);
+    return;
+  }
   if ((spec.kind == Smoother::hybrid_l1_gs_forward || spec.kind == Smoother::hybrid_l1_gs_backward) &&
       spec.sweeps == 1) {
     gs_sweep(*A, sched, l1d.get(), r, nullptr, w0.get(), zacc,

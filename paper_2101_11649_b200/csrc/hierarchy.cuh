@@ -37,6 +37,7 @@ struct BoundRelax {
   void apply(const double* r, const int* rrow, double* z, cudaStream_t st);
   // Same, but fused accumulate: zacc += smoother(r). r contiguous.
   void apply_add(const double* r, double* zacc, cudaStream_t st);
+  void jacobi_sweeps(const double* rc, const int* rrow, double* z, double* zacc, cudaStream_t st);
   void check(cudaStream_t st);
 };
 

@@ -214,11 +214,28 @@ namespace {
 // matrices still launch several waves of CTAs; each CTA stages 8 entries per
 // thread per chunk.
 
-template <int kRows, class Epi>
+// x sources: the vector itself, or the first Jacobi iterate w*(dinv*r)
+// formed on the fly (so the zero-start sweep needs no separate pass).
+struct XPlain {
+  const double* x;
+  __device__ __forceinline__ double operator()(int c) const { return __ldg(x + c); }
+};
+struct XJac0 {
+  double w;
+  const double* dinv;
+  const double* r;
+  const int* rrow;
+  __device__ __forceinline__ double operator()(int c) const {
+    const double rv = rrow ? __ldg(r + __ldg(rrow + c)) : __ldg(r + c);
+    return __dmul_rn(w, __dmul_rn(__ldg(dinv + c), rv));
+  }
+};
+
+template <int kRows, class Epi, class Xs>
 __global__ void __launch_bounds__(kRows) k_spmv(int rows, const int* __restrict__ ptr,
                                                 const int* __restrict__ col,
                                                 const double* __restrict__ val,
-                                                const double* __restrict__ x, Epi epi) {
+                                                Xs x, Epi epi) {
   constexpr int kCap = 8 * kRows;
   __shared__ double prod[kCap];
   const int r0 = blockIdx.x * kRows;
@@ -235,7 +252,7 @@ __global__ void __launch_bounds__(kRows) k_spmv(int rows, const int* __restrict_
     const int c1 = min(c0 + kCap, p1);
 #pragma unroll 4
     for (int q = c0 + threadIdx.x; q < c1; q += kRows)
-      prod[q - c0] = __dmul_rn(__ldcs(val + q), __ldg(x + __ldcs(col + q)));
+      prod[q - c0] = __dmul_rn(__ldcs(val + q), x(__ldcs(col + q)));
     __syncthreads();
     const int a = max(lo, c0), b = min(hi, c1);
     for (int q = a; q < b; ++q) sum = __dadd_rn(sum, prod[q - c0]);
@@ -250,11 +267,11 @@ __global__ void __launch_bounds__(kRows) k_spmv(int rows, const int* __restrict_
 // which keeps enough loads in flight when the matrix has few rows.
 constexpr int kWarps = 8;
 
-template <class Epi>
+template <class Epi, class Xs>
 __global__ void __launch_bounds__(kWarps * 32) k_spmv_wpr(int rows, const int* __restrict__ ptr,
                                                           const int* __restrict__ col,
                                                           const double* __restrict__ val,
-                                                          const double* __restrict__ x, Epi epi) {
+                                                          Xs x, Epi epi) {
   __shared__ double prod[kWarps][32];
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   for (int r = blockIdx.x * kWarps + w; r < rows; r += gridDim.x * kWarps) {
@@ -262,7 +279,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_spmv_wpr(int rows, const int* _
     double sum = 0.0;
     for (int c0 = lo; c0 < hi; c0 += 32) {
       const int q = c0 + l;
-      prod[w][l] = q < hi ? __dmul_rn(__ldg(val + q), __ldg(x + __ldg(col + q))) : 0.0;
+      prod[w][l] = q < hi ? __dmul_rn(__ldg(val + q), x(__ldg(col + q))) : 0.0;
       __syncwarp();
       if (l == 0) {
         const int m = min(32, hi - c0);
@@ -277,11 +294,11 @@ __global__ void __launch_bounds__(kWarps * 32) k_spmv_wpr(int rows, const int* _
 // Thread per row for very short rows (MGR prolongation: 1-2 entries per
 // row): no staging, every thread's few loads are independent, so the warp
 // keeps many requests in flight. Same sequential row sum.
-template <class Epi>
+template <class Epi, class Xs>
 __global__ void __launch_bounds__(256) k_spmv_tpr(int rows, const int* __restrict__ ptr,
                                                   const int* __restrict__ col,
                                                   const double* __restrict__ val,
-                                                  const double* __restrict__ x, Epi epi) {
+                                                  Xs x, Epi epi) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows) return;
   const int lo = __ldg(ptr + r), hi = __ldg(ptr + r + 1);
@@ -290,11 +307,11 @@ __global__ void __launch_bounds__(256) k_spmv_tpr(int rows, const int* __restric
   for (; k + 4 <= hi; k += 4) {
     const int c0 = __ldg(col + k), c1 = __ldg(col + k + 1), c2 = __ldg(col + k + 2), c3 = __ldg(col + k + 3);
     const double a0 = __ldg(val + k), a1 = __ldg(val + k + 1), a2 = __ldg(val + k + 2), a3 = __ldg(val + k + 3);
-    const double p0 = __dmul_rn(a0, __ldg(x + c0)), p1 = __dmul_rn(a1, __ldg(x + c1));
-    const double p2 = __dmul_rn(a2, __ldg(x + c2)), p3 = __dmul_rn(a3, __ldg(x + c3));
+    const double p0 = __dmul_rn(a0, x(c0)), p1 = __dmul_rn(a1, x(c1));
+    const double p2 = __dmul_rn(a2, x(c2)), p3 = __dmul_rn(a3, x(c3));
     sum = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(sum, p0), p1), p2), p3);
   }
-  for (; k < hi; ++k) sum = __dadd_rn(sum, __dmul_rn(__ldg(val + k), __ldg(x + __ldg(col + k))));
+  for (; k < hi; ++k) sum = __dadd_rn(sum, __dmul_rn(__ldg(val + k), x(__ldg(col + k))));
   epi(r, sum);
 }
 
@@ -339,8 +356,30 @@ struct EpiJacobi {
   }
 };
 
-template <class Epi>
-void launch_spmv(const DCsr& A, const double* x, Epi epi, cudaStream_t s) {
+// Jacobi sweep, general form: zold == null means the zero-start iterate
+// w*(dinv*b) (formed on the fly, both as x and as zold_r); zacc != null adds
+// the sweep result into zacc instead of storing it.
+struct EpiJacobiEx {
+  XJac0 z0;
+  const double* zold;
+  const double* b;
+  const int* brow;
+  const double* dinv;
+  double w;
+  double* znew;
+  double* zacc;
+  __device__ void operator()(int r, double s) const {
+    const double bv = brow ? b[brow[r]] : b[r];
+    const double d = __dsub_rn(bv, __dadd_rn(0.0, s));
+    const double zo = zold ? zold[r] : z0(r);
+    const double v = __dadd_rn(zo, __dmul_rn(w, __dmul_rn(dinv[r], d)));
+    if (zacc) zacc[r] = __dadd_rn(zacc[r], v);
+    else znew[r] = v;
+  }
+};
+
+template <class Epi, class Xs = XPlain>
+void launch_spmv(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
   if (A.rows == 0) return;
   if (A.rows > 65536 && A.nnz <= 3LL * A.rows) {
     k_spmv_tpr<<<blocks_for(A.rows, 256), 256, 0, s>>>(A.rows, A.ptr.get(), A.col.get(), A.val.get(), x, epi);
@@ -369,22 +408,29 @@ void launch_spmv(const DCsr& A, const double* x, Epi epi, cudaStream_t s) {
 }  // namespace
 
 void spmv(const DCsr& A, const double* x, double* y, cudaStream_t s) {
-  launch_spmv(A, x, EpiStore{y}, s);
+  launch_spmv(A, XPlain{x}, EpiStore{y}, s);
 }
 void spmv_residual(const DCsr& A, const double* x, const double* b, const int* brow, double* y,
                    cudaStream_t s) {
-  launch_spmv(A, x, EpiResidual{b, brow, y}, s);
+  launch_spmv(A, XPlain{x}, EpiResidual{b, brow, y}, s);
 }
 void spmv_add(const DCsr& A, const double* x, double* y, cudaStream_t s) {
-  launch_spmv(A, x, EpiAdd{y}, s);
+  launch_spmv(A, XPlain{x}, EpiAdd{y}, s);
 }
 void spmv_prolong(const DCsr& P, const double* e, const int* fpos, const double* zF, double* z,
                   cudaStream_t s) {
-  launch_spmv(P, e, EpiProlong{fpos, zF, z}, s);
+  launch_spmv(P, XPlain{e}, EpiProlong{fpos, zF, z}, s);
 }
 void spmv_jacobi(const DCsr& A, const double* zold, const double* b, const int* brow,
                  const double* dinv, double w, double* znew, cudaStream_t s) {
-  launch_spmv(A, zold, EpiJacobi{zold, b, brow, dinv, w, znew}, s);
+  launch_spmv(A, XPlain{zold}, EpiJacobi{zold, b, brow, dinv, w, znew}, s);
+}
+void spmv_jacobi_ex(const DCsr& A, const double* zold, const double* b, const int* brow, const double* dinv,
+                    double w, double* znew, double* zacc, cudaStream_t s) {
+  const XJac0 z0{w, dinv, b, brow};
+  const EpiJacobiEx epi{z0, zold, b, brow, dinv, w, znew, zacc};
+  if (zold) launch_spmv(A, XPlain{zold}, epi, s);
+  else launch_spmv(A, z0, epi, s);
 }
 
 // ============================================================================

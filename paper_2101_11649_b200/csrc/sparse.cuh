@@ -49,6 +49,11 @@ void spmv_prolong(const DCsr& P, const double* e, const int* fpos, const double*
 // Jacobi correction sweep: znew = zold + w*(dinv*(b - A zold)), b gathered via brow.
 void spmv_jacobi(const DCsr& A, const double* zold, const double* b, const int* brow,
                  const double* dinv, double w, double* znew, cudaStream_t s);
+// Generalised sweep: zold == nullptr starts from the zero-guess iterate
+// w*(dinv*b) computed on the fly (fusing the first sweep into this one);
+// zacc != nullptr accumulates the result into zacc (fusing apply_add).
+void spmv_jacobi_ex(const DCsr& A, const double* zold, const double* b, const int* brow, const double* dinv,
+                    double w, double* znew, double* zacc, cudaStream_t s);
 
 // ---- setup kernels (bit-exact) --------------------------------------------
 DCsr extract(const DCsr& A, const int* rows, int nrows, const int* cols, int ncols, cudaStream_t s);
