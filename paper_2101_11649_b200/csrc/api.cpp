@@ -230,6 +230,7 @@ int mgrx_matrix_csr(mgrx_ctx* ctx, int rows, int cols, const int* rowptr, const 
     auto m = std::make_unique<mgrx_mat>();
     m->ctx = ctx;
     m->A = csr_from_host(rows, cols, rowptr, colidx, values, ctx->stream);
+    spmv_prepare(m->A, ctx->stream);
     *out = m.release();
     return MGRX_OK;
   });
@@ -242,6 +243,7 @@ int mgrx_matrix_csr_device(mgrx_ctx* ctx, int rows, int cols, const int* d_rowpt
     auto m = std::make_unique<mgrx_mat>();
     m->ctx = ctx;
     m->A = csr_from_device(rows, cols, d_rowptr, d_colidx, d_values, ctx->stream);
+    spmv_prepare(m->A, ctx->stream);
     *out = m.release();
     return MGRX_OK;
   });
@@ -297,6 +299,7 @@ int mgrx_setup(mgrx_ctx* ctx, mgrx_mat* A, const int* labels, int nfields, const
     EventTimer t(s);
     h->A = csr_copy(A->A, s);
     h->H.setup(h->A, lab, fields, unknown_map ? &umap : nullptr, strat, s);
+    spmv_prepare(h->A, s);
     h->setup_s = t.stop();
     h->vin.alloc(n > 0 ? n : 1, s);
     h->vout.alloc(n > 0 ? n : 1, s);

@@ -58,7 +58,8 @@ class DVec {
     release();
     n_ = n;
     s_ = s;
-    if (n_) MGRX_CK(cudaMallocAsync(reinterpret_cast<void**>(&p_), n_ * sizeof(T), s_));
+    // +32 bytes: bulk (TMA) copies round slices out to 16-byte multiples
+    if (n_) MGRX_CK(cudaMallocAsync(reinterpret_cast<void**>(&p_), n_ * sizeof(T) + 32, s_));
   }
   void release() {
     if (p_) cudaFreeAsync(p_, s_);

@@ -502,6 +502,18 @@ void AmgHier::vcycle_level(int l, const double* r, double* z, cudaStream_t s) {
 // ============================================================================
 // MGR (proj/src/mgr.cpp:223-326)
 // ============================================================================
+void prepare_amg(AmgHier& h, cudaStream_t s);
+void prepare_relax(BoundRelax& b, cudaStream_t s) {
+  if (b.amg) prepare_amg(*b.amg, s);
+}
+void prepare_amg(AmgHier& h, cudaStream_t s) {
+  for (auto& L : h.levels) {
+    for (DCsr* M : {&L.A, &L.P, &L.R}) spmv_prepare(*M, s);
+    prepare_relax(L.pre, s);
+    prepare_relax(L.post, s);
+  }
+}
+
 void MgrHier::setup(const DCsr& A, const std::vector<int>& labels, const std::vector<std::string>& fields,
                     const std::vector<int>* umap_in, const Strategy& strat, cudaStream_t s) {
   if (A.rows != A.cols) throw InvalidArgument("mgr_setup: matrix must be square");
@@ -649,6 +661,14 @@ void MgrHier::setup(const DCsr& A, const std::vector<int>& labels, const std::ve
   const int ncs = A_coarse.rows > 0 ? A_coarse.rows : 1;
   ct.alloc(ncs, s);
   cd.alloc(ncs, s);
+  // block plans of the staged SpMV for every solve-path matrix
+  for (auto& L : levels) {
+    for (DCsr* M : {&L.A, &L.P, &L.R, &L.Acf, &L.Aff}) spmv_prepare(*M, s);
+    prepare_relax(L.f_relax, s);
+    if (L.g_relax) prepare_relax(*L.g_relax, s);
+  }
+  spmv_prepare(A_coarse, s);
+  if (coarse_amg) prepare_amg(*coarse_amg, s);
 }
 
 void MgrHier::coarse_solve(const double* v, double* z, cudaStream_t s) {

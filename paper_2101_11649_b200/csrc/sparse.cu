@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "sparse.cuh"
 
@@ -315,32 +316,157 @@ __global__ void __launch_bounds__(256) k_spmv_tpr(int rows, const int* __restric
   epi(r, sum);
 }
 
+// ---------------------------------------------------------------------------
+// Staged SpMV for large matrices: persistent CTAs walk row blocks of <= 256
+// rows and <= kStE nonzeros (block bounds precomputed by spmv_prepare). The
+// block's row offsets, values and column indices arrive in shared memory by
+// bulk copies (cp.async.bulk, completion on an mbarrier) issued two blocks
+// ahead, so the HBM stream is kept deep without spending registers on it;
+// each thread then forms its row's products left to right (x gathered from
+// L2) exactly like the serial loop.
+// Stage geometry: one thread per row of a block of <= kR rows / <= kE nonzeros.
+template <int kR, int kE>
+struct StGeom {
+  static constexpr int T = kR, R = kR, E = kE;
+  struct Stage {
+    int rp[kR + 8];
+    int col[kE + 8];
+    double val[kE + 4];
+  };
+  static constexpr int kStages = 2;
+  static constexpr size_t smem = kStages * sizeof(Stage) + 16 * kStages;
+};
+using StA = StGeom<256, 2048>;  // 4 CTAs / SM
+using StB = StGeom<128, 1024>;  // 8 CTAs / SM
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+template <class Gm, class Epi, class Xs>
+__global__ void __launch_bounds__(Gm::T) k_spmv_staged(int nblk, const int* __restrict__ plan,
+                                                       const int* __restrict__ ptr, const int* __restrict__ col,
+                                                       const double* __restrict__ val, Xs x, Epi epi) {
+  using Stage = typename Gm::Stage;
+  constexpr int kStages = Gm::kStages;
+  extern __shared__ __align__(128) unsigned char st_raw[];
+  Stage* stg = reinterpret_cast<Stage*>(st_raw);
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(st_raw + kStages * sizeof(Stage));
+  const int t = threadIdx.x;
+  const int* prow = plan;
+  const int* pnnz = plan + nblk + 1;
+  if (t == 0) {
+    for (int s = 0; s < kStages; ++s) asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(bar + s)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int b, int s) {
+    const int r0 = prow[b], r1 = prow[b + 1];
+    const int p0 = pnnz[b], p1 = pnnz[b + 1];
+    const int ra = r0 & ~3, pa4 = p0 & ~3, pa2 = p0 & ~1;
+    const unsigned brp = ((r1 + 1 - ra + 3) & ~3) * 4u;
+    const unsigned bc = p1 > p0 ? ((p1 - pa4 + 3) & ~3) * 4u : 0u;
+    const unsigned bv = p1 > p0 ? ((p1 - pa2 + 1) & ~1) * 8u : 0u;
+    const unsigned mb = smem_u32(bar + s);
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(mb), "r"(brp + bc + bv) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(stg[s].rp)),
+                 "l"(ptr + ra), "r"(brp), "r"(mb)
+                 : "memory");
+    if (bc) {
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(stg[s].col)),
+                   "l"(col + pa4), "r"(bc), "r"(mb)
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(stg[s].val)),
+                   "l"(val + pa2), "r"(bv), "r"(mb)
+                   : "memory");
+    }
+  };
+  const int G = gridDim.x;
+  if (t == 0)
+    for (int s = 0; s < kStages; ++s)
+      if (blockIdx.x + s * G < nblk) issue(blockIdx.x + s * G, s);
+  unsigned phase = 0;  // bit s: parity of stage s
+  int it = 0;
+  for (int b = blockIdx.x; b < nblk; b += G, ++it) {
+    const int s = it % kStages;
+    const int r0 = prow[b], r1 = prow[b + 1];
+    const int p0 = pnnz[b], p1 = pnnz[b + 1];
+    const int r = r0 + t;
+    // row operands of the epilogue: independent of the stage, issue first
+    decltype(epi.load(0)) pre{};
+    if (r < r1) pre = epi.load(r);
+    const unsigned mb = smem_u32(bar + s);
+    const unsigned par = (phase >> s) & 1u;
+    unsigned done = 0;
+    do {
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done)
+          : "r"(mb), "r"(par)
+          : "memory");
+    } while (!done);
+    phase ^= 1u << s;
+    Stage& S = stg[s];
+    const int ra = r0 & ~3, pa4 = p0 & ~3, pa2 = p0 & ~1;
+    if (r < r1) {
+      const int lo = S.rp[r - ra], hi = S.rp[r + 1 - ra];
+      double sum = 0.0;
+      int k = lo;
+      for (; k + 4 <= hi; k += 4) {
+        const int c0 = S.col[k - pa4], c1 = S.col[k + 1 - pa4], c2 = S.col[k + 2 - pa4], c3 = S.col[k + 3 - pa4];
+        const double x0 = x(c0), x1 = x(c1), x2 = x(c2), x3 = x(c3);
+        const double q0 = __dmul_rn(S.val[k - pa2], x0), q1 = __dmul_rn(S.val[k + 1 - pa2], x1);
+        const double q2 = __dmul_rn(S.val[k + 2 - pa2], x2), q3 = __dmul_rn(S.val[k + 3 - pa2], x3);
+        sum = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(sum, q0), q1), q2), q3);
+      }
+      for (; k < hi; ++k) sum = __dadd_rn(sum, __dmul_rn(S.val[k - pa2], x(S.col[k - pa4])));
+      epi.store(r, sum, pre);
+    }
+    __syncthreads();  // stage s consumed
+    if (t == 0 && b + kStages * G < nblk) issue(b + kStages * G, s);
+  }
+}
+
+// Epilogues: load(r) fetches the row's operands (issued before the row's
+// products in the staged kernel, so their latency overlaps the gathers);
+// store(r, s, pre) combines them with the row sum s.
+struct NoPre {};
 struct EpiStore {
   double* y;
-  __device__ void operator()(int r, double s) const { y[r] = __dadd_rn(0.0, s); }
+  __device__ NoPre load(int) const { return {}; }
+  __device__ void store(int r, double s, const NoPre&) const { y[r] = __dadd_rn(0.0, s); }
+  __device__ void operator()(int r, double s) const { store(r, s, load(r)); }
 };
 struct EpiResidual {
   const double* b;
   const int* brow;
   double* y;
-  __device__ void operator()(int r, double s) const {
-    const double bv = brow ? b[brow[r]] : b[r];
-    y[r] = __dsub_rn(bv, __dadd_rn(0.0, s));
-  }
+  __device__ double load(int r) const { return brow ? b[brow[r]] : b[r]; }
+  __device__ void store(int r, double s, double bv) const { y[r] = __dsub_rn(bv, __dadd_rn(0.0, s)); }
+  __device__ void operator()(int r, double s) const { store(r, s, load(r)); }
 };
 struct EpiAdd {
   double* y;
-  __device__ void operator()(int r, double s) const { y[r] = __dadd_rn(y[r], s); }
+  __device__ double load(int r) const { return y[r]; }
+  __device__ void store(int r, double s, double yv) const { y[r] = __dadd_rn(yv, s); }
+  __device__ void operator()(int r, double s) const { store(r, s, load(r)); }
 };
 struct EpiProlong {
   const int* fpos;
   const double* zF;
   double* z;
-  __device__ void operator()(int r, double s) const {
+  __device__ double load(int r) const {
     const int f = fpos[r];
-    const double zp = f >= 0 ? __dadd_rn(0.0, zF[f]) : 0.0;
-    z[r] = __dadd_rn(zp, s);
+    return f >= 0 ? __dadd_rn(0.0, zF[f]) : 0.0;
   }
+  __device__ void store(int r, double s, double zp) const { z[r] = __dadd_rn(zp, s); }
+  __device__ void operator()(int r, double s) const { store(r, s, load(r)); }
+};
+struct JacPre {
+  double bv, zo, di, za;
 };
 struct EpiJacobi {
   const double* zold;
@@ -349,11 +475,12 @@ struct EpiJacobi {
   const double* dinv;
   double w;
   double* znew;
-  __device__ void operator()(int r, double s) const {
-    const double bv = brow ? b[brow[r]] : b[r];
-    const double d = __dsub_rn(bv, __dadd_rn(0.0, s));
-    znew[r] = __dadd_rn(zold[r], __dmul_rn(w, __dmul_rn(dinv[r], d)));
+  __device__ JacPre load(int r) const { return {brow ? b[brow[r]] : b[r], zold[r], dinv[r], 0.0}; }
+  __device__ void store(int r, double s, const JacPre& p) const {
+    const double d = __dsub_rn(p.bv, __dadd_rn(0.0, s));
+    znew[r] = __dadd_rn(p.zo, __dmul_rn(w, __dmul_rn(p.di, d)));
   }
+  __device__ void operator()(int r, double s) const { store(r, s, load(r)); }
 };
 
 // Jacobi sweep, general form: zold == null means the zero-start iterate
@@ -368,19 +495,71 @@ struct EpiJacobiEx {
   double w;
   double* znew;
   double* zacc;
-  __device__ void operator()(int r, double s) const {
-    const double bv = brow ? b[brow[r]] : b[r];
-    const double d = __dsub_rn(bv, __dadd_rn(0.0, s));
-    const double zo = zold ? zold[r] : z0(r);
-    const double v = __dadd_rn(zo, __dmul_rn(w, __dmul_rn(dinv[r], d)));
-    if (zacc) zacc[r] = __dadd_rn(zacc[r], v);
+  __device__ JacPre load(int r) const {
+    return {brow ? b[brow[r]] : b[r], zold ? zold[r] : z0(r), dinv[r], zacc ? zacc[r] : 0.0};
+  }
+  __device__ void store(int r, double s, const JacPre& p) const {
+    const double d = __dsub_rn(p.bv, __dadd_rn(0.0, s));
+    const double v = __dadd_rn(p.zo, __dmul_rn(w, __dmul_rn(p.di, d)));
+    if (zacc) zacc[r] = __dadd_rn(p.za, v);
     else znew[r] = v;
   }
+  __device__ void operator()(int r, double s) const { store(r, s, load(r)); }
 };
+
+bool staged_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("MGRX_SPMV_STAGED");
+    return !v || std::atoi(v) != 0;
+  }();
+  return on;
+}
+int staged_ctas_per_sm() {
+  static const int c = [] {
+    const char* v = std::getenv("MGRX_SPMV_CTAS");
+    return v ? std::max(1, std::atoi(v)) : 8;
+  }();
+  return c;
+}
+
+bool staged_force() {
+  static const bool f = [] {
+    const char* v = std::getenv("MGRX_SPMV_STAGED");
+    return v && std::atoi(v) == 2;
+  }();
+  return f;
+}
+int staged_geom() {
+  static const int g = [] {
+    const char* v = std::getenv("MGRX_SPMV_GEOM");
+    return v ? std::atoi(v) : 0;
+  }();
+  return g;
+}
+template <class Gm, class Epi, class Xs>
+void launch_staged(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
+  static bool attr = false;  // per instantiation
+  if (!attr) {
+    MGRX_CK(cudaFuncSetAttribute(k_spmv_staged<Gm, Epi, Xs>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(Gm::smem)));
+    attr = true;
+  }
+  const int per_sm = static_cast<int>(std::min<size_t>(8, 227 * 1024 / Gm::smem));
+  const int grid = std::min(A.nblk, 148 * std::min(per_sm, staged_ctas_per_sm()));
+  k_spmv_staged<Gm, Epi, Xs><<<grid, Gm::T, Gm::smem, s>>>(A.nblk, A.plan.get(), A.ptr.get(), A.col.get(),
+                                                          A.val.get(), x, epi);
+  MGRX_LAUNCH_CK();
+  count_launch();
+}
 
 template <class Epi, class Xs = XPlain>
 void launch_spmv(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
   if (A.rows == 0) return;
+  if (A.nblk > 0 && staged_enabled()) {
+    if (staged_geom() == 0) launch_staged<StA>(A, x, epi, s);
+    else launch_staged<StB>(A, x, epi, s);
+    return;
+  }
   if (A.rows > 65536 && A.nnz <= 3LL * A.rows) {
     k_spmv_tpr<<<blocks_for(A.rows, 256), 256, 0, s>>>(A.rows, A.ptr.get(), A.col.get(), A.val.get(), x, epi);
     MGRX_LAUNCH_CK();
@@ -406,6 +585,60 @@ void launch_spmv(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
 }
 
 }  // namespace
+
+void spmv_prepare(DCsr& A, cudaStream_t s) {
+  A.nblk = 0;
+  A.plan.release();
+  if (A.rows < 65536) return;
+  const int kStRows = staged_geom() == 0 ? StA::R : StB::R;
+  const int kStE = staged_geom() == 0 ? StA::E : StB::E;
+  const std::vector<int> p = A.ptr.download(A.rows + 1);
+  std::vector<int> rs{0}, ns{0};
+  int r = 0;
+  while (r < A.rows) {
+    if (p[r + 1] - p[r] > kStE) return;  // a row longer than a stage: keep the direct kernels
+    int q = r + 1;
+    while (q < A.rows && q - r < kStRows && p[q + 1] - p[r] <= kStE) ++q;
+    rs.push_back(q);
+    ns.push_back(p[q]);
+    r = q;
+  }
+  const int nb = static_cast<int>(rs.size()) - 1;
+  std::vector<int> h(rs);
+  h.insert(h.end(), ns.begin(), ns.end());
+  DVec<int> plan(h.size(), s);
+  plan.upload(h.data(), h.size());
+  // Keep the staged kernel only where it measures faster than the direct one
+  // on this matrix (it wins on the square stencil operators; the direct
+  // kernels win on the rectangular transfer operators at cfg2).
+  DVec<double> xs(A.cols > 0 ? A.cols : 1, s), ys(A.rows, s);
+  xs.zero();
+  cudaEvent_t e0, e1;
+  MGRX_CK(cudaEventCreate(&e0));
+  MGRX_CK(cudaEventCreate(&e1));
+  auto time = [&](bool staged) {
+    A.nblk = staged ? nb : 0;
+    A.plan = DVec<int>();
+    if (staged) A.plan = std::move(plan);
+    spmv(A, xs.get(), ys.get(), s);  // warm
+    MGRX_CK(cudaEventRecord(e0, s));
+    for (int k = 0; k < 5; ++k) spmv(A, xs.get(), ys.get(), s);
+    MGRX_CK(cudaEventRecord(e1, s));
+    MGRX_CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    MGRX_CK(cudaEventElapsedTime(&ms, e0, e1));
+    if (staged) plan = std::move(A.plan);
+    return ms;
+  };
+  const float td = time(false), ts = time(true);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  A.nblk = 0;
+  if (ts < 0.97f * td || staged_force()) {
+    A.plan = std::move(plan);
+    A.nblk = nb;
+  }
+}
 
 void spmv(const DCsr& A, const double* x, double* y, cudaStream_t s) {
   launch_spmv(A, XPlain{x}, EpiStore{y}, s);

@@ -13,6 +13,10 @@ struct DCsr {
   int rows = 0, cols = 0, nnz = 0;
   DVec<int> ptr, col;
   DVec<double> val;
+  // Staged-SpMV block plan (spmv_prepare): nblk row blocks, plan holds the
+  // nblk+1 first rows then the nblk+1 first nonzeros. nblk == 0: no plan.
+  int nblk = 0;
+  DVec<int> plan;
   bool empty() const { return rows == 0; }
 };
 
@@ -35,6 +39,10 @@ void csr_validate(const DCsr& A, cudaStream_t s);
 DCsr csr_copy(const DCsr& A, cudaStream_t s);
 
 // ---- SpMV family (solve path) ---------------------------------------------
+// Build the block plan of the bulk-copy-staged SpMV for a solve-path matrix
+// (rows >= 65536); matrices without a plan use the direct kernels. Host-
+// synchronising: call at setup, never inside a captured region.
+void spmv_prepare(DCsr& A, cudaStream_t s);
 // y = A x                                (Eigen y = A*x: 0 + row sum)
 void spmv(const DCsr& A, const double* x, double* y, cudaStream_t s);
 // y = b - A x ; if brow != null, b is gathered: b[brow[r]]

@@ -1,5 +1,4 @@
 #!/bin/bash
 mkdir -p gpurun_out
-TRACE=1 TAG=tmpl timeout 300 python tools/probe_arnoldi.py > gpurun_out/probe_arn.log 2>&1
-timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-variant > gpurun_out/ba_1.json 2>gpurun_out/ba_1.err
+timeout 1200 python -m pytest tests -q -m gpu -k "staged or solve_paths" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 echo done

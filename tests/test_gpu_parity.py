@@ -118,6 +118,31 @@ def test_spmv_bit_exact():
     assert np.array_equal(y.view(np.int64), yr.view(np.int64))
 
 
+def test_staged_spmv_bit_exact():
+    """The bulk-copy-staged SpMV (forced on, MGRX_SPMV_STAGED=2) on ragged
+    large matrices: empty rows, unaligned block starts, blocks cut at the
+    nonzero cap by rows of ~2000 entries, and a matrix with a row longer than
+    a stage (which keeps the direct kernels)."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
+        "import paper_2101_11649_b200 as mx, refcpu;"
+        "rng = np.random.default_rng(11)\n"
+        "for n, big in ((100003, 2000), (70001, 3000)):\n"
+        "    lens = rng.integers(0, 13, n); lens[rng.integers(0, n, 40)] = 0; lens[[5, 777, n - 2]] = big\n"
+        "    ptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)\n"
+        "    col = np.concatenate([np.sort(rng.choice(n, size=l, replace=False)) for l in lens]).astype(np.int32)\n"
+        "    val = rng.standard_normal(ptr[-1]); x = rng.standard_normal(n)\n"
+        "    y = mx.Matrix(ptr, col, val).spmv(x); yr = refcpu.spmv(ptr, col, val, x)\n"
+        "    assert np.array_equal(y.view(np.int64), yr.view(np.int64)), n\n"
+        "print('ok')")
+    root = make_golden.ROOT
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                         env={**__import__("os").environ, "MGRX_SPMV_STAGED": "2"}, timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
 def test_zero_rhs_and_errors():
     P = mx.mfd_problem(4, 4, 3, "iid")
     A = mx.Matrix(P.ptr, P.col, P.val)
@@ -220,12 +245,15 @@ def test_alternative_gs_sweeps_are_bit_exact(mode):
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
 
 
-@pytest.mark.parametrize("arnoldi", ["0", "1"])
-def test_arnoldi_paths_are_bit_exact(arnoldi):
-    """The fused persistent Arnoldi kernel (w resident in shared memory, one
-    launch per GMRES step) and the launch-per-projection MGS path
-    (MGRX_ARNOLDI=0) both reproduce the oracle's residual history bitwise, on
-    a system large enough (n > 5 * 151552) that every lane owns several rows."""
+@pytest.mark.parametrize("env", [{"MGRX_ARNOLDI": "0"}, {"MGRX_ARNOLDI": "1"}, {"MGRX_SPMV_STAGED": "2"},
+                                 {"MGRX_SPMV_STAGED": "0"}], ids=["mgs", "arnoldi", "staged", "direct"])
+def test_solve_paths_are_bit_exact(env):
+    """Every device path choice reproduces the oracle's residual history and
+    solution bitwise on a system large enough (n > 5 * 151552) that every
+    Arnoldi lane owns several rows and every large operator is a staged-SpMV
+    candidate: the fused persistent Arnoldi kernel vs the launch-per-
+    projection MGS (MGRX_ARNOLDI), and the bulk-copy-staged SpMV forced on
+    every large matrix vs the direct kernels only (MGRX_SPMV_STAGED)."""
     import subprocess
     import sys
     code = (
@@ -242,7 +270,7 @@ def test_arnoldi_paths_are_bit_exact(arnoldi):
         "print('ok', rep.iterations)")
     root = make_golden.ROOT
     out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
-                         env={**__import__("os").environ, "MGRX_ARNOLDI": arnoldi}, timeout=600)
+                         env={**__import__("os").environ, **env}, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
 
 
