@@ -31,6 +31,40 @@ struct RuntimeError : std::runtime_error {
 
 #define MGRX_LAUNCH_CK() MGRX_CK(cudaGetLastError())
 
+// Programmatic dependent launch (PDL): solve-path kernels are launched with
+// the programmatic-serialization attribute and begin with pdl_enter(), which
+// waits until the previous grid has completed and its writes are visible.
+// Every memory access comes after the wait, so stream order is preserved;
+// what overlaps is the launch processing between dependent kernels. An
+// early launch_dependents trigger (MGRX_PDL_TRIGGER=1) measured slower at
+// cfg2 (74.8 vs 72.6 ms per solve; no PDL: 73.0): resident waiting CTAs
+// crowd the running grid.
+#ifndef MGRX_PDL_TRIGGER
+#define MGRX_PDL_TRIGGER 0
+#endif
+__device__ __forceinline__ void pdl_enter() {
+#if MGRX_PDL_TRIGGER
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+bool pdl_enabled();
+
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  MGRX_CK(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
+
 // Process-wide launch counter (the bench reports kernels launched in the
 // timed region; graph replays add their node count).
 extern long long g_launches;

@@ -90,6 +90,7 @@ __global__ void __launch_bounds__(kT) k_lu(int n, double* M, int* perm, double t
 __global__ void __launch_bounds__(kT) k_lu_solve(int n, const double* __restrict__ M,
                                                  const int* __restrict__ perm,
                                                  const double* __restrict__ b, double* __restrict__ x) {
+  pdl_enter();
   extern __shared__ double xs[];
   for (int i = threadIdx.x; i < n; i += kT) xs[i] = b[perm[i]];
   __syncthreads();
@@ -120,6 +121,7 @@ constexpr int kWarpLuR = (kWarpLuMax + 31) / 32;
 __global__ void __launch_bounds__(32) k_lu_solve_warp(int n, const double* __restrict__ M,
                                                       const int* __restrict__ perm, const double* __restrict__ b,
                                                       double* __restrict__ x) {
+  pdl_enter();
   extern __shared__ double Ms[];
   const int l = threadIdx.x;
   for (int e = l; e < n * n; e += 32) Ms[e] = M[e];
@@ -199,13 +201,13 @@ void dense_factor(const DCsr& A, DenseLU& out, cudaStream_t s, double pivot_tol)
 void dense_solve(const DenseLU& f, const double* b, double* x, cudaStream_t s) {
   if (f.n == 0) return;
   if (f.n <= kWarpLuMax) {
-    k_lu_solve_warp<<<1, 32, sizeof(double) * f.n * f.n, s>>>(f.n, f.lu.get(), f.perm.get(), b, x);
+    launch_pdl(k_lu_solve_warp, 1, 32, sizeof(double) * f.n * f.n, s, f.n, f.lu.get(), f.perm.get(), b, x);
     MGRX_LAUNCH_CK();
     count_launch();
     return;
   }
   const size_t sm = sizeof(double) * f.n;
-  k_lu_solve<<<1, kT, sm, s>>>(f.n, f.lu.get(), f.perm.get(), b, x);
+  launch_pdl(k_lu_solve, 1, kT, sm, s, f.n, f.lu.get(), f.perm.get(), b, x);
   MGRX_LAUNCH_CK();
   count_launch();
 }

@@ -29,11 +29,6 @@ __global__ void k_gather_int(int n, const int* __restrict__ idx, const int* __re
   if (i < n) out[i] = in[idx[i]];
 }
 
-__global__ void k_iota(int n, int* a) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) a[i] = i;
-}
-
 __global__ void k_scatter_add(int n, const int* __restrict__ idx, const double* __restrict__ a,
                               double* __restrict__ z) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;

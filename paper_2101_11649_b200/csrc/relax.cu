@@ -608,17 +608,20 @@ __global__ void k_sweep_fill(int n, const int* __restrict__ order, const int* __
 __global__ void k_jacobi0(int n, double w, const double* __restrict__ dinv,
                           const double* __restrict__ r, const int* __restrict__ rrow,
                           double* __restrict__ z) {
+  pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double rv = rrow ? r[rrow[i]] : r[i];
   z[i] = __dmul_rn(w, __dmul_rn(dinv[i], rv));
 }
 __global__ void k_vec_add(int n, const double* __restrict__ a, double* __restrict__ y) {
+  pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) y[i] = __dadd_rn(y[i], a[i]);
 }
 __global__ void k_gather(int n, const int* __restrict__ idx, const double* __restrict__ x,
                          double* __restrict__ y) {
+  pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) y[i] = x[idx[i]];
 }
@@ -974,21 +977,21 @@ void gs_check(GsScratch& scr, cudaStream_t s) {
 void jacobi0(int n, double w, const double* dinv, const double* r, const int* rrow, double* z,
              cudaStream_t s) {
   if (n == 0) return;
-  k_jacobi0<<<blocks_for(n, 256), 256, 0, s>>>(n, w, dinv, r, rrow, z);
+  launch_pdl(k_jacobi0, blocks_for(n, 256), 256, 0, s, n, w, dinv, r, rrow, z);
   MGRX_LAUNCH_CK();
   count_launch();
 }
 
 void vec_add(int n, const double* a, double* y, cudaStream_t s) {
   if (n == 0) return;
-  k_vec_add<<<blocks_for(n, 256), 256, 0, s>>>(n, a, y);
+  launch_pdl(k_vec_add, blocks_for(n, 256), 256, 0, s, n, a, y);
   MGRX_LAUNCH_CK();
   count_launch();
 }
 
 void gather(int n, const int* idx, const double* x, double* y, cudaStream_t s) {
   if (n == 0) return;
-  k_gather<<<blocks_for(n, 256), 256, 0, s>>>(n, idx, x, y);
+  launch_pdl(k_gather, blocks_for(n, 256), 256, 0, s, n, idx, x, y);
   MGRX_LAUNCH_CK();
   count_launch();
 }

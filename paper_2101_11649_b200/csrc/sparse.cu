@@ -10,6 +10,14 @@
 
 namespace mgrx {
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("MGRX_PDL");
+    return !v || std::atoi(v) != 0;
+  }();
+  return on;
+}
+
 long long g_launches = 0;
 
 // ============================================================================
@@ -237,6 +245,7 @@ __global__ void __launch_bounds__(kRows) k_spmv(int rows, const int* __restrict_
                                                 const int* __restrict__ col,
                                                 const double* __restrict__ val,
                                                 Xs x, Epi epi) {
+  pdl_enter();
   constexpr int kCap = 8 * kRows;
   __shared__ double prod[kCap];
   const int r0 = blockIdx.x * kRows;
@@ -273,6 +282,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_spmv_wpr(int rows, const int* _
                                                           const int* __restrict__ col,
                                                           const double* __restrict__ val,
                                                           Xs x, Epi epi) {
+  pdl_enter();
   __shared__ double prod[kWarps][32];
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   for (int r = blockIdx.x * kWarps + w; r < rows; r += gridDim.x * kWarps) {
@@ -300,6 +310,7 @@ __global__ void __launch_bounds__(256) k_spmv_tpr(int rows, const int* __restric
                                                   const int* __restrict__ col,
                                                   const double* __restrict__ val,
                                                   Xs x, Epi epi) {
+  pdl_enter();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows) return;
   const int lo = __ldg(ptr + r), hi = __ldg(ptr + r + 1);
@@ -347,6 +358,7 @@ template <class Gm, class Epi, class Xs>
 __global__ void __launch_bounds__(Gm::T) k_spmv_staged(int nblk, const int* __restrict__ plan,
                                                        const int* __restrict__ ptr, const int* __restrict__ col,
                                                        const double* __restrict__ val, Xs x, Epi epi) {
+  pdl_enter();
   using Stage = typename Gm::Stage;
   constexpr int kStages = Gm::kStages;
   extern __shared__ __align__(128) unsigned char st_raw[];
@@ -393,7 +405,7 @@ __global__ void __launch_bounds__(Gm::T) k_spmv_staged(int nblk, const int* __re
   for (int b = blockIdx.x; b < nblk; b += G, ++it) {
     const int s = it % kStages;
     const int r0 = prow[b], r1 = prow[b + 1];
-    const int p0 = pnnz[b], p1 = pnnz[b + 1];
+    const int p0 = pnnz[b];
     const int r = r0 + t;
     // row operands of the epilogue: independent of the stage, issue first
     decltype(epi.load(0)) pre{};
@@ -546,8 +558,8 @@ void launch_staged(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
   }
   const int per_sm = static_cast<int>(std::min<size_t>(8, 227 * 1024 / Gm::smem));
   const int grid = std::min(A.nblk, 148 * std::min(per_sm, staged_ctas_per_sm()));
-  k_spmv_staged<Gm, Epi, Xs><<<grid, Gm::T, Gm::smem, s>>>(A.nblk, A.plan.get(), A.ptr.get(), A.col.get(),
-                                                          A.val.get(), x, epi);
+  launch_pdl(k_spmv_staged<Gm, Epi, Xs>, grid, Gm::T, Gm::smem, s, A.nblk, A.plan.get(), A.ptr.get(), A.col.get(),
+             A.val.get(), x, epi);
   MGRX_LAUNCH_CK();
   count_launch();
 }
@@ -561,7 +573,8 @@ void launch_spmv(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
     return;
   }
   if (A.rows > 65536 && A.nnz <= 3LL * A.rows) {
-    k_spmv_tpr<<<blocks_for(A.rows, 256), 256, 0, s>>>(A.rows, A.ptr.get(), A.col.get(), A.val.get(), x, epi);
+    launch_pdl(k_spmv_tpr<Epi, Xs>, blocks_for(A.rows, 256), 256, 0, s, A.rows, A.ptr.get(), A.col.get(), A.val.get(),
+               x, epi);
     MGRX_LAUNCH_CK();
     count_launch();
     return;
@@ -569,17 +582,20 @@ void launch_spmv(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
   const bool small = A.rows <= 65536 || A.nnz > 24LL * A.rows;
   if (small) {
     const int grid = std::min(blocks_for(A.rows, kWarps), 148 * 8);
-    k_spmv_wpr<<<grid, kWarps * 32, 0, s>>>(A.rows, A.ptr.get(), A.col.get(), A.val.get(), x, epi);
+    launch_pdl(k_spmv_wpr<Epi, Xs>, grid, kWarps * 32, 0, s, A.rows, A.ptr.get(), A.col.get(), A.val.get(), x, epi);
     MGRX_LAUNCH_CK();
     count_launch();
     return;
   }
   if (A.rows >= 2000000)
-    k_spmv<256><<<blocks_for(A.rows, 256), 256, 0, s>>>(A.rows, A.ptr.get(), A.col.get(), A.val.get(), x, epi);
+    launch_pdl(k_spmv<256, Epi, Xs>, blocks_for(A.rows, 256), 256, 0, s, A.rows, A.ptr.get(), A.col.get(),
+               A.val.get(), x, epi);
   else if (A.rows >= 300000)
-    k_spmv<128><<<blocks_for(A.rows, 128), 128, 0, s>>>(A.rows, A.ptr.get(), A.col.get(), A.val.get(), x, epi);
+    launch_pdl(k_spmv<128, Epi, Xs>, blocks_for(A.rows, 128), 128, 0, s, A.rows, A.ptr.get(), A.col.get(),
+               A.val.get(), x, epi);
   else
-    k_spmv<64><<<blocks_for(A.rows, 64), 64, 0, s>>>(A.rows, A.ptr.get(), A.col.get(), A.val.get(), x, epi);
+    launch_pdl(k_spmv<64, Epi, Xs>, blocks_for(A.rows, 64), 64, 0, s, A.rows, A.ptr.get(), A.col.get(), A.val.get(),
+               x, epi);
   MGRX_LAUNCH_CK();
   count_launch();
 }

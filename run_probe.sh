@@ -1,4 +1,8 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -q -m gpu -k "staged or solve_paths" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+for r in 1 2; do
+MGRX_PDL=1 timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-variant > gpurun_out/bp_trig_$r.json 2>&1
+MGRX_LIB=$PWD/variants/libmgrx_notrig.so MGRX_PDL=1 timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-variant > gpurun_out/bp_notrig_$r.json 2>&1
+MGRX_PDL=0 timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-variant > gpurun_out/bp_off_$r.json 2>&1
+done
 echo done
