@@ -6,6 +6,7 @@
 // reproducible. The host reads the Hessenberg column once per step (one
 // small D2H copy), exactly where the reference needs scalar control flow.
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 #include "krylov.cuh"
@@ -480,8 +481,45 @@ double device_dot(int n, const double* a, const double* b, GmresWork& ws, cudaSt
   return read_scalar(ws.scal.get(), s);
 }
 
+namespace {
+// MGRX_GMRES_PROF=1: per-step event timeline of the fused-Arnoldi loop,
+// printed at the end of the solve (prec / spmv / arnoldi / D2H / gap from the
+// previous step's D2H to this step's first kernel = host bubble).
+struct StepProf {
+  bool on = false;
+  cudaEvent_t ev[5] = {};
+  cudaEvent_t last = nullptr;
+  double acc[5] = {};
+  int steps = 0;
+  StepProf() {
+    const char* v = std::getenv("MGRX_GMRES_PROF");
+    on = v && v[0] == '1';
+    if (!on) return;
+    for (auto& e : ev) cudaEventCreate(&e);
+    cudaEventCreate(&last);
+  }
+  void rec(int i, cudaStream_t s) { cudaEventRecord(ev[i], s); }
+  void step() {
+    float t[5] = {};
+    if (steps > 0) cudaEventElapsedTime(&t[0], last, ev[0]);
+    for (int i = 1; i < 5; ++i) cudaEventElapsedTime(&t[i], ev[i - 1], ev[i]);
+    for (int i = 0; i < 5; ++i) acc[i] += t[i];
+    std::swap(last, ev[4]);
+    ++steps;
+  }
+  ~StepProf() {
+    if (!on) return;
+    std::fprintf(stderr, "GMRES_PROF steps %d ms: gap %.3f prec %.3f spmv %.3f arnoldi %.3f d2h %.3f\n", steps, acc[0],
+                 acc[1], acc[2], acc[3], acc[4]);
+    for (auto& e : ev) cudaEventDestroy(e);
+    cudaEventDestroy(last);
+  }
+};
+}  // namespace
+
 GmresResult gmres_device(const DCsr& A, const double* b, double* x, const KrylovSpec& cfg,
                          const DevOp& precond, GmresWork& ws, cudaStream_t s) {
+  StepProf prof;
   const int n = A.rows;
   if (cfg.restart < 1) throw InvalidArgument("gmres: restart must be >= 1");
   const int m = cfg.restart;
@@ -540,14 +578,20 @@ GmresResult gmres_device(const DCsr& A, const double* b, double* x, const Krylov
       int k = 0;
       bool breakdown = false;
       for (; k < m && res.iterations < cfg.max_iters; ++k) {
+        if (prof.on) prof.rec(0, s);
         prec(col(k), ws.z.get());
+        if (prof.on) prof.rec(1, s);
         spmv(A, ws.z.get(), ws.w.get(), s);  // w = A M^{-1} v_k
+        if (prof.on) prof.rec(2, s);
         double wn;
         if (const int slots = arnoldi_slots(n)) {
           // both MGS passes + re-orthogonalisation test + v_{k+1} in one kernel
           arnoldi_launch(n, k, slots, 0, ws, s);
+          if (prof.on) prof.rec(3, s);
           MGRX_CK(cudaMemcpyAsync(H_pin, S, col_bytes, cudaMemcpyDeviceToHost, s));
+          if (prof.on) prof.rec(4, s);
           MGRX_CK(cudaStreamSynchronize(s));
+          if (prof.on) prof.step();
           wn = std::sqrt(H_pin[1]);
         } else {
           // pass 1: h_i = v_i . w ; w -= h_i v_i  (krylov.cpp:84-89)

@@ -534,6 +534,13 @@ int staged_ctas_per_sm() {
   return c;
 }
 
+int staged_min_rows() {
+  static const int m = [] {
+    const char* v = std::getenv("MGRX_SPMV_STAGED_MIN");
+    return v ? std::atoi(v) : 2048;
+  }();
+  return m;
+}
 bool staged_force() {
   static const bool f = [] {
     const char* v = std::getenv("MGRX_SPMV_STAGED");
@@ -605,7 +612,7 @@ void launch_spmv(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
 void spmv_prepare(DCsr& A, cudaStream_t s) {
   A.nblk = 0;
   A.plan.release();
-  if (A.rows < 65536) return;
+  if (A.rows < staged_min_rows()) return;
   const int kStRows = staged_geom() == 0 ? StA::R : StB::R;
   const int kStE = staged_geom() == 0 ? StA::E : StB::E;
   const std::vector<int> p = A.ptr.download(A.rows + 1);
@@ -646,9 +653,17 @@ void spmv_prepare(DCsr& A, cudaStream_t s) {
     if (staged) plan = std::move(A.plan);
     return ms;
   };
-  const float td = time(false), ts = time(true);
+  // best of three trials each, interleaved (robust to clock / neighbour noise)
+  float td = 1e30f, ts = 1e30f;
+  for (int trial = 0; trial < 3; ++trial) {
+    td = std::min(td, time(false));
+    ts = std::min(ts, time(true));
+  }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  if (const char* v = std::getenv("MGRX_VERBOSE"); v && v[0] == '1')
+    std::fprintf(stderr, "spmv_prepare rows %d cols %d nnz %d: direct %.1f us staged %.1f us -> %s\n", A.rows, A.cols,
+                 A.nnz, 200.f * td, 200.f * ts, (ts < 0.97f * td || staged_force()) ? "staged" : "direct");
   A.nblk = 0;
   if (ts < 0.97f * td || staged_force()) {
     A.plan = std::move(plan);

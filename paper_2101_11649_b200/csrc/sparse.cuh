@@ -40,7 +40,8 @@ DCsr csr_copy(const DCsr& A, cudaStream_t s);
 
 // ---- SpMV family (solve path) ---------------------------------------------
 // Build the block plan of the bulk-copy-staged SpMV for a solve-path matrix
-// (rows >= 65536); matrices without a plan use the direct kernels. Host-
+// (rows >= 2048; kept only where it times faster than the direct kernels);
+// matrices without a plan use the direct kernels. Host-
 // synchronising: call at setup, never inside a captured region.
 void spmv_prepare(DCsr& A, cudaStream_t s);
 // y = A x                                (Eigen y = A*x: 0 + row sum)
