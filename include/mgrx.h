@@ -107,9 +107,14 @@ MGRX_API int mgrx_apply(mgrx_hier* h, const double* v, double* z, int on_device)
 
 /* Right-preconditioned restarted GMRES with M = mgr_apply (gmres()). x holds
  * the initial guess on entry and the solution on exit. Returns MGRX_OK or
- * MGRX_NOT_CONVERGED (report filled in both cases). */
+ * MGRX_NOT_CONVERGED (report filled in both cases).
+ * flags: bit 0 (MGRX_ON_DEVICE) b and x are device pointers (else host; use
+ * pinned host memory for full copy bandwidth); bit 1 (MGRX_ZERO_GUESS) the
+ * initial guess is zero and x is not read (no host->device copy of x). */
+#define MGRX_ON_DEVICE 1
+#define MGRX_ZERO_GUESS 2
 MGRX_API int mgrx_solve(mgrx_hier* h, const double* b, double* x, const mgrx_krylov* cfg,
-               mgrx_report* report, int on_device);
+               mgrx_report* report, int flags);
 
 /* Parity dumps. path grammar:
  *   mgr.<l>.{A,P,R,F,C,frelax.dinv}   mgr.coarse.A

@@ -251,14 +251,26 @@ class Hierarchy:
         _check(lib().mgrx_apply(self._h, C.c_void_p(v_ptr), C.c_void_p(z_ptr), 1))
 
     def solve(self, b: np.ndarray, x: Optional[np.ndarray] = None, cfg: Optional[KrylovConfig] = None,
-              history_cap: int = 4096) -> tuple:
+              history_cap: int = 4096, out: Optional[np.ndarray] = None) -> tuple:
+        """gmres(A, b, x0, cfg, M) with host arrays. x (initial guess) is not
+        modified; None means a zero guess (nothing copied to the device). The
+        solution goes to `out` when given (contiguous float64 of size n, e.g.
+        pinned memory), else to a new array."""
         cfg = cfg or KrylovConfig()
         b = np.ascontiguousarray(b, dtype=np.float64)
-        x = np.zeros(self.n) if x is None else np.ascontiguousarray(x, dtype=np.float64).copy()
+        if out is None:
+            out = np.empty(self.n)
+        elif out.dtype != np.float64 or out.size != self.n or not out.flags.c_contiguous:
+            raise MgrxError(INVALID_ARGUMENT, "solve: out must be a contiguous float64 array of size n")
+        flags = 0
+        if x is None:
+            flags |= 2  # MGRX_ZERO_GUESS
+        else:
+            np.copyto(out, np.asarray(x, dtype=np.float64).reshape(-1))
         rep, hist = self._report(history_cap)
         k = _Krylov(cfg.restart, cfg.max_iters, cfg.rel_tol, cfg.abs_tol)
-        _check(lib().mgrx_solve(self._h, _ptr(b), _ptr(x), C.byref(k), C.byref(rep), 0))
-        return x, self._to_report(rep, hist)
+        _check(lib().mgrx_solve(self._h, _ptr(b), _ptr(out), C.byref(k), C.byref(rep), flags))
+        return out, self._to_report(rep, hist)
 
     def solve_device(self, b_ptr: int, x_ptr: int, cfg: Optional[KrylovConfig] = None,
                      history_cap: int = 4096) -> SolveReport:

@@ -338,7 +338,9 @@ int mgrx_apply(mgrx_hier* h, const double* v, double* z, int on_device) {
 }
 
 int mgrx_solve(mgrx_hier* h, const double* b, double* x, const mgrx_krylov* cfg, mgrx_report* rep,
-               int on_device) {
+               int flags) {
+  const bool on_device = flags & MGRX_ON_DEVICE;
+  const bool zero_guess = flags & MGRX_ZERO_GUESS;
   return guarded([&] {
     use(h->ctx);
     if (!cfg) throw InvalidArgument("mgrx_solve: null config");
@@ -354,9 +356,12 @@ int mgrx_solve(mgrx_hier* h, const double* b, double* x, const mgrx_krylov* cfg,
     double* dx = x;
     if (!on_device) {
       h->vin.upload(b, n);
-      MGRX_CK(cudaMemcpyAsync(h->vout.get(), x, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+      if (zero_guess) MGRX_CK(cudaMemsetAsync(h->vout.get(), 0, sizeof(double) * n, s));
+      else MGRX_CK(cudaMemcpyAsync(h->vout.get(), x, sizeof(double) * n, cudaMemcpyHostToDevice, s));
       db = h->vin.get();
       dx = h->vout.get();
+    } else if (zero_guess) {
+      MGRX_CK(cudaMemsetAsync(dx, 0, sizeof(double) * n, s));
     }
     MgrHier* H = &h->H;
     const DevOp prec = [H](const double* in, double* out, cudaStream_t st) { H->apply_graph(in, out, st); };

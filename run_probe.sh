@@ -1,6 +1,5 @@
 #!/bin/bash
 mkdir -p gpurun_out
-for r in 1 2 3; do
-MGRX_VERBOSE=1 timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-variant > gpurun_out/bv_$r.json 2>gpurun_out/bv_$r.err
-done
+timeout 1200 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-variant > gpurun_out/be.json 2>gpurun_out/be.err
 echo done
