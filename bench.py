@@ -290,8 +290,8 @@ def main():
     try:
         with open(os.path.join(ROOT, "profiles", "r01", "roofline_traffic.json")) as f:
             tr = json.load(f)
-        if tr.get("kernel") == dom and tr.get("config") == CONFIG:
-            traffic = tr["dram_bytes_per_launch"]
+        if tr.get("config") == CONFIG and dom in tr.get("kernels", {}):
+            traffic = tr["kernels"][dom]["dram_bytes_per_launch"]
     except Exception:
         pass
     roof = {"bound": "hbm", "kernel": dom, "achieved": d["GBps"], "peak": peak, "unit": "GB/s",

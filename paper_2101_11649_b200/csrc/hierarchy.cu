@@ -276,7 +276,13 @@ void BoundRelax::apply(const double* r, const int* rrow, double* z, cudaStream_t
   }
 }
 
-constexpr int kFoldSweep0MaxRows = 65536;
+int fold_sweep0_max_rows() {
+  static const int m = [] {
+    const char* v = std::getenv("MGRX_FOLD_MAX");
+    return v ? std::atoi(v) : 65536;
+  }();
+  return m;
+}
 
 // sweep 0: z = w*(dinv*r); later: z += w*(dinv*(r - A z)) (relax.cpp:168-174).
 // Sweep 0 is folded into sweep 1 (its iterate is formed on the fly from r),
@@ -293,7 +299,7 @@ void BoundRelax::jacobi_sweeps(const double* rc, const int* rrow, double* z, dou
   // <= 64K rows faster, the 1M / 366K-row levels 15-20% slower).
   const double* cur = nullptr;
   double* bufs[2] = {w1.get(), w2.get()};
-  if (n > kFoldSweep0MaxRows) {
+  if (n > fold_sweep0_max_rows()) {
     jacobi0(n, spec.weight, dinv.get(), rc, rrow, w2.get(), st);
     cur = w2.get();
     bufs[1] = w0.get();  // w2 holds sweep 0; w0 is free (no gather when jacobi)

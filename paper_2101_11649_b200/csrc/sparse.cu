@@ -653,11 +653,36 @@ void spmv_prepare(DCsr& A, cudaStream_t s) {
     if (staged) plan = std::move(A.plan);
     return ms;
   };
-  // best of three trials each, interleaved (robust to clock / neighbour noise)
+  // best of three trials each, interleaved (robust to clock / neighbour noise).
+  // MGRX_SPMV_PLAN_FILE replays decisions recorded by an earlier run (so a
+  // profiler, which distorts these timings, sees the production choices).
   float td = 1e30f, ts = 1e30f;
-  for (int trial = 0; trial < 3; ++trial) {
-    td = std::min(td, time(false));
-    ts = std::min(ts, time(true));
+  const char* pf = std::getenv("MGRX_SPMV_PLAN_FILE");
+  bool replayed = false;
+  if (pf) {
+    if (FILE* f = std::fopen(pf, "r")) {
+      int r, c, z;
+      char what[16];
+      while (std::fscanf(f, "%d %d %d %15s", &r, &c, &z, what) == 4)
+        if (r == A.rows && c == A.cols && z == A.nnz) {
+          replayed = true;
+          const bool st = what[0] == 's';
+          ts = st ? 1.f : 2.f;
+          td = st ? 2.f : 1.f;
+        }
+      std::fclose(f);
+    }
+  }
+  if (!replayed) {
+    for (int trial = 0; trial < 3; ++trial) {
+      td = std::min(td, time(false));
+      ts = std::min(ts, time(true));
+    }
+    if (pf)
+      if (FILE* f = std::fopen(pf, "a")) {
+        std::fprintf(f, "%d %d %d %s\n", A.rows, A.cols, A.nnz, ts < 0.97f * td ? "staged" : "direct");
+        std::fclose(f);
+      }
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
