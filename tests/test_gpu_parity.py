@@ -84,6 +84,38 @@ def test_solve_parity(case):
     assert np.linalg.norm(rhs - M @ x) <= case["rtol"] * np.linalg.norm(rhs) * (1 + 1e-9)
 
 
+def test_solve_entry_modes():
+    """mgrx_solve's host / device / zero-guess paths give the same bits: x0 =
+    None (MGRX_ZERO_GUESS, nothing copied for x), an explicit zero x0, a
+    pinned-style `out` buffer, and device pointers; a nonzero x0 matches the
+    oracle started from the same x0."""
+    import torch
+    P = mx.mfd_problem(12, 12, 6, "iid")
+    t = mx.load_strategy("mfd_mgr_pi_c1_l1j")
+    H = mx.Hierarchy(mx.Matrix(P.ptr, P.col, P.val), P.partition, t)
+    cfg = mx.KrylovConfig(restart=30, rel_tol=1e-8)
+    x1, r1 = H.solve(P.rhs, None, cfg)
+    x2, r2 = H.solve(P.rhs, np.zeros(P.n), cfg)
+    out = np.full(P.n, np.nan)
+    x3, r3 = H.solve(P.rhs, None, cfg, out=out)
+    assert x3 is out
+    b = torch.from_numpy(P.rhs).cuda()
+    xd = torch.full((P.n,), 7.0, dtype=torch.float64, device="cuda")
+    xd.zero_()
+    r4 = H.solve_device(b.data_ptr(), xd.data_ptr(), cfg)
+    for x, r in ((x2, r2), (x3, r3), (xd.cpu().numpy(), r4)):
+        assert np.array_equal(x.view(np.int64), x1.view(np.int64))
+        assert r.residual_history == r1.residual_history
+    x0 = np.random.default_rng(4).uniform(-1, 1, P.n)
+    R = refcpu.RefHierarchy(P.ptr, P.col, P.val, P.partition.field_order, P.partition.labels, t)
+    x5, r5 = H.solve(P.rhs, x0, cfg)
+    xr, rr = R.solve(P.rhs, restart=30, rel_tol=1e-8, x0=x0)
+    assert r5.residual_history == rr["history"]
+    assert np.array_equal(x5.view(np.int64), xr.view(np.int64))
+    with pytest.raises(mx.MgrxError, match="out must be"):
+        H.solve(P.rhs, None, cfg, out=np.zeros(P.n, np.float32))
+
+
 @pytest.mark.parametrize("case", make_golden.CASES, ids=lambda c: c["id"])
 def test_apply_matches_oracle(case):
     ptr, col, val, fields, labels, um, rhs = make_golden.build_problem(case["problem"])

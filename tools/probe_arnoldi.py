@@ -18,5 +18,5 @@ for dbg in ("0", "1", "2", "3"):
         res.append(f"k={k}: {ms * 1e3:7.1f} us ({by / ms / 1e6:6.0f} GB/s)")
     print(os.environ.get("TAG", ""), "dbg", dbg, " | ".join(res), flush=True)
 if os.environ.get("TRACE"):
-    os.environ["MGRX_ARNOLDI_DBG"] = "8"
+    os.environ["MGRX_ARNOLDI_DBG"] = os.environ.get("TRACE_DBG", "8")
     H.time_kernel("arnoldi.9", reps=1)
