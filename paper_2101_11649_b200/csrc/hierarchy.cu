@@ -110,6 +110,87 @@ __global__ void k_mgr_restrict(int nc, bool injection, const int* __restrict__ p
   if (!kFill) cnt[j] = c;
 }
 
+// P from W = A_FF^{-1} A_FC (ideal interpolation through a block or dense
+// solve): F rows -W(fpos, :), C rows the identity (build_interp,
+// proj/src/mgr.cpp:105-113).
+template <bool kFill>
+__global__ void k_interp_from_w(int n, const int* __restrict__ fpos, const int* __restrict__ cpos,
+                                const int* __restrict__ wptr, const int* __restrict__ wcol,
+                                const double* __restrict__ wval, int* __restrict__ cnt,
+                                const int* __restrict__ optr, int* __restrict__ ocol, double* __restrict__ oval) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  if (cpos[r] >= 0) {
+    if (kFill) {
+      ocol[optr[r]] = cpos[r];
+      oval[optr[r]] = 1.0;
+    } else {
+      cnt[r] = 1;
+    }
+    return;
+  }
+  const int f = fpos[r];
+  if (!kFill) {
+    cnt[r] = wptr[f + 1] - wptr[f];
+    return;
+  }
+  int o = optr[r];
+  for (int k = wptr[f]; k < wptr[f + 1]; ++k, ++o) {
+    ocol[o] = wcol[k];
+    oval[o] = -wval[k];
+  }
+}
+
+// R from Z = A_CF A_FF^{-1} (ideal restriction): row j holds -Z(j, :) at the
+// global F columns and (C[j], 1), in column order (proj/src/mgr.cpp:137-145).
+template <bool kFill>
+__global__ void k_restrict_from_z(int nc, const int* __restrict__ C, const int* __restrict__ F,
+                                  const int* __restrict__ zptr, const int* __restrict__ zcol,
+                                  const double* __restrict__ zval, int* __restrict__ cnt,
+                                  const int* __restrict__ optr, int* __restrict__ ocol, double* __restrict__ oval) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nc) return;
+  if (!kFill) {
+    cnt[j] = zptr[j + 1] - zptr[j] + 1;
+    return;
+  }
+  const int r = C[j];
+  int o = optr[j];
+  bool placed = false;
+  for (int k = zptr[j]; k < zptr[j + 1]; ++k) {
+    const int g = F[zcol[k]];
+    if (!placed && g > r) {
+      ocol[o] = r;
+      oval[o++] = 1.0;
+      placed = true;
+    }
+    ocol[o] = g;
+    oval[o++] = -zval[k];
+  }
+  if (!placed) {
+    ocol[o] = r;
+    oval[o] = 1.0;
+  }
+}
+
+// X = A_FF^{-1} B by the exact routes of ff_inverse_times
+// (proj/src/mgr.cpp:46-65) other than the structurally diagonal one.
+DCsr ff_solve(const DCsr& Aff, const DCsr& B, const std::optional<std::vector<int>>& layout, cudaStream_t s) {
+  if (layout) {
+    BlockLU f;
+    block_factor(Aff, *layout, f, s);
+    return block_solve_columns(f, B, s);
+  }
+  if (Aff.rows <= 2000) {
+    DenseLU f;
+    dense_factor(Aff, f, s);
+    return dense_solve_columns(f, B, s);
+  }
+  throw RuntimeError(
+      "ideal transfer operators require a structurally diagonal A_FF, a declared block "
+      "layout, or |F| <= 2000 for a dense factorization");
+}
+
 __global__ void k_scatter_count(int m, const int* __restrict__ idx, const int* __restrict__ sptr,
                                 int* __restrict__ cnt) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
@@ -189,8 +270,10 @@ void BoundRelax::bind(const SmootherSpec& s, const DCsr& mat, const std::vector<
     }
     case Smoother::hybrid_l1_gs_forward:
     case Smoother::hybrid_l1_gs_backward: {
-      // Normalise the partition exactly like proj/src/relax.cpp:12-23; the
-      // device sweep implements the single-range case.
+      // Normalise the partition exactly like proj/src/relax.cpp:12-23. With
+      // several ranges, rows read the snapshot across ranges: the sweep's
+      // dependencies and the L1 diagonal follow the range owner of each row.
+      const int* own = nullptr;
       if (!s.partition.empty()) {
         int expect = 0;
         for (const auto& [b, e] : s.partition) {
@@ -199,17 +282,25 @@ void BoundRelax::bind(const SmootherSpec& s, const DCsr& mat, const std::vector<
           expect = e;
         }
         if (expect != n) throw InvalidArgument("smoother partition does not cover the matrix");
-        if (s.partition.size() > 1)
-          throw RuntimeError("smoother: multi-range hybrid partitions are not supported on the device");
+        if (s.partition.size() > 1) {
+          std::vector<int> ho(n);
+          for (int k = 0; k < static_cast<int>(s.partition.size()); ++k)
+            for (int i = s.partition[k].first; i < s.partition[k].second; ++i) ho[i] = k;
+          owner.alloc(n, st);
+          owner.upload(ho.data(), n);
+          own = owner.get();
+        }
       }
-      l1_diagonal(mat, false, l1d, st);
-      gs_schedule(mat, s.kind == Smoother::hybrid_l1_gs_forward, l1d.get(), s.sweeps > 1, sched, st);
+      l1_diagonal(mat, false, l1d, st, own);
+      gs_schedule(mat, s.kind == Smoother::hybrid_l1_gs_forward, l1d.get(), s.sweeps > 1, sched, st, own);
       gs_bind_scratch(gs, st);
       break;
     }
     case Smoother::block_jacobi_exact:
+      // proj/src/relax.cpp:126-131, block LU per diagonal block
       if (s.block_sizes.empty()) throw InvalidArgument("smoother: block_jacobi_exact requires block sizes");
-      throw RuntimeError("smoother: block_jacobi_exact is not supported on the device path");
+      block_factor(mat, s.block_sizes, blk, st);
+      break;
     case Smoother::dense_lu:
       dense_factor(mat, lu, st);
       break;
@@ -244,6 +335,9 @@ void BoundRelax::apply(const double* r, const int* rrow, double* z, cudaStream_t
   switch (spec.kind) {
     case Smoother::dense_lu:
       dense_solve(lu, rc, z, st);
+      return;
+    case Smoother::block_jacobi_exact:
+      block_solve(blk, rc, z, st);
       return;
     case Smoother::jacobi:
     case Smoother::l1_jacobi:
@@ -567,19 +661,23 @@ void MgrHier::setup(const DCsr& A, const std::vector<int>& labels, const std::ve
     rank_flags(isf.get(), nl, L.fpos, s);
     rank_flags(isc.get(), nl, cpos, s);
 
-    if (spec.ff_block_sizes)
-      throw RuntimeError("ff_block_sizes layouts are not supported on the device path");
     L.Aff = extract(L.A, L.F.get(), nf, L.F.get(), nf, s);
+    // Diagonal A_FF (jacobi transfers, or ideal with a structurally diagonal
+    // A_FF): W = dinv_F * A_FC in the interpolation / restriction kernels.
+    // Otherwise ideal transfers solve with the declared block layout or a
+    // dense LU (ff_inverse_times).
+    const bool ideal_any = spec.interp == Interp::ideal || spec.restrict_kind == Restrict::ideal;
+    const bool diag_ff = ideal_any ? structurally_diagonal(L.Aff, s) : true;
     DVec<double> dinv_f;
-    if (spec.interp == Interp::ideal || spec.restrict_kind == Restrict::ideal) {
-      if (!structurally_diagonal(L.Aff, s))
-        throw RuntimeError(
-            "ideal transfer operators with a non-diagonal A_FF are not supported on the device path");
-    }
-    diag_inverse(L.Aff, dinv_f, s);
+    bool have_dinv = false;
+    auto need_dinv = [&] {
+      if (!have_dinv) diag_inverse(L.Aff, dinv_f, s);
+      have_dinv = true;
+    };
 
     // P (build_interp)
-    {
+    if (spec.interp == Interp::jacobi || diag_ff) {
+      need_dinv();
       DVec<int> cnt(nl, s);
       L.P.rows = nl;
       L.P.cols = nc;
@@ -593,23 +691,58 @@ void MgrHier::setup(const DCsr& A, const std::vector<int>& labels, const std::ve
       launch1d(k_mgr_interp<true>, nl, s, L.A.ptr.get(), L.A.col.get(), L.A.val.get(), L.fpos.get(),
                cpos.get(), dinv_f.get(), static_cast<int*>(nullptr), L.P.ptr.get(), L.P.col.get(),
                L.P.val.get());
+    } else {
+      const DCsr Afc = extract(L.A, L.F.get(), nf, L.C.get(), nc, s);
+      const DCsr W = ff_solve(L.Aff, Afc, spec.ff_block_sizes, s);
+      DVec<int> cnt(nl, s);
+      L.P.rows = nl;
+      L.P.cols = nc;
+      L.P.ptr.alloc(nl + 1, s);
+      launch1d(k_interp_from_w<false>, nl, s, L.fpos.get(), cpos.get(), W.ptr.get(), W.col.get(), W.val.get(),
+               cnt.get(), static_cast<const int*>(nullptr), static_cast<int*>(nullptr),
+               static_cast<double*>(nullptr));
+      L.P.nnz = static_cast<int>(exclusive_scan(cnt.get(), L.P.ptr.get(), nl, s));
+      L.P.col.alloc(L.P.nnz, s);
+      L.P.val.alloc(L.P.nnz, s);
+      launch1d(k_interp_from_w<true>, nl, s, L.fpos.get(), cpos.get(), W.ptr.get(), W.col.get(), W.val.get(),
+               static_cast<int*>(nullptr), L.P.ptr.get(), L.P.col.get(), L.P.val.get());
     }
     // R (build_restrict)
     L.injection = spec.restrict_kind == Restrict::injection;
-    {
+    if (L.injection || spec.restrict_kind == Restrict::jacobi || diag_ff) {
+      if (!L.injection) need_dinv();
       DVec<int> cnt(nc, s);
       L.R.rows = nc;
       L.R.cols = nl;
       L.R.ptr.alloc(nc + 1, s);
       launch1d(k_mgr_restrict<false>, nc, s, L.injection, L.A.ptr.get(), L.A.col.get(), L.A.val.get(),
-               L.C.get(), L.fpos.get(), dinv_f.get(), cnt.get(), static_cast<const int*>(nullptr),
-               static_cast<int*>(nullptr), static_cast<double*>(nullptr));
+               L.C.get(), L.fpos.get(), static_cast<const double*>(dinv_f.get()), cnt.get(),
+               static_cast<const int*>(nullptr), static_cast<int*>(nullptr), static_cast<double*>(nullptr));
       L.R.nnz = static_cast<int>(exclusive_scan(cnt.get(), L.R.ptr.get(), nc, s));
       L.R.col.alloc(L.R.nnz, s);
       L.R.val.alloc(L.R.nnz, s);
       launch1d(k_mgr_restrict<true>, nc, s, L.injection, L.A.ptr.get(), L.A.col.get(), L.A.val.get(),
-               L.C.get(), L.fpos.get(), dinv_f.get(), static_cast<int*>(nullptr), L.R.ptr.get(),
-               L.R.col.get(), L.R.val.get());
+               L.C.get(), L.fpos.get(), static_cast<const double*>(dinv_f.get()), static_cast<int*>(nullptr),
+               L.R.ptr.get(), L.R.col.get(), L.R.val.get());
+    } else {
+      // A_CF A_FF^{-1} = (A_FF^{-T} A_CF^T)^T (proj/src/mgr.cpp:128-133)
+      const DCsr Acf = extract(L.A, L.C.get(), nc, L.F.get(), nf, s);
+      const DCsr AffT = transpose(L.Aff, s);
+      const DCsr AcfT = transpose(Acf, s);
+      const DCsr Zt = ff_solve(AffT, AcfT, spec.ff_block_sizes, s);
+      const DCsr Z = transpose(Zt, s);
+      DVec<int> cnt(nc, s);
+      L.R.rows = nc;
+      L.R.cols = nl;
+      L.R.ptr.alloc(nc + 1, s);
+      launch1d(k_restrict_from_z<false>, nc, s, L.C.get(), L.F.get(), Z.ptr.get(), Z.col.get(), Z.val.get(),
+               cnt.get(), static_cast<const int*>(nullptr), static_cast<int*>(nullptr),
+               static_cast<double*>(nullptr));
+      L.R.nnz = static_cast<int>(exclusive_scan(cnt.get(), L.R.ptr.get(), nc, s));
+      L.R.col.alloc(L.R.nnz, s);
+      L.R.val.alloc(L.R.nnz, s);
+      launch1d(k_restrict_from_z<true>, nc, s, L.C.get(), L.F.get(), Z.ptr.get(), Z.col.get(), Z.val.get(),
+               static_cast<int*>(nullptr), L.R.ptr.get(), L.R.col.get(), L.R.val.get());
     }
     // F-relaxation smoother on A_FF (+ optional global relaxation on A)
     std::vector<int> umap_f;

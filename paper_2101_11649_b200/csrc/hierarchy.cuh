@@ -11,6 +11,7 @@
 #include <string>
 #include <vector>
 
+#include "blocklu.cuh"
 #include "dense.cuh"
 #include "relax.cuh"
 #include "strategy.hpp"
@@ -27,6 +28,8 @@ struct BoundRelax {
   DVec<double> dinv;  // jacobi / l1_jacobi
   DVec<double> l1d;   // gauss-seidel
   GsSchedule sched;
+  DVec<int> owner;    // gauss-seidel with a multi-range hybrid partition: range id per row
+  BlockLU blk;        // block_jacobi_exact
   std::unique_ptr<AmgHier> amg;
   DenseLU lu;
   DVec<double> w0, w1, w2;  // workspace

@@ -554,14 +554,20 @@ std::vector<int> pipe_steps(const std::vector<int>& level_ptr, const std::vector
 
 // Dependency levels by monotone in-place relaxation: lev[i] = 1 + max over
 // dependencies; converges to the longest-path level.
+// Dependency test of a sweep: j is visited before i in i's own range
+// (hybrid partitions, proj/src/relax.cpp:68-73: other ranges read the
+// snapshot). owner == nullptr: one range.
+__device__ __forceinline__ bool is_dep(int i, int j, int fwd, const int* __restrict__ owner) {
+  return (fwd ? (j < i) : (j > i)) && (owner == nullptr || owner[j] == owner[i]);
+}
 __global__ void k_levels(int n, const int* __restrict__ ptr, const int* __restrict__ col, int fwd,
-                         int* lev, int* changed) {
+                         const int* __restrict__ owner, int* lev, int* changed) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int m = 0;
   for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
     const int j = col[k];
-    if (fwd ? (j < i) : (j > i)) {
+    if (is_dep(i, j, fwd, owner)) {
       const int l = ld_relaxed_int(lev + j) + 1;
       m = l > m ? l : m;
     }
@@ -577,28 +583,29 @@ __global__ void k_iota(int n, int* a) {
 }
 // Sweep CSR construction (positions p in sweep order).
 __global__ void k_sweep_count(int n, const int* __restrict__ order, const int* __restrict__ ptr,
-                              const int* __restrict__ col, int fwd, int full, int* __restrict__ cnt) {
+                              const int* __restrict__ col, int fwd, const int* __restrict__ owner, int full,
+                              int* __restrict__ cnt) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const int i = order[p];
   int c = 0;
   for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
     const int j = col[k];
-    c += (full || (fwd ? j < i : j > i)) ? 1 : 0;
+    c += (full || is_dep(i, j, fwd, owner)) ? 1 : 0;
   }
   cnt[p] = c;
 }
 __global__ void k_sweep_fill(int n, const int* __restrict__ order, const int* __restrict__ ptr,
                              const int* __restrict__ col, const double* __restrict__ val, int fwd,
-                             int full, const int* __restrict__ sptr, int* __restrict__ scol,
-                             double* __restrict__ sval) {
+                             const int* __restrict__ owner, int full, const int* __restrict__ sptr,
+                             int* __restrict__ scol, double* __restrict__ sval) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const int i = order[p];
   int o = sptr[p];
   for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
     const int j = col[k];
-    const bool dep = fwd ? j < i : j > i;
+    const bool dep = is_dep(i, j, fwd, owner);
     if (!full && !dep) continue;
     scol[o] = (full && dep) ? (j | kDepBit) : j;
     sval[o] = val[k];
@@ -630,21 +637,21 @@ __global__ void k_recip(int n, const double* __restrict__ d, double* __restrict_
   if (i < n) y[i] = __ddiv_rn(1.0, d[i]);
 }
 
-void build_sweep_csr(const DCsr& A, const GsSchedule& sch, bool forward, bool full, DVec<int>& sptr,
-                     DVec<int>& scol, DVec<double>& sval, cudaStream_t s) {
+void build_sweep_csr(const DCsr& A, const GsSchedule& sch, bool forward, const int* owner, bool full,
+                     DVec<int>& sptr, DVec<int>& scol, DVec<double>& sval, cudaStream_t s) {
   const int n = A.rows;
   DVec<int> cnt(n, s);
   sptr.alloc(n + 1, s);
   const int nb = blocks_for(n, 256);
   k_sweep_count<<<nb, 256, 0, s>>>(n, sch.order.get(), A.ptr.get(), A.col.get(), forward ? 1 : 0,
-                                   full ? 1 : 0, cnt.get());
+                                   owner, full ? 1 : 0, cnt.get());
   MGRX_LAUNCH_CK();
   count_launch();
   const int nnz = static_cast<int>(exclusive_scan(cnt.get(), sptr.get(), n, s));
   scol.alloc(nnz > 0 ? nnz : 1, s);
   sval.alloc(nnz > 0 ? nnz : 1, s);
   k_sweep_fill<<<nb, 256, 0, s>>>(n, sch.order.get(), A.ptr.get(), A.col.get(), A.val.get(),
-                                  forward ? 1 : 0, full ? 1 : 0, sptr.get(), scol.get(), sval.get());
+                                  forward ? 1 : 0, owner, full ? 1 : 0, sptr.get(), scol.get(), sval.get());
   MGRX_LAUNCH_CK();
   count_launch();
 }
@@ -695,7 +702,7 @@ void trace_end(Trace& tr, const char* dir, const GsSchedule& sch, int n, cudaStr
 }
 
 void gs_schedule(const DCsr& A, bool forward, const double* d, bool full, GsSchedule& out,
-                 cudaStream_t s) {
+                 cudaStream_t s, const int* owner) {
   const int n = A.rows;
   out.order.alloc(n > 0 ? n : 1, s);
   out.levels = 0;
@@ -707,7 +714,8 @@ void gs_schedule(const DCsr& A, bool forward, const double* d, bool full, GsSche
   while (true) {
     flag.zero();
     for (int it = 0; it < 8; ++it)
-      k_levels<<<nb, 256, 0, s>>>(n, A.ptr.get(), A.col.get(), forward ? 1 : 0, lev.get(), flag.get());
+      k_levels<<<nb, 256, 0, s>>>(n, A.ptr.get(), A.col.get(), forward ? 1 : 0, owner, lev.get(),
+                                  flag.get());
     MGRX_LAUNCH_CK();
     count_launch(8);
     if (read_scalar(flag.get(), s) == 0) break;
@@ -729,9 +737,9 @@ void gs_schedule(const DCsr& A, bool forward, const double* d, bool full, GsSche
   for (int p = 0; p < n; ++p) ++out.level_ptr[ls[p] + 1];
   for (int l = 0; l < out.levels; ++l) out.level_ptr[l + 1] += out.level_ptr[l];
 
-  build_sweep_csr(A, out, forward, false, out.dptr, out.dcol, out.dval, s);
+  build_sweep_csr(A, out, forward, owner, false, out.dptr, out.dcol, out.dval, s);
   out.has_full = full;
-  if (full) build_sweep_csr(A, out, forward, true, out.fptr, out.fcol, out.fval, s);
+  if (full) build_sweep_csr(A, out, forward, owner, true, out.fptr, out.fcol, out.fval, s);
   out.sd.alloc(n, s);
   gather(n, out.order.get(), d, out.sd.get(), s);
   int dep_nnz = 0;

@@ -1,5 +1,6 @@
 // Smoother kernels: pointwise Jacobi/l1-Jacobi and the exact, sync-free
-// Gauss-Seidel sweep (proj/src/relax.cpp:55-78 with one range).
+// Gauss-Seidel sweep (proj/src/relax.cpp:55-78, one range or a hybrid
+// partition of ranges).
 #pragma once
 
 #include "sparse.cuh"
@@ -37,8 +38,10 @@ struct GsSchedule {
   int ndsteps = 0, nfsteps = 0;
   DVec<double> bp;                 // rhs gathered into sweep order (pipelined sweep)
 };
+// owner (nullable): range id per row for a multi-range hybrid partition;
+// dependencies are then only the earlier rows of the row's own range.
 void gs_schedule(const DCsr& A, bool forward, const double* d, bool full, GsSchedule& out,
-                 cudaStream_t s);
+                 cudaStream_t s, const int* owner = nullptr);
 
 // Scratch for a GS sweep (ticket counter + error flag).
 struct GsScratch {

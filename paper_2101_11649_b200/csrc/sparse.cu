@@ -863,15 +863,15 @@ __global__ void k_diag_inverse(int n, const int* __restrict__ ptr, const int* __
   else if (d == 0.0) atomicMin(err, static_cast<unsigned long long>(i) * 2ull + 1ull);
   dinv[i] = __ddiv_rn(1.0, d);
 }
-__global__ void k_l1_diag(int n, bool singleton, const int* __restrict__ ptr, const int* __restrict__ col,
-                          const double* __restrict__ val, double* __restrict__ d,
+__global__ void k_l1_diag(int n, bool singleton, const int* __restrict__ owner, const int* __restrict__ ptr,
+                          const int* __restrict__ col, const double* __restrict__ val, double* __restrict__ d,
                           unsigned long long* __restrict__ err) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double s = 0.0;
   for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
     if (col[k] == i) s = __dadd_rn(s, val[k]);
-    else if (singleton) s = __dadd_rn(s, fabs(val[k]));
+    else if (singleton || (owner != nullptr && owner[col[k]] != owner[i])) s = __dadd_rn(s, fabs(val[k]));
   }
   d[i] = s;
   if (s == 0.0) atomicMin(err, static_cast<unsigned long long>(i));
@@ -1051,12 +1051,12 @@ void diag_inverse(const DCsr& A, DVec<double>& dinv, cudaStream_t s) {
   }
 }
 
-void l1_diagonal(const DCsr& A, bool singleton, DVec<double>& d, cudaStream_t s) {
+void l1_diagonal(const DCsr& A, bool singleton, DVec<double>& d, cudaStream_t s, const int* owner) {
   d.alloc(A.rows, s);
   DVec<unsigned long long> err(1, s);
   MGRX_CK(cudaMemsetAsync(err.get(), 0xff, sizeof(unsigned long long), s));
   if (A.rows) {
-    k_l1_diag<<<blocks_for(A.rows, 256), 256, 0, s>>>(A.rows, singleton, A.ptr.get(), A.col.get(),
+    k_l1_diag<<<blocks_for(A.rows, 256), 256, 0, s>>>(A.rows, singleton, owner, A.ptr.get(), A.col.get(),
                                                      A.val.get(), d.get(), err.get());
     MGRX_LAUNCH_CK();
     count_launch();

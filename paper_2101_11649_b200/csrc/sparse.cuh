@@ -75,7 +75,8 @@ DCsr gather_rows(const DCsr& A, const int* rows, int nrows, cudaStream_t s);
 void diag_inverse(const DCsr& A, DVec<double>& dinv, cudaStream_t s);
 // L1 diagonal with singleton (l1 = true) or whole-matrix range (l1 = false:
 // d_i = sum of stored diagonal entries), proj/src/relax.cpp:34-48.
-void l1_diagonal(const DCsr& A, bool singleton_ranges, DVec<double>& d, cudaStream_t s);
+void l1_diagonal(const DCsr& A, bool singleton_ranges, DVec<double>& d, cudaStream_t s,
+                 const int* owner = nullptr);
 bool structurally_diagonal(const DCsr& A, cudaStream_t s);
 
 // Host copies (tests / dumps).

@@ -45,6 +45,28 @@ GLOBAL_RELAX = {"name": "global_relax", "levels": [{"f_fields": ["f"], "interp":
                                                     "f_relax": {"kind": "jacobi"},
                                                     "global_relax": {"kind": "jacobi", "sweeps": 2, "weight": 0.7}}],
                 "coarse": {"kind": "dense_lu"}}
+# Device coverage of the non-default relaxation / transfer routes
+# (proj/src/relax.cpp:55-78 hybrid partitions, :126-131 block Jacobi;
+# proj/src/mgr.cpp:46-65 ideal transfers through a block layout or a dense LU).
+GS_PARTITION = {"name": "gs_partition", "levels": [
+    {"f_fields": ["f"], "interp": "jacobi", "restrict": "injection",
+     "f_relax": {"kind": "hybrid_l1_gs_forward", "sweeps": 2,
+                 "partition": [[0, 30], [30, 75], [75, 100]]},
+     "global_relax": {"kind": "hybrid_l1_gs_backward", "sweeps": 1,
+                      "partition": [[0, 64], [64, 130], [130, 200]]}}],
+    "coarse": {"kind": "dense_lu"}}
+BLOCK_IDEAL = {"name": "block_ideal", "levels": [
+    {"f_fields": ["f"], "interp": "ideal", "restrict": "ideal", "ff_block_sizes": [4] * 25,
+     "f_relax": {"kind": "block_jacobi_exact", "block_sizes": [5] * 20}}],
+    "coarse": {"kind": "dense_lu"}}
+DENSE_IDEAL = {"name": "dense_ideal", "levels": [
+    {"f_fields": ["f"], "interp": "ideal", "restrict": "jacobi",
+     "f_relax": {"kind": "block_jacobi_exact", "block_sizes": [10] * 10, "sweeps": 1}}],
+    "coarse": {"kind": "amg_vcycle", "cycles": 1, "amg": {"coarse_size": 20}}}
+DENSE_IDEAL_R = {"name": "dense_ideal_r", "levels": [
+    {"f_fields": ["f"], "interp": "jacobi", "restrict": "ideal",
+     "f_relax": {"kind": "l1_jacobi", "sweeps": 2}}],
+    "coarse": {"kind": "dense_lu"}}
 
 
 def laplace2d(nx, ny):
@@ -157,6 +179,14 @@ CASES = [
      "strategy": "comp_mgr", "rtol": 1e-5},
     {"id": "frac_m6_mgr_u", "problem": {"kind": "frac", "m": 6}, "strategy": "frac_mgr_u", "rtol": 1e-6},
     {"id": "frac_m10_mgr_u", "problem": {"kind": "frac", "m": 10}, "strategy": "frac_mgr_u", "rtol": 1e-6},
+    {"id": "sdd200_gs_partition", "problem": {"kind": "sdd2", "n": 200}, "strategy": GS_PARTITION,
+     "rtol": 1e-9},
+    {"id": "sdd200_block_ideal", "problem": {"kind": "sdd2", "n": 200}, "strategy": BLOCK_IDEAL,
+     "rtol": 1e-9},
+    {"id": "sdd200_dense_ideal", "problem": {"kind": "sdd2", "n": 200}, "strategy": DENSE_IDEAL,
+     "rtol": 1e-9},
+    {"id": "sdd300_dense_ideal_r", "problem": {"kind": "sdd2", "n": 300, "seed": 62}, "strategy": DENSE_IDEAL_R,
+     "rtol": 1e-9},
     {"id": "sdd400_restrict_jacobi", "problem": {"kind": "sdd2", "n": 400}, "strategy": TWO_FIELD_RJAC,
      "rtol": 1e-9},
 ]

@@ -205,6 +205,44 @@ def test_zero_rhs_and_errors():
         mx.Matrix(np.array([0, 2, 3], np.int32), np.array([1, 0, 1], np.int32), np.ones(3))
 
 
+def test_block_layout_and_partition_errors():
+    """Errors of the block / dense / partitioned routes carry the reference's
+    messages (proj/src/sparse.cpp:167-183, proj/src/mgr.cpp:62-64,
+    proj/src/relax.cpp:12-23)."""
+    ptr, col, val, fields, labels, um, rhs = make_golden.build_problem({"kind": "sdd2", "n": 200})
+    A = mx.Matrix(ptr, col, val)
+    part = mx.DofPartition(fields, labels)
+
+    def lvl(**kw):
+        base = {"f_fields": ["f"], "interp": "jacobi", "restrict": "injection", "f_relax": {"kind": "jacobi"}}
+        base.update(kw)
+        return json.dumps({"levels": [base], "coarse": {"kind": "dense_lu"}})
+
+    with pytest.raises(mx.MgrxError, match="block layout does not cover the matrix"):
+        mx.Hierarchy(A, part, lvl(interp="ideal", ff_block_sizes=[4] * 24))
+    with pytest.raises(mx.MgrxError, match="block layout does not cover the matrix"):
+        mx.Hierarchy(A, part, lvl(f_relax={"kind": "block_jacobi_exact", "block_sizes": [3] * 10}))
+    with pytest.raises(mx.MgrxInvalidArgument, match="requires block sizes"):
+        mx.Hierarchy(A, part, lvl(f_relax={"kind": "block_jacobi_exact"}))
+    with pytest.raises(mx.MgrxInvalidArgument, match="partition ranges must tile"):
+        mx.Hierarchy(A, part, lvl(f_relax={"kind": "hybrid_l1_gs_forward", "partition": [[0, 50], [40, 100]]}))
+    with pytest.raises(mx.MgrxInvalidArgument, match="partition does not cover the matrix"):
+        mx.Hierarchy(A, part, lvl(f_relax={"kind": "hybrid_l1_gs_forward", "partition": [[0, 50], [50, 99]]}))
+    # a singular diagonal block (block 1 = [[1, 1], [1, 1]], nonzero diagonal)
+    sp = np.array([0, 1, 2, 4, 6, 7, 8], np.int32)
+    sc = np.array([0, 1, 2, 3, 2, 3, 4, 5], np.int32)
+    sv = np.array([2.0, 3.0, 1.0, 1.0, 1.0, 1.0, 4.0, 5.0])
+    B = mx.Matrix(sp, sc, sv)
+    pb = mx.DofPartition(["f", "c"], np.array([0, 0, 0, 0, 1, 1], np.int32))
+    with pytest.raises(mx.MgrxError, match="block Jacobi: singular block 1"):
+        mx.Hierarchy(B, pb, json.dumps({"levels": [{"f_fields": ["f"], "f_relax": {
+            "kind": "block_jacobi_exact", "block_sizes": [2, 2]}}], "coarse": {"kind": "dense_lu"}}))
+    # ideal transfers with a non-diagonal A_FF, no layout and |F| > 2000
+    ptr, col, val, fields, labels, um, rhs = make_golden.build_problem({"kind": "sdd2", "n": 4200})
+    with pytest.raises(mx.MgrxError, match="require a structurally diagonal A_FF"):
+        mx.Hierarchy(mx.Matrix(ptr, col, val), mx.DofPartition(fields, labels), lvl(interp="ideal"))
+
+
 def test_identity_truncates_to_dense():
     n = 30
     ptr = np.arange(n + 1, dtype=np.int32)
