@@ -142,6 +142,36 @@ MGRX_API int mgrx_info(mgrx_hier* h, int* mgr_levels, int* coarse_amg_levels, in
 MGRX_API int mgrx_time_kernel(mgrx_hier* h, const char* which, int reps, double* avg_ms,
                               double* bytes);
 
+/* ---- Row-slab sharded solve (one rank per GPU) ----------
+ * The reference is single-process (proj/src/krylov.cpp:37-147 over
+ * proj/src/mgr.cpp:196-219); these calls distribute that same solve over
+ * ranks that each hold the same hierarchy (built by mgrx_setup on every
+ * rank) and own a contiguous block of fine rows; coarse levels follow (the
+ * C points inside each rank's range). Halo exchanges and the inner-product
+ * all-gathers run over NCCL (libnccl.so.2 is loaded at the first NCCL call),
+ * or, for tests, between ranks that are threads of one process sharing a
+ * "local group". Collective semantics: every rank of a group makes the same
+ * sequence of shard calls. */
+typedef struct mgrx_shard mgrx_shard;
+typedef struct mgrx_group mgrx_group;
+
+/* ncclGetUniqueId; rank 0 calls it and distributes the 128 bytes. */
+MGRX_API int mgrx_nccl_unique_id(unsigned char* out128);
+/* In-process ranks (threads on one device) for parity tests. */
+MGRX_API int mgrx_local_group_create(int size, mgrx_group** out);
+MGRX_API int mgrx_local_group_destroy(mgrx_group* g);
+/* row_starts: size+1 fine-row offsets (NULL = even split). Exactly one of
+ * nccl_id / group when size > 1. */
+MGRX_API int mgrx_shard_create(mgrx_hier* h, int rank, int size, const int* row_starts,
+                               const unsigned char* nccl_id, mgrx_group* group, mgrx_shard** out);
+MGRX_API int mgrx_shard_rows(mgrx_shard* sd, int* row_begin, int* row_end);
+/* z = M^{-1} v on the owned rows (bitwise equal to the owned rows of mgrx_apply). */
+MGRX_API int mgrx_shard_apply(mgrx_shard* sd, const double* v, double* z, int on_device);
+/* GMRES on the owned rows of b / x (flags as mgrx_solve). */
+MGRX_API int mgrx_shard_solve(mgrx_shard* sd, const double* b, double* x, const mgrx_krylov* cfg,
+                              mgrx_report* report, int flags);
+MGRX_API int mgrx_shard_destroy(mgrx_shard* sd);
+
 #ifdef __cplusplus
 }
 #endif

@@ -84,6 +84,14 @@ def lib() -> C.CDLL:
         L.mgrx_info.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_int]
         L.mgrx_time_kernel.argtypes = [vp, C.c_char_p, C.c_int, C.POINTER(C.c_double),
                                        C.POINTER(C.c_double)]
+        L.mgrx_nccl_unique_id.argtypes = [C.c_char_p]
+        L.mgrx_local_group_create.argtypes = [C.c_int, C.POINTER(vp)]
+        L.mgrx_local_group_destroy.argtypes = [vp]
+        L.mgrx_shard_create.argtypes = [vp, C.c_int, C.c_int, vp, C.c_char_p, vp, C.POINTER(vp)]
+        L.mgrx_shard_rows.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.mgrx_shard_apply.argtypes = [vp, vp, vp, C.c_int]
+        L.mgrx_shard_solve.argtypes = [vp, vp, vp, C.POINTER(_Krylov), C.POINTER(_Report), C.c_int]
+        L.mgrx_shard_destroy.argtypes = [vp]
         _lib = L
     return _lib
 
@@ -339,6 +347,116 @@ class Hierarchy:
             self.close()
         except Exception:
             pass
+
+
+# ---- row-slab sharded solve -----------------------------------
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId (rank 0 creates it and distributes it)."""
+    buf = C.create_string_buffer(128)
+    _check(lib().mgrx_nccl_unique_id(buf))
+    return buf.raw
+
+
+class LocalGroup:
+    """Ranks that are threads of this process on one device (parity tests)."""
+
+    def __init__(self, size: int):
+        self.size = size
+        self._h = C.c_void_p()
+        _check(lib().mgrx_local_group_create(size, C.byref(self._h)))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().mgrx_local_group_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Shard:
+    """This rank's slab of a hierarchy (every rank builds the same Hierarchy):
+    owned fine rows [row_begin, row_end); apply / solve on owned slices.
+    Collective: every rank of the group makes the same sequence of calls."""
+
+    def __init__(self, H: Hierarchy, rank: int, size: int, row_starts=None, nccl_id: Optional[bytes] = None,
+                 group: Optional[LocalGroup] = None):
+        self.H = H
+        st = None
+        if row_starts is not None:
+            st = np.ascontiguousarray(row_starts, dtype=np.int32)
+            if st.size != size + 1:
+                raise MgrxInvalidArgument(INVALID_ARGUMENT, "row_starts must have size+1 entries")
+        self._st = st
+        self._h = C.c_void_p()
+        _check(lib().mgrx_shard_create(H._h, rank, size, _ptr(st) if st is not None else None,
+                                       nccl_id, group._h if group is not None else None, C.byref(self._h)))
+        b, e = C.c_int(), C.c_int()
+        _check(lib().mgrx_shard_rows(self._h, C.byref(b), C.byref(e)))
+        self.row_begin, self.row_end = b.value, e.value
+        self.n = self.row_end - self.row_begin
+
+    def apply(self, v: np.ndarray) -> np.ndarray:
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        z = np.empty(self.n)
+        _check(lib().mgrx_shard_apply(self._h, _ptr(v), _ptr(z), 0))
+        return z
+
+    def solve(self, b: np.ndarray, x: Optional[np.ndarray] = None, cfg: Optional[KrylovConfig] = None,
+              history_cap: int = 4096, out: Optional[np.ndarray] = None) -> tuple:
+        cfg = cfg or KrylovConfig()
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        if out is None:
+            out = np.empty(self.n)
+        flags = 0
+        if x is None:
+            flags |= 2
+        else:
+            np.copyto(out, np.asarray(x, dtype=np.float64).reshape(-1))
+        rep, hist = Hierarchy._report(history_cap)
+        k = _Krylov(cfg.restart, cfg.max_iters, cfg.rel_tol, cfg.abs_tol)
+        _check(lib().mgrx_shard_solve(self._h, _ptr(b), _ptr(out), C.byref(k), C.byref(rep), flags))
+        return out, Hierarchy._to_report(rep, hist)
+
+    def solve_device(self, b_ptr: int, x_ptr: int, cfg: Optional[KrylovConfig] = None, zero_guess=False,
+                     history_cap: int = 4096) -> SolveReport:
+        cfg = cfg or KrylovConfig()
+        rep, hist = Hierarchy._report(history_cap)
+        k = _Krylov(cfg.restart, cfg.max_iters, cfg.rel_tol, cfg.abs_tol)
+        _check(lib().mgrx_shard_solve(self._h, C.c_void_p(b_ptr), C.c_void_p(x_ptr), C.byref(k), C.byref(rep),
+                                      1 | (2 if zero_guess else 0)))
+        return Hierarchy._to_report(rep, hist)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().mgrx_shard_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def slab_row_starts(problem: "Problem", size: int) -> np.ndarray:
+    """Fine-row offsets for `size` ranks cut at z-slab boundaries of a
+    generated bundle (slab-major numbering): ranks own whole
+    z-layers; falls back to an even split for bundles without slab metadata."""
+    n = problem.n
+    meta = problem.meta or {}
+    slabs = None
+    if meta.get("problem") == "mfd" and meta.get("numbering") == "slab-major-z":
+        nx, ny, nz = meta["dims"]
+        per = nx * ny + (nx + 1) * ny + nx * (ny + 1) + nx * ny
+        slabs = [k * per for k in range(nz)]
+    if not slabs or len(slabs) < size:
+        return np.array([n * q // size for q in range(size + 1)], np.int32)
+    k = len(slabs)
+    return np.array([slabs[(q * k) // size] for q in range(size)] + [n], np.int32)
 
 
 # ---- reference-named entry points -----------------------------------------

@@ -11,6 +11,7 @@
 #include "../../include/mgrx.h"
 #include "hierarchy.cuh"
 #include "krylov.cuh"
+#include "shard.cuh"
 
 using namespace mgrx;
 
@@ -32,6 +33,27 @@ struct mgrx_hier {
   double setup_s = 0.0;
   DVec<double> vin, vout;  // staging for host-pointer calls
   DVec<double> px, py, pz;  // roofline-probe operands
+};
+
+struct mgrx_group {
+  std::shared_ptr<LocalHub> hub;
+  int size = 0;
+};
+
+struct mgrx_shard {
+  mgrx_hier* h = nullptr;
+  cudaStream_t stream = nullptr;
+  std::unique_ptr<Shard> sh;
+  DVec<double> vin, vout;
+  ~mgrx_shard() {
+    sh.reset();
+    vin.release();
+    vout.release();
+    if (stream) {
+      cudaStreamSynchronize(stream);
+      cudaStreamDestroy(stream);
+    }
+  }
 };
 
 namespace {
@@ -499,6 +521,157 @@ int mgrx_time_kernel(mgrx_hier* h, const char* which, int reps, double* avg_ms, 
     for (int i = 0; i < reps; ++i) fn();
     *avg_ms = t.stop() * 1e3 / (reps > 0 ? reps : 1);
     *bytes = b;
+    return MGRX_OK;
+  });
+}
+
+// ---------------------------------------------------------------------------
+// Row-slab sharded solve
+// ---------------------------------------------------------------------------
+int mgrx_nccl_unique_id(unsigned char* out) {
+  return guarded([&] {
+    if (!out) throw InvalidArgument("mgrx_nccl_unique_id: null buffer");
+    nccl_unique_id(out);
+    return MGRX_OK;
+  });
+}
+
+int mgrx_local_group_create(int size, mgrx_group** out) {
+  return guarded([&] {
+    if (size < 1 || !out) throw InvalidArgument("mgrx_local_group_create: bad arguments");
+    auto* g = new mgrx_group;
+    g->hub = make_local_hub(size);
+    g->size = size;
+    *out = g;
+    return MGRX_OK;
+  });
+}
+
+int mgrx_local_group_destroy(mgrx_group* g) {
+  delete g;
+  return MGRX_OK;
+}
+
+int mgrx_shard_create(mgrx_hier* h, int rank, int size, const int* row_starts, const unsigned char* nccl_id,
+                      mgrx_group* group, mgrx_shard** out) {
+  return guarded([&] {
+    use(h->ctx);
+    if (!out || size < 1 || rank < 0 || rank >= size) throw InvalidArgument("mgrx_shard_create: bad rank/size");
+    if ((nccl_id == nullptr) == (group == nullptr) && size > 1)
+      throw InvalidArgument("mgrx_shard_create: give exactly one of nccl_id and group");
+    const int n = h->A.rows;
+    std::vector<int> st(size + 1);
+    if (row_starts) {
+      st.assign(row_starts, row_starts + size + 1);
+    } else {
+      for (int q = 0; q <= size; ++q) st[q] = static_cast<int>(static_cast<long long>(n) * q / size);
+    }
+    std::unique_ptr<Comm> cm;
+    if (group) {
+      if (group->size != size) throw InvalidArgument("mgrx_shard_create: group size mismatch");
+      cm = make_local_comm(group->hub, rank);
+    } else if (nccl_id) {
+      cm = make_nccl_comm(nccl_id, rank, size);
+    } else {
+      auto hub = make_local_hub(1);
+      cm = make_local_comm(hub, 0);
+    }
+    auto* sd = new mgrx_shard;
+    sd->h = h;
+    try {
+      MGRX_CK(cudaStreamCreateWithFlags(&sd->stream, cudaStreamNonBlocking));
+      MGRX_CK(cudaStreamSynchronize(h->ctx->stream));
+      sd->sh = std::make_unique<Shard>();
+      sd->sh->build(h->H, h->A, st, std::move(cm), sd->stream);
+      const int own = sd->sh->row_end - sd->sh->row_begin;
+      sd->vin.alloc(own, sd->stream);
+      sd->vout.alloc(own, sd->stream);
+    } catch (...) {
+      delete sd;
+      throw;
+    }
+    *out = sd;
+    return MGRX_OK;
+  });
+}
+
+int mgrx_shard_rows(mgrx_shard* sd, int* row_begin, int* row_end) {
+  return guarded([&] {
+    *row_begin = sd->sh->row_begin;
+    *row_end = sd->sh->row_end;
+    return MGRX_OK;
+  });
+}
+
+int mgrx_shard_apply(mgrx_shard* sd, const double* v, double* z, int on_device) {
+  return guarded([&] {
+    use(sd->h->ctx);
+    const int n = sd->sh->row_end - sd->sh->row_begin;
+    cudaStream_t s = sd->stream;
+    if (on_device) {
+      sd->sh->apply(v, z);
+      return MGRX_OK;
+    }
+    sd->vin.upload(v, n);
+    sd->sh->apply(sd->vin.get(), sd->vout.get());
+    MGRX_CK(cudaMemcpyAsync(z, sd->vout.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    MGRX_CK(cudaStreamSynchronize(s));
+    return MGRX_OK;
+  });
+}
+
+int mgrx_shard_solve(mgrx_shard* sd, const double* b, double* x, const mgrx_krylov* cfg, mgrx_report* rep,
+                     int flags) {
+  const bool on_device = flags & MGRX_ON_DEVICE;
+  const bool zero_guess = flags & MGRX_ZERO_GUESS;
+  return guarded([&] {
+    use(sd->h->ctx);
+    if (!cfg) throw InvalidArgument("mgrx_shard_solve: null config");
+    cudaStream_t s = sd->stream;
+    const int n = sd->sh->row_end - sd->sh->row_begin;
+    KrylovSpec k;
+    k.restart = cfg->restart;
+    k.max_iters = cfg->max_iters;
+    k.rel_tol = cfg->rel_tol;
+    k.abs_tol = cfg->abs_tol;
+    const long long l0 = g_launches;
+    const double* db = b;
+    double* dx = x;
+    if (!on_device) {
+      sd->vin.upload(b, n);
+      if (zero_guess) MGRX_CK(cudaMemsetAsync(sd->vout.get(), 0, sizeof(double) * n, s));
+      else MGRX_CK(cudaMemcpyAsync(sd->vout.get(), x, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+      db = sd->vin.get();
+      dx = sd->vout.get();
+    } else if (zero_guess) {
+      MGRX_CK(cudaMemsetAsync(dx, 0, sizeof(double) * n, s));
+    }
+    EventTimer t(s);
+    GmresResult r = sd->sh->solve(db, dx, k);
+    const double solve_s = t.stop();
+    if (!on_device) {
+      MGRX_CK(cudaMemcpyAsync(x, dx, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+      MGRX_CK(cudaStreamSynchronize(s));
+    }
+    if (rep) {
+      rep->converged = r.converged ? 1 : 0;
+      rep->iterations = r.iterations;
+      rep->final_residual = r.final_residual;
+      rep->history_len = static_cast<int>(r.history.size());
+      if (rep->history)
+        for (int i = 0; i < rep->history_len && i < rep->history_cap; ++i) rep->history[i] = r.history[i];
+      rep->setup_s = sd->h->setup_s;
+      rep->solve_s = solve_s;
+      rep->gpu_launches = g_launches - l0;
+    }
+    return r.converged ? MGRX_OK : MGRX_NOT_CONVERGED;
+  });
+}
+
+int mgrx_shard_destroy(mgrx_shard* sd) {
+  return guarded([&] {
+    if (sd) use(sd->h->ctx);
+    delete sd;
     return MGRX_OK;
   });
 }

@@ -1,0 +1,205 @@
+// Comm implementations: NCCL (dlopen'ed) and in-process local ranks.
+#include "comm.hpp"
+
+#include <dlfcn.h>
+
+#include <condition_variable>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "/usr/include/nccl.h"
+#include "common.cuh"
+
+namespace mgrx {
+
+// ---------------------------------------------------------------------------
+// NCCL
+// ---------------------------------------------------------------------------
+namespace {
+
+struct NcclApi {
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*errorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+  static const NcclApi api = [] {
+    NcclApi a;
+    // the process may already hold a libnccl.so.2 (torch's); dlopen by soname
+    // then returns that copy
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) throw RuntimeError(std::string("sharded solve: cannot load libnccl.so.2: ") + dlerror());
+    auto sym = [&](const char* n) {
+      void* p = dlsym(h, n);
+      if (!p) throw RuntimeError(std::string("sharded solve: libnccl lacks ") + n);
+      return p;
+    };
+    a.getUniqueId = reinterpret_cast<decltype(a.getUniqueId)>(sym("ncclGetUniqueId"));
+    a.commInitRank = reinterpret_cast<decltype(a.commInitRank)>(sym("ncclCommInitRank"));
+    a.commDestroy = reinterpret_cast<decltype(a.commDestroy)>(sym("ncclCommDestroy"));
+    a.send = reinterpret_cast<decltype(a.send)>(sym("ncclSend"));
+    a.recv = reinterpret_cast<decltype(a.recv)>(sym("ncclRecv"));
+    a.groupStart = reinterpret_cast<decltype(a.groupStart)>(sym("ncclGroupStart"));
+    a.groupEnd = reinterpret_cast<decltype(a.groupEnd)>(sym("ncclGroupEnd"));
+    a.allGather = reinterpret_cast<decltype(a.allGather)>(sym("ncclAllGather"));
+    a.errorString = reinterpret_cast<decltype(a.errorString)>(sym("ncclGetErrorString"));
+    return a;
+  }();
+  return api;
+}
+
+void nck(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw RuntimeError(std::string("NCCL ") + what + ": " + nccl().errorString(r));
+}
+
+class NcclComm final : public Comm {
+ public:
+  NcclComm(const unsigned char* id, int r, int n) {
+    static_assert(sizeof(ncclUniqueId) == kNcclIdBytes, "ncclUniqueId size");
+    rank = r;
+    size = n;
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof u);
+    nck(nccl().commInitRank(&c_, n, u, r), "ncclCommInitRank");
+  }
+  ~NcclComm() override {
+    if (c_) nccl().commDestroy(c_);
+  }
+  void exchange(const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs, cudaStream_t s) override {
+    if (sends.empty() && recvs.empty()) return;
+    nck(nccl().groupStart(), "ncclGroupStart");
+    for (const Xfer& x : recvs) nck(nccl().recv(x.ptr, x.count, ncclFloat64, x.peer, c_, s), "ncclRecv");
+    for (const Xfer& x : sends) nck(nccl().send(x.ptr, x.count, ncclFloat64, x.peer, c_, s), "ncclSend");
+    nck(nccl().groupEnd(), "ncclGroupEnd");
+  }
+  void allgather(const double* in, double* out, int count, cudaStream_t s) override {
+    nck(nccl().allGather(in, out, count, ncclFloat64, c_, s), "ncclAllGather");
+  }
+  bool graph_safe() const override { return true; }
+  const char* kind() const override { return "nccl"; }
+
+ private:
+  ncclComm_t c_ = nullptr;
+};
+
+}  // namespace
+
+void nccl_unique_id(unsigned char* out) {
+  ncclUniqueId u;
+  nck(nccl().getUniqueId(&u), "ncclGetUniqueId");
+  std::memcpy(out, &u, sizeof u);
+}
+
+std::unique_ptr<Comm> make_nccl_comm(const unsigned char* id, int rank, int size) {
+  return std::make_unique<NcclComm>(id, rank, size);
+}
+
+// ---------------------------------------------------------------------------
+// Local ranks (threads of one process, one device)
+// ---------------------------------------------------------------------------
+struct LocalHub {
+  explicit LocalHub(int n) : size(n), posts(n), ready(n), done(n) {
+    for (int q = 0; q < n; ++q) {
+      MGRX_CK(cudaEventCreateWithFlags(&ready[q], cudaEventDisableTiming));
+      MGRX_CK(cudaEventCreateWithFlags(&done[q], cudaEventDisableTiming));
+    }
+  }
+  ~LocalHub() {
+    for (int q = 0; q < size; ++q) {
+      cudaEventDestroy(ready[q]);
+      cudaEventDestroy(done[q]);
+    }
+  }
+  void barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    const long g = gen;
+    if (++arrived == size) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+  struct Post {
+    std::vector<Xfer> sends;
+    const double* gather_in = nullptr;
+  };
+  int size;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  long gen = 0;
+  std::vector<Post> posts;
+  std::vector<cudaEvent_t> ready, done;
+};
+
+namespace {
+
+class LocalComm final : public Comm {
+ public:
+  LocalComm(std::shared_ptr<LocalHub> hub, int r) : hub_(std::move(hub)) {
+    rank = r;
+    size = hub_->size;
+  }
+  void exchange(const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs, cudaStream_t s) override {
+    LocalHub& h = *hub_;
+    h.posts[rank].sends = sends;
+    MGRX_CK(cudaEventRecord(h.ready[rank], s));
+    h.barrier();
+    for (const Xfer& r : recvs) {
+      const Xfer* src = nullptr;
+      for (const Xfer& x : h.posts[r.peer].sends)
+        if (x.peer == rank) src = &x;
+      if (!src || src->count != r.count) throw RuntimeError("local comm: unmatched halo transfer");
+      MGRX_CK(cudaStreamWaitEvent(s, h.ready[r.peer], 0));
+      MGRX_CK(cudaMemcpyAsync(r.ptr, src->ptr, sizeof(double) * r.count, cudaMemcpyDeviceToDevice, s));
+    }
+    finish(s);
+  }
+  void allgather(const double* in, double* out, int count, cudaStream_t s) override {
+    LocalHub& h = *hub_;
+    h.posts[rank].gather_in = in;
+    MGRX_CK(cudaEventRecord(h.ready[rank], s));
+    h.barrier();
+    for (int q = 0; q < size; ++q) {
+      MGRX_CK(cudaStreamWaitEvent(s, h.ready[q], 0));
+      MGRX_CK(cudaMemcpyAsync(out + static_cast<size_t>(q) * count, h.posts[q].gather_in, sizeof(double) * count,
+                              cudaMemcpyDeviceToDevice, s));
+    }
+    finish(s);
+  }
+  bool graph_safe() const override { return false; }
+  const char* kind() const override { return "local"; }
+
+ private:
+  // peers must have finished reading this rank's buffers before it reuses them
+  void finish(cudaStream_t s) {
+    LocalHub& h = *hub_;
+    MGRX_CK(cudaEventRecord(h.done[rank], s));
+    h.barrier();
+    for (int q = 0; q < size; ++q)
+      if (q != rank) MGRX_CK(cudaStreamWaitEvent(s, h.done[q], 0));
+    h.barrier();  // nobody re-records ready/done before everyone has waited
+  }
+  std::shared_ptr<LocalHub> hub_;
+};
+
+}  // namespace
+
+std::shared_ptr<LocalHub> make_local_hub(int size) { return std::make_shared<LocalHub>(size); }
+
+std::unique_ptr<Comm> make_local_comm(const std::shared_ptr<LocalHub>& hub, int rank) {
+  return std::make_unique<LocalComm>(hub, rank);
+}
+
+}  // namespace mgrx

@@ -1,0 +1,54 @@
+// Communication layer of the sharded (row-slab) solve, SURVEY.md §8(e).
+//
+// Two primitives cover every exchange the path needs:
+//   exchange  - point-to-point halo transfer (one send / recv segment per
+//               neighbour), issued on the solve stream;
+//   allgather - fixed-size all-gather of a few fp64 partials (inner
+//               products, summed afterwards in rank order on the device, so
+//               every rank gets the same bits) or of a coarse vector.
+// Implementations:
+//   NCCL  (one process per GPU; libnccl is dlopen'ed, so libmgrx itself has
+//          no NCCL dependency): ncclSend/ncclRecv inside a group, ncclAllGather;
+//          both stream-ordered and CUDA-graph capturable;
+//   local (several ranks as threads of one process on one device, for the
+//          parity tests): device-to-device copies ordered by events and host
+//          barriers. Not capturable, not a performance path.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <vector>
+
+namespace mgrx {
+
+struct Xfer {
+  int peer;
+  double* ptr;
+  int count;
+};
+
+class Comm {
+ public:
+  int rank = 0, size = 1;
+  virtual ~Comm() = default;
+  // Every send {peer, ptr, count} is matched by a recv on `peer` naming this
+  // rank with the same count.
+  virtual void exchange(const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs, cudaStream_t s) = 0;
+  // out[q * count + i] = in_q[i] for every rank q.
+  virtual void allgather(const double* in, double* out, int count, cudaStream_t s) = 0;
+  virtual bool graph_safe() const = 0;
+  virtual const char* kind() const = 0;
+};
+
+constexpr int kNcclIdBytes = 128;
+// ncclGetUniqueId (rank 0 creates it; the caller distributes it).
+void nccl_unique_id(unsigned char* out);
+// ncclCommInitRank on the current device.
+std::unique_ptr<Comm> make_nccl_comm(const unsigned char* id, int rank, int size);
+
+struct LocalHub;
+std::shared_ptr<LocalHub> make_local_hub(int size);
+std::unique_ptr<Comm> make_local_comm(const std::shared_ptr<LocalHub>& hub, int rank);
+
+}  // namespace mgrx

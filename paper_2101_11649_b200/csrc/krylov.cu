@@ -437,6 +437,25 @@ void arnoldi_launch(int n, int k, int slots, int dbg, GmresWork& ws, cudaStream_
 
 }  // namespace
 
+void mgs_step(int n, double* w, const double* vprev, const double* hprev, const double* a, bool want2,
+              GmresWork& ws, double* out1, double* hacc, bool accumulate, double* out2, cudaStream_t s) {
+  mgs_launch(n, w, vprev, hprev, a, want2, ws, out1, hacc, accumulate, out2, s);
+}
+
+void vec_scale(int n, const double* in, double d, double* out, cudaStream_t s) {
+  if (n == 0) return;
+  k_scale<<<blocks_for(n, 256), 256, 0, s>>>(n, in, d, out);
+  MGRX_LAUNCH_CK();
+  count_launch();
+}
+
+void basis_combine(int n, int k, const double* V, const double* y, double* u, cudaStream_t s) {
+  if (n == 0) return;
+  k_gemv<<<blocks_for(n, 256), 256, 0, s>>>(n, k, V, y, u);
+  MGRX_LAUNCH_CK();
+  count_launch();
+}
+
 void GmresWork::ensure(int n_, int m_, cudaStream_t s) {
   if (n_ == n && m_ == m) return;
   n = n_;

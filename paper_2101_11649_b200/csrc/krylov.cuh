@@ -49,6 +49,16 @@ void mgs_probe(int n, double* w, const double* vprev, const double* h, const dou
 // fused kernel is unavailable for n.
 int arnoldi_probe(int n, int k, int dbg, GmresWork& ws, cudaStream_t s);
 
+// Building blocks of the sharded GMRES (shard.cu):
+// one MGS kernel on local rows, partial results in out1 / out2 (canonical
+// per-rank reduction order); see k_mgs in krylov.cu for the argument roles.
+void mgs_step(int n, double* w, const double* vprev, const double* hprev, const double* a, bool want2,
+              GmresWork& ws, double* out1, double* hacc, bool accumulate, double* out2, cudaStream_t s);
+// out = in / d
+void vec_scale(int n, const double* in, double d, double* out, cudaStream_t s);
+// u = sum_{j<k} V[j] y[j], j ascending (V column-major, n rows)
+void basis_combine(int n, int k, const double* V, const double* y, double* u, cudaStream_t s);
+
 // Deterministic device dot product (fixed grid, fixed reduction tree).
 double device_dot(int n, const double* a, const double* b, GmresWork& ws, cudaStream_t s);
 
