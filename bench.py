@@ -38,12 +38,22 @@ CONFIGS = {
                      "FGMRES(30) rtol 1e-6, MGR_pi (exact pi elimination) + 1 AMG V-cycle "
                      "(l1-Jacobi x2 AMG smoothing; variant: the AMG default hybrid Gauss-Seidel)"},
     "cfg3": {"kind": "comp", "dims": (100, 100, 50), "wells": 8, "seed": 20210130,
-             "strategy": "comp_mgr", "rtol": 1e-5,
+             "strategy": "comp_mgr_l1j", "rtol": 1e-5, "variant": "comp_mgr",
              "desc": "cfg3: compositional p+3 densities 100x100x50 (4x4 blocks) + 8 wells x 50 elements x 5 dofs, "
-                     "FGMRES(30) rtol 1e-5, MGR rho3 -> rho1,rho2 -> p(AMG) -> wells(dense LU)"},
-    "cfg4": {"kind": "frac", "m": 64, "seed": 20210131, "strategy": "frac_mgr_u", "rtol": 1e-6,
+                     "FGMRES(30) rtol 1e-5, MGR rho3 -> rho1,rho2 -> p(AMG, l1-Jacobi x2; variant: hybrid GS) "
+                     "-> wells(dense LU)"},
+    "cfg4": {"kind": "frac", "m": 64, "seed": 20210131, "strategy": "frac_mgr_u_l1j", "rtol": 1e-6,
+             "variant": "frac_mgr_u",
              "desc": "cfg4: 3-D Q1 elasticity 64^3 nodes (81 nnz/row) + mid-plane fracture lubrication, "
-                     "FGMRES(30) rtol 1e-6, MGR_u with unknown-based AMG on A_uu, AMG coarse on p"},
+                     "FGMRES(30) rtol 1e-6, MGR_u with unknown-based AMG on A_uu (l1-Jacobi x2; variant: "
+                     "hybrid GS), AMG coarse on p"},
+    # cfg5: cfg3 physics weak-scaled to 1,048,576 cells per GPU (z-slabs),
+    # 8 wells per 500k cells; dims for N = 1/2/4/8 GPUs follow SURVEY §8(d).
+    "cfg5": {"kind": "comp", "dims_by_n": {1: (128, 128, 64), 2: (128, 128, 128), 4: (256, 128, 128),
+                                           8: (256, 256, 128)},
+             "seed": 20210134, "strategy": "comp_mgr_l1j", "rtol": 1e-5, "weak": True,
+             "desc": "cfg5: cfg3 physics weak-scaled, 1,048,576 cells (4 dofs) per GPU + 8 wells per 500k cells, "
+                     "z-slab partition with NCCL halo exchanges, FGMRES(30) rtol 1e-5, comp_mgr_l1j"},
 }
 CONFIG = "cfg2"
 STRATEGY = CONFIGS[CONFIG]["strategy"]
@@ -111,9 +121,13 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def make_problem():
+def make_problem(n_gpus=1):
     import paper_2101_11649_b200 as mx
     c = CONFIGS[CONFIG]
+    if "dims_by_n" in c:
+        dims = c["dims_by_n"].get(n_gpus) or (128, 128, 64 * n_gpus)
+        cells = dims[0] * dims[1] * dims[2]
+        return mx.comp_problem(*dims, wells=max(1, (8 * cells) // 500000), seed=c["seed"])
     if c["kind"] == "mfd":
         return mx.mfd_problem(*c["dims"], c["field"], sigma=1.5, seed=c["seed"])
     if c["kind"] == "frac":
@@ -145,25 +159,130 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    P = make_problem()
+    P = make_problem(world)
     threads = os.cpu_count() or 1
     v, t, its, setup_s = cpu_reference(P, args.steps, args.warmup, args.ref_iters, threads)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / max(args.steps, 1),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": scaling_kind(world), "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": workload_config(P, args.gpus),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": f"cfg2 MGR-GMRES solves capped at {args.ref_iters} iterations "
+                             "sample": f"{CONFIG} MGR-GMRES solves capped at {args.ref_iters} iterations "
                                        f"({its} iterations over {args.steps} steps), setup {setup_s:.1f}s excluded"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
 
+def scaling_kind(n_gpus):
+    """cfg5 fixes the work per GPU; the other configs split one problem."""
+    return "weak" if (CONFIGS[CONFIG].get("weak") or n_gpus == 1) else "strong"
+
+
 def workload_config(P, n_gpus):
     return {"workload": CONFIGS[CONFIG]["desc"],
             "dofs": int(P.n), "nnz": int(P.ptr[-1]), "strategy": STRATEGY, "restart": RESTART,
-            "rel_tol": RTOL, "parallelism": f"replicas{n_gpus}" if n_gpus > 1 else "single",
+            "rel_tol": RTOL,
+            "parallelism": f"zslab{n_gpus} (NCCL halo exchange + all-gathered inner products)"
+            if n_gpus > 1 else "single",
             "l2_flush": "inputs exceed L2 (matrix+hierarchy > 126 MB)"}
+
+
+def probe_names(H):
+    info = H.info()
+    names = ["arnoldi.15", "mgs", "spmv.A"]
+    if info["mgr_levels"]:
+        names += ["mgr.0.rres", "mgr.0.prolong"]
+    for k in range(max(info["coarse_amg_levels"] - 1, 0)):
+        names += [f"amg.{k}.resid", f"amg.{k}.pre", f"amg.{k}.post"]
+    return names
+
+
+def run_sharded(args):
+    """N > 1 (torchrun, one rank per GPU): every rank builds the same
+    hierarchy on its GPU, keeps its z-slab (mgrx_shard_create over NCCL) and
+    runs the sharded solve; gloo carries only the NCCL id and the max-over-
+    ranks timing. value = global DOF x iterations / (max over ranks of the
+    device-timed solve)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2101_11649_b200 as mx
+
+    rank, world, local = dist_env()
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(local)
+    P = make_problem(world)
+    ctx = mx.Context(local)
+    A = mx.Matrix(P.ptr, P.col, P.val, ctx=ctx)
+    t0 = time.perf_counter()
+    H = mx.Hierarchy(A, P.partition, mx.load_strategy(STRATEGY), P.unknown_map)
+    setup_wall = time.perf_counter() - t0
+    obj = [mx.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    starts = mx.slab_row_starts(P, world)
+    S = mx.Shard(H, rank, world, starts, nccl_id=obj[0])
+    lo, hi = S.row_begin, S.row_end
+    cfg = mx.KrylovConfig(restart=RESTART, max_iters=500, rel_tol=RTOL)
+    dev = torch.device("cuda", local)
+    b = torch.from_numpy(np.ascontiguousarray(P.rhs[lo:hi])).to(dev)
+    x = torch.zeros(hi - lo, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+
+    def step():
+        return S.solve_device(b.data_ptr(), x.data_ptr(), cfg, zero_guess=True)
+
+    for _ in range(args.warmup):
+        step()
+    dist.barrier()
+    torch.cuda.synchronize()
+    its, launches, dev_s = 0, 0, 0.0
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            rep = step()
+            its += rep.iterations
+            launches += rep.gpu_launches
+            dev_s += rep.solve_s  # CUDA events on the shard's stream
+        torch.cuda.synchronize()
+    dist.barrier()
+    t = torch.tensor([dev_s], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_max = float(t.item())
+    value = P.n * its / t_max
+    # e2e: the public API with pinned host slices (H2D of b, D2H of x)
+    b_host = torch.empty(hi - lo, dtype=torch.float64, pin_memory=True).numpy()
+    b_host[:] = P.rhs[lo:hi]
+    x_host = torch.empty(hi - lo, dtype=torch.float64, pin_memory=True).numpy()
+    S.solve(b_host, None, cfg, out=x_host)
+    dist.barrier()
+    te, e_its = 0.0, 0
+    for _ in range(args.steps):
+        t1 = time.perf_counter()
+        _, rep_e = S.solve(b_host, None, cfg, out=x_host)
+        te += time.perf_counter() - t1
+        e_its += rep_e.iterations
+    tt = torch.tensor([te], dtype=torch.float64)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    e2e = P.n * e_its / float(tt.item())
+    nb = torch.tensor([8.0 * (hi - lo)], dtype=torch.float64)
+    dist.all_reduce(nb, op=dist.ReduceOp.SUM)
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
+                "scaling": scaling_kind(world), "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {**workload_config(P, world), "row_starts": [int(v) for v in starts]},
+                "iterations_per_solve": its / args.steps, "solve_time_s": t_max / args.steps,
+                "setup_wall_s": setup_wall, "hierarchy": H.info(),
+                "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(nb.item()),
+                        "d2h_bytes_per_step": int(nb.item()),
+                        "path": "Shard.solve -> mgrx_shard_solve (C ABI) per rank, pinned host slices"},
+                "gpu_launches": launches, "roofline": None, "cpu_baseline": None,
+                "clocks": clk.summary()}
+        print(json.dumps(line))
+    S.close()
+    dist.barrier()
+    dist.destroy_process_group()
 
 
 def main():
@@ -177,6 +296,8 @@ def main():
     ap.add_argument("--ref-iters", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-variant", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the z-slab sharded solve even at N=1 (exercises the NCCL path on one GPU)")
     ap.add_argument("--strategy", default=None, help="strategies/<name>.json (default: %s)" % STRATEGY)
     args = ap.parse_args()
     CONFIG = args.config
@@ -193,8 +314,8 @@ def main():
     import paper_2101_11649_b200 as mx
 
     rank, world, local = dist_env()
-    if world > 1:
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    if world > 1 or args.sharded:
+        return run_sharded(args)
     torch.cuda.set_device(local)
     P = make_problem()
     ctx = mx.Context(local)
@@ -216,8 +337,6 @@ def main():
 
     for _ in range(args.warmup):
         step()
-    if world > 1:
-        dist.barrier()
     torch.cuda.synchronize()
     its, launches, solve_dev = 0, 0, 0.0
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -235,16 +354,8 @@ def main():
         torch.cuda.synchronize()
         if prof:
             torch.cuda.profiler.stop()
-    if world > 1:
-        dist.barrier()
     ms = start.elapsed_time(end)
-    t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
-    its_all = torch.tensor([float(its)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-        dist.all_reduce(its_all, op=dist.ReduceOp.SUM)
-    ms = float(t_max.item())
-    value = P.n * float(its_all.item()) / (ms * 1e-3)
+    value = P.n * its / (ms * 1e-3)
 
     # e2e: public API with pinned host buffers: H2D of b, zero initial guess
     # (set on the device), D2H of x, all inside the timed region (host clock)
@@ -259,16 +370,13 @@ def main():
         _, rep_e = H.solve(b_host, None, cfg, out=x_host)
         te += time.perf_counter() - t1
         e_its += rep_e.iterations
-    e2e = P.n * e_its / te * world
+    e2e = P.n * e_its / te
 
     # roofline: dominant kernel probes (device events on the library stream)
     peak, peak_kind = peaks()
     info = H.info()
     probes = {}
-    names = ["arnoldi.15", "mgs", "spmv.A", "mgr.0.rres", "mgr.0.prolong"]
-    for k in range(max(info["coarse_amg_levels"] - 1, 0)):
-        names += [f"amg.{k}.resid", f"amg.{k}.pre", f"amg.{k}.post"]
-    for name in names:
+    for name in probe_names(H):
         try:
             ms_k, by = H.time_kernel(name, reps=20)
             probes[name] = {"avg_ms": ms_k, "bytes": by, "GBps": by / (ms_k * 1e-3) / 1e9}
@@ -311,26 +419,27 @@ def main():
         torch.cuda.synchronize()
         msv = ev0.elapsed_time(ev1) / len(rv)
         itv = sum(r.iterations for r in rv) / len(rv)
-        gs_ms, gs_by = Hv.time_kernel("amg.0.pre", reps=5)
         variants[vname] = {"value": P.n * itv / (msv * 1e-3), "unit": UNIT, "ms_per_step": msv,
                            "iterations_per_solve": itv,
-                           "smoother": "hybrid_l1_gs (exact sequential Gauss-Seidel, sync-free sweep)",
-                           "dominant_kernel": {"name": "k_gs (fine AMG level, forward sweep)", "avg_ms": gs_ms,
-                                               "achieved_GBps": gs_by / (gs_ms * 1e-3) / 1e9,
-                                               "frac": gs_by / (gs_ms * 1e-3) / 1e9 / peak,
-                                               "bound": "latency (dependency chain, 318 levels)"}}
+                           "smoother": "hybrid_l1_gs (exact sequential Gauss-Seidel, sync-free sweep)"}
+        if "amg.0.pre" in probe_names(Hv):
+            gs_ms, gs_by = Hv.time_kernel("amg.0.pre", reps=5)
+            variants[vname]["dominant_kernel"] = {
+                "name": "k_gs (fine coarse-AMG level, forward sweep)", "avg_ms": gs_ms,
+                "achieved_GBps": gs_by / (gs_ms * 1e-3) / 1e9, "frac": gs_by / (gs_ms * 1e-3) / 1e9 / peak,
+                "bound": "latency (dependency chain of the sequential sweep)"}
         del Hv
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         v, t, cits, setup_s = cpu_reference(P, 1, 0, args.ref_iters, threads)
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"refcpu oracle, cfg2, one solve capped at {args.ref_iters} iterations "
+               "sample": f"refcpu oracle, {CONFIG}, one solve capped at {args.ref_iters} iterations "
                          f"({cits} its in {t:.1f}s; setup {setup_s:.1f}s excluded)"}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "scaling": scaling_kind(world), "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": workload_config(P, world),
                 "iterations_per_solve": its / args.steps, "solve_time_s": ms * 1e-3 / args.steps,
                 "setup_s": rep.setup_s, "setup_wall_s": setup_wall,
@@ -341,8 +450,6 @@ def main():
                 "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "variants": variants,
                 "clocks": clk.summary()}
         print(json.dumps(line))
-    if world > 1:
-        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

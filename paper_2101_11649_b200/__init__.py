@@ -453,6 +453,10 @@ def slab_row_starts(problem: "Problem", size: int) -> np.ndarray:
         nx, ny, nz = meta["dims"]
         per = nx * ny + (nx + 1) * ny + nx * (ny + 1) + nx * ny
         slabs = [k * per for k in range(nz)]
+    elif meta.get("problem") == "comp":
+        nx, ny, nz = meta["dims"]
+        per = nx * ny * meta.get("dofs_per_cell", 4)
+        slabs = [k * per for k in range(nz)]  # wells are numbered last: the last rank owns them
     if not slabs or len(slabs) < size:
         return np.array([n * q // size for q in range(size + 1)], np.int32)
     k = len(slabs)

@@ -1,5 +1,9 @@
 // Single-CTA dense LU with partial pivoting and its triangular solves. The
 // pivot is the first row of maximal |a_ik| (Eigen maxCoeff semantics).
+#include <algorithm>
+#include <climits>
+#include <numeric>
+
 #include "dense.cuh"
 
 namespace mgrx {
@@ -169,13 +173,225 @@ __global__ void __launch_bounds__(32) k_lu_solve_warp(int n, const double* __res
   }
 }
 
+// ---- per-component (block-diagonal) factorization and solve ---------------
+// Block b: rows rows[bst[b] .. bst[b+1]) (ascending), factors column-major at
+// blu + boff[b]. One CTA per block for the factorization (the k_lu algorithm
+// on the block), one warp per block for the solve.
+__global__ void k_densify_blocks(int nb, const int* __restrict__ bst, const long long* __restrict__ boff,
+                                 const int* __restrict__ rows, const int* __restrict__ lpos,
+                                 const int* __restrict__ ptr, const int* __restrict__ col,
+                                 const double* __restrict__ val, double* __restrict__ blu) {
+  const int b = blockIdx.x;
+  const int lo = bst[b], s = bst[b + 1] - lo;
+  double* M = blu + boff[b];
+  for (long long e = threadIdx.x; e < static_cast<long long>(s) * s; e += blockDim.x) M[e] = 0.0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < s; i += blockDim.x) {
+    const int g = rows[lo + i];
+    for (int k = ptr[g]; k < ptr[g + 1]; ++k) M[static_cast<size_t>(lpos[col[k]]) * s + i] = val[k];
+  }
+}
+
+__global__ void __launch_bounds__(kT) k_lu_blocks(const int* __restrict__ bst, const long long* __restrict__ boff,
+                                                  const int* __restrict__ rows, double* blu, int* perm, double tol,
+                                                  int* bad) {
+  __shared__ double sv[kT];
+  __shared__ int si[kT];
+  __shared__ int piv;
+  const int b = blockIdx.x;
+  const int lo = bst[b], n = bst[b + 1] - lo;
+  double* M = blu + boff[b];
+  int* pm = perm + lo;
+  for (int i = threadIdx.x; i < n; i += kT) pm[i] = i;
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    double best = -1.0;
+    int bi = n;
+    for (int i = k + threadIdx.x; i < n; i += kT) {
+      const double a = fabs(M[static_cast<size_t>(k) * n + i]);
+      if (a > best || (a == best && i < bi)) {
+        best = a;
+        bi = i;
+      }
+    }
+    sv[threadIdx.x] = best;
+    si[threadIdx.x] = bi;
+    __syncthreads();
+    for (int w = kT / 2; w > 0; w >>= 1) {
+      if (threadIdx.x < w) {
+        const double a = sv[threadIdx.x + w];
+        const int ai = si[threadIdx.x + w];
+        if (a > sv[threadIdx.x] || (a == sv[threadIdx.x] && ai < si[threadIdx.x])) {
+          sv[threadIdx.x] = a;
+          si[threadIdx.x] = ai;
+        }
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) piv = si[0];
+    __syncthreads();
+    const int p = piv;
+    if (p != k) {
+      for (int j = threadIdx.x; j < n; j += kT) {
+        const size_t a = static_cast<size_t>(j) * n;
+        const double t = M[a + k];
+        M[a + k] = M[a + p];
+        M[a + p] = t;
+      }
+      if (threadIdx.x == 0) {
+        const int t = pm[k];
+        pm[k] = pm[p];
+        pm[p] = t;
+      }
+    }
+    __syncthreads();
+    const double pv = M[static_cast<size_t>(k) * n + k];
+    if (pv != 0.0)
+      for (int i = k + 1 + threadIdx.x; i < n; i += kT)
+        M[static_cast<size_t>(k) * n + i] = __ddiv_rn(M[static_cast<size_t>(k) * n + i], pv);
+    __syncthreads();
+    const int m = n - k - 1;
+    for (int t = threadIdx.x; t < m * m; t += kT) {
+      const int jj = k + 1 + t / m, ii = k + 1 + t % m;
+      const double ukj = M[static_cast<size_t>(jj) * n + k];
+      if (ukj != 0.0)
+        M[static_cast<size_t>(jj) * n + ii] =
+            __dsub_rn(M[static_cast<size_t>(jj) * n + ii], __dmul_rn(M[static_cast<size_t>(k) * n + ii], ukj));
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int i = 0; i < n; ++i)
+      if (fabs(M[static_cast<size_t>(i) * n + i]) < tol) {
+        atomicMin(bad, rows[lo + i]);
+        break;
+      }
+}
+
+// One warp per block; the block's iterate in shared memory. Same update
+// order as k_lu_solve restricted to the block.
+constexpr int kBW = 4;  // warps (blocks) per CTA
+__global__ void __launch_bounds__(32 * kBW) k_lu_solve_blocks(int nb, const int* __restrict__ bst,
+                                                              const long long* __restrict__ boff,
+                                                              const int* __restrict__ rows,
+                                                              const double* __restrict__ blu,
+                                                              const int* __restrict__ perm, int smax,
+                                                              const double* __restrict__ bvec,
+                                                              double* __restrict__ x) {
+  pdl_enter();
+  extern __shared__ double sx[];
+  const int wv = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int b = blockIdx.x * kBW + wv;
+  if (b >= nb) return;
+  double* xs = sx + static_cast<size_t>(wv) * smax;
+  const int lo = bst[b], n = bst[b + 1] - lo;
+  const double* M = blu + boff[b];
+  const int* pm = perm + lo;
+  const int* rw = rows + lo;
+  for (int i = l; i < n; i += 32) xs[i] = bvec[rw[pm[i]]];
+  __syncwarp();
+  for (int j = 0; j < n; ++j) {
+    const double xj = xs[j];
+    const double* Mj = M + static_cast<size_t>(j) * n;
+    for (int i = j + 1 + l; i < n; i += 32) xs[i] = __dsub_rn(xs[i], __dmul_rn(Mj[i], xj));
+    __syncwarp();
+  }
+  for (int j = n - 1; j >= 0; --j) {
+    const double* Mj = M + static_cast<size_t>(j) * n;
+    if (l == 0) xs[j] = __ddiv_rn(xs[j], Mj[j]);
+    __syncwarp();
+    const double xj = xs[j];
+    for (int i = l; i < j; i += 32) xs[i] = __dsub_rn(xs[i], __dmul_rn(Mj[i], xj));
+    __syncwarp();
+  }
+  for (int i = l; i < n; i += 32) x[rw[i]] = xs[i];
+}
+
+// Connected components of the symmetrised pattern of A (host; A is a
+// coarse system): component lists ascending, components ordered by their
+// smallest row.
+std::vector<std::vector<int>> components(int n, const std::vector<int>& ptr, const std::vector<int>& col) {
+  std::vector<int> par(n);
+  std::iota(par.begin(), par.end(), 0);
+  auto find = [&](int a) {
+    while (par[a] != a) a = par[a] = par[par[a]];
+    return a;
+  };
+  for (int i = 0; i < n; ++i)
+    for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
+      const int a = find(i), c = find(col[k]);
+      if (a != c) par[std::max(a, c)] = std::min(a, c);
+    }
+  std::vector<int> id(n, -1);
+  std::vector<std::vector<int>> out;
+  for (int i = 0; i < n; ++i) {
+    const int r = find(i);
+    if (id[r] < 0) {
+      id[r] = static_cast<int>(out.size());
+      out.emplace_back();
+    }
+    out[id[r]].push_back(i);
+  }
+  return out;
+}
+
 }  // namespace
 
-void dense_factor(const DCsr& A, DenseLU& out, cudaStream_t s, double pivot_tol) {
+void dense_factor(const DCsr& A, DenseLU& out, cudaStream_t s, double pivot_tol, bool allow_blocks) {
   if (A.rows != A.cols) throw RuntimeError("dense LU: matrix not square");
   const int n = A.rows;
-  if (n > 6000) throw RuntimeError("dense LU: matrix too large for the single-CTA factorization");
   out.n = n;
+  out.nb = 1;
+  // block-diagonal systems: factor per connected component
+  if (n > 1 && allow_blocks) {
+    const std::vector<int> ptr = A.ptr.download(n + 1);
+    const std::vector<int> col = A.col.download(ptr[n]);
+    const std::vector<std::vector<int>> comp = components(n, ptr, col);
+    if (comp.size() > 1) {
+      out.nb = static_cast<int>(comp.size());
+      std::vector<int> rows, bst(1, 0), lpos(n);
+      std::vector<long long> boff(1, 0);
+      out.max_block = 0;
+      for (const auto& c : comp) {
+        for (size_t i = 0; i < c.size(); ++i) lpos[c[i]] = static_cast<int>(i);
+        rows.insert(rows.end(), c.begin(), c.end());
+        bst.push_back(static_cast<int>(rows.size()));
+        boff.push_back(boff.back() + static_cast<long long>(c.size()) * c.size());
+        out.max_block = std::max(out.max_block, static_cast<int>(c.size()));
+      }
+      if (out.max_block > 6000) throw RuntimeError("dense LU: block too large for the single-CTA factorization");
+      out.rows.alloc(n, s);
+      out.rows.upload(rows.data(), n);
+      out.bst.alloc(out.nb + 1, s);
+      out.bst.upload(bst.data(), out.nb + 1);
+      out.boff.alloc(out.nb + 1, s);
+      out.boff.upload(boff.data(), out.nb + 1);
+      out.blu.alloc(boff.back(), s);
+      out.perm.alloc(n, s);
+      out.lu.alloc(1, s);
+      DVec<int> dl(n, s);
+      dl.upload(lpos.data(), n);
+      k_densify_blocks<<<out.nb, 256, 0, s>>>(out.nb, out.bst.get(), out.boff.get(), out.rows.get(), dl.get(),
+                                             A.ptr.get(), A.col.get(), A.val.get(), out.blu.get());
+      DVec<int> bad(1, s);
+      const int big = INT_MAX;
+      bad.upload(&big, 1);
+      k_lu_blocks<<<out.nb, kT, 0, s>>>(out.bst.get(), out.boff.get(), out.rows.get(), out.blu.get(),
+                                        out.perm.get(), pivot_tol, bad.get());
+      MGRX_LAUNCH_CK();
+      count_launch(2);
+      const size_t sm = sizeof(double) * out.max_block * kBW;
+      if (sm > 200 * 1024) throw RuntimeError("dense LU solve: block too large for shared memory");
+      if (sm > 48 * 1024)
+        MGRX_CK(cudaFuncSetAttribute(k_lu_solve_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(sm)));
+      const int b = read_scalar(bad.get(), s);
+      // the dense algorithm reports the first singular pivot in row order
+      if (b != INT_MAX) throw RuntimeError("dense LU: matrix numerically singular (pivot " + std::to_string(b) + ")");
+      return;
+    }
+  }
+  if (n > 6000) throw RuntimeError("dense LU: matrix too large for the single-CTA factorization");
   out.lu.alloc(static_cast<size_t>(n) * n, s);
   out.perm.alloc(n > 0 ? n : 1, s);
   out.lu.zero();
@@ -200,6 +416,13 @@ void dense_factor(const DCsr& A, DenseLU& out, cudaStream_t s, double pivot_tol)
 
 void dense_solve(const DenseLU& f, const double* b, double* x, cudaStream_t s) {
   if (f.n == 0) return;
+  if (f.nb > 1) {
+    launch_pdl(k_lu_solve_blocks, blocks_for(f.nb, kBW), 32 * kBW, sizeof(double) * f.max_block * kBW, s, f.nb,
+               f.bst.get(), f.boff.get(), f.rows.get(), f.blu.get(), f.perm.get(), f.max_block, b, x);
+    MGRX_LAUNCH_CK();
+    count_launch();
+    return;
+  }
   if (f.n <= kWarpLuMax) {
     launch_pdl(k_lu_solve_warp, 1, 32, sizeof(double) * f.n * f.n, s, f.n, f.lu.get(), f.perm.get(), b, x);
     MGRX_LAUNCH_CK();

@@ -11,11 +11,24 @@ struct DenseLU {
   int n = 0;
   DVec<double> lu;   // column-major n x n, unit-lower L below the diagonal, U on/above
   DVec<int> perm;    // row i of PA is row perm[i] of A
+  // Block-diagonal matrices (several connected components, e.g. the MGR
+  // coarse system of independent wells) are factored per component: nb > 1,
+  // rows = the components' row lists back to back (each ascending), bst =
+  // component starts in rows, boff = factor offsets (column-major s x s per
+  // component), perm holds component-local permutations. lu is then unused.
+  int nb = 1, max_block = 0;
+  DVec<int> rows, bst;
+  DVec<long long> boff;
+  DVec<double> blu;
 };
 
-// Densify CSR A and factor it; throws "dense LU: matrix numerically singular
+// Densify CSR A and factor it (per connected component when A is block
+// diagonal: the same operations as the dense factorization restricted to
+// each block, since every cross-block entry is an exact zero); throws "dense LU: matrix numerically singular
 // (pivot i)" when |u_ii| < pivot_tol.
-void dense_factor(const DCsr& A, DenseLU& out, cudaStream_t s, double pivot_tol = 1e-300);
+// allow_blocks = false keeps the single dense factor (callers that read lu).
+void dense_factor(const DCsr& A, DenseLU& out, cudaStream_t s, double pivot_tol = 1e-300,
+                  bool allow_blocks = true);
 // x = A^{-1} b (x may alias nothing).
 void dense_solve(const DenseLU& f, const double* b, double* x, cudaStream_t s);
 

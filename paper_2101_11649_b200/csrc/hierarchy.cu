@@ -183,7 +183,7 @@ DCsr ff_solve(const DCsr& Aff, const DCsr& B, const std::optional<std::vector<in
   }
   if (Aff.rows <= 2000) {
     DenseLU f;
-    dense_factor(Aff, f, s);
+    dense_factor(Aff, f, s, 1e-300, false);
     return dense_solve_columns(f, B, s);
   }
   throw RuntimeError(

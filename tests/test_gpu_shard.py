@@ -105,3 +105,17 @@ def test_single_rank_shard_equals_global():
     x2, r2 = S.solve(P.rhs, None, cfg)
     assert r2.residual_history == r1.residual_history
     assert np.array_equal(x2.view(np.int64), x1.view(np.int64))
+
+
+def test_nccl_single_rank():
+    """The NCCL communicator (libnccl dlopen'ed, ncclCommInitRank, the
+    all-gathered inner products) on one rank reproduces the global solve."""
+    P = mx.mfd_problem(10, 10, 5, "iid")
+    H = mx.Hierarchy(mx.Matrix(P.ptr, P.col, P.val), P.partition, mx.load_strategy("mfd_mgr_pi_c1_l1j"))
+    S = mx.Shard(H, 0, 1, None, nccl_id=mx.nccl_unique_id())
+    cfg = mx.KrylovConfig(restart=30, rel_tol=1e-8)
+    x1, r1 = H.solve(P.rhs, None, cfg)
+    x2, r2 = S.solve(P.rhs, None, cfg)
+    assert r2.residual_history == r1.residual_history
+    assert np.array_equal(x2.view(np.int64), x1.view(np.int64))
+    S.close()
