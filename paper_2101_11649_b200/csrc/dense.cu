@@ -268,43 +268,80 @@ __global__ void __launch_bounds__(kT) k_lu_blocks(const int* __restrict__ bst, c
       }
 }
 
-// One warp per block; the block's iterate in shared memory. Same update
-// order as k_lu_solve restricted to the block.
-constexpr int kBW = 4;  // warps (blocks) per CTA
-__global__ void __launch_bounds__(32 * kBW) k_lu_solve_blocks(int nb, const int* __restrict__ bst,
-                                                              const long long* __restrict__ boff,
-                                                              const int* __restrict__ rows,
-                                                              const double* __restrict__ blu,
-                                                              const int* __restrict__ perm, int smax,
-                                                              const double* __restrict__ bvec,
-                                                              double* __restrict__ x) {
+// Triangular solves of one block per CTA, panel-blocked: 32 columns at a
+// time, warp 0 runs the panel's triangle with the lane-owned iterate in
+// registers (its row entries preloaded), then all threads apply the panel's
+// columns to the remaining rows. Every x_i still receives its updates in the
+// unblocked order (j ascending forward, descending backward, the division
+// by u_ii right after the last update from j > i), so results are bitwise
+// those of k_lu_solve / DenseLU::solve. rows == nullptr: identity row map.
+constexpr int kPT = 256;
+__global__ void __launch_bounds__(kPT) k_lu_solve_panel(const int* __restrict__ bst, const long long* __restrict__ boff,
+                                                        const int* __restrict__ rows, const double* __restrict__ blu,
+                                                        const int* __restrict__ perm, int n1,
+                                                        const double* __restrict__ bvec, double* __restrict__ x) {
   pdl_enter();
-  extern __shared__ double sx[];
-  const int wv = threadIdx.x >> 5, l = threadIdx.x & 31;
-  const int b = blockIdx.x * kBW + wv;
-  if (b >= nb) return;
-  double* xs = sx + static_cast<size_t>(wv) * smax;
-  const int lo = bst[b], n = bst[b + 1] - lo;
-  const double* M = blu + boff[b];
+  extern __shared__ double xs[];
+  const int b = blockIdx.x;
+  const int lo = bst ? bst[b] : 0;
+  const int n = bst ? bst[b + 1] - lo : n1;
+  const double* M = blu + (boff ? boff[b] : 0);
   const int* pm = perm + lo;
-  const int* rw = rows + lo;
-  for (int i = l; i < n; i += 32) xs[i] = bvec[rw[pm[i]]];
-  __syncwarp();
-  for (int j = 0; j < n; ++j) {
-    const double xj = xs[j];
-    const double* Mj = M + static_cast<size_t>(j) * n;
-    for (int i = j + 1 + l; i < n; i += 32) xs[i] = __dsub_rn(xs[i], __dmul_rn(Mj[i], xj));
-    __syncwarp();
+  const int T = threadIdx.x, l = T & 31;
+  for (int i = T; i < n; i += kPT) xs[i] = bvec[rows ? rows[lo + pm[i]] : pm[i]];
+  __syncthreads();
+  // forward: unit lower triangle
+  for (int j0 = 0; j0 < n; j0 += 32) {
+    const int jn = min(32, n - j0);
+    if (T < 32) {
+      const int i = j0 + l;
+      double m[32];
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) m[jj] = (jj < l && l < jn) ? M[static_cast<size_t>(j0 + jj) * n + i] : 0.0;
+      double xv = l < jn ? xs[i] : 0.0;
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) {
+        const double xj = __shfl_sync(0xffffffffu, xv, jj);
+        if (jj < l && l < jn) xv = __dsub_rn(xv, __dmul_rn(m[jj], xj));
+      }
+      if (l < jn) xs[i] = xv;
+    }
+    __syncthreads();
+    for (int i = j0 + jn + T; i < n; i += kPT) {
+      double v = xs[i];
+      for (int jj = 0; jj < jn; ++jj) v = __dsub_rn(v, __dmul_rn(M[static_cast<size_t>(j0 + jj) * n + i], xs[j0 + jj]));
+      xs[i] = v;
+    }
+    __syncthreads();
   }
-  for (int j = n - 1; j >= 0; --j) {
-    const double* Mj = M + static_cast<size_t>(j) * n;
-    if (l == 0) xs[j] = __ddiv_rn(xs[j], Mj[j]);
-    __syncwarp();
-    const double xj = xs[j];
-    for (int i = l; i < j; i += 32) xs[i] = __dsub_rn(xs[i], __dmul_rn(Mj[i], xj));
-    __syncwarp();
+  // backward: upper triangle, division before the updates of each column
+  for (int j1 = n; j1 > 0; j1 -= 32) {
+    const int j0 = j1 > 32 ? j1 - 32 : 0, jn = j1 - j0;
+    if (T < 32) {
+      const int i = j0 + l;
+      double m[32];
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) m[jj] = (jj >= l && jj < jn && l < jn) ? M[static_cast<size_t>(j0 + jj) * n + i] : 1.0;
+      double xv = l < jn ? xs[i] : 0.0;
+#pragma unroll
+      for (int jj = 31; jj >= 0; --jj) {
+        if (jj < jn) {
+          if (l == jj) xv = __ddiv_rn(xv, m[jj]);
+          const double xj = __shfl_sync(0xffffffffu, xv, jj);
+          if (l < jj) xv = __dsub_rn(xv, __dmul_rn(m[jj], xj));
+        }
+      }
+      if (l < jn) xs[i] = xv;
+    }
+    __syncthreads();
+    for (int i = T; i < j0; i += kPT) {
+      double v = xs[i];
+      for (int jj = jn - 1; jj >= 0; --jj) v = __dsub_rn(v, __dmul_rn(M[static_cast<size_t>(j0 + jj) * n + i], xs[j0 + jj]));
+      xs[i] = v;
+    }
+    __syncthreads();
   }
-  for (int i = l; i < n; i += 32) x[rw[i]] = xs[i];
+  for (int i = T; i < n; i += kPT) x[rows ? rows[lo + i] : i] = xs[i];
 }
 
 // Connected components of the symmetrised pattern of A (host; A is a
@@ -380,10 +417,10 @@ void dense_factor(const DCsr& A, DenseLU& out, cudaStream_t s, double pivot_tol,
                                         out.perm.get(), pivot_tol, bad.get());
       MGRX_LAUNCH_CK();
       count_launch(2);
-      const size_t sm = sizeof(double) * out.max_block * kBW;
+      const size_t sm = sizeof(double) * out.max_block;
       if (sm > 200 * 1024) throw RuntimeError("dense LU solve: block too large for shared memory");
       if (sm > 48 * 1024)
-        MGRX_CK(cudaFuncSetAttribute(k_lu_solve_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        MGRX_CK(cudaFuncSetAttribute(k_lu_solve_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(sm)));
       const int b = read_scalar(bad.get(), s);
       // the dense algorithm reports the first singular pivot in row order
@@ -408,8 +445,10 @@ void dense_factor(const DCsr& A, DenseLU& out, cudaStream_t s, double pivot_tol,
   }
   const size_t sm = sizeof(double) * n;
   if (sm > 200 * 1024) throw RuntimeError("dense LU solve: system too large for shared memory");
-  if (sm > 48 * 1024)
+  if (sm > 48 * 1024) {
     MGRX_CK(cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+    MGRX_CK(cudaFuncSetAttribute(k_lu_solve_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+  }
   const int b = read_scalar(bad.get(), s);
   if (b >= 0) throw RuntimeError("dense LU: matrix numerically singular (pivot " + std::to_string(b) + ")");
 }
@@ -417,20 +456,38 @@ void dense_factor(const DCsr& A, DenseLU& out, cudaStream_t s, double pivot_tol,
 void dense_solve(const DenseLU& f, const double* b, double* x, cudaStream_t s) {
   if (f.n == 0) return;
   if (f.nb > 1) {
-    launch_pdl(k_lu_solve_blocks, blocks_for(f.nb, kBW), 32 * kBW, sizeof(double) * f.max_block * kBW, s, f.nb,
-               f.bst.get(), f.boff.get(), f.rows.get(), f.blu.get(), f.perm.get(), f.max_block, b, x);
+    launch_pdl(k_lu_solve_panel, f.nb, kPT, sizeof(double) * f.max_block, s, static_cast<const int*>(f.bst.get()),
+               static_cast<const long long*>(f.boff.get()), static_cast<const int*>(f.rows.get()),
+               static_cast<const double*>(f.blu.get()), static_cast<const int*>(f.perm.get()), 0, b, x);
     MGRX_LAUNCH_CK();
     count_launch();
     return;
   }
-  if (f.n <= kWarpLuMax) {
+  // MGRX_DENSE_SOLVE=warp|cta: the earlier one-warp (factors in shared
+  // memory) / one-CTA column-sweep kernels; default: the panel-blocked CTA
+  // solve (all three bitwise identical)
+  static const int mode = [] {
+    const char* e = std::getenv("MGRX_DENSE_SOLVE");
+    if (e && e[0] == 'w') return 1;
+    if (e && e[0] == 'c') return 2;
+    return 0;
+  }();
+  if (mode == 1 && f.n <= kWarpLuMax) {
     launch_pdl(k_lu_solve_warp, 1, 32, sizeof(double) * f.n * f.n, s, f.n, f.lu.get(), f.perm.get(), b, x);
     MGRX_LAUNCH_CK();
     count_launch();
     return;
   }
   const size_t sm = sizeof(double) * f.n;
-  launch_pdl(k_lu_solve, 1, kT, sm, s, f.n, f.lu.get(), f.perm.get(), b, x);
+  if (mode == 2) {
+    launch_pdl(k_lu_solve, 1, kT, sm, s, f.n, f.lu.get(), f.perm.get(), b, x);
+    MGRX_LAUNCH_CK();
+    count_launch();
+    return;
+  }
+  launch_pdl(k_lu_solve_panel, 1, kPT, sm, s, static_cast<const int*>(nullptr), static_cast<const long long*>(nullptr),
+             static_cast<const int*>(nullptr), static_cast<const double*>(f.lu.get()),
+             static_cast<const int*>(f.perm.get()), f.n, b, x);
   MGRX_LAUNCH_CK();
   count_launch();
 }

@@ -423,7 +423,21 @@ __global__ void __launch_bounds__(Gm::T) k_spmv_staged(int nblk, const int* __re
     phase ^= 1u << s;
     Stage& S = stg[s];
     const int ra = r0 & ~3, pa4 = p0 & ~3, pa2 = p0 & ~1;
-    if (r < r1) {
+    const int p1 = pnnz[b + 1];
+    if (p1 - p0 > 48 * (r1 - r0)) {
+      // long rows (> 48 entries on average, e.g. 3-D Q1 elasticity): all threads form the block's
+      // products in place (every gather of the block in flight at once),
+      // then each row sums its products left to right from shared memory
+#pragma unroll 8
+      for (int q = p0 + t; q < p1; q += Gm::T) S.val[q - pa2] = __dmul_rn(S.val[q - pa2], x(S.col[q - pa4]));
+      __syncthreads();
+      if (r < r1) {
+        const int lo = S.rp[r - ra], hi = S.rp[r + 1 - ra];
+        double sum = 0.0;
+        for (int k = lo; k < hi; ++k) sum = __dadd_rn(sum, S.val[k - pa2]);
+        epi.store(r, sum, pre);
+      }
+    } else if (r < r1) {
       const int lo = S.rp[r - ra], hi = S.rp[r + 1 - ra];
       double sum = 0.0;
       int k = lo;
