@@ -1,10 +1,12 @@
 #!/bin/bash
-# profiling pass: ncu --set full on the level-1 AMG smoother SpMV and the MGR
-# prolongation (cfg2), launch list of one timed cfg3 (comp_mgr_l1j) solve
+# launch lists of one timed solve (cfg2 / cfg3 / cfg4 default strategies), SpMV
+# staged/direct choices replayed from a plain run (ncu distorts the setup timing)
 mkdir -p gpurun_out
 export PYTHONUNBUFFERED=1
-python tools/probe_spmv.py amg.1.pre mgr.0.prolong > gpurun_out/probe_plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:k_spmv -c 2 -o gpurun_out/amg1_prolong_full -f python tools/probe_spmv.py amg.1.pre mgr.0.prolong > gpurun_out/ncu_amg1.log 2>&1
-python bench.py --config cfg3 --steps 1 --warmup 3 --no-cpu-baseline --no-variant > gpurun_out/bench_cfg3_plain.log 2>&1 && \
-MGRX_PROFILE_TIMED=1 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/launches_cfg3.csv python bench.py --config cfg3 --steps 1 --warmup 3 --no-cpu-baseline --no-variant > gpurun_out/ncu_cfg3.log 2>&1
+for c in cfg2 cfg3 cfg4; do
+rm -f gpurun_out/plan_$c.txt
+MGRX_SPMV_PLAN_FILE=gpurun_out/plan_$c.txt python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline --no-variant > gpurun_out/prof_plain_$c.log 2>&1 && \
+MGRX_SPMV_PLAN_FILE=gpurun_out/plan_$c.txt MGRX_PROFILE_TIMED=1 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/launches_$c.csv python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline --no-variant > gpurun_out/ncu_$c.log 2>&1
+done
+MGRX_GMRES_PROF=1 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-variant > gpurun_out/bench_steps.log 2>&1
 echo done
