@@ -268,39 +268,73 @@ __global__ void __launch_bounds__(kT) k_lu_blocks(const int* __restrict__ bst, c
       }
 }
 
-// Triangular solves of one block per CTA, panel-blocked: 32 columns at a
+// Triangular solves of one block per CTA, panel-blocked: kW columns at a
 // time, warp 0 runs the panel's triangle with the lane-owned iterate in
 // registers (its row entries preloaded), then all threads apply the panel's
 // columns to the remaining rows. Every x_i still receives its updates in the
 // unblocked order (j ascending forward, descending backward, the division
 // by u_ii right after the last update from j > i), so results are bitwise
 // those of k_lu_solve / DenseLU::solve. rows == nullptr: identity row map.
+// kStage: the panels' columns (contiguous in the column-major factors) are
+// staged in shared memory with cp.async, double-buffered one panel ahead, so
+// the triangle and the update read shared memory instead of paying an L2 /
+// HBM round trip per panel.
 constexpr int kPT = 256;
+__device__ __forceinline__ void cpa8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cpa_commit_group() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait_group() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int kW, bool kStage>
 __global__ void __launch_bounds__(kPT) k_lu_solve_panel(const int* __restrict__ bst, const long long* __restrict__ boff,
                                                         const int* __restrict__ rows, const double* __restrict__ blu,
                                                         const int* __restrict__ perm, int n1,
                                                         const double* __restrict__ bvec, double* __restrict__ x) {
   pdl_enter();
-  extern __shared__ double xs[];
+  extern __shared__ double sh[];
   const int b = blockIdx.x;
   const int lo = bst ? bst[b] : 0;
   const int n = bst ? bst[b + 1] - lo : n1;
   const double* M = blu + (boff ? boff[b] : 0);
   const int* pm = perm + lo;
   const int T = threadIdx.x, l = T & 31;
+  double* xs = sh;
+  double* pbuf = sh + ((n + 1) & ~1);  // two panel buffers of kW * n
+  auto stage = [&](int j0, int jn, int slot) {
+    if (kStage) {
+      const double* src = M + static_cast<size_t>(j0) * n;
+      double* dst = pbuf + static_cast<size_t>(slot) * kW * n;
+      for (int e = T; e < jn * n; e += kPT) cpa8(dst + e, src + e);
+      cpa_commit_group();
+    }
+  };
+  auto panel = [&](int j0, int slot) -> const double* {
+    return kStage ? pbuf + static_cast<size_t>(slot) * kW * n : M + static_cast<size_t>(j0) * n;
+  };
   for (int i = T; i < n; i += kPT) xs[i] = bvec[rows ? rows[lo + pm[i]] : pm[i]];
-  __syncthreads();
+  const int np = (n + kW - 1) / kW;
   // forward: unit lower triangle
-  for (int j0 = 0; j0 < n; j0 += 32) {
-    const int jn = min(32, n - j0);
+  stage(0, n < kW ? n : kW, 0);
+  for (int p = 0; p < np; ++p) {
+    const int j0 = p * kW, jn = min(kW, n - j0);
+    if (kStage) cpa_wait_group<0>();  // panel p (issued one panel ago) has landed
+    __syncthreads();                   // ... for every thread; panel p-1's readers are done
+    if (p + 1 < np) stage(j0 + kW, min(kW, n - j0 - kW), (p + 1) & 1);
+    const double* P = panel(j0, p & 1);  // P[jj * n + i] = M(i, j0 + jj)
     if (T < 32) {
       const int i = j0 + l;
-      double m[32];
+      double m[kW];
 #pragma unroll
-      for (int jj = 0; jj < 32; ++jj) m[jj] = (jj < l && l < jn) ? M[static_cast<size_t>(j0 + jj) * n + i] : 0.0;
+      for (int jj = 0; jj < kW; ++jj) m[jj] = (jj < l && l < jn) ? P[jj * n + i] : 0.0;
       double xv = l < jn ? xs[i] : 0.0;
 #pragma unroll
-      for (int jj = 0; jj < 32; ++jj) {
+      for (int jj = 0; jj < kW; ++jj) {
         const double xj = __shfl_sync(0xffffffffu, xv, jj);
         if (jj < l && l < jn) xv = __dsub_rn(xv, __dmul_rn(m[jj], xj));
       }
@@ -309,22 +343,30 @@ __global__ void __launch_bounds__(kPT) k_lu_solve_panel(const int* __restrict__ 
     __syncthreads();
     for (int i = j0 + jn + T; i < n; i += kPT) {
       double v = xs[i];
-      for (int jj = 0; jj < jn; ++jj) v = __dsub_rn(v, __dmul_rn(M[static_cast<size_t>(j0 + jj) * n + i], xs[j0 + jj]));
+      for (int jj = 0; jj < jn; ++jj) v = __dsub_rn(v, __dmul_rn(P[jj * n + i], xs[j0 + jj]));
       xs[i] = v;
     }
-    __syncthreads();
   }
+  __syncthreads();
   // backward: upper triangle, division before the updates of each column
-  for (int j1 = n; j1 > 0; j1 -= 32) {
-    const int j0 = j1 > 32 ? j1 - 32 : 0, jn = j1 - j0;
+  {
+    const int j0f = (np - 1) * kW;
+    stage(j0f, n - j0f, 0);
+  }
+  for (int p = np - 1, it = 0; p >= 0; --p, ++it) {
+    const int j0 = p * kW, jn = min(kW, n - j0);
+    if (kStage) cpa_wait_group<0>();
+    __syncthreads();
+    if (p > 0) stage(j0 - kW, kW, (it + 1) & 1);
+    const double* P = panel(j0, it & 1);
     if (T < 32) {
       const int i = j0 + l;
-      double m[32];
+      double m[kW];
 #pragma unroll
-      for (int jj = 0; jj < 32; ++jj) m[jj] = (jj >= l && jj < jn && l < jn) ? M[static_cast<size_t>(j0 + jj) * n + i] : 1.0;
+      for (int jj = 0; jj < kW; ++jj) m[jj] = (jj >= l && jj < jn && l < jn) ? P[jj * n + i] : 1.0;
       double xv = l < jn ? xs[i] : 0.0;
 #pragma unroll
-      for (int jj = 31; jj >= 0; --jj) {
+      for (int jj = kW - 1; jj >= 0; --jj) {
         if (jj < jn) {
           if (l == jj) xv = __ddiv_rn(xv, m[jj]);
           const double xj = __shfl_sync(0xffffffffu, xv, jj);
@@ -336,12 +378,52 @@ __global__ void __launch_bounds__(kPT) k_lu_solve_panel(const int* __restrict__ 
     __syncthreads();
     for (int i = T; i < j0; i += kPT) {
       double v = xs[i];
-      for (int jj = jn - 1; jj >= 0; --jj) v = __dsub_rn(v, __dmul_rn(M[static_cast<size_t>(j0 + jj) * n + i], xs[j0 + jj]));
+      for (int jj = jn - 1; jj >= 0; --jj) v = __dsub_rn(v, __dmul_rn(P[jj * n + i], xs[j0 + jj]));
       xs[i] = v;
     }
-    __syncthreads();
   }
+  __syncthreads();
   for (int i = T; i < n; i += kPT) x[rows ? rows[lo + i] : i] = xs[i];
+}
+
+// The panel solve variant for blocks of up to n rows: the widest panel whose
+// double buffer fits in shared memory. prepare (at factorization, outside
+// any graph capture) raises the kernel's shared-memory limit.
+using PanelKern = void (*)(const int*, const long long*, const int*, const double*, const int*, int, const double*,
+                           double*);
+PanelKern panel_variant(int n, size_t& sm) {
+  const size_t xs = sizeof(double) * ((n + 1) & ~1);
+  auto smem = [&](int w) { return xs + 2 * sizeof(double) * w * static_cast<size_t>(n); };
+  constexpr size_t kMax = 200 * 1024;
+  PanelKern k = k_lu_solve_panel<32, false>;
+  sm = xs;
+  if (smem(8) <= kMax) {
+    k = k_lu_solve_panel<8, true>;
+    sm = smem(8);
+  }
+  if (smem(16) <= kMax) {
+    k = k_lu_solve_panel<16, true>;
+    sm = smem(16);
+  }
+  if (smem(32) <= kMax) {
+    k = k_lu_solve_panel<32, true>;
+    sm = smem(32);
+  }
+  return k;
+}
+void prepare_panel_solve(int n) {
+  size_t sm = 0;
+  PanelKern k = panel_variant(n, sm);
+  if (sm > 48 * 1024)
+    MGRX_CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+}
+void launch_panel_solve(int grid, int n, const int* bst, const long long* boff, const int* rows, const double* lu,
+                        const int* perm, int n1, const double* b, double* x, cudaStream_t s) {
+  size_t sm = 0;
+  PanelKern k = panel_variant(n, sm);
+  launch_pdl(k, grid, kPT, sm, s, bst, boff, rows, lu, perm, n1, b, x);
+  MGRX_LAUNCH_CK();
+  count_launch();
 }
 
 // Connected components of the symmetrised pattern of A (host; A is a
@@ -417,11 +499,9 @@ void dense_factor(const DCsr& A, DenseLU& out, cudaStream_t s, double pivot_tol,
                                         out.perm.get(), pivot_tol, bad.get());
       MGRX_LAUNCH_CK();
       count_launch(2);
-      const size_t sm = sizeof(double) * out.max_block;
-      if (sm > 200 * 1024) throw RuntimeError("dense LU solve: block too large for shared memory");
-      if (sm > 48 * 1024)
-        MGRX_CK(cudaFuncSetAttribute(k_lu_solve_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(sm)));
+      if (sizeof(double) * out.max_block > 200 * 1024)
+        throw RuntimeError("dense LU solve: block too large for shared memory");
+      prepare_panel_solve(out.max_block);
       const int b = read_scalar(bad.get(), s);
       // the dense algorithm reports the first singular pivot in row order
       if (b != INT_MAX) throw RuntimeError("dense LU: matrix numerically singular (pivot " + std::to_string(b) + ")");
@@ -445,10 +525,9 @@ void dense_factor(const DCsr& A, DenseLU& out, cudaStream_t s, double pivot_tol,
   }
   const size_t sm = sizeof(double) * n;
   if (sm > 200 * 1024) throw RuntimeError("dense LU solve: system too large for shared memory");
-  if (sm > 48 * 1024) {
+  if (sm > 48 * 1024)
     MGRX_CK(cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
-    MGRX_CK(cudaFuncSetAttribute(k_lu_solve_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
-  }
+  prepare_panel_solve(n);
   const int b = read_scalar(bad.get(), s);
   if (b >= 0) throw RuntimeError("dense LU: matrix numerically singular (pivot " + std::to_string(b) + ")");
 }
@@ -456,11 +535,8 @@ void dense_factor(const DCsr& A, DenseLU& out, cudaStream_t s, double pivot_tol,
 void dense_solve(const DenseLU& f, const double* b, double* x, cudaStream_t s) {
   if (f.n == 0) return;
   if (f.nb > 1) {
-    launch_pdl(k_lu_solve_panel, f.nb, kPT, sizeof(double) * f.max_block, s, static_cast<const int*>(f.bst.get()),
-               static_cast<const long long*>(f.boff.get()), static_cast<const int*>(f.rows.get()),
-               static_cast<const double*>(f.blu.get()), static_cast<const int*>(f.perm.get()), 0, b, x);
-    MGRX_LAUNCH_CK();
-    count_launch();
+    launch_panel_solve(f.nb, f.max_block, f.bst.get(), f.boff.get(), f.rows.get(), f.blu.get(), f.perm.get(), 0, b, x,
+                       s);
     return;
   }
   // MGRX_DENSE_SOLVE=warp|cta: the earlier one-warp (factors in shared
@@ -485,11 +561,7 @@ void dense_solve(const DenseLU& f, const double* b, double* x, cudaStream_t s) {
     count_launch();
     return;
   }
-  launch_pdl(k_lu_solve_panel, 1, kPT, sm, s, static_cast<const int*>(nullptr), static_cast<const long long*>(nullptr),
-             static_cast<const int*>(nullptr), static_cast<const double*>(f.lu.get()),
-             static_cast<const int*>(f.perm.get()), f.n, b, x);
-  MGRX_LAUNCH_CK();
-  count_launch();
+  launch_panel_solve(1, f.n, nullptr, nullptr, nullptr, f.lu.get(), f.perm.get(), f.n, b, x, s);
 }
 
 }  // namespace mgrx
