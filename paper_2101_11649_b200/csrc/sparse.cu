@@ -354,7 +354,12 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
 
-template <class Gm, class Epi, class Xs>
+// Average entries per row above which a staged block forms its products
+// block-wide (MGRX_SPMV_TWOPHASE, set once from the host).
+__constant__ int c_two_phase_min = 48;
+__device__ __forceinline__ int two_phase_min() { return c_two_phase_min; }
+
+template <class Gm, class Epi, class Xs, bool kLong>
 __global__ void __launch_bounds__(Gm::T) k_spmv_staged(int nblk, const int* __restrict__ plan,
                                                        const int* __restrict__ ptr, const int* __restrict__ col,
                                                        const double* __restrict__ val, Xs x, Epi epi) {
@@ -424,12 +429,34 @@ __global__ void __launch_bounds__(Gm::T) k_spmv_staged(int nblk, const int* __re
     Stage& S = stg[s];
     const int ra = r0 & ~3, pa4 = p0 & ~3, pa2 = p0 & ~1;
     const int p1 = pnnz[b + 1];
-    if (p1 - p0 > 48 * (r1 - r0)) {
-      // long rows (> 48 entries on average, e.g. 3-D Q1 elasticity): all threads form the block's
-      // products in place (every gather of the block in flight at once),
-      // then each row sums its products left to right from shared memory
+    if (!kLong && p1 - p0 > 48 * (r1 - r0)) {
+      // (short-row matrices: rare long blocks, simple strided product pass)
 #pragma unroll 8
       for (int q = p0 + t; q < p1; q += Gm::T) S.val[q - pa2] = __dmul_rn(S.val[q - pa2], x(S.col[q - pa4]));
+      __syncthreads();
+      if (r < r1) {
+        const int lo = S.rp[r - ra], hi = S.rp[r + 1 - ra];
+        double sum = 0.0;
+        for (int k = lo; k < hi; ++k) sum = __dadd_rn(sum, S.val[k - pa2]);
+        epi.store(r, sum, pre);
+      }
+    } else if (kLong && p1 - p0 > two_phase_min() * (r1 - r0)) {
+      // long rows: all threads form the block's products in place (column
+      // indices, then gathers, then products, in explicit batches so every
+      // gather of the batch is in flight at once), then each row sums its
+      // products left to right from shared memory
+      constexpr int kB = (Gm::E + Gm::T - 1) / Gm::T;
+      for (int q0 = p0 + t; q0 < p1; q0 += kB * Gm::T) {
+        int c[kB];
+        double xv[kB];
+#pragma unroll
+        for (int u = 0; u < kB; ++u) c[u] = q0 + u * Gm::T < p1 ? S.col[q0 + u * Gm::T - pa4] : 0;
+#pragma unroll
+        for (int u = 0; u < kB; ++u) xv[u] = q0 + u * Gm::T < p1 ? x(c[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < kB; ++u)
+          if (q0 + u * Gm::T < p1) S.val[q0 + u * Gm::T - pa2] = __dmul_rn(S.val[q0 + u * Gm::T - pa2], xv[u]);
+      }
       __syncthreads();
       if (r < r1) {
         const int lo = S.rp[r - ra], hi = S.rp[r + 1 - ra];
@@ -565,24 +592,37 @@ bool staged_force() {
 int staged_geom() {
   static const int g = [] {
     const char* v = std::getenv("MGRX_SPMV_GEOM");
+    const char* t = std::getenv("MGRX_SPMV_TWOPHASE");
+    if (t) {
+      const int m = std::atoi(t);
+      MGRX_CK(cudaMemcpyToSymbol(c_two_phase_min, &m, sizeof m));
+    }
     return v ? std::atoi(v) : 0;
   }();
   return g;
 }
-template <class Gm, class Epi, class Xs>
-void launch_staged(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
+template <class Gm, class Epi, class Xs, bool kLong>
+void launch_staged_k(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
   static bool attr = false;  // per instantiation
   if (!attr) {
-    MGRX_CK(cudaFuncSetAttribute(k_spmv_staged<Gm, Epi, Xs>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    MGRX_CK(cudaFuncSetAttribute(k_spmv_staged<Gm, Epi, Xs, kLong>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(Gm::smem)));
     attr = true;
   }
   const int per_sm = static_cast<int>(std::min<size_t>(8, 227 * 1024 / Gm::smem));
   const int grid = std::min(A.nblk, 148 * std::min(per_sm, staged_ctas_per_sm()));
-  launch_pdl(k_spmv_staged<Gm, Epi, Xs>, grid, Gm::T, Gm::smem, s, A.nblk, A.plan.get(), A.ptr.get(), A.col.get(),
-             A.val.get(), x, epi);
+  launch_pdl(k_spmv_staged<Gm, Epi, Xs, kLong>, grid, Gm::T, Gm::smem, s, A.nblk, A.plan.get(), A.ptr.get(),
+             A.col.get(), A.val.get(), x, epi);
   MGRX_LAUNCH_CK();
   count_launch();
+}
+// Matrices with long rows on average get the variant with the block-wide
+// product pass (a separate instantiation keeps the common kernel's
+// registers free of the batch arrays).
+template <class Gm, class Epi, class Xs>
+void launch_staged(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
+  if (static_cast<long long>(A.nnz) > 24LL * A.rows) launch_staged_k<Gm, Epi, Xs, true>(A, x, epi, s);
+  else launch_staged_k<Gm, Epi, Xs, false>(A, x, epi, s);
 }
 
 template <class Epi, class Xs = XPlain>
@@ -659,7 +699,7 @@ void spmv_prepare(DCsr& A, cudaStream_t s) {
     if (staged) A.plan = std::move(plan);
     spmv(A, xs.get(), ys.get(), s);  // warm
     MGRX_CK(cudaEventRecord(e0, s));
-    for (int k = 0; k < 5; ++k) spmv(A, xs.get(), ys.get(), s);
+    for (int k = 0; k < 10; ++k) spmv(A, xs.get(), ys.get(), s);
     MGRX_CK(cudaEventRecord(e1, s));
     MGRX_CK(cudaEventSynchronize(e1));
     float ms = 0.f;
@@ -688,7 +728,7 @@ void spmv_prepare(DCsr& A, cudaStream_t s) {
     }
   }
   if (!replayed) {
-    for (int trial = 0; trial < 3; ++trial) {
+    for (int trial = 0; trial < 5; ++trial) {
       td = std::min(td, time(false));
       ts = std::min(ts, time(true));
     }
@@ -702,7 +742,7 @@ void spmv_prepare(DCsr& A, cudaStream_t s) {
   cudaEventDestroy(e1);
   if (const char* v = std::getenv("MGRX_VERBOSE"); v && v[0] == '1')
     std::fprintf(stderr, "spmv_prepare rows %d cols %d nnz %d: direct %.1f us staged %.1f us -> %s\n", A.rows, A.cols,
-                 A.nnz, 200.f * td, 200.f * ts, (ts < 0.97f * td || staged_force()) ? "staged" : "direct");
+                 A.nnz, 100.f * td, 100.f * ts, (ts < 0.97f * td || staged_force()) ? "staged" : "direct");
   A.nblk = 0;
   if (ts < 0.97f * td || staged_force()) {
     A.plan = std::move(plan);

@@ -1,7 +1,8 @@
 #!/bin/bash
 mkdir -p gpurun_out
 export PYTHONUNBUFFERED=1
-for g in 0 1; do for c in cfg2 cfg4; do
-MGRX_SPMV_GEOM=$g timeout 600 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline --no-variant > gpurun_out/exp_g${g}_$c.log 2>&1
-done; done
+for r in 1 2; do
+timeout 600 python bench.py --config cfg2 --steps 5 --warmup 3 --no-cpu-baseline --no-variant > gpurun_out/exp_new_r$r.log 2>&1
+done
+timeout 600 python bench.py --config cfg4 --steps 5 --warmup 3 --no-cpu-baseline --no-variant > gpurun_out/exp_new_cfg4.log 2>&1
 echo done

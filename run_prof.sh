@@ -1,12 +1,9 @@
 #!/bin/bash
-# launch lists of one timed solve (cfg2 / cfg3 / cfg4 default strategies), SpMV
-# staged/direct choices replayed from a plain run (ncu distorts the setup timing)
+# ncu --set full of the level-1 / level-2 AMG residual SpMV (cfg2), staged
+# choices replayed from a plain run
 mkdir -p gpurun_out
 export PYTHONUNBUFFERED=1
-for c in cfg2 cfg3 cfg4; do
-rm -f gpurun_out/plan_$c.txt
-MGRX_SPMV_PLAN_FILE=gpurun_out/plan_$c.txt python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline --no-variant > gpurun_out/prof_plain_$c.log 2>&1 && \
-MGRX_SPMV_PLAN_FILE=gpurun_out/plan_$c.txt MGRX_PROFILE_TIMED=1 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/launches_$c.csv python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline --no-variant > gpurun_out/ncu_$c.log 2>&1
-done
-MGRX_GMRES_PROF=1 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-variant > gpurun_out/bench_steps.log 2>&1
+rm -f gpurun_out/plan_probe.txt
+MGRX_SPMV_PLAN_FILE=gpurun_out/plan_probe.txt python tools/probe_spmv.py amg.1.resid amg.2.resid spmv.A > gpurun_out/probe_plain.log 2>&1
+MGRX_SPMV_PLAN_FILE=gpurun_out/plan_probe.txt ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:k_spmv -c 3 -o gpurun_out/amg12_full -f python tools/probe_spmv.py amg.1.resid amg.2.resid spmv.A > gpurun_out/ncu_amg12.log 2>&1
 echo done
