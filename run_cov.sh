@@ -1,4 +1,4 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_shard.py -q -x > gpurun_out/pytest_shard.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_shard.log
-tail -n 40 gpurun_out/pytest_shard.log
+timeout 1500 python -m pytest tests/test_gpu_fullsize.py -q -x --durations=5 > gpurun_out/pytest_full.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_full.log
+tail -n 15 gpurun_out/pytest_full.log
