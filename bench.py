@@ -404,7 +404,8 @@ def main():
         pass
     roof = {"bound": "hbm", "kernel": dom, "achieved": d["GBps"], "peak": peak, "unit": "GB/s",
             "frac": d["GBps"] / peak, "traffic": traffic, "algorithmic_bytes": d["bytes"],
-            "peak_source": peak_kind, "kernels": probes}
+            "peak_source": peak_kind, "kernels": probes,
+            "probe_method": "CUDA events on the library stream over 20 back-to-back launches (inputs in HBM; the L2 may retain part of a working set near its 126 MB size)"}
 
     variants = {}
     vname = CONFIGS[CONFIG].get("variant")

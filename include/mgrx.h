@@ -129,8 +129,9 @@ MGRX_API int mgrx_dump(mgrx_hier* h, const char* path, int* kind, int* rows, int
 MGRX_API int mgrx_info(mgrx_hier* h, int* mgr_levels, int* coarse_amg_levels, int* frelax_amg_levels,
               int max_levels);
 
-/* Roofline probe: replay one hot kernel of the hierarchy `reps` times with
- * its inputs resident in HBM and report its average device time (CUDA events
+/* Roofline probe: replay one hot kernel of the hierarchy `reps` times back
+ * to back with its inputs resident in HBM (MGRX_PROBE_FLUSH=1: each launch
+ * after a 256 MB L2 flush) and report its average device time (CUDA events
  * on the library stream) and its algorithmic bytes per launch (SURVEY §8d
  * compulsory-traffic model). which:
  *   "spmv.A"            y = A x on the fine matrix (GMRES operator)

@@ -597,6 +597,7 @@ void AmgHier::vcycle_level(int l, const double* r, double* z, cudaStream_t s) {
 // ============================================================================
 // MGR (proj/src/mgr.cpp:223-326)
 // ============================================================================
+bool split_prolong_enabled();
 void prepare_amg(AmgHier& h, cudaStream_t s);
 void prepare_relax(BoundRelax& b, cudaStream_t s) {
   if (b.amg) prepare_amg(*b.amg, s);
@@ -798,6 +799,9 @@ void MgrHier::setup(const DCsr& A, const std::vector<int>& labels, const std::ve
   // block plans of the staged SpMV for every solve-path matrix
   for (auto& L : levels) {
     for (DCsr* M : {&L.A, &L.P, &L.R, &L.Acf, &L.Aff}) spmv_prepare(*M, s);
+    if (L.injection && !L.g_relax && split_prolong_enabled())
+      prolong_prepare(L.P, L.F.get(), static_cast<int>(L.F.size()), L.C.get(), static_cast<int>(L.C.size()), L.pplan,
+                      s);
     prepare_relax(L.f_relax, s);
     if (L.g_relax) prepare_relax(*L.g_relax, s);
   }
@@ -820,6 +824,20 @@ void MgrHier::coarse_solve(const double* v, double* z, cudaStream_t s) {
 }
 
 void MgrHier::apply(const double* v, double* z, cudaStream_t s) { apply_level(0, v, z, s); }
+
+bool split_prolong_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("MGRX_SPLIT_PROLONG");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+void MgrHier::prolong(int l, const double* e, const double* zF, double* z, cudaStream_t s) {
+  MgrLevelD& L = levels[l];
+  if (L.pplan.w > 0) spmv_prolong_split(L.pplan, e, zF, z, s);
+  else spmv_prolong(L.P, e, L.fpos.get(), zF, z, s);
+}
 
 void MgrHier::apply_graph(const double* v, double* z, cudaStream_t s) {
   static const bool enabled = [] {
@@ -874,7 +892,7 @@ void MgrHier::apply_level(int l, const double* v, double* z, cudaStream_t s) {
     L.f_relax.apply(v, L.F.get(), L.zF.get(), s);
     spmv_residual(L.Acf, L.zF.get(), v, L.C.get(), L.rc.get(), s);
     apply_level(l + 1, L.rc.get(), L.e.get(), s);
-    spmv_prolong(L.P, L.e.get(), L.fpos.get(), L.zF.get(), z, s);
+    prolong(l, L.e.get(), L.zF.get(), z, s);
     (void)nf;
     (void)nc;
     return;

@@ -71,6 +71,7 @@ struct MgrLevelD {
   DCsr A;
   DVec<int> F, C, fpos;
   DCsr P, R, Acf, Aff;
+  ProlongPlan pplan;  // split-form prolongation (fast path), w == 0 if unused
   bool injection = true;
   BoundRelax f_relax;
   std::optional<BoundRelax> g_relax;
@@ -89,6 +90,8 @@ struct MgrHier {
   void setup(const DCsr& A, const std::vector<int>& labels, const std::vector<std::string>& fields,
              const std::vector<int>* umap, const Strategy& strat, cudaStream_t s);
   void apply(const double* v, double* z, cudaStream_t s);
+  // z = [0 + zF; 0] + P e of level l (split form when available)
+  void prolong(int l, const double* e, const double* zF, double* z, cudaStream_t s);
   // Same, replayed from a CUDA graph captured once per (v, z) address pair.
   void apply_graph(const double* v, double* z, cudaStream_t s);
   void check(cudaStream_t s);

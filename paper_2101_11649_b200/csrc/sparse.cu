@@ -764,6 +764,97 @@ void spmv_prolong(const DCsr& P, const double* e, const int* fpos, const double*
                   cudaStream_t s) {
   launch_spmv(P, XPlain{e}, EpiProlong{fpos, zF, z}, s);
 }
+namespace {
+template <int kW>
+__global__ void __launch_bounds__(256) k_prolong_split(int nf, int nc, const int* __restrict__ F,
+                                                       const int* __restrict__ C, const int* __restrict__ ecol,
+                                                       const double* __restrict__ eval, const int* __restrict__ ccol,
+                                                       const double* __restrict__ cval, const double* __restrict__ e,
+                                                       const double* __restrict__ zF, double* __restrict__ z) {
+  pdl_enter();
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < nf) {
+    int c[kW];
+    double v[kW], x[kW];
+#pragma unroll
+    for (int k = 0; k < kW; ++k) {
+      c[k] = __ldcs(ecol + static_cast<size_t>(k) * nf + t);
+      v[k] = __ldcs(eval + static_cast<size_t>(k) * nf + t);
+    }
+    const int r = __ldcs(F + t);
+    const double zp = __dadd_rn(0.0, __ldcs(zF + t));
+#pragma unroll
+    for (int k = 0; k < kW; ++k) x[k] = c[k] >= 0 ? __ldg(e + c[k]) : 0.0;
+    double sum = 0.0;
+#pragma unroll
+    for (int k = 0; k < kW; ++k)
+      if (c[k] >= 0) sum = __dadd_rn(sum, __dmul_rn(v[k], x[k]));
+    z[r] = __dadd_rn(zp, sum);
+  } else if (t < nf + nc) {
+    const int j = t - nf;
+    const int r = __ldcs(C + j);
+    const double sum = __dadd_rn(0.0, __dmul_rn(__ldcs(cval + j), __ldg(e + __ldcs(ccol + j))));
+    z[r] = __dadd_rn(0.0, sum);
+  }
+}
+}  // namespace
+
+void prolong_prepare(const DCsr& P, const int* F, int nf, const int* C, int nc, ProlongPlan& out, cudaStream_t s) {
+  out = ProlongPlan();
+  if (nf + nc != P.rows || nf == 0) return;
+  std::vector<int> ptr(P.rows + 1), col(P.nnz), hf(nf), hc(nc);
+  std::vector<double> val(P.nnz);
+  MGRX_CK(cudaMemcpyAsync(ptr.data(), P.ptr.get(), sizeof(int) * (P.rows + 1), cudaMemcpyDeviceToHost, s));
+  if (P.nnz) {
+    MGRX_CK(cudaMemcpyAsync(col.data(), P.col.get(), sizeof(int) * P.nnz, cudaMemcpyDeviceToHost, s));
+    MGRX_CK(cudaMemcpyAsync(val.data(), P.val.get(), sizeof(double) * P.nnz, cudaMemcpyDeviceToHost, s));
+  }
+  MGRX_CK(cudaMemcpyAsync(hf.data(), F, sizeof(int) * nf, cudaMemcpyDeviceToHost, s));
+  if (nc) MGRX_CK(cudaMemcpyAsync(hc.data(), C, sizeof(int) * nc, cudaMemcpyDeviceToHost, s));
+  MGRX_CK(cudaStreamSynchronize(s));
+  int w = 0;
+  for (int i = 0; i < nf; ++i) w = std::max(w, ptr[hf[i] + 1] - ptr[hf[i]]);
+  if (w > 4) return;
+  for (int j = 0; j < nc; ++j)
+    if (ptr[hc[j] + 1] - ptr[hc[j]] != 1) return;
+  w = w < 1 ? 1 : (w <= 2 ? 2 : 4);
+  std::vector<int> ec(static_cast<size_t>(w) * nf, -1), cc(nc);
+  std::vector<double> ev(static_cast<size_t>(w) * nf, 0.0), cv(nc);
+  for (int i = 0; i < nf; ++i)
+    for (int k = ptr[hf[i]], q = 0; k < ptr[hf[i] + 1]; ++k, ++q) {
+      ec[static_cast<size_t>(q) * nf + i] = col[k];
+      ev[static_cast<size_t>(q) * nf + i] = val[k];
+    }
+  for (int j = 0; j < nc; ++j) {
+    cc[j] = col[ptr[hc[j]]];
+    cv[j] = val[ptr[hc[j]]];
+  }
+  out.nf = nf;
+  out.nc = nc;
+  out.w = w;
+  out.F = F;
+  out.C = C;
+  out.ecol.alloc(ec.size(), s);
+  out.ecol.upload(ec.data(), ec.size());
+  out.eval.alloc(ev.size(), s);
+  out.eval.upload(ev.data(), ev.size());
+  out.ccol.alloc(nc > 0 ? nc : 1, s);
+  out.ccol.upload(cc.data(), nc);
+  out.cval.alloc(nc > 0 ? nc : 1, s);
+  out.cval.upload(cv.data(), nc);
+}
+
+void spmv_prolong_split(const ProlongPlan& pl, const double* e, const double* zF, double* z, cudaStream_t s) {
+  const int n = pl.nf + pl.nc;
+  if (n == 0) return;
+  auto* k = pl.w == 1 ? k_prolong_split<1> : pl.w == 2 ? k_prolong_split<2> : k_prolong_split<4>;
+  launch_pdl(k, blocks_for(n, 256), 256, 0, s, pl.nf, pl.nc, pl.F, pl.C, static_cast<const int*>(pl.ecol.get()),
+             static_cast<const double*>(pl.eval.get()), static_cast<const int*>(pl.ccol.get()),
+             static_cast<const double*>(pl.cval.get()), e, zF, z);
+  MGRX_LAUNCH_CK();
+  count_launch();
+}
+
 void spmv_jacobi(const DCsr& A, const double* zold, const double* b, const int* brow,
                  const double* dinv, double w, double* znew, cudaStream_t s) {
   launch_spmv(A, XPlain{zold}, EpiJacobi{zold, b, brow, dinv, w, znew}, s);

@@ -55,6 +55,20 @@ void spmv_add(const DCsr& A, const double* x, double* y, cudaStream_t s);
 // (MGR prolongation, proj/src/mgr.cpp:210-217)
 void spmv_prolong(const DCsr& P, const double* e, const int* fpos, const double* zF, double* z,
                   cudaStream_t s);
+// MGR prolongation in split form: F rows of P as a column-major ELL of
+// width w <= 4 (indexed by F position, so zF is read contiguously), C rows
+// as their single identity entry; one launch covers both. Same arithmetic
+// as spmv_prolong (row sums left to right, z = (0 + zF) + sum, C rows
+// 0 + (0 + 1*e)). w == 0: P does not have that shape (use spmv_prolong).
+struct ProlongPlan {
+  int nf = 0, nc = 0, w = 0;
+  const int* F = nullptr;  // level F / C lists (owned by the MGR level)
+  const int* C = nullptr;
+  DVec<int> ecol, ccol;
+  DVec<double> eval, cval;
+};
+void prolong_prepare(const DCsr& P, const int* F, int nf, const int* C, int nc, ProlongPlan& out, cudaStream_t s);
+void spmv_prolong_split(const ProlongPlan& pl, const double* e, const double* zF, double* z, cudaStream_t s);
 // Jacobi correction sweep: znew = zold + w*(dinv*(b - A zold)), b gathered via brow.
 void spmv_jacobi(const DCsr& A, const double* zold, const double* b, const int* brow,
                  const double* dinv, double w, double* znew, cudaStream_t s);

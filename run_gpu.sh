@@ -1,5 +1,6 @@
 #!/bin/bash
 mkdir -p gpurun_out
 export PYTHONUNBUFFERED=1
-timeout 900 python -m pytest tests -q -m gpu -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-tail -n 3 gpurun_out/pytest_gpu.log
+for c in cfg2 cfg3 cfg4; do
+timeout 600 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline --no-variant > gpurun_out/bench_$c.log 2>&1
+done
