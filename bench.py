@@ -135,7 +135,7 @@ def make_problem(n_gpus=1):
     return mx.comp_problem(*c["dims"], wells=c["wells"], seed=c["seed"])
 
 
-def cpu_reference(P, steps, warmup, max_iters, threads):
+def cpu_reference(P, steps, warmup, max_iters, threads, single_iters=0):
     """refcpu oracle: setup once, then each step = a GMRES solve capped at
     max_iters iterations (bounded sample). Returns DOF*iters/s."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -152,7 +152,17 @@ def cpu_reference(P, steps, warmup, max_iters, threads):
         _, rep = H.solve(P.rhs, restart=RESTART, max_iters=max_iters, rel_tol=RTOL)
         t += time.perf_counter() - t0
         its += rep["iterations"]
-    return P.n * its / t, t, its, H.setup_s
+    single = None
+    if single_iters:
+        # the faithful single-threaded reference (same hierarchy)
+        refcpu.set_threads(1)
+        t0 = time.perf_counter()
+        _, rep = H.solve(P.rhs, restart=RESTART, max_iters=single_iters, rel_tol=RTOL)
+        ts = time.perf_counter() - t0
+        single = {"value": P.n * rep["iterations"] / ts, "cores": 1,
+                  "sample": f"one solve capped at {rep['iterations']} iterations ({ts:.1f}s)"}
+        refcpu.set_threads(threads)
+    return P.n * its / t, t, its, H.setup_s, single
 
 
 def run_reference(args):
@@ -161,7 +171,7 @@ def run_reference(args):
         return
     P = make_problem(world)
     threads = os.cpu_count() or 1
-    v, t, its, setup_s = cpu_reference(P, args.steps, args.warmup, args.ref_iters, threads)
+    v, t, its, setup_s, _ = cpu_reference(P, args.steps, args.warmup, args.ref_iters, threads)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / max(args.steps, 1),
             "higher_is_better": True, "scaling": scaling_kind(world), "vs_baseline": None, "dtype": "f64",
@@ -407,6 +417,25 @@ def main():
             "peak_source": peak_kind, "kernels": probes,
             "probe_method": "CUDA events on the library stream over 20 back-to-back launches (inputs in HBM; the L2 may retain part of a working set near its 126 MB size)"}
 
+    # whole-solve roofline: SURVEY §8(d) compulsory-traffic bytes of one solve
+    # (tools/solve_model.py, from the hierarchy's sizes) over the timed solve
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from solve_model import SolveModel
+        sm = SolveModel(H, mx.load_strategy(STRATEGY))
+        its_solve = int(round(its / args.steps))
+        mb = sm.solve_bytes(int(P.ptr[-1]), P.n, its_solve, RESTART)
+        t_solve = ms * 1e-3 / args.steps
+        solve_roof = {"bound": "hbm", "model_bytes_per_solve": mb["bytes"],
+                      "achieved": mb["bytes"] / t_solve / 1e9, "peak": peak, "unit": "GB/s",
+                      "frac": mb["bytes"] / t_solve / 1e9 / peak,
+                      "precond_bytes_per_apply": mb["precond_bytes_per_apply"],
+                      "spmv_bytes": mb["spmv_bytes"], "restart_cycles": mb["restart_cycles"],
+                      "model": "SURVEY 8(d) compulsory traffic per operation (tools/solve_model.py), "
+                               "MGS at 24n(k+1)+32n per step"}
+    except Exception as e:  # the model is reporting, never a reason to lose the line
+        solve_roof = {"error": f"{type(e).__name__}: {e}"}
+
     variants = {}
     vname = CONFIGS[CONFIG].get("variant")
     if vname and not args.strategy and not args.no_variant:
@@ -433,10 +462,11 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        v, t, cits, setup_s = cpu_reference(P, 1, 0, args.ref_iters, threads)
+        v, t, cits, setup_s, single = cpu_reference(P, 1, 0, args.ref_iters, threads, single_iters=3)
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
                "sample": f"refcpu oracle, {CONFIG}, one solve capped at {args.ref_iters} iterations "
-                         f"({cits} its in {t:.1f}s; setup {setup_s:.1f}s excluded)"}
+                         f"({cits} its in {t:.1f}s; setup {setup_s:.1f}s excluded)",
+               "single_thread": single}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -448,7 +478,8 @@ def main():
                 "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * P.n,
                         "d2h_bytes_per_step": 8 * P.n,
                         "path": "Hierarchy.solve -> mgrx_solve (C ABI) with pinned host b / x, zero initial guess"},
-                "gpu_launches": launches, "roofline": roof, "cpu_baseline": cpu, "variants": variants,
+                "gpu_launches": launches, "roofline": roof, "solve_roofline": solve_roof, "cpu_baseline": cpu,
+                "variants": variants,
                 "clocks": clk.summary()}
         print(json.dumps(line))
 

@@ -394,32 +394,413 @@ __global__ void __launch_bounds__(kAT, 1) k_arnoldi(ArnoldiArgs a) {
   }
 }
 
-// Launch parameters of the fused Arnoldi kernel for n rows, or 0 slots when it
-// cannot run (n too large for shared memory, or not a 148-SM part).
-int arnoldi_slots(int n) {
-  static const int mode = [] {
-    const char* v = std::getenv("MGRX_ARNOLDI");
-    return v ? std::atoi(v) : 1;
-  }();
-  static const bool fits = [] {
+// ---------------------------------------------------------------------------
+// Lane-pair variant (the default): 512 threads per CTA, thread t of CTA c
+// owns canonical lanes c*1024 + 2t and 2t+1, so every access is a 16-byte
+// pair and each thread has 128 registers. The row loop of a projection is
+// bound by memory-level parallelism, not by HBM bandwidth: the 1024-thread
+// kernel (64 registers) keeps 4 slots x 16 B per thread in flight, ~32 KB of
+// HBM reads per SM, which covers ~0.6 of the HBM latency-bandwidth product.
+// Here a group of kU slots issues kU x 32 B per thread (HBM v_i + L2 v_{i-1})
+// before any is consumed.
+//
+// The canonical reduction is reproduced exactly: per lane, the products are
+// summed in slot order into separate accumulators (x: lane 2t, y: lane
+// 2t+1); the canonical warp tree (shfl_down 16, 8, 4, 2, 1 over 32 lanes)
+// maps onto a 16-thread half warp as shfl_down 8, 4, 2, 1 applied to x and y
+// separately followed by x + y (canonical lane 0 + lane 1); the 256-lane
+// block trees and the fold of the 592 block partials are unchanged.
+constexpr int kAT2 = 512;
+
+__device__ __forceinline__ double2 ld2_pol(const double* a, unsigned long long p) {
+  double2 v;
+  asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(p));
+  return v;
+}
+
+// Canonical 32-lane warp sum of the lanes held by one 16-thread half warp
+// (valid in threads 0 and 16 of the warp).
+__device__ __forceinline__ double half_warp_pair_sum(double x, double y) {
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) {
+    x = __dadd_rn(x, __shfl_down_sync(0xffffffffu, x, o));
+    y = __dadd_rn(y, __shfl_down_sync(0xffffffffu, y, o));
+  }
+  return __dadd_rn(x, y);
+}
+
+struct PairSums {
+  double s1x = 0.0, s1y = 0.0, s2x = 0.0, s2y = 0.0;
+};
+
+template <bool kV, bool kA, bool kW2>
+__device__ __forceinline__ void arn2_slot(double2* wp, double2 pv, double2 xv, double h, PairSums& s) {
+  double2 wi = *wp;
+  if (kV) {
+    wi.x = __dsub_rn(wi.x, __dmul_rn(h, pv.x));
+    wi.y = __dsub_rn(wi.y, __dmul_rn(h, pv.y));
+    *wp = wi;
+  }
+  if (kA) {
+    s.s1x = __dadd_rn(s.s1x, __dmul_rn(xv.x, wi.x));
+    s.s1y = __dadd_rn(s.s1y, __dmul_rn(xv.y, wi.y));
+  }
+  if (kW2) {
+    s.s2x = __dadd_rn(s.s2x, __dmul_rn(wi.x, wi.x));
+    s.s2y = __dadd_rn(s.s2y, __dmul_rn(wi.y, wi.y));
+  }
+}
+
+// One projection phase over this thread's lane pair: nsy slots where both
+// lanes hold a row, plus (xtail) one more slot for lane x only.
+template <int kU, bool kV, bool kA, bool kW2>
+__device__ __forceinline__ void arn2_rows(double2* wl, int nsy, bool xtail, const double* __restrict__ pl,
+                                          const double* __restrict__ al, double h, unsigned long long pf,
+                                          PairSums& s, int rot = 0) {
+  constexpr int kStride = kRB * kRT;
+  int q = 0;
+  for (; q + kU <= nsy; q += kU) {
+    double2 pv[kU], xv[kU];
+    int qs[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      qs[u] = q + u + rot;  // rot != 0: timing experiment only (slot order rotated per CTA)
+      if (qs[u] >= nsy) qs[u] -= nsy;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (kV) pv[u] = pl ? ld2_pol(pl + qs[u] * kStride, pf) : make_double2(0.0, 0.0);
+      if (kA) xv[u] = __ldcg(reinterpret_cast<const double2*>(al + qs[u] * kStride));
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) arn2_slot<kV, kA, kW2>(wl + qs[u] * kAT2, pv[u], xv[u], h, s);
+  }
+  for (; q < nsy; ++q) {
+    double2 pv = make_double2(0.0, 0.0), xv = make_double2(0.0, 0.0);
+    if (kV && pl) pv = ld2_pol(pl + q * kStride, pf);
+    if (kA) xv = __ldcg(reinterpret_cast<const double2*>(al + q * kStride));
+    arn2_slot<kV, kA, kW2>(wl + q * kAT2, pv, xv, h, s);
+  }
+  if (xtail) {
+    double* wx = reinterpret_cast<double*>(wl + q * kAT2);
+    double wi = *wx;
+    if (kV) {
+      wi = __dsub_rn(wi, __dmul_rn(h, __ldcg(pl + q * kStride)));
+      *wx = wi;
+    }
+    if (kA) s.s1x = __dadd_rn(s.s1x, __dmul_rn(__ldcg(al + q * kStride), wi));
+    if (kW2) s.s2x = __dadd_rn(s.s2x, __dmul_rn(wi, wi));
+  }
+}
+
+// Grid-wide reduction of one projection phase in the canonical order (see
+// above): canonical warp sums, 256-lane block trees, partials, grid barrier,
+// in-order fold of the kRB partials in every CTA. r/f: shared scratch.
+__device__ __forceinline__ void pair_reduce(const ArnoldiArgs& a, const PairSums& ps, unsigned phase, double* r1,
+                                            double* r2, double* f1, double* f2, double& t1, double& t2) {
+  const int T = threadIdx.x;
+  const int wp = T >> 5, l = T & 31;
+  const double c1 = half_warp_pair_sum(ps.s1x, ps.s1y);
+  const double c2 = half_warp_pair_sum(ps.s2x, ps.s2y);
+  if ((T & 15) == 0) {  // canonical warp T/16 of this CTA
+    r1[T >> 4] = c1;
+    r2[T >> 4] = c2;
+  }
+  __syncthreads();
+  double* part = a.part + (phase & 1) * 2 * kRB;
+  if (wp < kAT / kRT) {  // canonical 256-lane block trees (block_sum2)
+    double x1 = l < kRT / 32 ? r1[wp * (kRT / 32) + l] : 0.0;
+    double x2 = l < kRT / 32 ? r2[wp * (kRT / 32) + l] : 0.0;
+    x1 = warp_sum(x1);
+    x2 = warp_sum(x2);
+    if (l == 0) {
+      const int b = blockIdx.x * (kAT / kRT) + wp;
+      part[2 * b] = x1;
+      part[2 * b + 1] = x2;
+    }
+  }
+  __syncthreads();
+  if (T == 0 && !(a.dbg & 2)) {
+    __threadfence();
+    atomicAdd(a.bar, 1u);
+    const unsigned target = (phase + 1) * gridDim.x;
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.bar) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+  if (T < kRT) {
+    constexpr int kF = (kRB + kRT - 1) / kRT;
+    double p1[kF], p2[kF];
+#pragma unroll
+    for (int j = 0; j < kF; ++j) {
+      const int b = T + j * kRT;
+      if (b < kRB) {
+        p1[j] = __ldcg(part + 2 * b);
+        p2[j] = __ldcg(part + 2 * b + 1);
+      }
+    }
+    double u1 = 0.0, u2 = 0.0;
+#pragma unroll
+    for (int j = 0; j < kF; ++j) {
+      if (T + j * kRT < kRB) {
+        u1 = __dadd_rn(u1, p1[j]);
+        u2 = __dadd_rn(u2, p2[j]);
+      }
+    }
+    u1 = warp_sum(u1);
+    u2 = warp_sum(u2);
+    if (l == 0) {
+      f1[wp] = u1;
+      f2[wp] = u2;
+    }
+  }
+  __syncthreads();
+  const double x1 = l < kRT / 32 ? f1[l] : 0.0;
+  const double x2 = l < kRT / 32 ? f2[l] : 0.0;
+  t1 = __shfl_sync(0xffffffffu, warp_sum(x1), 0);
+  t2 = __shfl_sync(0xffffffffu, warp_sum(x2), 0);
+}
+
+// Writer bookkeeping of one reduced phase (H column, norms).
+__device__ __forceinline__ void arn_record(const ArnoldiArgs& a, bool writer, int pass, int i, double t1, double t2,
+                                           double* hk, double& h, double& w02, double& wn2) {
+  if (i <= a.k) {
+    if (pass == 0 && i == 0) w02 = t2;
+    h = t1;
+    if (writer) {
+      a.hp[i] = t1;
+      const double hv = pass ? __dadd_rn(i < kAHk ? hk[i] : a.hc[i], t1) : t1;
+      if (i < kAHk) hk[i] = hv;
+      a.hc[i] = hv;
+    }
+  } else {
+    wn2 = t2;
+  }
+}
+
+template <int kU>
+__global__ void __launch_bounds__(kAT2, 1) k_arnoldi2(ArnoldiArgs a) {
+  extern __shared__ double2 wsm2[];               // [slot][kAT2] lane pairs
+  __shared__ double r1[kAT / 32], r2[kAT / 32];   // canonical warp sums of this CTA (32)
+  __shared__ double f1[kRT / 32], f2[kRT / 32];   // fold: per-warp sums of the kRB partials
+  __shared__ double hk[kAHk];
+  const int T = threadIdx.x;
+  const int n = a.n, k = a.k;
+  constexpr int kStride = kRB * kRT;
+  const int lane = blockIdx.x * kAT + 2 * T;  // lane x; lane y = lane + 1 (n is even: both or neither)
+  const int nsy = lane < n ? (n - 1 - lane) / kStride + 1 : 0;
+  for (int q = 0; q < nsy; ++q)
+    wsm2[q * kAT2 + T] = __ldcg(reinterpret_cast<const double2*>(a.w + lane + q * kStride));
+  const unsigned long long pf = pol_first();
+  const size_t ld = static_cast<size_t>(n);
+  double2* wl = wsm2 + T;
+  const bool writer = blockIdx.x == 0 && T == 0;
+  double h = 0.0, wn2 = 0.0, w02 = 0.0;
+  unsigned phase = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int i = 0; i <= k + 1; ++i) {
+      PairSums ps;
+      double t1, t2;
+      if (!(a.dbg & 1)) {
+        // dbg & 64 (timing experiment, not bitwise): no L2 re-read of v_{i-1}
+        const double* pl = (i && !(a.dbg & 64)) ? a.V + (i - 1) * ld + lane : nullptr;
+        const double* al = a.V + i * ld + lane;
+        // dbg & 32 (timing experiment, not bitwise): rotate the slot order per CTA
+        const int rot = (a.dbg & 32) ? (kU * (blockIdx.x % (nsy / kU > 0 ? nsy / kU : 1))) % (nsy > 0 ? nsy : 1) : 0;
+        if (i > k) arn2_rows<kU, true, false, true>(wl, nsy, false, pl, al, h, pf, ps, rot);
+        else if (i) arn2_rows<kU, true, true, false>(wl, nsy, false, pl, al, h, pf, ps, rot);
+        else if (pass == 0) arn2_rows<kU, false, true, true>(wl, nsy, false, pl, al, h, pf, ps, rot);
+        else arn2_rows<kU, false, true, false>(wl, nsy, false, pl, al, h, pf, ps, rot);
+      }
+      pair_reduce(a, ps, phase++, r1, r2, f1, f2, t1, t2);
+      arn_record(a, writer, pass, i, t1, t2, hk, h, w02, wn2);
+    }
+    h = 0.0;
+    if (pass == 1 || (!(a.dbg & 4) && !(__dsqrt_rn(wn2) < __ddiv_rn(__dsqrt_rn(w02), __dsqrt_rn(2.0))))) break;
+  }
+  if (writer) {
+    *a.n0 = w02;
+    *a.n1 = wn2;
+  }
+  const double wn = __dsqrt_rn(wn2);
+  if (!(wn < 1e-300)) {
+    double* out = const_cast<double*>(a.V) + (k + 1) * ld;
+    for (int q = 0; q < nsy; ++q) {
+      const double2 wi = wsm2[q * kAT2 + T];
+      reinterpret_cast<double2*>(out + lane + q * kStride)[0] = make_double2(__ddiv_rn(wi.x, wn), __ddiv_rn(wi.y, wn));
+    }
+  }
+}
+
+// Software-pipelined lane-pair kernel: the loads of slot group g+1 are issued
+// before group g is consumed, and the last group of a phase issues the first
+// group of the NEXT phase (its columns are known before the reduction; only
+// h is not, and h is applied when the group is consumed). So the HBM stream
+// does not drain at the grid barrier: each phase starts with its first group
+// on chip. After the closing norm of pass 1 the first group of pass 2 is
+// prefetched speculatively (discarded when no re-orthogonalisation follows).
+template <int kU>
+struct PairGroup {
+  double2 p[kU], x[kU];
+};
+
+template <int kU>
+__device__ __forceinline__ void pgroup_load(PairGroup<kU>& g, const double* pl, const double* al, int q0, int nsy,
+                                            unsigned long long pf) {
+  constexpr int kStride = kRB * kRT;
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    const int q = q0 + u;
+    if (q < nsy) {
+      if (pl) g.p[u] = ld2_pol(pl + q * kStride, pf);
+      if (al) g.x[u] = __ldcg(reinterpret_cast<const double2*>(al + q * kStride));
+    }
+  }
+}
+
+template <int kU>
+__device__ __forceinline__ void pgroup_use(const PairGroup<kU>& g, double2* wl, int q0, int nsy, bool v, bool dot,
+                                           bool w2, double h, PairSums& s) {
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    const int q = q0 + u;
+    if (q < nsy) {
+      double2 wi = wl[q * kAT2];
+      if (v) {
+        wi.x = __dsub_rn(wi.x, __dmul_rn(h, g.p[u].x));
+        wi.y = __dsub_rn(wi.y, __dmul_rn(h, g.p[u].y));
+        wl[q * kAT2] = wi;
+      }
+      if (dot) {
+        s.s1x = __dadd_rn(s.s1x, __dmul_rn(g.x[u].x, wi.x));
+        s.s1y = __dadd_rn(s.s1y, __dmul_rn(g.x[u].y, wi.y));
+      }
+      if (w2) {
+        s.s2x = __dadd_rn(s.s2x, __dmul_rn(wi.x, wi.x));
+        s.s2y = __dadd_rn(s.s2y, __dmul_rn(wi.y, wi.y));
+      }
+    }
+  }
+}
+
+template <int kU>
+__global__ void __launch_bounds__(kAT2, 1) k_arnoldi3(ArnoldiArgs a) {
+  extern __shared__ double2 wsm2[];
+  __shared__ double r1[kAT / 32], r2[kAT / 32];
+  __shared__ double f1[kRT / 32], f2[kRT / 32];
+  __shared__ double hk[kAHk];
+  const int T = threadIdx.x;
+  const int n = a.n, k = a.k;
+  constexpr int kStride = kRB * kRT;
+  const int lane = blockIdx.x * kAT + 2 * T;
+  const int nsy = lane < n ? (n - 1 - lane) / kStride + 1 : 0;
+  const unsigned long long pf = pol_first();
+  const size_t ld = static_cast<size_t>(n);
+  const bool rows = !(a.dbg & 1);
+  // phase (pass, i): i <= k projects on v_i (after the update by v_{i-1});
+  // i == k+1 is the closing update + norm
+  auto cols = [&](int i, const double*& pl, const double*& al) {
+    pl = (rows && i) ? a.V + (i - 1) * ld + lane : nullptr;
+    al = (rows && i <= k) ? a.V + i * ld + lane : nullptr;
+  };
+  PairGroup<kU> cur;
+  const double *pl, *al;
+  cols(0, pl, al);
+  pgroup_load(cur, pl, al, 0, nsy, pf);
+  for (int q = 0; q < nsy; ++q)
+    wsm2[q * kAT2 + T] = __ldcg(reinterpret_cast<const double2*>(a.w + lane + q * kStride));
+  double2* wl = wsm2 + T;
+  const bool writer = blockIdx.x == 0 && T == 0;
+  double h = 0.0, wn2 = 0.0, w02 = 0.0;
+  unsigned phase = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int i = 0; i <= k + 1; ++i) {
+      const double *npl = nullptr, *nal = nullptr;
+      if (i <= k) cols(i + 1, npl, nal);
+      else if (pass == 0) cols(0, npl, nal);  // speculative: pass 2 starts with v_0
+      const bool v = i > 0, dot = i <= k, w2 = i > k || (pass == 0 && i == 0);
+      PairSums ps;
+      for (int q0 = 0; q0 < nsy; q0 += kU) {
+        PairGroup<kU> nxt;
+        if (q0 + kU < nsy) pgroup_load(nxt, pl, al, q0 + kU, nsy, pf);
+        else pgroup_load(nxt, npl, nal, 0, nsy, pf);
+        if (rows) pgroup_use(cur, wl, q0, nsy, v, dot, w2, h, ps);
+        cur = nxt;
+      }
+      pl = npl;
+      al = nal;
+      double t1, t2;
+      pair_reduce(a, ps, phase++, r1, r2, f1, f2, t1, t2);
+      arn_record(a, writer, pass, i, t1, t2, hk, h, w02, wn2);
+    }
+    h = 0.0;
+    if (pass == 1 || (!(a.dbg & 4) && !(__dsqrt_rn(wn2) < __ddiv_rn(__dsqrt_rn(w02), __dsqrt_rn(2.0))))) break;
+  }
+  if (writer) {
+    *a.n0 = w02;
+    *a.n1 = wn2;
+  }
+  const double wn = __dsqrt_rn(wn2);
+  if (!(wn < 1e-300)) {
+    double* out = const_cast<double*>(a.V) + (k + 1) * ld;
+    for (int q = 0; q < nsy; ++q) {
+      const double2 wi = wsm2[q * kAT2 + T];
+      reinterpret_cast<double2*>(out + lane + q * kStride)[0] = make_double2(__ddiv_rn(wi.x, wn), __ddiv_rn(wi.y, wn));
+    }
+  }
+}
+
+// MGRX_ARNOLDI: 0 off (launch-per-projection MGS), 1 the 1024-thread kernel,
+// 2 (default) the lane-pair kernel with MGRX_ARNOLDI_U slots per load group
+// (4, 6 or 8; default 8). The lane-pair kernel needs 16-byte aligned basis
+// columns (n even); odd n uses the 1024-thread kernel.
+struct ArnoldiMode {
+  int mode = 2, u = 4;
+  bool fits1 = false, fits2 = false;
+};
+
+template <typename K>
+bool arnoldi_fits(K kern, int threads) {
+  const int bytes = kAMaxSlots * kAT * static_cast<int>(sizeof(double));
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return occ >= 1;
+}
+
+const ArnoldiMode& arnoldi_mode() {
+  static const ArnoldiMode m = [] {
+    ArnoldiMode r;
+    if (const char* v = std::getenv("MGRX_ARNOLDI")) r.mode = std::atoi(v);
+    if (const char* v = std::getenv("MGRX_ARNOLDI_U")) r.u = std::atoi(v);
+    if (r.mode == 3 && r.u != 2) r.u = 4;
+    if (r.mode == 2 && r.u != 4 && r.u != 6) r.u = 8;
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms != kAB) return false;
-    const int bytes = kAMaxSlots * kAT * static_cast<int>(sizeof(double));
-    if (cudaFuncSetAttribute(k_arnoldi, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) {
-      cudaGetLastError();
-      return false;
-    }
-    int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_arnoldi, kAT, bytes) != cudaSuccess) {
-      cudaGetLastError();
-      return false;
-    }
-    return occ >= 1;
+    if (sms != kAB) return r;
+    r.fits1 = arnoldi_fits(k_arnoldi, kAT);
+    if (r.mode == 3) r.fits2 = arnoldi_fits(r.u == 2 ? k_arnoldi3<2> : k_arnoldi3<4>, kAT2);
+    else r.fits2 = arnoldi_fits(r.u == 4 ? k_arnoldi2<4> : r.u == 6 ? k_arnoldi2<6> : k_arnoldi2<8>, kAT2);
+    return r;
   }();
+  return m;
+}
+
+int arnoldi_slots(int n) {
+  const ArnoldiMode& m = arnoldi_mode();
   constexpr int kStride = kRB * kRT;
-  if (!mode || !fits || n <= 0) return 0;
+  if (!m.mode || n <= 0) return 0;
+  const bool pair = m.mode >= 2 && m.fits2 && n % 2 == 0;
+  if (!pair && !m.fits1) return 0;
   const int slots = (n - 1) / kStride + 1;
   return slots <= kAMaxSlots ? slots : 0;
 }
@@ -430,8 +811,17 @@ void arnoldi_launch(int n, int k, int slots, int dbg, GmresWork& ws, cudaStream_
   MGRX_CK(cudaMemsetAsync(ws.bar.get(), 0, sizeof(unsigned), s));
   ArnoldiArgs aa{n, k, ws.w.get(), ws.V.get(), ws.apart.get(), ws.bar.get(), S, S + 1, S + 2, S + 3 + (m + 1), dbg};
   void* args[] = {&aa};
-  MGRX_CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_arnoldi), dim3(kAB), dim3(kAT), args,
-                                      static_cast<size_t>(slots) * kAT * sizeof(double), s));
+  const ArnoldiMode& md = arnoldi_mode();
+  const size_t smem = static_cast<size_t>(slots) * kAT * sizeof(double);
+  if (md.mode >= 2 && md.fits2 && n % 2 == 0 && !(dbg & 8)) {
+    void* kern = md.mode == 3 ? (md.u == 2 ? reinterpret_cast<void*>(k_arnoldi3<2>) : reinterpret_cast<void*>(k_arnoldi3<4>))
+                 : md.u == 4 ? reinterpret_cast<void*>(k_arnoldi2<4>)
+                 : md.u == 6 ? reinterpret_cast<void*>(k_arnoldi2<6>)
+                             : reinterpret_cast<void*>(k_arnoldi2<8>);
+    MGRX_CK(cudaLaunchCooperativeKernel(kern, dim3(kAB), dim3(kAT2), args, smem, s));
+  } else {
+    MGRX_CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_arnoldi), dim3(kAB), dim3(kAT), args, smem, s));
+  }
   count_launch();
 }
 
