@@ -160,7 +160,17 @@ void prepare_probe(mgrx_hier* h, const std::string& w, std::function<void()>& fn
     bytes = spmv_model_bytes(*A);
     return;
   }
-  if (w.rfind("mgr.", 0) == 0) {
+  std::string wa = w;
+  AmgHier* amg_src = h->H.coarse_amg.get();
+  if (w.rfind("mgr.", 0) == 0 && w.find(".frelax.amg.") != std::string::npos) {
+    // mgr.<l>.frelax.amg.<k>.<what>: the F-relaxation AMG of MGR level l
+    const size_t d = w.find('.', 4);
+    const int l = std::stoi(w.substr(4, d - 4));
+    if (l < 0 || l >= static_cast<int>(h->H.levels.size())) throw InvalidArgument("probe: no MGR level " + w);
+    amg_src = h->H.levels[l].f_relax.amg.get();
+    wa = w.substr(w.find(".frelax.") + 8);
+  }
+  if (wa == w && w.rfind("mgr.", 0) == 0) {
     const size_t d = w.find('.', 4);
     const int l = std::stoi(w.substr(4, d - 4));
     if (l < 0 || l >= static_cast<int>(h->H.levels.size())) throw InvalidArgument("probe: no MGR level " + w);
@@ -180,13 +190,13 @@ void prepare_probe(mgrx_hier* h, const std::string& w, std::function<void()>& fn
       return;
     }
   }
-  if (w.rfind("amg.", 0) == 0) {
-    const size_t d = w.find('.', 4);
-    const int k = std::stoi(w.substr(4, d - 4));
-    AmgHier* amg = h->H.coarse_amg.get();
+  if (wa.rfind("amg.", 0) == 0) {
+    const size_t d = wa.find('.', 4);
+    const int k = std::stoi(wa.substr(4, d - 4));
+    AmgHier* amg = amg_src;
     if (!amg || k < 0 || k + 1 >= static_cast<int>(amg->levels.size())) throw InvalidArgument("probe: no AMG level " + w);
     AmgLevelD* L = &amg->levels[k];
-    const std::string what = w.substr(d + 1);
+    const std::string what = wa.substr(d + 1);
     const double m = L->A.rows;
     if (what == "resid") {
       fn = [=] { spmv_residual(L->A, x, y, nullptr, z, s); };
