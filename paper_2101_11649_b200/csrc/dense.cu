@@ -426,6 +426,230 @@ void launch_panel_solve(int grid, int n, const int* bst, const long long* boff, 
   count_launch();
 }
 
+// ---------------------------------------------------------------------------
+// Cluster-parallel triangular solves for blocks of <= 256 rows (the MGR
+// coarse well blocks of the compositional strategy, 250 rows each; small
+// AMG coarsest grids). The single-CTA panel solve streams the whole n x n
+// factor through one SM twice per solve (cfg3: 96 us of an 856 us GMRES
+// step). Here block b is solved by a thread-block cluster of C = ceil(n/32)
+// CTAs: CTA c owns rows 32c..32c+31 (one warp, one lane per row) and holds
+// those rows of L and U in shared memory (its "slab", re-laid out at
+// factorization time, one bulk copy per solve). Forward: CTA c applies the
+// panels of the CTAs before it as their solved values arrive, in panel
+// order and column order within a panel, then runs its own panel triangle
+// and stores its 32 values into the shared memory of every later CTA of the
+// cluster (DSMEM) behind a per-panel flag. Backward mirrors it. Every x_i
+// receives exactly the updates of the unblocked algorithm in the same order
+// (the panel solve's k_lu_solve_panel bodies), so results are bitwise equal.
+constexpr int kClMax = 8;  // CTAs per cluster (portable limit) -> blocks of <= 256 rows
+
+// slab[((b * C + c) * ns + j) * 32 + r] = M_b(32c + r, j) (0 outside the block)
+__global__ void k_slabify(int nb, int C, int ns, const int* __restrict__ bst, const long long* __restrict__ boff,
+                          int n1, const double* __restrict__ blu, double* __restrict__ slab) {
+  const long long total = static_cast<long long>(nb) * C * ns * 32;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(e & 31);
+    const long long q = e >> 5;
+    const int j = static_cast<int>(q % ns);
+    const long long bc = q / ns;
+    const int c = static_cast<int>(bc % C), b = static_cast<int>(bc / C);
+    const int n = bst ? bst[b + 1] - bst[b] : n1;
+    const int i = 32 * c + r;
+    const double* M = blu + (boff ? boff[b] : 0);
+    slab[e] = (i < n && j < n) ? M[static_cast<size_t>(j) * n + i] : 0.0;
+  }
+}
+
+__device__ __forceinline__ unsigned cl_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned cl_map(const void* p, unsigned cta) {
+  unsigned a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+               : "=r"(a)
+               : "r"(static_cast<unsigned>(__cvta_generic_to_shared(p))), "r"(cta));
+  return a;
+}
+__device__ __forceinline__ void cl_st_f64(unsigned a, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void cl_st_u32(unsigned a, unsigned v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(32) k_lu_solve_cluster(int ns, const int* __restrict__ bst,
+                                                         const int* __restrict__ rows,
+                                                         const double* __restrict__ slab,
+                                                         const int* __restrict__ perm, int n1,
+                                                         const double* __restrict__ bvec, double* __restrict__ x) {
+  pdl_enter();
+  extern __shared__ __align__(16) double csm[];
+  double* S = csm;                 // [ns][32] this CTA's rows of L and U
+  double* xf = csm + ns * 32;      // solved values of the other CTAs' rows
+  __shared__ volatile unsigned flag[2][kClMax];
+  __shared__ __align__(8) unsigned long long mbar;
+  const unsigned c = cl_rank();
+  unsigned nc;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(nc));
+  const int b = blockIdx.x / nc;
+  const int l = threadIdx.x;
+  const int lo = bst ? bst[b] : 0;
+  const int n = bst ? bst[b + 1] - lo : n1;
+  const int* pm = perm + lo;
+  const int r0 = 32 * c;
+  const int np = (n + 31) / 32;  // panels = active CTAs of this block
+  if (l < 2 * kClMax) flag[l / kClMax][l % kClMax] = 0u;
+  const unsigned mb = static_cast<unsigned>(__cvta_generic_to_shared(&mbar));
+  if (l == 0) {
+    asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(mb));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  cl_sync();  // flags initialised cluster-wide before any remote store
+  const bool active = r0 < n;
+  if (active) {
+    const unsigned bytes = static_cast<unsigned>(ns) * 32u * 8u;
+    if (l == 0) {
+      asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              static_cast<unsigned>(__cvta_generic_to_shared(S))),
+          "l"(slab + (static_cast<size_t>(blockIdx.x) * ns) * 32), "r"(bytes), "r"(mb)
+          : "memory");
+    }
+    const int i = r0 + l;
+    const int jn_own = min(32, n - r0);
+    double xv = l < jn_own ? bvec[rows ? rows[lo + pm[i]] : pm[i]] : 0.0;
+    unsigned done = 0;
+    do {
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done)
+                   : "r"(mb), "r"(0u)
+                   : "memory");
+    } while (!done);
+    // forward: panels of the earlier CTAs, in order, as they arrive
+    for (int p = 0; p < static_cast<int>(c); ++p) {
+      while (flag[0][p] == 0u) {
+      }
+      asm volatile("fence.acq_rel.cluster;" ::: "memory");
+      const int j0 = 32 * p, jn = min(32, n - j0);
+      for (int jj = 0; jj < jn; ++jj) xv = __dsub_rn(xv, __dmul_rn(S[(j0 + jj) * 32 + l], xf[j0 + jj]));
+    }
+    // own panel triangle (unit lower)
+    {
+      double m[32];
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) m[jj] = (jj < l && l < jn_own) ? S[(r0 + jj) * 32 + l] : 0.0;
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) {
+        const double xj = __shfl_sync(0xffffffffu, xv, jj);
+        if (jj < l && l < jn_own) xv = __dsub_rn(xv, __dmul_rn(m[jj], xj));
+      }
+    }
+    // publish to the later CTAs of the block
+    for (int q = static_cast<int>(c) + 1; q < np; ++q) {
+      if (l < jn_own) cl_st_f64(cl_map(xf + i, q), xv);
+      __syncwarp();
+      if (l == 0) {
+        asm volatile("fence.acq_rel.cluster;" ::: "memory");
+        cl_st_u32(cl_map(const_cast<unsigned*>(&flag[0][c]), q), 1u);
+      }
+    }
+    // backward: panels of the later CTAs, last first
+    for (int p = np - 1; p > static_cast<int>(c); --p) {
+      while (flag[1][p] == 0u) {
+      }
+      asm volatile("fence.acq_rel.cluster;" ::: "memory");
+      const int j0 = 32 * p, jn = min(32, n - j0);
+      for (int jj = jn - 1; jj >= 0; --jj) xv = __dsub_rn(xv, __dmul_rn(S[(j0 + jj) * 32 + l], xf[j0 + jj]));
+    }
+    // own panel triangle (upper, division before the column's updates)
+    {
+      double m[32];
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) m[jj] = (jj >= l && jj < jn_own && l < jn_own) ? S[(r0 + jj) * 32 + l] : 1.0;
+#pragma unroll
+      for (int jj = 31; jj >= 0; --jj) {
+        if (jj < jn_own) {
+          if (l == jj) xv = __ddiv_rn(xv, m[jj]);
+          const double xj = __shfl_sync(0xffffffffu, xv, jj);
+          if (l < jj) xv = __dsub_rn(xv, __dmul_rn(m[jj], xj));
+        }
+      }
+    }
+    for (int q = static_cast<int>(c) - 1; q >= 0; --q) {
+      if (l < jn_own) cl_st_f64(cl_map(xf + i, q), xv);
+      __syncwarp();
+      if (l == 0) {
+        asm volatile("fence.acq_rel.cluster;" ::: "memory");
+        cl_st_u32(cl_map(const_cast<unsigned*>(&flag[1][c]), q), 1u);
+      }
+    }
+    if (l < jn_own) x[rows ? rows[lo + i] : i] = xv;
+  }
+  cl_sync();  // no CTA leaves while a peer may still store into its shared memory
+}
+
+bool cluster_solve_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("MGRX_DENSE_CLUSTER");
+    return !v || std::atoi(v) != 0;
+  }();
+  return on;
+}
+
+// Re-lay the factors out as per-CTA slabs (after factorization).
+void build_slabs(DenseLU& f, cudaStream_t s) {
+  f.ccl = 0;
+  const int nmax = f.nb > 1 ? f.max_block : f.n;
+  if (!cluster_solve_enabled() || nmax <= 0 || nmax > 32 * kClMax) return;
+  const int C = (nmax + 31) / 32;
+  const int ns = nmax;
+  const size_t smem = sizeof(double) * (static_cast<size_t>(ns) * 32 + ns + 2);
+  if (smem > 48 * 1024)
+    MGRX_CK(cudaFuncSetAttribute(k_lu_solve_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  f.slab.alloc(static_cast<size_t>(f.nb) * C * ns * 32, s);
+  const long long total = static_cast<long long>(f.nb) * C * ns * 32;
+  const int grid = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 16));
+  if (f.nb > 1)
+    k_slabify<<<grid, 256, 0, s>>>(f.nb, C, ns, f.bst.get(), f.boff.get(), 0, f.blu.get(), f.slab.get());
+  else
+    k_slabify<<<grid, 256, 0, s>>>(1, C, ns, nullptr, nullptr, f.n, f.lu.get(), f.slab.get());
+  MGRX_LAUNCH_CK();
+  count_launch();
+  f.ccl = C;
+  f.slab_n = ns;
+}
+
+void launch_cluster_solve(const DenseLU& f, const double* b, double* x, cudaStream_t s) {
+  const int C = f.ccl, ns = f.slab_n;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(f.nb * C);
+  cfg.blockDim = dim3(32);
+  cfg.dynamicSmemBytes = sizeof(double) * (static_cast<size_t>(ns) * 32 + ns + 2);
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = C;
+  at[1].val.clusterDim.y = 1;
+  at[1].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  const int* bst = f.nb > 1 ? f.bst.get() : nullptr;
+  const int* rows = f.nb > 1 ? f.rows.get() : nullptr;
+  MGRX_CK(cudaLaunchKernelEx(&cfg, k_lu_solve_cluster, ns, bst, rows, static_cast<const double*>(f.slab.get()),
+                             static_cast<const int*>(f.perm.get()), f.n, b, x));
+  count_launch();
+}
+
 // Connected components of the symmetrised pattern of A (host; A is a
 // coarse system): component lists ascending, components ordered by their
 // smallest row.
@@ -502,6 +726,7 @@ void dense_factor(const DCsr& A, DenseLU& out, cudaStream_t s, double pivot_tol,
       if (sizeof(double) * out.max_block > 200 * 1024)
         throw RuntimeError("dense LU solve: block too large for shared memory");
       prepare_panel_solve(out.max_block);
+      build_slabs(out, s);
       const int b = read_scalar(bad.get(), s);
       // the dense algorithm reports the first singular pivot in row order
       if (b != INT_MAX) throw RuntimeError("dense LU: matrix numerically singular (pivot " + std::to_string(b) + ")");
@@ -528,12 +753,17 @@ void dense_factor(const DCsr& A, DenseLU& out, cudaStream_t s, double pivot_tol,
   if (sm > 48 * 1024)
     MGRX_CK(cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
   prepare_panel_solve(n);
+  build_slabs(out, s);
   const int b = read_scalar(bad.get(), s);
   if (b >= 0) throw RuntimeError("dense LU: matrix numerically singular (pivot " + std::to_string(b) + ")");
 }
 
 void dense_solve(const DenseLU& f, const double* b, double* x, cudaStream_t s) {
   if (f.n == 0) return;
+  if (f.ccl > 0) {
+    launch_cluster_solve(f, b, x, s);
+    return;
+  }
   if (f.nb > 1) {
     launch_panel_solve(f.nb, f.max_block, f.bst.get(), f.boff.get(), f.rows.get(), f.blu.get(), f.perm.get(), 0, b, x,
                        s);

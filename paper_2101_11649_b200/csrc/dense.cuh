@@ -20,6 +20,10 @@ struct DenseLU {
   DVec<int> rows, bst;
   DVec<long long> boff;
   DVec<double> blu;
+  // cluster solve (blocks of <= 256 rows): per-CTA slabs of 32 factor rows,
+  // slab[((b * ccl + c) * slab_n + j) * 32 + r] = M_b(32c + r, j); ccl = 0: off
+  int ccl = 0, slab_n = 0;
+  DVec<double> slab;
 };
 
 // Densify CSR A and factor it (per connected component when A is block

@@ -634,127 +634,9 @@ __global__ void __launch_bounds__(kAT2, 1) k_arnoldi2(ArnoldiArgs a) {
   }
 }
 
-// Software-pipelined lane-pair kernel: the loads of slot group g+1 are issued
-// before group g is consumed, and the last group of a phase issues the first
-// group of the NEXT phase (its columns are known before the reduction; only
-// h is not, and h is applied when the group is consumed). So the HBM stream
-// does not drain at the grid barrier: each phase starts with its first group
-// on chip. After the closing norm of pass 1 the first group of pass 2 is
-// prefetched speculatively (discarded when no re-orthogonalisation follows).
-template <int kU>
-struct PairGroup {
-  double2 p[kU], x[kU];
-};
-
-template <int kU>
-__device__ __forceinline__ void pgroup_load(PairGroup<kU>& g, const double* pl, const double* al, int q0, int nsy,
-                                            unsigned long long pf) {
-  constexpr int kStride = kRB * kRT;
-#pragma unroll
-  for (int u = 0; u < kU; ++u) {
-    const int q = q0 + u;
-    if (q < nsy) {
-      if (pl) g.p[u] = ld2_pol(pl + q * kStride, pf);
-      if (al) g.x[u] = __ldcg(reinterpret_cast<const double2*>(al + q * kStride));
-    }
-  }
-}
-
-template <int kU>
-__device__ __forceinline__ void pgroup_use(const PairGroup<kU>& g, double2* wl, int q0, int nsy, bool v, bool dot,
-                                           bool w2, double h, PairSums& s) {
-#pragma unroll
-  for (int u = 0; u < kU; ++u) {
-    const int q = q0 + u;
-    if (q < nsy) {
-      double2 wi = wl[q * kAT2];
-      if (v) {
-        wi.x = __dsub_rn(wi.x, __dmul_rn(h, g.p[u].x));
-        wi.y = __dsub_rn(wi.y, __dmul_rn(h, g.p[u].y));
-        wl[q * kAT2] = wi;
-      }
-      if (dot) {
-        s.s1x = __dadd_rn(s.s1x, __dmul_rn(g.x[u].x, wi.x));
-        s.s1y = __dadd_rn(s.s1y, __dmul_rn(g.x[u].y, wi.y));
-      }
-      if (w2) {
-        s.s2x = __dadd_rn(s.s2x, __dmul_rn(wi.x, wi.x));
-        s.s2y = __dadd_rn(s.s2y, __dmul_rn(wi.y, wi.y));
-      }
-    }
-  }
-}
-
-template <int kU>
-__global__ void __launch_bounds__(kAT2, 1) k_arnoldi3(ArnoldiArgs a) {
-  extern __shared__ double2 wsm2[];
-  __shared__ double r1[kAT / 32], r2[kAT / 32];
-  __shared__ double f1[kRT / 32], f2[kRT / 32];
-  __shared__ double hk[kAHk];
-  const int T = threadIdx.x;
-  const int n = a.n, k = a.k;
-  constexpr int kStride = kRB * kRT;
-  const int lane = blockIdx.x * kAT + 2 * T;
-  const int nsy = lane < n ? (n - 1 - lane) / kStride + 1 : 0;
-  const unsigned long long pf = pol_first();
-  const size_t ld = static_cast<size_t>(n);
-  const bool rows = !(a.dbg & 1);
-  // phase (pass, i): i <= k projects on v_i (after the update by v_{i-1});
-  // i == k+1 is the closing update + norm
-  auto cols = [&](int i, const double*& pl, const double*& al) {
-    pl = (rows && i) ? a.V + (i - 1) * ld + lane : nullptr;
-    al = (rows && i <= k) ? a.V + i * ld + lane : nullptr;
-  };
-  PairGroup<kU> cur;
-  const double *pl, *al;
-  cols(0, pl, al);
-  pgroup_load(cur, pl, al, 0, nsy, pf);
-  for (int q = 0; q < nsy; ++q)
-    wsm2[q * kAT2 + T] = __ldcg(reinterpret_cast<const double2*>(a.w + lane + q * kStride));
-  double2* wl = wsm2 + T;
-  const bool writer = blockIdx.x == 0 && T == 0;
-  double h = 0.0, wn2 = 0.0, w02 = 0.0;
-  unsigned phase = 0;
-  for (int pass = 0; pass < 2; ++pass) {
-    for (int i = 0; i <= k + 1; ++i) {
-      const double *npl = nullptr, *nal = nullptr;
-      if (i <= k) cols(i + 1, npl, nal);
-      else if (pass == 0) cols(0, npl, nal);  // speculative: pass 2 starts with v_0
-      const bool v = i > 0, dot = i <= k, w2 = i > k || (pass == 0 && i == 0);
-      PairSums ps;
-      for (int q0 = 0; q0 < nsy; q0 += kU) {
-        PairGroup<kU> nxt;
-        if (q0 + kU < nsy) pgroup_load(nxt, pl, al, q0 + kU, nsy, pf);
-        else pgroup_load(nxt, npl, nal, 0, nsy, pf);
-        if (rows) pgroup_use(cur, wl, q0, nsy, v, dot, w2, h, ps);
-        cur = nxt;
-      }
-      pl = npl;
-      al = nal;
-      double t1, t2;
-      pair_reduce(a, ps, phase++, r1, r2, f1, f2, t1, t2);
-      arn_record(a, writer, pass, i, t1, t2, hk, h, w02, wn2);
-    }
-    h = 0.0;
-    if (pass == 1 || (!(a.dbg & 4) && !(__dsqrt_rn(wn2) < __ddiv_rn(__dsqrt_rn(w02), __dsqrt_rn(2.0))))) break;
-  }
-  if (writer) {
-    *a.n0 = w02;
-    *a.n1 = wn2;
-  }
-  const double wn = __dsqrt_rn(wn2);
-  if (!(wn < 1e-300)) {
-    double* out = const_cast<double*>(a.V) + (k + 1) * ld;
-    for (int q = 0; q < nsy; ++q) {
-      const double2 wi = wsm2[q * kAT2 + T];
-      reinterpret_cast<double2*>(out + lane + q * kStride)[0] = make_double2(__ddiv_rn(wi.x, wn), __ddiv_rn(wi.y, wn));
-    }
-  }
-}
-
 // MGRX_ARNOLDI: 0 off (launch-per-projection MGS), 1 the 1024-thread kernel,
 // 2 (default) the lane-pair kernel with MGRX_ARNOLDI_U slots per load group
-// (4, 6 or 8; default 8). The lane-pair kernel needs 16-byte aligned basis
+// (4, 6 or 8; default 4: 6 and 8 measured 2-5% slower per step at cfg2). The lane-pair kernel needs 16-byte aligned basis
 // columns (n even); odd n uses the 1024-thread kernel.
 struct ArnoldiMode {
   int mode = 2, u = 4;
@@ -781,15 +663,13 @@ const ArnoldiMode& arnoldi_mode() {
     ArnoldiMode r;
     if (const char* v = std::getenv("MGRX_ARNOLDI")) r.mode = std::atoi(v);
     if (const char* v = std::getenv("MGRX_ARNOLDI_U")) r.u = std::atoi(v);
-    if (r.mode == 3 && r.u != 2) r.u = 4;
-    if (r.mode == 2 && r.u != 4 && r.u != 6) r.u = 8;
+    if (r.u != 4 && r.u != 6) r.u = 8;
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms != kAB) return r;
     r.fits1 = arnoldi_fits(k_arnoldi, kAT);
-    if (r.mode == 3) r.fits2 = arnoldi_fits(r.u == 2 ? k_arnoldi3<2> : k_arnoldi3<4>, kAT2);
-    else r.fits2 = arnoldi_fits(r.u == 4 ? k_arnoldi2<4> : r.u == 6 ? k_arnoldi2<6> : k_arnoldi2<8>, kAT2);
+    r.fits2 = arnoldi_fits(r.u == 4 ? k_arnoldi2<4> : r.u == 6 ? k_arnoldi2<6> : k_arnoldi2<8>, kAT2);
     return r;
   }();
   return m;
@@ -814,8 +694,7 @@ void arnoldi_launch(int n, int k, int slots, int dbg, GmresWork& ws, cudaStream_
   const ArnoldiMode& md = arnoldi_mode();
   const size_t smem = static_cast<size_t>(slots) * kAT * sizeof(double);
   if (md.mode >= 2 && md.fits2 && n % 2 == 0 && !(dbg & 8)) {
-    void* kern = md.mode == 3 ? (md.u == 2 ? reinterpret_cast<void*>(k_arnoldi3<2>) : reinterpret_cast<void*>(k_arnoldi3<4>))
-                 : md.u == 4 ? reinterpret_cast<void*>(k_arnoldi2<4>)
+    void* kern = md.u == 4 ? reinterpret_cast<void*>(k_arnoldi2<4>)
                  : md.u == 6 ? reinterpret_cast<void*>(k_arnoldi2<6>)
                              : reinterpret_cast<void*>(k_arnoldi2<8>);
     MGRX_CK(cudaLaunchCooperativeKernel(kern, dim3(kAB), dim3(kAT2), args, smem, s));
