@@ -580,6 +580,10 @@ void AmgHier::vcycle(const double* r, double* z, cudaStream_t s) { vcycle_level(
 
 void AmgHier::vcycle_level(int l, const double* r, double* z, cudaStream_t s) {
   AmgLevelD& L = levels[l];
+  if (l == tail) {
+    launch_amg_tail(tail_desc, tail_blob.get(), r, z, s);
+    return;
+  }
   if (l == static_cast<int>(levels.size()) - 1) {
     dense_solve(coarse, r, z, s);
     return;
@@ -607,6 +611,69 @@ void prepare_amg(AmgHier& h, cudaStream_t s) {
     for (DCsr* M : {&L.A, &L.P, &L.R}) spmv_prepare(*M, s);
     prepare_relax(L.pre, s);
     prepare_relax(L.post, s);
+  }
+  h.build_tail(s);
+}
+
+// Choose the first level (>= 1) from which the rest of the V-cycle fits in
+// one CTA's shared memory (Jacobi / l1-Jacobi smoothing, single-block
+// coarsest LU) and pack it (MGRX_AMG_TAIL=0: off).
+void AmgHier::build_tail(cudaStream_t s) {
+  tail = -1;
+  static const bool on = [] {
+    const char* v = std::getenv("MGRX_AMG_TAIL");
+    return !v || std::atoi(v) != 0;
+  }();
+  const int nl = static_cast<int>(levels.size());  // levels[nl - 1] is the coarsest
+  if (!on || nl < 3 || coarse.nb != 1 || coarse.n <= 0 || coarse.n > 256) return;
+  auto jac = [](const BoundRelax& b) {
+    return (b.spec.kind == Smoother::jacobi || b.spec.kind == Smoother::l1_jacobi) && b.spec.sweeps >= 1;
+  };
+  constexpr size_t kBudget = 200 * 1024;
+  for (int t = std::max(1, nl - 1 - kTailMaxLevels); t <= nl - 2; ++t) {
+    bool ok = true;
+    size_t est = 8 * static_cast<size_t>(coarse.n) * coarse.n;
+    for (int l = t; l < nl - 1 && ok; ++l) {
+      const AmgLevelD& L = levels[l];
+      ok = jac(L.pre) && jac(L.post);
+      est += 12 * static_cast<size_t>(L.A.nnz + L.R.nnz + L.P.nnz) + 56 * static_cast<size_t>(L.A.rows);
+    }
+    if (!ok || est > kBudget) continue;
+    std::vector<TailLevelHost> lv;
+    for (int l = t; l < nl - 1; ++l) {
+      const AmgLevelD& L = levels[l];
+      TailLevelHost h;
+      h.m = L.A.rows;
+      h.mc = L.R.rows;
+      h.a_ptr = L.A.ptr.download(L.A.rows + 1);
+      h.a_col = L.A.col.download(L.A.nnz);
+      h.a_val = L.A.val.download(L.A.nnz);
+      h.r_ptr = L.R.ptr.download(L.R.rows + 1);
+      h.r_col = L.R.col.download(L.R.nnz);
+      h.r_val = L.R.val.download(L.R.nnz);
+      h.p_ptr = L.P.ptr.download(L.P.rows + 1);
+      h.p_col = L.P.col.download(L.P.nnz);
+      h.p_val = L.P.val.download(L.P.nnz);
+      h.dpre = L.pre.dinv.download(L.A.rows);
+      h.dpost = L.post.dinv.download(L.A.rows);
+      h.pre_sweeps = L.pre.spec.sweeps;
+      h.post_sweeps = L.post.spec.sweeps;
+      h.pre_w = L.pre.spec.weight;
+      h.post_w = L.post.spec.weight;
+      lv.push_back(std::move(h));
+    }
+    const int nc = coarse.n;
+    const std::vector<double> lu = coarse.lu.download(static_cast<size_t>(nc) * nc);
+    const std::vector<int> perm = coarse.perm.download(nc);
+    std::vector<unsigned char> blob;
+    if (!build_tail_blob(lv, nc, lu, perm, kBudget, tail_desc, blob)) continue;
+    tail_blob.alloc(blob.size(), s);
+    tail_blob.upload(blob.data(), blob.size());
+    prepare_amg_tail(tail_desc);
+    tail = t;
+    if (const char* v = std::getenv("MGRX_VERBOSE"); v && v[0] == '1')
+      std::fprintf(stderr, "[mgrx] amg tail from level %d of %d (%d shared bytes)\n", t, nl, tail_desc.total_bytes);
+    return;
   }
 }
 

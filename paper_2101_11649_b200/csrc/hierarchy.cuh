@@ -11,6 +11,7 @@
 #include <string>
 #include <vector>
 
+#include "amgtail.cuh"
 #include "blocklu.cuh"
 #include "dense.cuh"
 #include "relax.cuh"
@@ -58,10 +59,15 @@ struct AmgHier {
   std::vector<int> level_sizes;
   long long fallback_rows = 0;
   bool truncated = false;
+  // single-CTA tail (amgtail.cuh): levels >= tail run as one kernel; -1: off
+  int tail = -1;
+  TailDesc tail_desc;
+  DVec<unsigned char> tail_blob;
 
   void setup(const DCsr& A, const AmgSpec& cfg, const std::vector<int>& umap, cudaStream_t s);
   void vcycle(const double* r, double* z, cudaStream_t s);
   int fine_size() const { return levels.empty() ? 0 : levels.front().A.rows; }
+  void build_tail(cudaStream_t s);
 
  private:
   void vcycle_level(int l, const double* r, double* z, cudaStream_t s);

@@ -369,3 +369,33 @@ def test_edge_cases():
     with pytest.raises(mx.MgrxError, match="numerically singular"):
         mx.Hierarchy(mx.Matrix(np.array([0, 1, 2], np.int32), np.array([0, 1], np.int32), np.array([1.0, 0.0])),
                      mx.DofPartition(["x"], np.zeros(2, np.int32)), json.dumps({"coarse": {"kind": "dense_lu"}}))
+
+
+@pytest.mark.gpu
+def test_amg_tail_kernel_bit_exact():
+    """The single-CTA AMG tail (csrc/amgtail.cu) replaces the coarsest levels'
+    launches in the l1-Jacobi strategies: one preconditioner application and
+    the whole residual history stay bitwise equal to the oracle, and the tail
+    is actually in use (MGRX_VERBOSE reports it)."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
+        "import paper_2101_11649_b200 as mx, refcpu\n"
+        "cases = [(mx.mfd_problem(20, 20, 10, 'iid'), 'mfd_mgr_pi_c1_l1j'),"
+        "         (mx.comp_problem(16, 16, 8, wells=2), 'comp_mgr_l1j'), (mx.frac_problem(12), 'frac_mgr_u_l1j')]\n"
+        "for P, name in cases:\n"
+        "    t = mx.load_strategy(name)\n"
+        "    H = mx.Hierarchy(mx.Matrix(P.ptr, P.col, P.val), P.partition, t, P.unknown_map)\n"
+        "    R = refcpu.RefHierarchy(P.ptr, P.col, P.val, P.partition.field_order, P.partition.labels, t, P.unknown_map)\n"
+        "    v = np.random.default_rng(3).uniform(-1, 1, P.n)\n"
+        "    assert np.array_equal(H.apply(v).view(np.int64), R.apply(v).view(np.int64)), name\n"
+        "    x, rep = H.solve(P.rhs, cfg=mx.KrylovConfig(restart=30, rel_tol=1e-6))\n"
+        "    _, rr = R.solve(P.rhs, restart=30, rel_tol=1e-6)\n"
+        "    assert rep.iterations == rr['iterations'] and rep.residual_history == rr['history'], name\n"
+        "print('ok')")
+    root = make_golden.ROOT
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                         env={**__import__("os").environ, "MGRX_VERBOSE": "1"}, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
+    assert out.stderr.count("amg tail from level") >= 2, out.stderr[-3000:]
