@@ -3,6 +3,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 
@@ -483,6 +484,127 @@ __global__ void __launch_bounds__(Gm::T) k_spmv_staged(int nblk, const int* __re
   }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised staged SpMV for very long rows (> 96 entries per row on
+// average: the A_uu AMG level 1 of cfg4 has 218). In the two-phase staged
+// kernel a block of 2048 entries holds ~9 such rows, so after the block-wide
+// product pass one warp sums while seven wait at the block barrier (ncu
+// source view at cfg4 level 1: 34% of warp samples at the end-of-block
+// barrier, 39% of the kernel time in the in-order sums). Here warps 2-7
+// (product warps) form the products of block i+1 while warps 0-1 (sum warps,
+// one lane per row, <= 64 rows per block by the plan) sum block i: named
+// barriers hand a stage from the product warps to the sum warps, and the sum
+// warps re-issue the stage's bulk copy when they are done with it. Same
+// arithmetic as the staged kernel (products in place, left-to-right row sums).
+constexpr int kWsRows = 64, kWsE = 2048, kWsT = 256, kWsSumT = 64;
+using StW = StGeom<kWsRows, kWsE>;
+
+template <class Epi, class Xs>
+__global__ void __launch_bounds__(kWsT) k_spmv_wspec(int nblk, const int* __restrict__ plan,
+                                                     const int* __restrict__ ptr, const int* __restrict__ col,
+                                                     const double* __restrict__ val, Xs x, Epi epi) {
+  pdl_enter();
+  using Stage = StW::Stage;
+  extern __shared__ __align__(128) unsigned char st_raw[];
+  Stage* stg = reinterpret_cast<Stage*>(st_raw);
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(st_raw + 2 * sizeof(Stage));
+  const int t = threadIdx.x;
+  const int* prow = plan;
+  const int* pnnz = plan + nblk + 1;
+  if (t == 0) {
+    for (int s = 0; s < 2; ++s) asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(bar + s)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int b, int s) {
+    const int r0 = prow[b], r1 = prow[b + 1];
+    const int p0 = pnnz[b], p1 = pnnz[b + 1];
+    const int ra = r0 & ~3, pa4 = p0 & ~3, pa2 = p0 & ~1;
+    const unsigned brp = ((r1 + 1 - ra + 3) & ~3) * 4u;
+    const unsigned bc = p1 > p0 ? ((p1 - pa4 + 3) & ~3) * 4u : 0u;
+    const unsigned bv = p1 > p0 ? ((p1 - pa2 + 1) & ~1) * 8u : 0u;
+    const unsigned mb = smem_u32(bar + s);
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(mb), "r"(brp + bc + bv) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(stg[s].rp)),
+                 "l"(ptr + ra), "r"(brp), "r"(mb)
+                 : "memory");
+    if (bc) {
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(stg[s].col)),
+                   "l"(col + pa4), "r"(bc), "r"(mb)
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(stg[s].val)),
+                   "l"(val + pa2), "r"(bv), "r"(mb)
+                   : "memory");
+    }
+  };
+  const int G = gridDim.x;
+  if (t == 0)
+    for (int s = 0; s < 2; ++s)
+      if (blockIdx.x + s * G < nblk) issue(blockIdx.x + s * G, s);
+  if (t >= kWsSumT) {
+    // product warps
+    constexpr int kPT = kWsT - kWsSumT;
+    constexpr int kB = (kWsE + kPT - 1) / kPT;
+    const int tp = t - kWsSumT;
+    int it = 0;
+    for (int b = blockIdx.x; b < nblk; b += G, ++it) {
+      const int s = it & 1;
+      const unsigned mb = smem_u32(bar + s);
+      const unsigned par = (it >> 1) & 1u;
+      unsigned done = 0;
+      do {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done)
+                     : "r"(mb), "r"(par)
+                     : "memory");
+      } while (!done);
+      Stage& S = stg[s];
+      const int p0 = pnnz[b], p1 = pnnz[b + 1];
+      const int pa4 = p0 & ~3, pa2 = p0 & ~1;
+      int c[kB];
+      double xv[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) c[u] = p0 + tp + u * kPT < p1 ? S.col[p0 + tp + u * kPT - pa4] : 0;
+#pragma unroll
+      for (int u = 0; u < kB; ++u) xv[u] = p0 + tp + u * kPT < p1 ? x(c[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const int q = p0 + tp + u * kPT;
+        if (q < p1) S.val[q - pa2] = __dmul_rn(S.val[q - pa2], xv[u]);
+      }
+      // hand the stage to the sum warps (barrier 1 + s: 192 arrive, 64 sync)
+      asm volatile("bar.arrive %0, %1;" ::"r"(1 + s), "r"(kWsT) : "memory");
+    }
+  } else {
+    // sum warps: one lane per row
+    int it = 0;
+    for (int b = blockIdx.x; b < nblk; b += G, ++it) {
+      const int s = it & 1;
+      const int r0 = prow[b], r1 = prow[b + 1];
+      const int r = r0 + t;
+      decltype(epi.load(0)) pre{};
+      if (r < r1) pre = epi.load(r);
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + s), "r"(kWsT) : "memory");
+      const Stage& S = stg[s];
+      if (r < r1) {
+        const int ra = r0 & ~3, pa2 = pnnz[b] & ~1;
+        const int lo = S.rp[r - ra], hi = S.rp[r + 1 - ra];
+        double sum = 0.0;
+        for (int k = lo; k < hi; ++k) sum = __dadd_rn(sum, S.val[k - pa2]);
+        epi.store(r, sum, pre);
+      }
+      asm volatile("bar.sync 3, %0;" ::"r"(kWsSumT) : "memory");  // stage s consumed
+      if (t == 0 && b + 2 * G < nblk) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(b + 2 * G, s);
+      }
+    }
+  }
+}
+
 // Epilogues: load(r) fetches the row's operands (issued before the row's
 // products in the staged kernel, so their latency overlaps the gathers);
 // store(r, s, pre) combines them with the row sum s.
@@ -625,9 +747,41 @@ void launch_staged(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
   else launch_staged_k<Gm, Epi, Xs, false>(A, x, epi, s);
 }
 
+template <class Epi, class Xs>
+void launch_wspec(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
+  constexpr size_t smem = 2 * sizeof(StW::Stage) + 32;
+  static bool attr = false;  // per instantiation
+  if (!attr) {
+    MGRX_CK(cudaFuncSetAttribute(k_spmv_wspec<Epi, Xs>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+    attr = true;
+  }
+  const int per_sm = static_cast<int>(std::min<size_t>(8, 227 * 1024 / smem));
+  const int grid = std::min(A.nblk, 148 * per_sm);
+  launch_pdl(k_spmv_wspec<Epi, Xs>, grid, kWsT, smem, s, A.nblk, A.plan.get(), A.ptr.get(), A.col.get(),
+             A.val.get(), x, epi);
+  MGRX_LAUNCH_CK();
+  count_launch();
+}
+
 template <class Epi, class Xs = XPlain>
 void launch_spmv(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
   if (A.rows == 0) return;
+  if (A.nblk > 0 && A.plan_kind == 1) {
+    launch_wspec(A, x, epi, s);
+    return;
+  }
+  if constexpr (std::is_same_v<Epi, EpiJacobiEx>) {
+    if (A.nblk_w > 0) {
+      DCsr& M = const_cast<DCsr&>(A);
+      std::swap(M.nblk, M.nblk_w);
+      std::swap(M.plan, M.plan_w);
+      launch_wspec(A, x, epi, s);
+      std::swap(M.nblk, M.nblk_w);
+      std::swap(M.plan, M.plan_w);
+      return;
+    }
+  }
   if (A.nblk > 0 && staged_enabled()) {
     if (staged_geom() == 0) launch_staged<StA>(A, x, epi, s);
     else launch_staged<StB>(A, x, epi, s);
@@ -663,26 +817,54 @@ void launch_spmv(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
 
 }  // namespace
 
+// MGRX_SPMV_WSPEC: 0 off, 1 (default) the specialised kernel for the Jacobi
+// sweeps of very-long-row matrices, 2 chosen per matrix by the setup timing
+// for every product.
+bool wspec_jacobi_only() {
+  static const bool j = [] {
+    const char* v = std::getenv("MGRX_SPMV_WSPEC");
+    return !v || std::atoi(v) == 1;
+  }();
+  return j;
+}
+bool wspec_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("MGRX_SPMV_WSPEC");
+    return !v || std::atoi(v) != 0;
+  }();
+  return on;
+}
+
+// Row blocks of <= max_rows rows / <= max_e entries: the nb+1 first rows then
+// the nb+1 first entries; nb = -1 when a row is longer than max_e.
+std::vector<int> block_plan(const std::vector<int>& p, int rows, int max_rows, int max_e, int& nb) {
+  std::vector<int> rs{0}, ns{0};
+  int r = 0;
+  nb = -1;
+  while (r < rows) {
+    if (p[r + 1] - p[r] > max_e) return {};
+    int q = r + 1;
+    while (q < rows && q - r < max_rows && p[q + 1] - p[r] <= max_e) ++q;
+    rs.push_back(q);
+    ns.push_back(p[q]);
+    r = q;
+  }
+  nb = static_cast<int>(rs.size()) - 1;
+  rs.insert(rs.end(), ns.begin(), ns.end());
+  return rs;
+}
+
 void spmv_prepare(DCsr& A, cudaStream_t s) {
   A.nblk = 0;
+  A.plan_kind = 0;
   A.plan.release();
   if (A.rows < staged_min_rows()) return;
   const int kStRows = staged_geom() == 0 ? StA::R : StB::R;
   const int kStE = staged_geom() == 0 ? StA::E : StB::E;
   const std::vector<int> p = A.ptr.download(A.rows + 1);
-  std::vector<int> rs{0}, ns{0};
-  int r = 0;
-  while (r < A.rows) {
-    if (p[r + 1] - p[r] > kStE) return;  // a row longer than a stage: keep the direct kernels
-    int q = r + 1;
-    while (q < A.rows && q - r < kStRows && p[q + 1] - p[r] <= kStE) ++q;
-    rs.push_back(q);
-    ns.push_back(p[q]);
-    r = q;
-  }
-  const int nb = static_cast<int>(rs.size()) - 1;
-  std::vector<int> h(rs);
-  h.insert(h.end(), ns.begin(), ns.end());
+  int nb = -1;
+  const std::vector<int> h = block_plan(p, A.rows, kStRows, kStE, nb);
+  if (nb < 0) return;  // a row longer than a stage: keep the direct kernels
   DVec<int> plan(h.size(), s);
   plan.upload(h.data(), h.size());
   // Keep the staged kernel only where it measures faster than the direct one
@@ -695,6 +877,7 @@ void spmv_prepare(DCsr& A, cudaStream_t s) {
   MGRX_CK(cudaEventCreate(&e1));
   auto time = [&](bool staged) {
     A.nblk = staged ? nb : 0;
+    A.plan_kind = 0;
     A.plan = DVec<int>();
     if (staged) A.plan = std::move(plan);
     spmv(A, xs.get(), ys.get(), s);  // warm
@@ -710,7 +893,32 @@ void spmv_prepare(DCsr& A, cudaStream_t s) {
   // best of three trials each, interleaved (robust to clock / neighbour noise).
   // MGRX_SPMV_PLAN_FILE replays decisions recorded by an earlier run (so a
   // profiler, which distorts these timings, sees the production choices).
-  float td = 1e30f, ts = 1e30f;
+  // warp-specialised long-row candidate (> 96 entries per row on average)
+  int nbw = -1;
+  DVec<int> planw;
+  if (wspec_enabled() && static_cast<long long>(A.nnz) > 96LL * A.rows) {
+    const std::vector<int> hw = block_plan(p, A.rows, kWsRows, kWsE, nbw);
+    if (nbw > 0) {
+      planw.alloc(hw.size(), s);
+      planw.upload(hw.data(), hw.size());
+    }
+  }
+  auto time_w = [&]() {
+    A.nblk = nbw;
+    A.plan_kind = 1;
+    A.plan = std::move(planw);
+    spmv(A, xs.get(), ys.get(), s);  // warm
+    MGRX_CK(cudaEventRecord(e0, s));
+    for (int k = 0; k < 10; ++k) spmv(A, xs.get(), ys.get(), s);
+    MGRX_CK(cudaEventRecord(e1, s));
+    MGRX_CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    MGRX_CK(cudaEventElapsedTime(&ms, e0, e1));
+    planw = std::move(A.plan);
+    A.plan_kind = 0;
+    return ms;
+  };
+  float td = 1e30f, ts = 1e30f, tw = 1e30f;
   const char* pf = std::getenv("MGRX_SPMV_PLAN_FILE");
   bool replayed = false;
   if (pf) {
@@ -720,9 +928,10 @@ void spmv_prepare(DCsr& A, cudaStream_t s) {
       while (std::fscanf(f, "%d %d %d %15s", &r, &c, &z, what) == 4)
         if (r == A.rows && c == A.cols && z == A.nnz) {
           replayed = true;
-          const bool st = what[0] == 's';
+          const bool st = what[0] == 's', ws = what[0] == 'w' && nbw > 0;
           ts = st ? 1.f : 2.f;
           td = st ? 2.f : 1.f;
+          tw = ws ? 0.5f : 1e30f;
         }
       std::fclose(f);
     }
@@ -731,10 +940,13 @@ void spmv_prepare(DCsr& A, cudaStream_t s) {
     for (int trial = 0; trial < 5; ++trial) {
       td = std::min(td, time(false));
       ts = std::min(ts, time(true));
+      if (nbw > 0) tw = std::min(tw, time_w());
     }
     if (pf)
       if (FILE* f = std::fopen(pf, "a")) {
-        std::fprintf(f, "%d %d %d %s\n", A.rows, A.cols, A.nnz, ts < 0.97f * td ? "staged" : "direct");
+        const float tb = ts < 0.97f * td ? ts : td;
+        std::fprintf(f, "%d %d %d %s\n", A.rows, A.cols, A.nnz,
+                     tw < 0.97f * tb ? "wspec" : ts < 0.97f * td ? "staged" : "direct");
         std::fclose(f);
       }
   }
@@ -744,7 +956,25 @@ void spmv_prepare(DCsr& A, cudaStream_t s) {
     std::fprintf(stderr, "spmv_prepare rows %d cols %d nnz %d: direct %.1f us staged %.1f us -> %s\n", A.rows, A.cols,
                  A.nnz, 100.f * td, 100.f * ts, (ts < 0.97f * td || staged_force()) ? "staged" : "direct");
   A.nblk = 0;
-  if (ts < 0.97f * td || staged_force()) {
+  A.plan_kind = 0;
+  A.nblk_w = 0;
+  const float tbest = (ts < 0.97f * td || staged_force()) ? ts : td;
+  if (nbw > 0 && wspec_jacobi_only()) {
+    // the specialised kernel serves the Jacobi sweeps; the others keep the
+    // staged / direct choice
+    A.plan_w = std::move(planw);
+    A.nblk_w = nbw;
+    if (ts < 0.97f * td || staged_force()) {
+      A.plan = std::move(plan);
+      A.nblk = nb;
+    }
+  } else if (nbw > 0 && tw < 0.97f * tbest) {
+    if (const char* v = std::getenv("MGRX_VERBOSE"); v && v[0] == '1')
+      std::fprintf(stderr, "spmv_prepare rows %d: warp-specialised %.1f us -> wspec\n", A.rows, 100.f * tw);
+    A.plan = std::move(planw);
+    A.nblk = nbw;
+    A.plan_kind = 1;
+  } else if (ts < 0.97f * td || staged_force()) {
     A.plan = std::move(plan);
     A.nblk = nb;
   }

@@ -17,6 +17,14 @@ struct DCsr {
   // nblk+1 first rows then the nblk+1 first nonzeros. nblk == 0: no plan.
   int nblk = 0;
   DVec<int> plan;
+  // plan kind: 0 staged (<= 256 rows / 2048 entries per block), 1 warp-
+  // specialised long-row kernel (<= 64 rows / 2048 entries per block)
+  int plan_kind = 0;
+  // warp-specialised plan kept alongside for the Jacobi-sweep epilogues
+  // (their two gathers per entry make the product pass the long pole, which
+  // the specialised kernel overlaps with the sums): nblk_w == 0: none
+  int nblk_w = 0;
+  DVec<int> plan_w;
   bool empty() const { return rows == 0; }
 };
 
