@@ -896,7 +896,11 @@ void spmv_prepare(DCsr& A, cudaStream_t s) {
   // warp-specialised long-row candidate (> 96 entries per row on average)
   int nbw = -1;
   DVec<int> planw;
-  if (wspec_enabled() && static_cast<long long>(A.nnz) > 96LL * A.rows) {
+  static const long long wmin = [] {
+    const char* v = std::getenv("MGRX_SPMV_WSPEC_MIN");
+    return v ? std::atoll(v) : 96LL;
+  }();
+  if (wspec_enabled() && static_cast<long long>(A.nnz) > wmin * A.rows) {
     const std::vector<int> hw = block_plan(p, A.rows, kWsRows, kWsE, nbw);
     if (nbw > 0) {
       planw.alloc(hw.size(), s);
