@@ -1,11 +1,10 @@
 #!/bin/bash
 mkdir -p gpurun_out
 export PYTHONUNBUFFERED=1
-timeout 1200 python -m pytest tests -q -m gpu -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-tail -3 gpurun_out/pytest_gpu.log
-for c in cfg4; do for e in X=0 MGRX_SPMV_WSPEC=2 MGRX_SPMV_WSPEC=0; do echo "== $c $e"; env $e timeout 600 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline --no-variant 2>&1 | tail -1 | python -c "
-import json,sys
-d=json.loads(sys.stdin.read())
-print('ms', round(d['ms_per_step'],2), 'its', d['iterations_per_solve'], 'value %.3e'%d['value'], 'solvefrac', round(d['solve_roofline'].get('frac',0),3))
-"; done; done > gpurun_out/bench_ws.log 2>&1
-cat gpurun_out/bench_ws.log
+PROBE_CFG=cfg4 timeout 600 python tools/probe_spmv.py mgr.0.frelax.amg.1.pre > gpurun_out/probe_ws.log 2>&1 && \
+PROBE_CFG=cfg4 timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:k_spmv_wspec -c 1 -o gpurun_out/cfg4_wspec_full python tools/probe_spmv.py mgr.0.frelax.amg.1.pre > gpurun_out/ncu_ws.log 2>&1
+c=cfg2
+rm -f gpurun_out/plan_$c.txt
+MGRX_SPMV_PLAN_FILE=gpurun_out/plan_$c.txt python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline --no-variant > gpurun_out/prof_plain_$c.log 2>&1 && \
+MGRX_SPMV_PLAN_FILE=gpurun_out/plan_$c.txt MGRX_PROFILE_TIMED=1 timeout 1500 ncu --metrics gpu__time_duration.sum,launch__grid_size,launch__block_size --clock-control none --profile-from-start off --csv --log-file gpurun_out/launches_$c.csv python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline --no-variant > gpurun_out/ncu_$c.log 2>&1
+ls -la gpurun_out | tail -8
