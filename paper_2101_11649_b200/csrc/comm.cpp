@@ -87,8 +87,69 @@ class NcclComm final : public Comm {
   bool graph_safe() const override { return true; }
   const char* kind() const override { return "nccl"; }
 
+  bool map_peers(void* local, std::vector<void*>& peers) override {
+    peers.clear();
+    // gather (handle, ok) from every rank; an all-ranks verdict after the opens
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    double mine[9] = {};
+    cudaIpcMemHandle_t h{};
+    const bool got = cudaIpcGetMemHandle(&h, local) == cudaSuccess;
+    if (!got) cudaGetLastError();
+    std::memcpy(mine, &h, sizeof h);
+    mine[8] = got ? 1.0 : 0.0;
+    std::vector<double> all(9 * static_cast<size_t>(size));
+    gather_host(mine, all.data(), 9);
+    bool ok = true;
+    for (int q = 0; q < size; ++q) ok = ok && all[9 * q + 8] == 1.0;
+    std::vector<void*> p(size, nullptr);
+    p[rank] = local;
+    bool opened = ok;
+    for (int q = 0; q < size && ok; ++q) {
+      if (q == rank) continue;
+      cudaIpcMemHandle_t hq;
+      std::memcpy(&hq, &all[9 * q], sizeof hq);
+      if (cudaIpcOpenMemHandle(&p[q], hq, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        p[q] = nullptr;
+        opened = false;
+      }
+    }
+    double mine2[1] = {opened ? 1.0 : 0.0};
+    std::vector<double> all2(size);
+    gather_host(mine2, all2.data(), 1);
+    bool every = true;
+    for (double v : all2) every = every && v == 1.0;
+    if (!every) {
+      for (int q = 0; q < size; ++q)
+        if (q != rank && p[q]) cudaIpcCloseMemHandle(p[q]);
+      return false;
+    }
+    peers = p;
+    return true;
+  }
+  void unmap_peers(std::vector<void*>& peers) override {
+    for (int q = 0; q < static_cast<int>(peers.size()); ++q)
+      if (q != rank && peers[q]) cudaIpcCloseMemHandle(peers[q]);
+    peers.clear();
+  }
+
  private:
   ncclComm_t c_ = nullptr;
+  // host-to-host all-gather of a few doubles through the device (setup only)
+  void gather_host(const double* in, double* out, int count) {
+    cudaStream_t s;
+    MGRX_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    double *din = nullptr, *dout = nullptr;
+    MGRX_CK(cudaMalloc(&din, sizeof(double) * count));
+    MGRX_CK(cudaMalloc(&dout, sizeof(double) * count * size));
+    MGRX_CK(cudaMemcpyAsync(din, in, sizeof(double) * count, cudaMemcpyHostToDevice, s));
+    allgather(din, dout, count, s);
+    MGRX_CK(cudaMemcpyAsync(out, dout, sizeof(double) * count * size, cudaMemcpyDeviceToHost, s));
+    MGRX_CK(cudaStreamSynchronize(s));
+    cudaFree(din);
+    cudaFree(dout);
+    cudaStreamDestroy(s);
+  }
 };
 
 }  // namespace

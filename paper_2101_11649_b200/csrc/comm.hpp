@@ -37,6 +37,16 @@ class Comm {
   virtual void exchange(const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs, cudaStream_t s) = 0;
   // out[q * count + i] = in_q[i] for every rank q.
   virtual void allgather(const double* in, double* out, int count, cudaStream_t s) = 0;
+  // Map one device buffer of every rank into this process (CUDA IPC; stores
+  // to a peer's buffer travel over NVLink): peers[q] = rank q's buffer,
+  // peers[rank] = local. Collective; every rank returns the same verdict
+  // (false: no mapping, the caller keeps the collective path).
+  virtual bool map_peers(void* local, std::vector<void*>& peers) {
+    (void)local;
+    peers.clear();
+    return false;
+  }
+  virtual void unmap_peers(std::vector<void*>& peers) { peers.clear(); }
   virtual bool graph_safe() const = 0;
   virtual const char* kind() const = 0;
 };

@@ -208,6 +208,12 @@ struct ArnoldiArgs {
   double* hp;         // per-projection dots of the last pass
   double* hc;         // Hessenberg column H(0..k, k)
   int dbg;            // probe only: 1 skip the row loops, 2 skip the grid barrier, 4 force two passes, 8 trace
+  // sharded: cross-rank exchange of each phase's rank partial (nranks > 1)
+  int nranks = 1, rank = 0;
+  double* mbox = nullptr;             // this rank's mailbox
+  double* const* peers = nullptr;     // every rank's mailbox (device array)
+  unsigned long long epoch = 0;       // tag base of this launch
+  double* err = nullptr;              // set to 1 on a peer timeout
 };
 
 // One projection phase over this lane's rows (w in shared memory, column
@@ -493,9 +499,69 @@ __device__ __forceinline__ void arn2_rows(double2* wl, int nsy, bool xtail, cons
   }
 }
 
+__device__ __forceinline__ unsigned long long gtime_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Sharded: publish this rank's partial of the phase into every rank's
+// mailbox slot [phase][rank] (CTA 0; data, system fence, then the tag), wait
+// for every rank's tag in the local mailbox, and fold the partials in rank
+// order as k_fold2 does (v = p_0; v += p_q for q = 1..). Every CTA folds the
+// same values, so all CTAs and all ranks hold the same bits.
+__device__ __noinline__ void cross_rank(const ArnoldiArgs& a, unsigned phase, double& t1, double& t2, double* s1,
+                                        double* s2) {
+  const int T = threadIdx.x;
+  const int slot = static_cast<int>(phase % kMboxPhases);
+  const unsigned long long tag = a.epoch + phase + 1;
+  if (blockIdx.x == 0 && T < a.nranks) {
+    double* dst = a.peers[T] + (static_cast<size_t>(slot) * kMboxRanks + a.rank) * 4;
+    dst[0] = t1;
+    dst[1] = t2;
+    __threadfence_system();
+    asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(dst + 2), "l"(tag) : "memory");
+  }
+  __syncthreads();  // s1/s2 (the fold scratch) are free again
+  if (T < a.nranks) {
+    const double* src = a.mbox + (static_cast<size_t>(slot) * kMboxRanks + T) * 4;
+    unsigned long long v;
+    const unsigned long long t0 = gtime_ns();
+    bool late = false;
+    for (unsigned it = 0;; ++it) {
+      asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(src + 2) : "memory");
+      if (v == tag) break;
+      // a silent peer: give up after ~2 s (or at once when a previous phase
+      // already did) and flag the step; the host discards it
+      if ((it & 1023u) == 1023u &&
+          (gtime_ns() - t0 > 2000000000ull || *reinterpret_cast<volatile double*>(a.err) != 0.0)) {
+        late = true;
+        break;
+      }
+    }
+    __threadfence_system();
+    double p1, p2;
+    asm volatile("ld.volatile.global.f64 %0, [%1];" : "=d"(p1) : "l"(src) : "memory");
+    asm volatile("ld.volatile.global.f64 %0, [%1];" : "=d"(p2) : "l"(src + 1) : "memory");
+    s1[T] = p1;
+    s2[T] = p2;
+    if (late) *a.err = 1.0;
+  }
+  __syncthreads();
+  double v1 = s1[0], v2 = s2[0];
+  for (int q = 1; q < a.nranks; ++q) {
+    v1 = __dadd_rn(v1, s1[q]);
+    v2 = __dadd_rn(v2, s2[q]);
+  }
+  t1 = v1;
+  t2 = v2;
+  __syncthreads();  // scratch reused by the next phase
+}
+
 // Grid-wide reduction of one projection phase in the canonical order (see
 // above): canonical warp sums, 256-lane block trees, partials, grid barrier,
 // in-order fold of the kRB partials in every CTA. r/f: shared scratch.
+template <bool kShard>
 __device__ __forceinline__ void pair_reduce(const ArnoldiArgs& a, const PairSums& ps, unsigned phase, double* r1,
                                             double* r2, double* f1, double* f2, double& t1, double& t2) {
   const int T = threadIdx.x;
@@ -561,6 +627,7 @@ __device__ __forceinline__ void pair_reduce(const ArnoldiArgs& a, const PairSums
   const double x2 = l < kRT / 32 ? f2[l] : 0.0;
   t1 = __shfl_sync(0xffffffffu, warp_sum(x1), 0);
   t2 = __shfl_sync(0xffffffffu, warp_sum(x2), 0);
+  if (kShard) cross_rank(a, phase, t1, t2, f1, f2);
 }
 
 // Writer bookkeeping of one reduced phase (H column, norms).
@@ -580,7 +647,7 @@ __device__ __forceinline__ void arn_record(const ArnoldiArgs& a, bool writer, in
   }
 }
 
-template <int kU>
+template <int kU, bool kShard = false>
 __global__ void __launch_bounds__(kAT2, 1) k_arnoldi2(ArnoldiArgs a) {
   extern __shared__ double2 wsm2[];               // [slot][kAT2] lane pairs
   __shared__ double r1[kAT / 32], r2[kAT / 32];   // canonical warp sums of this CTA (32)
@@ -614,7 +681,7 @@ __global__ void __launch_bounds__(kAT2, 1) k_arnoldi2(ArnoldiArgs a) {
         else if (pass == 0) arn2_rows<kU, false, true, true>(wl, nsy, false, pl, al, h, pf, ps, rot);
         else arn2_rows<kU, false, true, false>(wl, nsy, false, pl, al, h, pf, ps, rot);
       }
-      pair_reduce(a, ps, phase++, r1, r2, f1, f2, t1, t2);
+      pair_reduce<kShard>(a, ps, phase++, r1, r2, f1, f2, t1, t2);
       arn_record(a, writer, pass, i, t1, t2, hk, h, w02, wn2);
     }
     h = 0.0;
@@ -705,6 +772,40 @@ void arnoldi_launch(int n, int k, int slots, int dbg, GmresWork& ws, cudaStream_
 }
 
 }  // namespace
+
+bool arnoldi_sharded_ok(int n) {
+  const ArnoldiMode& md = arnoldi_mode();
+  return md.mode >= 2 && md.fits2 && n > 0 && n % 2 == 0 && arnoldi_slots(n) > 0;
+}
+
+void arnoldi_sharded(int n, int k, int dbg, const ArnoldiPeers& pe, GmresWork& ws, cudaStream_t s) {
+  if (!arnoldi_sharded_ok(n) || pe.nranks > kMboxRanks) throw RuntimeError("sharded Arnoldi kernel unavailable");
+  const int slots = arnoldi_slots(n);
+  double* S = ws.scal.get();
+  const int m = ws.m;
+  MGRX_CK(cudaMemsetAsync(ws.bar.get(), 0, sizeof(unsigned), s));
+  MGRX_CK(cudaMemsetAsync(S + m + 3, 0, sizeof(double), s));
+  ArnoldiArgs aa{n, k, ws.w.get(), ws.V.get(), ws.apart.get(), ws.bar.get(), S, S + 1, S + 2, S + 3 + (m + 1), dbg};
+  aa.nranks = pe.nranks;
+  aa.rank = pe.rank;
+  aa.mbox = pe.mbox;
+  aa.peers = pe.peers;
+  aa.epoch = pe.epoch;
+  aa.err = S + m + 3;
+  void* args[] = {&aa};
+  const ArnoldiMode& md = arnoldi_mode();
+  static const bool attr = [&] {
+    const int bytes = kAMaxSlots * kAT * static_cast<int>(sizeof(double));
+    MGRX_CK(cudaFuncSetAttribute(k_arnoldi2<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    return true;
+  }();
+  (void)attr;
+  (void)md;
+  MGRX_CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_arnoldi2<4, true>), dim3(kAB), dim3(kAT2), args,
+                                      static_cast<size_t>(slots) * kAT * sizeof(double), s));
+  count_launch();
+}
+
 
 void mgs_step(int n, double* w, const double* vprev, const double* hprev, const double* a, bool want2,
               GmresWork& ws, double* out1, double* hacc, bool accumulate, double* out2, cudaStream_t s) {

@@ -59,6 +59,25 @@ void vec_scale(int n, const double* in, double d, double* out, cudaStream_t s);
 // u = sum_{j<k} V[j] y[j], j ascending (V column-major, n rows)
 void basis_combine(int n, int k, const double* V, const double* y, double* u, cudaStream_t s);
 
+// Sharded fused Arnoldi step (shard.cu): the lane-pair kernel on this rank's
+// slab, with every projection's rank partial exchanged through the peers'
+// mailboxes (CUDA IPC mappings, stores over NVLink) inside the kernel and
+// folded in rank order exactly like the all-gather path's k_fold2. mbox:
+// this rank's mailbox (kMboxDoubles doubles, zeroed once); peers: device
+// array of every rank's mailbox; epoch: per-launch tag, the same on every
+// rank (ranks launch in lockstep). A peer that does not answer within ~2 s
+// sets S[m + 3] = 1 (the caller falls back / throws).
+constexpr int kMboxRanks = 8, kMboxPhases = 64;
+constexpr int kMboxDoubles = kMboxPhases * kMboxRanks * 4;
+struct ArnoldiPeers {
+  int nranks = 1, rank = 0;
+  double* mbox = nullptr;
+  double* const* peers = nullptr;
+  unsigned long long epoch = 0;
+};
+bool arnoldi_sharded_ok(int n);
+void arnoldi_sharded(int n, int k, int dbg, const ArnoldiPeers& pe, GmresWork& ws, cudaStream_t s);
+
 // Deterministic device dot product (fixed grid, fixed reduction tree).
 double device_dot(int n, const double* a, const double* b, GmresWork& ws, cudaStream_t s);
 

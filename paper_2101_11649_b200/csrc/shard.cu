@@ -1,6 +1,10 @@
 // Row-slab sharded MGR-GMRES. See shard.cuh.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
 
 #include "shard.cuh"
 
@@ -27,6 +31,12 @@ __global__ void k_fold2(int size, const double* __restrict__ g, double* dh, doub
   if (dh) *dh = v0;
   if (hacc) *hacc = acc ? __dadd_rn(*hacc, v0) : v0;
   if (dn) *dn = v1;
+}
+
+void fold2(int size, const double* g, double* dh, double* hacc, bool acc, double* dn, cudaStream_t s) {
+  k_fold2<<<1, 1, 0, s>>>(size, g, dh, hacc, acc ? 1 : 0, dn);
+  MGRX_LAUNCH_CK();
+  count_launch();
 }
 
 void pack(int n, const int* idx, const double* x, double* y, cudaStream_t s) {
@@ -433,9 +443,115 @@ void Shard::build(MgrHier& h, const DCsr& A, const std::vector<int>& fine_starts
   loc.zero();
   gbuf.alloc(2 * c.size, c.s);
   MGRX_CK(cudaStreamSynchronize(c.s));
+  setup_fused();
+}
+
+namespace {
+// deterministic self-check data from the global row index
+__global__ void k_seed(int n, int row0, int salt, double* v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const unsigned h = (static_cast<unsigned>(row0 + i) * 2654435761u) ^ (static_cast<unsigned>(salt) * 40503u);
+    v[i] = static_cast<double>(h % 2000003u) / 2000003.0 - 0.5;
+  }
+}
+}  // namespace
+
+ArnoldiPeers Shard::peers_arg() {
+  ArnoldiPeers pe;
+  pe.nranks = c.size;
+  pe.rank = c.rank;
+  pe.mbox = mbox;
+  pe.peers = peer_dev.get();
+  epoch += 1ull << 16;
+  pe.epoch = epoch;
+  return pe;
+}
+
+void Shard::setup_fused() {
+  fused = false;
+  if (const char* e = std::getenv("MGRX_SHARD_FUSED"); e && std::atoi(e) == 0) return;
+  // ranks of the local comm share one device: the in-kernel exchange needs
+  // every rank's persistent kernel resident at once, i.e. one GPU per rank
+  if (c.size < 2 || c.size > kMboxRanks || std::string(comm->kind()) != "nccl") return;
+  const int n = spaces.front().own;
+  cudaStream_t s = c.s;
+  auto agree = [&](bool mine) {  // min over ranks
+    const double flag[2] = {mine ? 1.0 : 0.0, 0.0};
+    loc.upload(flag, 2);
+    c.comm->allgather(loc.get(), gbuf.get(), 2, s);
+    const std::vector<double> g = gbuf.download(2 * c.size);
+    bool all = true;
+    for (int q = 0; q < c.size; ++q) all = all && g[2 * q] == 1.0;
+    return all;
+  };
+  if (!agree(arnoldi_sharded_ok(n))) return;
+  MGRX_CK(cudaMalloc(&mbox, sizeof(double) * kMboxDoubles));
+  MGRX_CK(cudaMemset(mbox, 0, sizeof(double) * kMboxDoubles));
+  if (!c.comm->map_peers(mbox, peer_mbox)) {
+    cudaFree(mbox);
+    mbox = nullptr;
+    return;
+  }
+  std::vector<double*> pd(c.size);
+  for (int q = 0; q < c.size; ++q) pd[q] = static_cast<double*>(peer_mbox[q]);
+  peer_dev.alloc(c.size, s);
+  peer_dev.upload(pd.data(), c.size);
+  // self-check: one step (k = 1, both passes) through both paths
+  const int m = 30, k = 1;
+  ws.ensure(n, m, s);
+  double* V = ws.V.get();
+  for (int j = 0; j <= k; ++j) k_seed<<<blocks_for(n, 256), 256, 0, s>>>(n, row_begin, j + 1, V + static_cast<size_t>(j) * n);
+  k_seed<<<blocks_for(n, 256), 256, 0, s>>>(n, row_begin, 7, ws.w.get());
+  MGRX_LAUNCH_CK();
+  DVec<double> w0(n, s);
+  d2d(w0.get(), ws.w.get(), n, s);
+  double* S = ws.scal.get();
+  const int ns = 3 + 2 * (m + 1) + 1;
+  arnoldi_sharded(n, k, 4, peers_arg(), ws, s);
+  const std::vector<double> fusedS = ws.scal.download(ns);
+  d2d(ws.w.get(), w0.get(), n, s);
+  double* L = loc.get();
+  auto reduce = [&](double* dh, double* hacc, bool acc, double* dn) {
+    c.comm->allgather(L, gbuf.get(), 2, s);
+    fold2(c.size, gbuf.get(), dh, hacc, acc, dn, s);
+  };
+  double* s_hp = S + 2;
+  double* s_hc = S + 3 + (m + 1);
+  for (int pass = 0; pass < 2; ++pass) {
+    const bool second = pass == 1;
+    for (int i = 0; i <= k; ++i) {
+      mgs_step(n, ws.w.get(), i ? V + static_cast<size_t>(i - 1) * n : nullptr, i ? s_hp + (i - 1) : nullptr,
+               V + static_cast<size_t>(i) * n, i == 0 && !second, ws, L, nullptr, false,
+               (i == 0 && !second) ? L + 1 : nullptr, s);
+      reduce(s_hp + i, s_hc + i, second, (i == 0 && !second) ? S : nullptr);
+    }
+    mgs_step(n, ws.w.get(), V + static_cast<size_t>(k) * n, s_hp + k, nullptr, true, ws, nullptr, nullptr, false,
+             L + 1, s);
+    reduce(nullptr, nullptr, false, S + 1);
+  }
+  const std::vector<double> ncclS = ws.scal.download(ns);
+  bool same = fusedS[m + 3] == 0.0;  // no peer timeout
+  for (int idx : {0, 1}) same = same && std::memcmp(&fusedS[idx], &ncclS[idx], sizeof(double)) == 0;
+  for (int i = 0; i <= k; ++i)
+    same = same && std::memcmp(&fusedS[3 + (m + 1) + i], &ncclS[3 + (m + 1) + i], sizeof(double)) == 0;
+  fused = agree(same);
+  if (const char* v = std::getenv("MGRX_VERBOSE"); v && v[0] == '1')
+    std::fprintf(stderr, "[mgrx] shard %d/%d: fused sharded Arnoldi %s\n", c.rank, c.size,
+                 fused ? "on (self-check bitwise equal)" : "off (self-check failed)");
+  if (!fused) {
+    c.comm->unmap_peers(peer_mbox);
+    cudaFree(mbox);
+    mbox = nullptr;
+  }
 }
 
 Shard::~Shard() {
+  if (mbox) {
+    if (c.s) cudaStreamSynchronize(c.s);
+    if (comm) comm->unmap_peers(peer_mbox);
+    cudaFree(mbox);
+  }
   if (graph) cudaGraphExecDestroy(graph);
   // buffers are freed on c.s by their destructors; the stream is destroyed
   // after them by the owning API object (mgrx_shard_destroy)
@@ -617,15 +733,26 @@ GmresResult Shard::solve(const double* b, double* x, const KrylovSpec& cfg) {
       prec(col(k), zext.get());
       halo(Afine, zext.get(), c);
       spmv(Afine.M, zext.get(), ws.w.get(), s);  // w = A M^{-1} v_k
-      // pass 1: h_i = v_i . w ; w -= h_i v_i  (krylov.cpp:84-89)
-      mgs_pass(k, false);
-      const double w0 = std::sqrt(H_pin[0]);
-      double wn = std::sqrt(H_pin[1]);
-      if (wn < w0 / std::sqrt(2.0)) {
-        mgs_pass(k, true);  // pass 2 (krylov.cpp:90-96): H(i,k) += h_i
+      double wn;
+      if (fused) {
+        // both MGS passes, the re-orthogonalisation test and v_{k+1} in one
+        // kernel per rank, partials exchanged through the peers' mailboxes
+        arnoldi_sharded(n, k, 0, peers_arg(), ws, s);
+        MGRX_CK(cudaMemcpyAsync(H_pin, S, col_bytes, cudaMemcpyDeviceToHost, s));
+        MGRX_CK(cudaStreamSynchronize(s));
+        if (H_pin[m + 3] != 0.0) throw RuntimeError("sharded Arnoldi: a peer did not answer (exchange timed out)");
         wn = std::sqrt(H_pin[1]);
+      } else {
+        // pass 1: h_i = v_i . w ; w -= h_i v_i  (krylov.cpp:84-89)
+        mgs_pass(k, false);
+        const double w0 = std::sqrt(H_pin[0]);
+        wn = std::sqrt(H_pin[1]);
+        if (wn < w0 / std::sqrt(2.0)) {
+          mgs_pass(k, true);  // pass 2 (krylov.cpp:90-96): H(i,k) += h_i
+          wn = std::sqrt(H_pin[1]);
+        }
+        if (!(wn < 1e-300)) vec_scale(n, ws.w.get(), wn, col(k + 1), s);
       }
-      if (!(wn < 1e-300)) vec_scale(n, ws.w.get(), wn, col(k + 1), s);
       const double* hc = H_pin + 3 + (m + 1);
       for (int i = 0; i <= k; ++i) h(i, k) = hc[i];
       h(k + 1, k) = wn;

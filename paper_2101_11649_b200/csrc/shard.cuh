@@ -166,7 +166,21 @@ struct Shard {
   void apply(const double* v, double* z);
   GmresResult solve(const double* b, double* x, const KrylovSpec& cfg);
 
+  // Fused sharded Arnoldi (krylov.cu arnoldi_sharded): each GMRES step's
+  // whole MGS in one kernel per rank, the per-projection rank partials
+  // exchanged through IPC-mapped mailboxes over NVLink instead of one
+  // all-gather + fold launch pair per projection. Enabled at build when every
+  // rank can map every peer and a self-check step equals the all-gather path
+  // bit for bit (MGRX_SHARD_FUSED=0: off).
+  bool fused = false;
+  double* mbox = nullptr;
+  std::vector<void*> peer_mbox;
+  DVec<double*> peer_dev;
+  unsigned long long epoch = 0;
+
  private:
+  void setup_fused();
+  ArnoldiPeers peers_arg();
   void apply_level(int l, const double* v, double* z);
   void coarse_solve(const double* v, double* z);
   void prec(const double* v, double* z);
