@@ -506,12 +506,12 @@ __device__ __forceinline__ unsigned long long gtime_ns() {
 }
 
 // Sharded: publish this rank's partial of the phase into every rank's
-// mailbox slot [phase][rank] (CTA 0; data, system fence, then the tag), wait
+// mailbox slot [phase][rank] (CTA 0; data, then the tag with release), wait
 // for every rank's tag in the local mailbox, and fold the partials in rank
 // order as k_fold2 does (v = p_0; v += p_q for q = 1..). Every CTA folds the
 // same values, so all CTAs and all ranks hold the same bits.
-__device__ __noinline__ void cross_rank(const ArnoldiArgs& a, unsigned phase, double& t1, double& t2, double* s1,
-                                        double* s2) {
+__device__ __noinline__ void cross_rank(const ArnoldiArgs& a, unsigned phase, double& t1, double& t2) {
+  __shared__ double m1[kMboxRanks], m2[kMboxRanks];  // this phase's rank partials
   const int T = threadIdx.x;
   const int slot = static_cast<int>(phase % kMboxPhases);
   const unsigned long long tag = a.epoch + phase + 1;
@@ -519,17 +519,16 @@ __device__ __noinline__ void cross_rank(const ArnoldiArgs& a, unsigned phase, do
     double* dst = a.peers[T] + (static_cast<size_t>(slot) * kMboxRanks + a.rank) * 4;
     dst[0] = t1;
     dst[1] = t2;
-    __threadfence_system();
-    asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(dst + 2), "l"(tag) : "memory");
+    // release: the two values are visible to the peer before the tag
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst + 2), "l"(tag) : "memory");
   }
-  __syncthreads();  // s1/s2 (the fold scratch) are free again
   if (T < a.nranks) {
     const double* src = a.mbox + (static_cast<size_t>(slot) * kMboxRanks + T) * 4;
     unsigned long long v;
     const unsigned long long t0 = gtime_ns();
     bool late = false;
     for (unsigned it = 0;; ++it) {
-      asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(src + 2) : "memory");
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(src + 2) : "memory");
       if (v == tag) break;
       // a silent peer: give up after ~2 s (or at once when a previous phase
       // already did) and flag the step; the host discards it
@@ -539,23 +538,22 @@ __device__ __noinline__ void cross_rank(const ArnoldiArgs& a, unsigned phase, do
         break;
       }
     }
-    __threadfence_system();
     double p1, p2;
-    asm volatile("ld.volatile.global.f64 %0, [%1];" : "=d"(p1) : "l"(src) : "memory");
-    asm volatile("ld.volatile.global.f64 %0, [%1];" : "=d"(p2) : "l"(src + 1) : "memory");
-    s1[T] = p1;
-    s2[T] = p2;
+    asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(p1) : "l"(src) : "memory");
+    asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(p2) : "l"(src + 1) : "memory");
+    m1[T] = p1;
+    m2[T] = p2;
     if (late) *a.err = 1.0;
   }
   __syncthreads();
-  double v1 = s1[0], v2 = s2[0];
+  double v1 = m1[0], v2 = m2[0];
   for (int q = 1; q < a.nranks; ++q) {
-    v1 = __dadd_rn(v1, s1[q]);
-    v2 = __dadd_rn(v2, s2[q]);
+    v1 = __dadd_rn(v1, m1[q]);
+    v2 = __dadd_rn(v2, m2[q]);
   }
   t1 = v1;
   t2 = v2;
-  __syncthreads();  // scratch reused by the next phase
+  // m1/m2 are next written after the next phase's block barriers
 }
 
 // Grid-wide reduction of one projection phase in the canonical order (see
@@ -627,7 +625,7 @@ __device__ __forceinline__ void pair_reduce(const ArnoldiArgs& a, const PairSums
   const double x2 = l < kRT / 32 ? f2[l] : 0.0;
   t1 = __shfl_sync(0xffffffffu, warp_sum(x1), 0);
   t2 = __shfl_sync(0xffffffffu, warp_sum(x2), 0);
-  if (kShard) cross_rank(a, phase, t1, t2, f1, f2);
+  if (kShard) cross_rank(a, phase, t1, t2);
 }
 
 // Writer bookkeeping of one reduced phase (H column, norms).
@@ -906,6 +904,14 @@ struct StepProf {
 };
 }  // namespace
 
+bool self_exchange() {
+  static const bool on = [] {
+    const char* v = std::getenv("MGRX_ARNOLDI_SELFXCHG");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
 GmresResult gmres_device(const DCsr& A, const double* b, double* x, const KrylovSpec& cfg,
                          const DevOp& precond, GmresWork& ws, cudaStream_t s) {
   StepProf prof;
@@ -975,12 +981,34 @@ GmresResult gmres_device(const DCsr& A, const double* b, double* x, const Krylov
         double wn;
         if (const int slots = arnoldi_slots(n)) {
           // both MGS passes + re-orthogonalisation test + v_{k+1} in one kernel
-          arnoldi_launch(n, k, slots, 0, ws, s);
+          if (self_exchange() && arnoldi_sharded_ok(n)) {
+            // test mode (MGRX_ARNOLDI_SELFXCHG=1): the sharded kernel as a
+            // one-rank group exchanging with its own mailbox
+            static double* mbox = nullptr;
+            static double** peers = nullptr;
+            static unsigned long long epoch = 0;
+            if (!mbox) {
+              MGRX_CK(cudaMalloc(&mbox, sizeof(double) * kMboxDoubles));
+              MGRX_CK(cudaMemset(mbox, 0, sizeof(double) * kMboxDoubles));
+              MGRX_CK(cudaMalloc(&peers, sizeof(double*)));
+              MGRX_CK(cudaMemcpy(peers, &mbox, sizeof(double*), cudaMemcpyHostToDevice));
+            }
+            ArnoldiPeers pe;
+            pe.nranks = 1;
+            pe.mbox = mbox;
+            pe.peers = peers;
+            epoch += 1ull << 16;
+            pe.epoch = epoch;
+            arnoldi_sharded(n, k, 0, pe, ws, s);
+          } else {
+            arnoldi_launch(n, k, slots, 0, ws, s);
+          }
           if (prof.on) prof.rec(3, s);
           MGRX_CK(cudaMemcpyAsync(H_pin, S, col_bytes, cudaMemcpyDeviceToHost, s));
           if (prof.on) prof.rec(4, s);
           MGRX_CK(cudaStreamSynchronize(s));
           if (prof.on) prof.step();
+          if (self_exchange() && H_pin[m + 3] != 0.0) throw RuntimeError("Arnoldi self-exchange timed out");
           wn = std::sqrt(H_pin[1]);
         } else {
           // pass 1: h_i = v_i . w ; w -= h_i v_i  (krylov.cpp:84-89)

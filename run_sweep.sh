@@ -1,6 +1,3 @@
 #!/bin/bash
-for lib in paper_2101_11649_b200/libmgrx_head.so paper_2101_11649_b200/libmgrx.so paper_2101_11649_b200/libmgrx_head.so paper_2101_11649_b200/libmgrx.so; do MGRX_LIB=$PWD/$lib timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-variant 2>&1 | tail -1 | python -c "
-import json,sys
-d=json.loads(sys.stdin.read())
-print('$lib', 'ms', round(d['ms_per_step'],2), 'arn', round(d['roofline']['kernels']['arnoldi.15']['avg_ms']*1e3,1))
-"; done
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -m gpu -x -k "mailbox or tail" 2>&1 | tail -15
+MGRX_ARNOLDI_SELFXCHG=1 timeout 600 python bench.py --steps 3 --warmup 2 --no-cpu-baseline --no-variant 2>&1 | tail -1 | cut -c1-200

@@ -399,3 +399,31 @@ def test_amg_tail_kernel_bit_exact():
                          env={**__import__("os").environ, "MGRX_VERBOSE": "1"}, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
     assert out.stderr.count("amg tail from level") >= 2, out.stderr[-3000:]
+
+
+@pytest.mark.gpu
+def test_sharded_arnoldi_mailbox_exchange_single_gpu():
+    """The sharded fused Arnoldi kernel's in-kernel exchange (mailbox stores,
+    system fence, per-launch tags, rank-order fold), run as a one-rank group
+    that exchanges with its own mailbox (MGRX_ARNOLDI_SELFXCHG=1): every GMRES
+    step goes through it and the residual history stays bitwise equal to the
+    oracle's. (The multi-rank case needs one GPU per rank.)"""
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
+        "import paper_2101_11649_b200 as mx, refcpu\n"
+        "for P, name in ((mx.mfd_problem(20, 20, 10, 'iid'), 'mfd_mgr_pi_c1_l1j'),"
+        "                (mx.comp_problem(16, 16, 8, wells=2), 'comp_mgr_l1j')):\n"
+        "    t = mx.load_strategy(name)\n"
+        "    H = mx.Hierarchy(mx.Matrix(P.ptr, P.col, P.val), P.partition, t, P.unknown_map)\n"
+        "    R = refcpu.RefHierarchy(P.ptr, P.col, P.val, P.partition.field_order, P.partition.labels, t, P.unknown_map)\n"
+        "    x, rep = H.solve(P.rhs, cfg=mx.KrylovConfig(restart=30, rel_tol=1e-6))\n"
+        "    _, rr = R.solve(P.rhs, restart=30, rel_tol=1e-6)\n"
+        "    assert P.n % 2 == 0, P.n\n"
+        "    assert rep.iterations == rr['iterations'] and rep.residual_history == rr['history'], name\n"
+        "print('ok')")
+    root = make_golden.ROOT
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                         env={**__import__("os").environ, "MGRX_ARNOLDI_SELFXCHG": "1"}, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
