@@ -381,7 +381,19 @@ int fold_sweep0_max_rows() {
 // sweep 0: z = w*(dinv*r); later: z += w*(dinv*(r - A z)) (relax.cpp:168-174).
 // Sweep 0 is folded into sweep 1 (its iterate is formed on the fly from r),
 // and with zacc the last sweep adds its result into zacc (apply_add).
-void BoundRelax::jacobi_sweeps(const double* rc, const int* rrow, double* z, double* zacc, cudaStream_t st) {
+bool BoundRelax::z0_fusable() const {
+  static const bool on = [] {
+    const char* v = std::getenv("MGRX_FUSE_J0");
+    return !v || std::atoi(v) != 0;
+  }();
+  // (short rows only: on the long-row levels of cfg4 the extra epilogue
+  // traffic of the sum-bound staged kernel measured slower)
+  return on && (spec.kind == Smoother::jacobi || spec.kind == Smoother::l1_jacobi) && spec.sweeps >= 2 &&
+         n > fold_sweep0_max_rows() && A && static_cast<long long>(A->nnz) <= 24LL * A->rows;
+}
+
+void BoundRelax::jacobi_sweeps(const double* rc, const int* rrow, double* z, double* zacc, cudaStream_t st,
+                               bool have_z0) {
   if (spec.sweeps <= 1) {
     double* out = zacc ? w0.get() : z;
     jacobi0(n, spec.weight, dinv.get(), rc, rrow, out, st);
@@ -394,7 +406,7 @@ void BoundRelax::jacobi_sweeps(const double* rc, const int* rrow, double* z, dou
   const double* cur = nullptr;
   double* bufs[2] = {w1.get(), w2.get()};
   if (n > fold_sweep0_max_rows()) {
-    jacobi0(n, spec.weight, dinv.get(), rc, rrow, w2.get(), st);
+    if (!have_z0) jacobi0(n, spec.weight, dinv.get(), rc, rrow, w2.get(), st);
     cur = w2.get();
     bufs[1] = w0.get();  // w2 holds sweep 0; w0 is free (no gather when jacobi)
   }
@@ -589,13 +601,25 @@ void AmgHier::vcycle_level(int l, const double* r, double* z, cudaStream_t s) {
     return;
   }
   AmgLevelD& N = levels[l + 1];
-  L.pre.apply(r, nullptr, z, s);                       // z = pre(r)
-  spmv_residual(L.A, z, r, nullptr, L.t.get(), s);     // t = r - A z
-  spmv(L.R, L.t.get(), N.r.get(), s);                  // rc = R t
-  vcycle_level(l + 1, N.r.get(), N.z.get(), s);        // ec
-  spmv_add(L.P, N.z.get(), z, s);                      // z += P ec
-  spmv_residual(L.A, z, r, nullptr, L.t.get(), s);     // t = r - A z
-  L.post.apply_add(L.t.get(), z, s);                   // z += post(t)
+  // Jacobi sweep 0 of a pre/post smoother is written by the kernel that
+  // produces the smoother's input (restriction / residual) when the level
+  // is too large for the folded sweep 0: one launch and one pass fewer.
+  const bool pre0 = l > 0 && L.pre.z0_fusable();
+  if (pre0) L.pre.jacobi_sweeps(r, nullptr, z, nullptr, s, true);  // z0 from the restriction
+  else L.pre.apply(r, nullptr, z, s);                              // z = pre(r)
+  spmv_residual(L.A, z, r, nullptr, L.t.get(), s);                 // t = r - A z
+  const bool npre0 = l + 1 != tail && l + 1 < static_cast<int>(levels.size()) - 1 && N.pre.z0_fusable();
+  if (npre0) spmv_j0(L.R, L.t.get(), N.r.get(), N.pre.dinv.get(), N.pre.spec.weight, N.pre.w2.get(), s);
+  else spmv(L.R, L.t.get(), N.r.get(), s);                         // rc = R t
+  vcycle_level(l + 1, N.r.get(), N.z.get(), s);                    // ec
+  spmv_add(L.P, N.z.get(), z, s);                                  // z += P ec
+  if (L.post.z0_fusable()) {
+    spmv_residual_j0(L.A, z, r, L.t.get(), L.post.dinv.get(), L.post.spec.weight, L.post.w2.get(), s);
+    L.post.jacobi_sweeps(L.t.get(), nullptr, nullptr, z, s, true);  // z += post(t)
+  } else {
+    spmv_residual(L.A, z, r, nullptr, L.t.get(), s);               // t = r - A z
+    L.post.apply_add(L.t.get(), z, s);                             // z += post(t)
+  }
 }
 
 // ============================================================================

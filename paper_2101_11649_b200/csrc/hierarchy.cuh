@@ -41,7 +41,11 @@ struct BoundRelax {
   void apply(const double* r, const int* rrow, double* z, cudaStream_t st);
   // Same, but fused accumulate: zacc += smoother(r). r contiguous.
   void apply_add(const double* r, double* zacc, cudaStream_t st);
-  void jacobi_sweeps(const double* rc, const int* rrow, double* z, double* zacc, cudaStream_t st);
+  void jacobi_sweeps(const double* rc, const int* rrow, double* z, double* zacc, cudaStream_t st,
+                     bool have_z0 = false);
+  // Jacobi with >= 2 sweeps on a level too large for the folded first sweep:
+  // the producer of its input can write sweep 0 into w2 (fused k_jacobi0)
+  bool z0_fusable() const;
   void check(cudaStream_t st);
 };
 

@@ -623,6 +623,38 @@ struct EpiResidual {
   __device__ void store(int r, double s, double bv) const { y[r] = __dsub_rn(bv, __dadd_rn(0.0, s)); }
   __device__ void operator()(int r, double s) const { store(r, s, load(r)); }
 };
+// y = b - (0 + s) (EpiResidual) that also writes the zero-start Jacobi
+// iterate of y, z0 = w * (dinv * y), formed exactly as k_jacobi0 forms it
+// (the post-smoother's sweep 0 without its own launch).
+struct EpiResidualJ0 {
+  const double* b;
+  double* y;
+  const double* dinv;
+  double w;
+  double* z0;
+  __device__ double load(int r) const { return b[r]; }
+  __device__ void store(int r, double s, double bv) const {
+    const double t = __dsub_rn(bv, __dadd_rn(0.0, s));
+    y[r] = t;
+    z0[r] = __dmul_rn(w, __dmul_rn(dinv[r], t));
+  }
+  __device__ void operator()(int r, double s) const { store(r, s, load(r)); }
+};
+// y = 0 + s (EpiStore) plus z0 = w * (dinv * y): restriction into a level
+// whose pre-smoother starts with a Jacobi sweep from zero.
+struct EpiStoreJ0 {
+  double* y;
+  const double* dinv;
+  double w;
+  double* z0;
+  __device__ NoPre load(int) const { return {}; }
+  __device__ void store(int r, double s, const NoPre&) const {
+    const double v = __dadd_rn(0.0, s);
+    y[r] = v;
+    z0[r] = __dmul_rn(w, __dmul_rn(dinv[r], v));
+  }
+  __device__ void operator()(int r, double s) const { store(r, s, load(r)); }
+};
 struct EpiAdd {
   double* y;
   __device__ double load(int r) const { return y[r]; }
@@ -1093,6 +1125,14 @@ void spmv_jacobi(const DCsr& A, const double* zold, const double* b, const int* 
                  const double* dinv, double w, double* znew, cudaStream_t s) {
   launch_spmv(A, XPlain{zold}, EpiJacobi{zold, b, brow, dinv, w, znew}, s);
 }
+void spmv_residual_j0(const DCsr& A, const double* x, const double* b, double* y, const double* dinv, double w,
+                      double* z0, cudaStream_t s) {
+  launch_spmv(A, XPlain{x}, EpiResidualJ0{b, y, dinv, w, z0}, s);
+}
+void spmv_j0(const DCsr& A, const double* x, double* y, const double* dinv, double w, double* z0, cudaStream_t s) {
+  launch_spmv(A, XPlain{x}, EpiStoreJ0{y, dinv, w, z0}, s);
+}
+
 void spmv_jacobi_ex(const DCsr& A, const double* zold, const double* b, const int* brow, const double* dinv,
                     double w, double* znew, double* zacc, cudaStream_t s) {
   const XJac0 z0{w, dinv, b, brow};

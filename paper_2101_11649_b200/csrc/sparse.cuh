@@ -83,6 +83,11 @@ void spmv_jacobi(const DCsr& A, const double* zold, const double* b, const int* 
 // Generalised sweep: zold == nullptr starts from the zero-guess iterate
 // w*(dinv*b) computed on the fly (fusing the first sweep into this one);
 // zacc != nullptr accumulates the result into zacc (fusing apply_add).
+// Residual / plain product that also write the zero-start Jacobi iterate of
+// their output, z0 = w * (dinv * y) (a fused k_jacobi0).
+void spmv_residual_j0(const DCsr& A, const double* x, const double* b, double* y, const double* dinv, double w,
+                      double* z0, cudaStream_t s);
+void spmv_j0(const DCsr& A, const double* x, double* y, const double* dinv, double w, double* z0, cudaStream_t s);
 void spmv_jacobi_ex(const DCsr& A, const double* zold, const double* b, const int* brow, const double* dinv,
                     double w, double* znew, double* zacc, cudaStream_t s);
 
