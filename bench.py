@@ -277,6 +277,24 @@ def run_sharded(args):
     e2e = P.n * e_its / float(tt.item())
     nb = torch.tensor([8.0 * (hi - lo)], dtype=torch.float64)
     dist.all_reduce(nb, op=dist.ReduceOp.SUM)
+    solve_roof = None
+    if rank == 0:
+        # whole-job roofline: the single-GPU byte model of the global solve
+        # (halo traffic excluded) over N GPUs' HBM for the max-over-ranks time
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            from solve_model import SolveModel
+            peak, peak_kind = peaks()
+            mb = SolveModel(H, mx.load_strategy(STRATEGY)).solve_bytes(int(P.ptr[-1]), P.n,
+                                                                       int(round(its / args.steps)), RESTART)
+            ts = t_max / args.steps
+            solve_roof = {"bound": "hbm", "model_bytes_per_solve": mb["bytes"],
+                          "achieved": mb["bytes"] / ts / 1e9, "peak": peak * world, "unit": "GB/s",
+                          "frac": mb["bytes"] / ts / 1e9 / (peak * world), "peak_source": peak_kind,
+                          "model": "tools/solve_model.py (global solve, halo traffic not counted), "
+                                   "peak = N x per-GPU HBM"}
+        except Exception as e:
+            solve_roof = {"error": f"{type(e).__name__}: {e}"}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
@@ -287,7 +305,8 @@ def run_sharded(args):
                 "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(nb.item()),
                         "d2h_bytes_per_step": int(nb.item()),
                         "path": "Shard.solve -> mgrx_shard_solve (C ABI) per rank, pinned host slices"},
-                "gpu_launches": launches, "roofline": None, "cpu_baseline": None,
+                "gpu_launches": launches, "roofline": None, "solve_roofline": solve_roof, "cpu_baseline": None,
+                "fused_sharded_arnoldi": bool(getattr(S, "fused", False)),
                 "clocks": clk.summary()}
         print(json.dumps(line))
     S.close()

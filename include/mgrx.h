@@ -166,6 +166,11 @@ MGRX_API int mgrx_local_group_destroy(mgrx_group* g);
 MGRX_API int mgrx_shard_create(mgrx_hier* h, int rank, int size, const int* row_starts,
                                const unsigned char* nccl_id, mgrx_group* group, mgrx_shard** out);
 MGRX_API int mgrx_shard_rows(mgrx_shard* sd, int* row_begin, int* row_end);
+/* 1 when this shard's GMRES steps use the fused sharded Arnoldi kernel
+ * (in-kernel partial exchange over NVLink; enabled after a bitwise
+ * self-check on every rank), 0 for the all-gather path. No reference
+ * counterpart (the reference is single-process). */
+MGRX_API int mgrx_shard_fused(mgrx_shard* sd, int* fused);
 /* z = M^{-1} v on the owned rows (bitwise equal to the owned rows of mgrx_apply). */
 MGRX_API int mgrx_shard_apply(mgrx_shard* sd, const double* v, double* z, int on_device);
 /* GMRES on the owned rows of b / x (flags as mgrx_solve). */

@@ -89,6 +89,7 @@ def lib() -> C.CDLL:
         L.mgrx_local_group_destroy.argtypes = [vp]
         L.mgrx_shard_create.argtypes = [vp, C.c_int, C.c_int, vp, C.c_char_p, vp, C.POINTER(vp)]
         L.mgrx_shard_rows.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.mgrx_shard_fused.argtypes = [vp, C.POINTER(C.c_int)]
         L.mgrx_shard_apply.argtypes = [vp, vp, vp, C.c_int]
         L.mgrx_shard_solve.argtypes = [vp, vp, vp, C.POINTER(_Krylov), C.POINTER(_Report), C.c_int]
         L.mgrx_shard_destroy.argtypes = [vp]
@@ -398,6 +399,9 @@ class Shard:
         _check(lib().mgrx_shard_rows(self._h, C.byref(b), C.byref(e)))
         self.row_begin, self.row_end = b.value, e.value
         self.n = self.row_end - self.row_begin
+        f = C.c_int()
+        _check(lib().mgrx_shard_fused(self._h, C.byref(f)))
+        self.fused = bool(f.value)  # fused sharded Arnoldi in use (one GPU per rank)
 
     def apply(self, v: np.ndarray) -> np.ndarray:
         v = np.ascontiguousarray(v, dtype=np.float64)

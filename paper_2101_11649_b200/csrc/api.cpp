@@ -646,6 +646,14 @@ int mgrx_shard_rows(mgrx_shard* sd, int* row_begin, int* row_end) {
   });
 }
 
+int mgrx_shard_fused(mgrx_shard* sd, int* fused) {
+  return guarded([&] {
+    if (!fused) throw InvalidArgument("mgrx_shard_fused: null output");
+    *fused = sd->sh->fused ? 1 : 0;
+    return MGRX_OK;
+  });
+}
+
 int mgrx_shard_apply(mgrx_shard* sd, const double* v, double* z, int on_device) {
   return guarded([&] {
     use(sd->h->ctx);

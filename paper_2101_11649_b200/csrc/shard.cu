@@ -471,6 +471,12 @@ ArnoldiPeers Shard::peers_arg() {
 void Shard::setup_fused() {
   fused = false;
   if (const char* e = std::getenv("MGRX_SHARD_FUSED"); e && std::atoi(e) == 0) return;
+  // one rank: the exchange is the identity (k_fold2 of one partial is the
+  // partial), so the single-GPU fused kernel is the same computation
+  if (c.size == 1) {
+    fused = arnoldi_sharded_ok(spaces.front().own);
+    return;
+  }
   // ranks of the local comm share one device: the in-kernel exchange needs
   // every rank's persistent kernel resident at once, i.e. one GPU per rank
   if (c.size < 2 || c.size > kMboxRanks || std::string(comm->kind()) != "nccl") return;
@@ -737,7 +743,12 @@ GmresResult Shard::solve(const double* b, double* x, const KrylovSpec& cfg) {
       if (fused) {
         // both MGS passes, the re-orthogonalisation test and v_{k+1} in one
         // kernel per rank, partials exchanged through the peers' mailboxes
-        arnoldi_sharded(n, k, 0, peers_arg(), ws, s);
+        if (c.size == 1) {
+          MGRX_CK(cudaMemsetAsync(S + m + 3, 0, sizeof(double), s));
+          arnoldi_probe(n, k, 0, ws, s);
+        } else {
+          arnoldi_sharded(n, k, 0, peers_arg(), ws, s);
+        }
         MGRX_CK(cudaMemcpyAsync(H_pin, S, col_bytes, cudaMemcpyDeviceToHost, s));
         MGRX_CK(cudaStreamSynchronize(s));
         if (H_pin[m + 3] != 0.0) throw RuntimeError("sharded Arnoldi: a peer did not answer (exchange timed out)");
