@@ -21,6 +21,9 @@ namespace mgrx {
 
 struct AmgHier;
 
+// Largest level (rows) whose Jacobi sweep 0 is folded into sweep 1.
+int fold_sweep0_max_rows();
+
 // A smoother specialised to one matrix (BoundSmoother, proj/src/relax.cpp:90-192).
 struct BoundRelax {
   SmootherSpec spec;

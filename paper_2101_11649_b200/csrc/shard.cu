@@ -293,6 +293,92 @@ void SRelax::apply(const double* r, const int* rrow, double* z, double* zacc, Sh
 // ---------------------------------------------------------------------------
 // AMG
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// replicated coarse V-cycle
+// ---------------------------------------------------------------------------
+void RepAmg::build(const AmgHier& h, int l, const Part& p, cudaStream_t s) {
+  g = &h;
+  from = l;
+  part = p;
+  const int size = static_cast<int>(p.st.size()) - 1;
+  maxc = 1;
+  for (int q = 0; q < size; ++q) maxc = std::max(maxc, p.n(q));
+  std::vector<int> m(p.total());
+  for (int q = 0; q < size; ++q)
+    for (int gr = p.lo(q); gr < p.hi(q); ++gr) m[gr] = q * maxc + (gr - p.lo(q));
+  map = upload_ints(m, s);
+  pad.alloc(maxc, s);
+  pad.zero();
+  all.alloc(static_cast<size_t>(size) * maxc, s);
+  const int n0 = std::max(1, p.total());
+  rfull.alloc(n0, s);
+  zfull.alloc(n0, s);
+  const int nl = static_cast<int>(h.levels.size());
+  for (int k = l; k < nl; ++k) {
+    lv.emplace_back();
+    const int n = std::max(1, h.levels[k].A.rows);
+    for (DVec<double>* v : {&lv.back().r, &lv.back().z, &lv.back().t, &lv.back().w1, &lv.back().w2}) v->alloc(n, s);
+  }
+}
+
+// BoundRelax::apply / apply_add (Jacobi kinds, folded sweep 0: n <= 64K)
+void RepAmg::smooth(const BoundRelax& b, const double* r, double* z, double* zacc, Lv& w, cudaStream_t s) {
+  const int n = b.n;
+  if (b.spec.sweeps <= 1) {
+    double* out = zacc ? w.w1.get() : z;
+    jacobi0(n, b.spec.weight, b.dinv.get(), r, nullptr, out, s);
+    if (zacc) vec_add(n, out, zacc, s);
+    return;
+  }
+  const double* cur = nullptr;
+  double* bufs[2] = {w.w1.get(), w.w2.get()};
+  for (int sw = 1; sw < b.spec.sweeps; ++sw) {
+    const bool last = sw == b.spec.sweeps - 1;
+    double* nxt = last ? (zacc ? nullptr : z) : bufs[sw % 2];
+    spmv_jacobi_ex(*b.A, cur, r, nullptr, b.dinv.get(), b.spec.weight, nxt, last ? zacc : nullptr, s);
+    cur = nxt;
+  }
+}
+
+void RepAmg::level(int l, const double* r, double* z, cudaStream_t s) {
+  const int nl = static_cast<int>(g->levels.size());
+  if (l == g->tail) {
+    launch_amg_tail(g->tail_desc, g->tail_blob.get(), r, z, s);
+    return;
+  }
+  if (l == nl - 1) {
+    dense_solve(g->coarse, r, z, s);
+    return;
+  }
+  const AmgLevelD& G = g->levels[l];
+  Lv& W = lv[l - from];
+  Lv& N = lv[l + 1 - from];
+  smooth(G.pre, r, z, nullptr, W, s);
+  spmv_residual(G.A, z, r, nullptr, W.t.get(), s);
+  spmv(G.R, W.t.get(), N.r.get(), s);
+  level(l + 1, N.r.get(), N.z.get(), s);
+  spmv_add(G.P, N.z.get(), z, s);
+  spmv_residual(G.A, z, r, nullptr, W.t.get(), s);
+  smooth(G.post, W.t.get(), nullptr, z, W, s);
+}
+
+void RepAmg::vcycle(const double* r, double* z, ShardCtx& c) {
+  const int own = part.n(c.rank);
+  d2d(pad.get(), r, own, c.s);
+  c.comm->allgather(pad.get(), all.get(), maxc, c.s);
+  pack(part.total(), map.get(), all.get(), rfull.get(), c.s);
+  level(from, rfull.get(), zfull.get(), c.s);
+  d2d(z, zfull.get() + part.lo(c.rank), own, c.s);
+}
+
+int repl_rows() {
+  static const int m = [] {
+    const char* v = std::getenv("MGRX_SHARD_REPL_ROWS");
+    return v ? std::atoi(v) : 65536;
+  }();
+  return m;
+}
+
 void SAmg::build(const AmgHier& g, Space& fine, ShardCtx& c) {
   const int nl = static_cast<int>(g.levels.size());
   std::vector<Space*> sp(nl);
@@ -303,10 +389,30 @@ void SAmg::build(const AmgHier& g, Space& fine, ShardCtx& c) {
     spaces.push_back(make_space(sub_part(sp[l - 1]->part, C), c.rank));
     sp[l] = &spaces.back();
   }
+  // first level that is replicated: small, Jacobi-type smoothing from there
+  // on (the single-GPU smoother path without a gather), more than one rank
+  int from = -1;
+  if (c.size > 1 && repl_rows() > 0) {
+    for (int l = 1; l < nl && from < 0; ++l) {
+      if (g.levels[l].A.rows > repl_rows()) continue;
+      bool ok = true;
+      for (int k = l; k < nl - 1 && ok; ++k) {
+        const BoundRelax* bs[2] = {&g.levels[k].pre, &g.levels[k].post};
+        for (const BoundRelax* b : bs)
+          ok = ok && (b->spec.kind == Smoother::jacobi || b->spec.kind == Smoother::l1_jacobi) &&
+               (b->spec.sweeps <= 1 || b->n <= fold_sweep0_max_rows());
+      }
+      if (ok) from = l;
+    }
+  }
   for (int l = 0; l < nl; ++l) {
     L.emplace_back();
     SAmgLevel& S = L.back();
     S.sp = sp[l];
+    if (l == from) {
+      rep.build(g, l, sp[l]->part, c.s);
+      break;
+    }
     if (l == nl - 1) {
       coarse.build(&g.coarse, sp[l]->part, c.s);
       break;
@@ -336,6 +442,10 @@ void SAmg::alloc(cudaStream_t s) {
 // V(1,1) (proj/src/amg.cpp:232-242), with halos before each product.
 void SAmg::level(int l, const double* r, double* z, ShardCtx& c) {
   SAmgLevel& S = L[l];
+  if (l == rep.from) {
+    rep.vcycle(r, z, c);
+    return;
+  }
   if (l == static_cast<int>(L.size()) - 1) {
     coarse.solve(r, z, c);
     return;

@@ -111,10 +111,37 @@ struct SAmgLevel {
   DVec<double> r, z, t;
 };
 
+// Replicated coarse V-cycle (SURVEY 8(e) agglomeration): from level `from`
+// on (<= MGRX_SHARD_REPL_ROWS global rows, Jacobi-type smoothing), every
+// rank all-gathers the level's residual and runs the rest of the V-cycle on
+// the full vectors with the single-GPU kernels of its own replica of the
+// hierarchy (read-only) and shard-owned work vectors, then keeps its slice:
+// one all-gather replaces a halo exchange per operation on the small levels.
+// The operations are the single-GPU V-cycle's, so results stay bitwise.
+struct RepAmg {
+  const AmgHier* g = nullptr;
+  int from = -1;
+  Part part;  // partition of level `from`
+  int maxc = 1;
+  DVec<double> pad, all, rfull, zfull;
+  DVec<int> map;
+  struct Lv {
+    DVec<double> r, z, t, w1, w2;
+  };
+  std::deque<Lv> lv;  // levels from .. coarsest
+  void build(const AmgHier& h, int l, const Part& p, cudaStream_t s);
+  void vcycle(const double* r, double* z, ShardCtx& c);  // r, z: owned slices of level `from`
+
+ private:
+  void level(int l, const double* r, double* z, cudaStream_t s);
+  void smooth(const BoundRelax& b, const double* r, double* z, double* zacc, Lv& w, cudaStream_t s);
+};
+
 struct SAmg {
   std::deque<Space> spaces;  // spaces[0] unused when the fine space is external
   std::deque<SAmgLevel> L;
   Repl coarse;
+  RepAmg rep;  // rep.from >= 1: levels from rep.from on are replicated
   void build(const AmgHier& g, Space& fine, ShardCtx& c);
   void alloc(cudaStream_t s);
   void vcycle(const double* r, double* z, ShardCtx& c) { level(0, r, z, c); }

@@ -119,3 +119,31 @@ def test_nccl_single_rank():
     assert r2.residual_history == r1.residual_history
     assert np.array_equal(x2.view(np.int64), x1.view(np.int64))
     S.close()
+
+
+def test_sharded_without_replicated_coarse_levels():
+    """MGRX_SHARD_REPL_ROWS=0 keeps every AMG level sharded (halo exchanges
+    down to the coarsest); the default replicates the levels of <= 64K rows
+    (one all-gather, then the single-GPU kernels). Both are bitwise equal to
+    the single-GPU application."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, '.'); sys.path.insert(0, 'tests')\n"
+        "from concurrent.futures import ThreadPoolExecutor\n"
+        "import paper_2101_11649_b200 as mx\n"
+        "for size in (2, 3):\n"
+        "    P = mx.mfd_problem(12, 12, 8, 'layered')\n"
+        "    H = mx.Hierarchy(mx.Matrix(P.ptr, P.col, P.val), P.partition, mx.load_strategy('mfd_mgr_pi_c1_l1j'))\n"
+        "    g = mx.LocalGroup(size); st = mx.slab_row_starts(P, size)\n"
+        "    S = [mx.Shard(H, r, size, st, group=g) for r in range(size)]\n"
+        "    v = np.random.default_rng(7).uniform(-1, 1, P.n); z = H.apply(v)\n"
+        "    with ThreadPoolExecutor(size) as ex: zs = list(ex.map(lambda s: s.apply(v[s.row_begin:s.row_end]), S))\n"
+        "    for s, zr in zip(S, zs): assert np.array_equal(zr.view(np.int64), z[s.row_begin:s.row_end].view(np.int64))\n"
+        "    [s.close() for s in S]; g.close()\n"
+        "print('ok')")
+    root = make_golden.ROOT
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                         env={**os.environ, "MGRX_SHARD_REPL_ROWS": "0"}, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
