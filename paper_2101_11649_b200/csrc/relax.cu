@@ -468,7 +468,8 @@ constexpr size_t kSmallSmem = 2 * sizeof(SmallBuf) + kSmallN * sizeof(double);
 
 template <bool kFull>
 __global__ void __launch_bounds__(kPipeThreads)
-    k_gs_small(int nsteps, const int* __restrict__ steps, const int* __restrict__ order,
+    k_gs_small(int nsteps, const int* __restrict__ steps, int nchunks, const int* __restrict__ chunks,
+               const int* __restrict__ order,
                const int* __restrict__ sptr, const int* __restrict__ scol, const double* __restrict__ sval,
                const double* __restrict__ sd, const double* __restrict__ bp, const double* __restrict__ xold,
                double* xnew, double* zadd) {
@@ -486,10 +487,14 @@ __global__ void __launch_bounds__(kPipeThreads)
   __syncthreads();
   auto SP = [&](int q) { return st_smem ? stp[q] : steps[q]; };
   auto SE = [&](int q) { return st_smem ? ste[q] : steps[nsteps + 1 + q]; };
-  auto issue = [&](int st, SmallBuf& B) {
-    const int p0 = SP(st), p1 = SP(st + 1);
+  // chunk c = steps [chunks[c], chunks[c+1]): its rows and entries are
+  // contiguous, loaded by one cp.async group while the previous chunk's
+  // dependency levels are swept (one barrier per level)
+  auto issue = [&](int c, SmallBuf& B) {
+    const int sa = chunks[c], sb = chunks[c + 1];
+    const int p0 = SP(sa), p1 = SP(sb);
     const int nr = p1 - p0;
-    const int e0 = SE(st), e1 = SE(st + 1);
+    const int e0 = SE(sa), e1 = SE(sb);
     for (int q = tid; q < nr; q += kPipeThreads) {
       cpa4(&B.ord[q], order + p0 + q);
       cpa8(&B.sd[q], sd + p0 + q);
@@ -502,16 +507,19 @@ __global__ void __launch_bounds__(kPipeThreads)
     }
     cpa_commit();
   };
+  (void)nsteps;
   issue(0, buf[0]);
-  for (int st = 0; st < nsteps; ++st) {
-    SmallBuf& B = buf[st & 1];
-    if (st + 1 < nsteps) issue(st + 1, buf[(st + 1) & 1]);
+  for (int c = 0; c < nchunks; ++c) {
+    SmallBuf& B = buf[c & 1];
+    if (c + 1 < nchunks) issue(c + 1, buf[(c + 1) & 1]);
     else cpa_commit();
     cpa_wait1();
     __syncthreads();
-    const int nr = SP(st + 1) - SP(st);
+    const int cbase = SP(chunks[c]);
+    for (int st = chunks[c]; st < chunks[c + 1]; ++st) {
+    const int qa = SP(st) - cbase, qb = SP(st + 1) - cbase;
     const int e0 = B.ptr[0];
-    for (int q = tid; q < nr; q += kPipeThreads) {
+    for (int q = qa + tid; q < qb; q += kPipeThreads) {
       const int i = B.ord[q];
       double s = B.bp[q];
       const int k1 = B.ptr[q + 1] - e0;
@@ -532,7 +540,23 @@ __global__ void __launch_bounds__(kPipeThreads)
       if (zadd) zadd[i] = __dadd_rn(zadd[i], v);
     }
     __syncthreads();
+    }
   }
+}
+
+// Group consecutive sweep steps into chunks of <= rows_cap rows / ent_cap
+// entries (st: step row boundaries, ptr: the sweep CSR's row pointer).
+std::vector<int> small_chunks(const std::vector<int>& st, const std::vector<int>& ptr, int rows_cap, int ent_cap) {
+  std::vector<int> ch{0};
+  const int ns = static_cast<int>(st.size()) - 1;
+  int a = 0;
+  while (a < ns) {
+    int b = a + 1;
+    while (b < ns && st[b + 1] - st[a] <= rows_cap && ptr[st[b + 1]] - ptr[st[a]] <= ent_cap) ++b;
+    ch.push_back(b);
+    a = b;
+  }
+  return ch;
 }
 
 std::vector<int> pipe_steps(const std::vector<int>& level_ptr, const std::vector<int>& sptr,
@@ -789,12 +813,20 @@ void gs_schedule(const DCsr& A, bool forward, const double* d, bool full, GsSche
       const std::vector<int> stv = with_offsets(st, dp);
       out.dsteps.alloc(stv.size(), s);
       out.dsteps.upload(stv.data(), stv.size());
+      const std::vector<int> ch = small_chunks(st, dp, kSmallRows, kSmallEnt);
+      out.ndchunks = static_cast<int>(ch.size()) - 1;
+      out.dchunks.alloc(ch.size(), s);
+      out.dchunks.upload(ch.data(), ch.size());
       if (full) {
         const std::vector<int> st2 = pipe_steps(out.level_ptr, fp, kSmallRows, kSmallEnt);
         out.nfsteps = static_cast<int>(st2.size()) - 1;
         const std::vector<int> stv2 = with_offsets(st2, fp);
         out.fsteps.alloc(stv2.size(), s);
         out.fsteps.upload(stv2.data(), stv2.size());
+        const std::vector<int> ch2 = small_chunks(st2, fp, kSmallRows, kSmallEnt);
+        out.nfchunks = static_cast<int>(ch2.size()) - 1;
+        out.fchunks.alloc(ch2.size(), s);
+        out.fchunks.upload(ch2.data(), ch2.size());
       }
       out.bp.alloc(n, s);
       out.small = 1;
@@ -849,11 +881,13 @@ void gs_sweep(const DCsr& A, const GsSchedule& sch, const double* d, const doubl
     const int* sc = full_sweep ? sch.fcol.get() : sch.dcol.get();
     const double* sv = full_sweep ? sch.fval.get() : sch.dval.get();
     if (full_sweep)
-      k_gs_small<true><<<1, kPipeThreads, kSmallSmem, s>>>(sch.nfsteps, sch.fsteps.get(), sch.order.get(), sp, sc,
-                                                           sv, sch.sd.get(), sch.bp.get(), xold, xnew, zadd);
+      k_gs_small<true><<<1, kPipeThreads, kSmallSmem, s>>>(sch.nfsteps, sch.fsteps.get(), sch.nfchunks,
+                                                           sch.fchunks.get(), sch.order.get(), sp, sc, sv,
+                                                           sch.sd.get(), sch.bp.get(), xold, xnew, zadd);
     else
-      k_gs_small<false><<<1, kPipeThreads, kSmallSmem, s>>>(sch.ndsteps, sch.dsteps.get(), sch.order.get(), sp,
-                                                            sc, sv, sch.sd.get(), sch.bp.get(), xold, xnew, zadd);
+      k_gs_small<false><<<1, kPipeThreads, kSmallSmem, s>>>(sch.ndsteps, sch.dsteps.get(), sch.ndchunks,
+                                                            sch.dchunks.get(), sch.order.get(), sp, sc, sv,
+                                                            sch.sd.get(), sch.bp.get(), xold, xnew, zadd);
     MGRX_LAUNCH_CK();
     count_launch(2);
     return;

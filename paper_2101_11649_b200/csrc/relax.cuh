@@ -36,6 +36,11 @@ struct GsSchedule {
   int small = 0;                   // 1: single-CTA sweep with x in shared memory (n <= 12288)
   DVec<int> dsteps, fsteps;        // step boundaries (positions) for the pipelined sweep
   int ndsteps = 0, nfsteps = 0;
+  // single-CTA sweep: groups of consecutive steps loaded together (one
+  // cp.async chunk of <= kSmallRows rows / kSmallEnt entries holding many
+  // short dependency levels), double-buffered a chunk ahead
+  DVec<int> dchunks, fchunks;
+  int ndchunks = 0, nfchunks = 0;
   DVec<double> bp;                 // rhs gathered into sweep order (pipelined sweep)
 };
 // owner (nullable): range id per row for a multi-range hybrid partition;
