@@ -523,17 +523,23 @@ __global__ void __launch_bounds__(kPipeThreads)
       const int i = B.ord[q];
       double s = B.bp[q];
       const int k1 = B.ptr[q + 1] - e0;
-      for (int k = B.ptr[q] - e0; k < k1; ++k) {
-        int c = B.col[k];
-        double x;
-        if (kFull && !(c & kDepBit)) {
-          x = xold[c];
-        } else {
-          if (kFull) c &= ~kDepBit;
-          x = xs[c];
-        }
-        s = __dsub_rn(s, __dmul_rn(B.val[k], x));
+      // operand loads of 4 entries are issued together (the column index and
+      // the iterate value are dependent shared-memory loads; one entry at a
+      // time the row was bound by their latency), then the entries are
+      // subtracted in the row's order
+      auto xval = [&](int c) -> double {
+        if (kFull && !(c & kDepBit)) return xold[c];
+        return xs[kFull ? (c & ~kDepBit) : c];
+      };
+      int k = B.ptr[q] - e0;
+      for (; k + 4 <= k1; k += 4) {
+        const int c0 = B.col[k], c1 = B.col[k + 1], c2 = B.col[k + 2], c3 = B.col[k + 3];
+        const double x0 = xval(c0), x1 = xval(c1), x2 = xval(c2), x3 = xval(c3);
+        const double p0 = __dmul_rn(B.val[k], x0), p1 = __dmul_rn(B.val[k + 1], x1);
+        const double p2 = __dmul_rn(B.val[k + 2], x2), p3 = __dmul_rn(B.val[k + 3], x3);
+        s = __dsub_rn(__dsub_rn(__dsub_rn(__dsub_rn(s, p0), p1), p2), p3);
       }
+      for (; k < k1; ++k) s = __dsub_rn(s, __dmul_rn(B.val[k], xval(B.col[k])));
       const double v = __dadd_rn(kFull ? xold[i] : 0.0, __ddiv_rn(s, B.sd[q]));
       xs[i] = v;
       xnew[i] = v;
