@@ -411,12 +411,14 @@ def main():
             probes[name] = {"avg_ms": ms_k, "bytes": by, "GBps": by / (ms_k * 1e-3) / 1e9}
         except mx.MgrxError as e:
             probes[name] = {"error": str(e)}
-    # dominant kernel: the fused Arnoldi step (k_arnoldi: both MGS passes of one
-    # GMRES step in one persistent launch) carries the largest share of solve
-    # time in the l1-Jacobi strategy (~37% in the profiles/r01 launch list, the
-    # SpMV family k_spmv* next); arnoldi.15 is the step at the mean Krylov
-    # index of a 30-step restart cycle. For other strategies take the probe
-    # with the largest time.
+    # roofline object: the fused Arnoldi step (k_arnoldi2: both MGS passes of
+    # one GMRES step in one persistent launch), the largest single kernel (35%
+    # of cfg2 solve kernel time in 73 launches, profiles/r01/launch_shares.txt);
+    # the staged SpMV function k_spmv_staged has 40% spread over ~1,200
+    # launches on ~15 matrices and is reported beside it (dominant_by_share,
+    # with its largest instance, the fine operator). arnoldi.15 is the step at
+    # the mean Krylov index of a 30-step restart cycle. For other strategies
+    # take the probe with the largest time.
     share = {k: v["avg_ms"] for k, v in probes.items() if "avg_ms" in v}
     if "l1j" in STRATEGY:
         dom = "arnoldi.15" if "avg_ms" in probes.get("arnoldi.15", {}) else "mgs"
@@ -431,9 +433,16 @@ def main():
             traffic = tr["kernels"][dom]["dram_bytes_per_launch"]
     except Exception:
         pass
+    by_share = None
+    if "avg_ms" in probes.get("spmv.A", {}):
+        sa = probes["spmv.A"]
+        by_share = {"kernel": "k_spmv_staged (all staged SpMV launches: fine operator, AMG levels 0-2, "
+                              "restriction; ~40% of cfg2 solve kernel time)",
+                    "largest_instance": "spmv.A (fine operator)", "achieved": sa["GBps"], "peak": peak,
+                    "frac": sa["GBps"] / peak}
     roof = {"bound": "hbm", "kernel": dom, "achieved": d["GBps"], "peak": peak, "unit": "GB/s",
             "frac": d["GBps"] / peak, "traffic": traffic, "algorithmic_bytes": d["bytes"],
-            "peak_source": peak_kind, "kernels": probes,
+            "peak_source": peak_kind, "dominant_by_share": by_share, "kernels": probes,
             "probe_method": "CUDA events on the library stream over 20 back-to-back launches (inputs in HBM; the L2 may retain part of a working set near its 126 MB size)"}
 
     # whole-solve roofline: SURVEY §8(d) compulsory-traffic bytes of one solve
