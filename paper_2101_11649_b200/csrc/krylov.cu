@@ -214,6 +214,10 @@ struct ArnoldiArgs {
   double* const* peers = nullptr;     // every rank's mailbox (device array)
   unsigned long long epoch = 0;       // tag base of this launch
   double* err = nullptr;              // set to 1 on a peer timeout
+  // lane-pair kernel: merge pass 1's norm phase with pass 2's first
+  // projection (one grid reduction fewer per re-orthogonalised step)
+  int merge = 0;
+  double* npass = nullptr;            // out: passes run (1 or 2)
 };
 
 // One projection phase over this lane's rows (w in shared memory, column
@@ -664,30 +668,48 @@ __global__ void __launch_bounds__(kAT2, 1) k_arnoldi2(ArnoldiArgs a) {
   const bool writer = blockIdx.x == 0 && T == 0;
   double h = 0.0, wn2 = 0.0, w02 = 0.0;
   unsigned phase = 0;
+  // Merged phase (a.merge, set by the host when the previous step needed the
+  // second pass): pass 1's last phase (w -= h_k v_k; ||w||^2) also forms
+  // v_0 . w, which is exactly pass 2's first projection (same w, same slot
+  // order, same reduction: bitwise). If the test then skips pass 2, that dot
+  // is discarded (one extra column read).
+  const bool merge = !kShard && a.merge;
+  double h0 = 0.0;
+  int passes = 1;
   for (int pass = 0; pass < 2; ++pass) {
-    for (int i = 0; i <= k + 1; ++i) {
+    for (int i = (pass == 1 && merge) ? 1 : 0; i <= k + 1; ++i) {
+      const bool mphase = merge && pass == 0 && i == k + 1;
       PairSums ps;
       double t1, t2;
       if (!(a.dbg & 1)) {
         // dbg & 64 (timing experiment, not bitwise): no L2 re-read of v_{i-1}
         const double* pl = (i && !(a.dbg & 64)) ? a.V + (i - 1) * ld + lane : nullptr;
-        const double* al = a.V + i * ld + lane;
+        const double* al = a.V + (mphase ? 0 : i) * ld + lane;
         // dbg & 32 (timing experiment, not bitwise): rotate the slot order per CTA
         const int rot = (a.dbg & 32) ? (kU * (blockIdx.x % (nsy / kU > 0 ? nsy / kU : 1))) % (nsy > 0 ? nsy : 1) : 0;
-        if (i > k) arn2_rows<kU, true, false, true>(wl, nsy, false, pl, al, h, pf, ps, rot);
+        if (mphase) arn2_rows<kU, true, true, true>(wl, nsy, false, pl, al, h, pf, ps, rot);
+        else if (i > k) arn2_rows<kU, true, false, true>(wl, nsy, false, pl, al, h, pf, ps, rot);
         else if (i) arn2_rows<kU, true, true, false>(wl, nsy, false, pl, al, h, pf, ps, rot);
         else if (pass == 0) arn2_rows<kU, false, true, true>(wl, nsy, false, pl, al, h, pf, ps, rot);
         else arn2_rows<kU, false, true, false>(wl, nsy, false, pl, al, h, pf, ps, rot);
       }
       pair_reduce<kShard>(a, ps, phase++, r1, r2, f1, f2, t1, t2);
-      arn_record(a, writer, pass, i, t1, t2, hk, h, w02, wn2);
+      if (mphase) {
+        wn2 = t2;
+        h0 = t1;
+      } else {
+        arn_record(a, writer, pass, i, t1, t2, hk, h, w02, wn2);
+      }
     }
     h = 0.0;
     if (pass == 1 || (!(a.dbg & 4) && !(__dsqrt_rn(wn2) < __ddiv_rn(__dsqrt_rn(w02), __dsqrt_rn(2.0))))) break;
+    passes = 2;
+    if (merge) arn_record(a, writer, 1, 0, h0, 0.0, hk, h, w02, wn2);  // pass 2, projection 0
   }
   if (writer) {
     *a.n0 = w02;
     *a.n1 = wn2;
+    if (a.npass) *a.npass = passes;
   }
   const double wn = __dsqrt_rn(wn2);
   if (!(wn < 1e-300)) {
@@ -740,6 +762,16 @@ const ArnoldiMode& arnoldi_mode() {
   return m;
 }
 
+// MGRX_ARNOLDI_MERGE=0: never merge the pass-1 norm phase with pass 2's
+// first projection.
+bool arnoldi_merge_on() {
+  static const bool on = [] {
+    const char* v = std::getenv("MGRX_ARNOLDI_MERGE");
+    return !v || std::atoi(v) != 0;
+  }();
+  return on;
+}
+
 int arnoldi_slots(int n) {
   const ArnoldiMode& m = arnoldi_mode();
   constexpr int kStride = kRB * kRT;
@@ -750,11 +782,15 @@ int arnoldi_slots(int n) {
   return slots <= kAMaxSlots ? slots : 0;
 }
 
-void arnoldi_launch(int n, int k, int slots, int dbg, GmresWork& ws, cudaStream_t s) {
+// merge: see k_arnoldi2 (lane-pair kernel only). The pass count lands in
+// scalar slot 2m+5, inside the Hessenberg-column D2H.
+void arnoldi_launch(int n, int k, int slots, int dbg, GmresWork& ws, cudaStream_t s, bool merge = false) {
   double* S = ws.scal.get();
   const int m = ws.m;
   MGRX_CK(cudaMemsetAsync(ws.bar.get(), 0, sizeof(unsigned), s));
   ArnoldiArgs aa{n, k, ws.w.get(), ws.V.get(), ws.apart.get(), ws.bar.get(), S, S + 1, S + 2, S + 3 + (m + 1), dbg};
+  aa.merge = merge && arnoldi_merge_on() ? 1 : 0;
+  aa.npass = S + 2 * m + 5;
   void* args[] = {&aa};
   const ArnoldiMode& md = arnoldi_mode();
   const size_t smem = static_cast<size_t>(slots) * kAT * sizeof(double);
@@ -857,7 +893,7 @@ void mgs_probe(int n, double* w, const double* vprev, const double* h, const dou
 int arnoldi_probe(int n, int k, int dbg, GmresWork& ws, cudaStream_t s) {
   const int slots = arnoldi_slots(n);
   if (!slots || k < 0 || k >= ws.m) return 0;
-  arnoldi_launch(n, k, slots, dbg, ws, s);
+  arnoldi_launch(n, k, slots, dbg, ws, s, true);
   return 1;
 }
 
@@ -955,6 +991,7 @@ GmresResult gmres_device(const DCsr& A, const double* b, double* x, const Krylov
     double* V = ws.V.get();
     auto col = [&](int j) { return V + static_cast<size_t>(j) * n; };
 
+    bool merge_next = true;  // the previous step ran the second MGS pass
     while (res.iterations < cfg.max_iters) {
       spmv_residual(A, x, b, nullptr, ws.r.get(), s);  // r = b - A x
       const double rnorm = std::sqrt(norm2(ws.r.get()));
@@ -1001,7 +1038,7 @@ GmresResult gmres_device(const DCsr& A, const double* b, double* x, const Krylov
             pe.epoch = epoch;
             arnoldi_sharded(n, k, 0, pe, ws, s);
           } else {
-            arnoldi_launch(n, k, slots, 0, ws, s);
+            arnoldi_launch(n, k, slots, 0, ws, s, merge_next);
           }
           if (prof.on) prof.rec(3, s);
           MGRX_CK(cudaMemcpyAsync(H_pin, S, col_bytes, cudaMemcpyDeviceToHost, s));
@@ -1010,6 +1047,7 @@ GmresResult gmres_device(const DCsr& A, const double* b, double* x, const Krylov
           if (prof.on) prof.step();
           if (self_exchange() && H_pin[m + 3] != 0.0) throw RuntimeError("Arnoldi self-exchange timed out");
           wn = std::sqrt(H_pin[1]);
+          merge_next = H_pin[2 * m + 5] == 2.0;
         } else {
           // pass 1: h_i = v_i . w ; w -= h_i v_i  (krylov.cpp:84-89)
           for (int i = 0; i <= k; ++i)
