@@ -315,14 +315,17 @@ def test_alternative_gs_sweeps_are_bit_exact(mode):
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
 
 
-@pytest.mark.parametrize("env", [{"MGRX_ARNOLDI": "0"}, {"MGRX_ARNOLDI": "1"}, {"MGRX_SPMV_STAGED": "2"},
-                                 {"MGRX_SPMV_STAGED": "0"}], ids=["mgs", "arnoldi", "staged", "direct"])
+@pytest.mark.parametrize("env", [{"MGRX_ARNOLDI": "0"}, {"MGRX_ARNOLDI": "1"}, {"MGRX_ARNOLDI_MERGE": "0"},
+                                 {"MGRX_SPMV_STAGED": "2"}, {"MGRX_SPMV_STAGED": "0"}],
+                         ids=["mgs", "arnoldi", "unmerged", "staged", "direct"])
 def test_solve_paths_are_bit_exact(env):
     """Every device path choice reproduces the oracle's residual history and
     solution bitwise on a system large enough (n > 5 * 151552) that every
     Arnoldi lane owns several rows and every large operator is a staged-SpMV
     candidate: the fused persistent Arnoldi kernel vs the launch-per-
-    projection MGS (MGRX_ARNOLDI), and the bulk-copy-staged SpMV forced on
+    projection MGS (MGRX_ARNOLDI), the lane-pair kernel with separate pass-1
+    norm and pass-2 first-projection phases (MGRX_ARNOLDI_MERGE=0; the default
+    merges them), and the bulk-copy-staged SpMV forced on
     every large matrix vs the direct kernels only (MGRX_SPMV_STAGED)."""
     import subprocess
     import sys
