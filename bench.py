@@ -233,6 +233,14 @@ def run_sharded(args):
     dist.broadcast_object_list(obj, src=0)
     starts = mx.slab_row_starts(P, world)
     S = mx.Shard(H, rank, world, starts, nccl_id=obj[0])
+    # NCCL communicator of this rank is up: log it and count the ranks that got there
+    print(f"[bench rank {rank}/{world}] NCCL communicator ready on cuda:{local} "
+          f"(rows {S.row_begin}..{S.row_end}, fused Arnoldi exchange {bool(getattr(S, 'fused', False))})",
+          file=sys.stderr, flush=True)
+    ready = torch.ones(1)
+    dist.all_reduce(ready)
+    nccl_ranks = int(ready.item())
+    assert nccl_ranks == world, (nccl_ranks, world)
     lo, hi = S.row_begin, S.row_end
     cfg = mx.KrylovConfig(restart=RESTART, max_iters=500, rel_tol=RTOL)
     dev = torch.device("cuda", local)
@@ -306,12 +314,31 @@ def run_sharded(args):
                         "d2h_bytes_per_step": int(nb.item()),
                         "path": "Shard.solve -> mgrx_shard_solve (C ABI) per rank, pinned host slices"},
                 "gpu_launches": launches, "roofline": None, "solve_roofline": solve_roof, "cpu_baseline": None,
-                "fused_sharded_arnoldi": bool(getattr(S, "fused", False)),
+                "fused_sharded_arnoldi": bool(getattr(S, "fused", False)), "nccl_ranks": nccl_ranks,
                 "clocks": clk.summary()}
         print(json.dumps(line))
     S.close()
     dist.barrier()
     dist.destroy_process_group()
+
+
+def spawn_ranks(args):
+    """`python bench.py --gpus N` without a launcher: start N ranks (one per
+    GPU) through torch.distributed.run on 127.0.0.1 and pass rank 0's line
+    through. Fails loudly when fewer than N GPUs are visible."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} requested but {have} CUDA device(s) visible")
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    rc = subprocess.call(cmd)
+    if rc:
+        raise SystemExit(rc)
 
 
 def main():
@@ -336,6 +363,10 @@ def main():
         STRATEGY = args.strategy
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}")
 
     import numpy as np
     import torch

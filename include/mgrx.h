@@ -51,12 +51,24 @@ typedef struct mgrx_ctx mgrx_ctx;
 typedef struct mgrx_mat mgrx_mat;
 typedef struct mgrx_hier mgrx_hier;
 
-/* KrylovConfig, proj/include/mgrkit/krylov.hpp:14-19 */
+/* KrylovConfig, proj/include/mgrkit/krylov.hpp:14-19, plus the choice of
+ * orthogonalisation (a zero-initialised struct gets the default):
+ *   MGRX_ORTHO_DEFAULT / MGRX_ORTHO_CGS2  low-synchronisation lagged CGS2
+ *       (two basis sweeps and two reductions per step, device-resident
+ *       restart cycle); matches the reference to the north_star bar
+ *       (history 1e-10 relative, iterations +-1);
+ *   MGRX_ORTHO_MGS  the reference's modified Gram-Schmidt with conditional
+ *       re-orthogonalisation (proj/src/krylov.cpp:80-101), bitwise
+ *       reproducible against the CPU oracle. */
+#define MGRX_ORTHO_DEFAULT 0
+#define MGRX_ORTHO_MGS 1
+#define MGRX_ORTHO_CGS2 2
 typedef struct mgrx_krylov {
   int restart;
   int max_iters;
   double rel_tol;
   double abs_tol;
+  int ortho;
 } mgrx_krylov;
 
 /* SolveReport, proj/include/mgrkit/krylov.hpp:21-28, plus timings. The
@@ -115,6 +127,14 @@ MGRX_API int mgrx_apply(mgrx_hier* h, const double* v, double* z, int on_device)
 #define MGRX_ZERO_GUESS 2
 MGRX_API int mgrx_solve(mgrx_hier* h, const double* b, double* x, const mgrx_krylov* cfg,
                mgrx_report* report, int flags);
+
+/* AmgSetupInfo of an AMG hierarchy (proj/include/mgrkit/amg.hpp:35-39):
+ * which = -1 the MGR coarse solver's AMG, l >= 0 the F-relaxation AMG of MGR
+ * level l. level_sizes receives up to cap sizes (nlevels = full count);
+ * fallback_rows = interpolation rows on the diagonally scaled fallback
+ * (proj/src/amg.cpp:115-122); truncated = coarsening stalled. */
+MGRX_API int mgrx_amg_info(mgrx_hier* h, int which, int* nlevels, int* level_sizes, int cap,
+                           long long* fallback_rows, int* truncated);
 
 /* Parity dumps. path grammar:
  *   mgr.<l>.{A,P,R,F,C,frelax.dinv}   mgr.coarse.A

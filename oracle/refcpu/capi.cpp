@@ -113,6 +113,7 @@ extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
 void ref_set_threads(int n) { set_threads(n); }
+void ref_set_dot_order(int m) { set_dot_order(m); }
 
 int ref_spmv(int n, int ncols, const int* ptr, const int* col, const double* val, const double* x,
              double* y) {
@@ -244,6 +245,23 @@ int ref_info(void* hp, int* mgr_levels, int* coarse_amg_levels, int* frelax_amg_
     const AmgHierarchy* a = h->H.levels[l].f_relax.amg_hierarchy();
     frelax_amg_levels[l] = a ? a->num_levels() : 0;
   }
+  return 0;
+}
+
+int ref_amg_info(void* hp, int which, int* nlevels, int* level_sizes, int cap, long long* fallback_rows,
+                 int* truncated) {
+  auto* h = static_cast<RefHandle*>(hp);
+  const AmgHierarchy* a = nullptr;
+  if (which < 0) a = h->H.coarse_amg ? h->H.coarse_amg.get() : nullptr;
+  else if (which < h->H.num_reduction_levels()) a = h->H.levels[which].f_relax.amg_hierarchy();
+  if (!a) {
+    g_err = "no AMG hierarchy";
+    return 2;
+  }
+  *nlevels = static_cast<int>(a->info.level_sizes.size());
+  for (int i = 0; i < *nlevels && i < cap; ++i) level_sizes[i] = a->info.level_sizes[i];
+  *fallback_rows = a->info.interp_fallback_rows;
+  *truncated = a->info.truncated ? 1 : 0;
   return 0;
 }
 

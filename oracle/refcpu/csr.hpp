@@ -115,6 +115,10 @@ Vec sub(const Vec& a, const Vec& b);
 // Number of OpenMP threads used by the row-parallel kernels (1 = faithful
 // serial reference). Results never depend on it.
 void set_threads(int n);
+// inner-product order of dot()/norm(): 0 canonical (device) tree, 1 sequential,
+// 2 Eigen SSE2 packet order (see csr_ops.cpp)
+void set_dot_order(int m);
+int dot_order();
 int threads();
 
 }  // namespace refcpu

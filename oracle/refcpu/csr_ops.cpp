@@ -407,7 +407,61 @@ Real fold_block(const Real* lane) {  // kRT lane values -> block value
 }
 }  // namespace
 
+namespace {
+int g_dot_order = 0;  // 0 canonical tree, 1 sequential, 2 Eigen SSE2 packet order
+}  // namespace
+
+void set_dot_order(int m) { g_dot_order = (m >= 0 && m <= 2) ? m : 0; }
+int dot_order() { return g_dot_order; }
+
+// Independent reduction orders (dot_order 1 and 2), used by the parity tests
+// to check the north_star tolerance bar against an order the device does NOT
+// share:
+//  1: one accumulator, left to right (the literal loop of proj/src/krylov.cpp:
+//     84-97 written as `for i: s += a_i b_i`);
+//  2: the order of Eigen 3.3/3.4's vectorised redux at the x86-64 baseline the
+//     reference builds for (SSE2, 2 doubles per packet; proj/CMakeLists.txt:30
+//     sets no -march): two packet accumulators over alternating packets, the
+//     two packets added lane-wise, one more packet if 2 remain, the two lanes
+//     added, then the scalar tail left to right. Restated from knowledge of
+//     Eigen's Redux.h (Eigen is not in this container), hence "unpinned".
+static Real dot_sequential(const Vec& a, const Vec& b) {
+  Real s = 0.0;
+  for (size_t i = 0; i < a.size(); ++i) s = s + a[i] * b[i];
+  return s;
+}
+
+static Real dot_eigen_sse2(const Vec& a, const Vec& b) {
+  const size_t n = a.size();
+  if (n < 2) return n ? a[0] * b[0] : 0.0;
+  const size_t aligned = n - n % 2;  // packets of 2 doubles
+  Real p0[2] = {a[0] * b[0], a[1] * b[1]};
+  size_t i = 2;
+  if (aligned >= 4) {
+    Real p1[2] = {a[2] * b[2], a[3] * b[3]};
+    const size_t end2 = aligned - aligned % 4;
+    for (i = 4; i < end2; i += 4) {
+      p0[0] = p0[0] + a[i] * b[i];
+      p0[1] = p0[1] + a[i + 1] * b[i + 1];
+      p1[0] = p1[0] + a[i + 2] * b[i + 2];
+      p1[1] = p1[1] + a[i + 3] * b[i + 3];
+    }
+    p0[0] = p0[0] + p1[0];
+    p0[1] = p0[1] + p1[1];
+    if (end2 < aligned) {
+      p0[0] = p0[0] + a[end2] * b[end2];
+      p0[1] = p0[1] + a[end2 + 1] * b[end2 + 1];
+    }
+    i = aligned;
+  }
+  Real s = p0[0] + p0[1];
+  for (; i < n; ++i) s = s + a[i] * b[i];
+  return s;
+}
+
 Real dot(const Vec& a, const Vec& b) {
+  if (g_dot_order == 1) return dot_sequential(a, b);
+  if (g_dot_order == 2) return dot_eigen_sse2(a, b);
   const int64_t n = static_cast<int64_t>(a.size());
   const int64_t stride = static_cast<int64_t>(kRB) * kRT;
   std::vector<Real> part(kRB);

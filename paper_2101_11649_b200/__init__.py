@@ -42,7 +42,16 @@ class MgrxInvalidArgument(MgrxError, ValueError):
 
 class _Krylov(C.Structure):
     _fields_ = [("restart", C.c_int), ("max_iters", C.c_int), ("rel_tol", C.c_double),
-                ("abs_tol", C.c_double)]
+                ("abs_tol", C.c_double), ("ortho", C.c_int)]
+
+
+_ORTHO = {"default": 0, "mgs": 1, "cgs2": 2}
+
+
+def _krylov(cfg) -> "_Krylov":
+    if cfg.ortho not in _ORTHO:
+        raise MgrxInvalidArgument(INVALID_ARGUMENT, f"gmres: unknown orthogonalisation '{cfg.ortho}'")
+    return _Krylov(cfg.restart, cfg.max_iters, cfg.rel_tol, cfg.abs_tol, _ORTHO[cfg.ortho])
 
 
 class _Report(C.Structure):
@@ -82,6 +91,8 @@ def lib() -> C.CDLL:
         L.mgrx_dump.argtypes = [vp, C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                 C.POINTER(C.c_int), C.POINTER(C.c_longlong), vp, vp, vp]
         L.mgrx_info.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_int]
+        L.mgrx_amg_info.argtypes = [vp, C.c_int, C.POINTER(C.c_int), vp, C.c_int, C.POINTER(C.c_longlong),
+                                    C.POINTER(C.c_int)]
         L.mgrx_time_kernel.argtypes = [vp, C.c_char_p, C.c_int, C.POINTER(C.c_double),
                                        C.POINTER(C.c_double)]
         L.mgrx_nccl_unique_id.argtypes = [C.c_char_p]
@@ -192,11 +203,15 @@ class Matrix:
 
 @dataclass
 class KrylovConfig:
-    """proj/include/mgrkit/krylov.hpp:14-19 (same defaults)."""
+    """proj/include/mgrkit/krylov.hpp:14-19 (same defaults), plus `ortho`:
+    "default"/"cgs2" the low-synchronisation lagged CGS2 Arnoldi (north_star
+    tolerance parity), "mgs" the reference's modified Gram-Schmidt (bitwise
+    against the oracle)."""
     restart: int = 50
     max_iters: int = 500
     rel_tol: float = 1e-7
     abs_tol: float = 0.0
+    ortho: str = "default"
 
 
 @dataclass
@@ -277,7 +292,7 @@ class Hierarchy:
         else:
             np.copyto(out, np.asarray(x, dtype=np.float64).reshape(-1))
         rep, hist = self._report(history_cap)
-        k = _Krylov(cfg.restart, cfg.max_iters, cfg.rel_tol, cfg.abs_tol)
+        k = _krylov(cfg)
         _check(lib().mgrx_solve(self._h, _ptr(b), _ptr(out), C.byref(k), C.byref(rep), flags))
         return out, self._to_report(rep, hist)
 
@@ -285,7 +300,7 @@ class Hierarchy:
                      history_cap: int = 4096) -> SolveReport:
         cfg = cfg or KrylovConfig()
         rep, hist = self._report(history_cap)
-        k = _Krylov(cfg.restart, cfg.max_iters, cfg.rel_tol, cfg.abs_tol)
+        k = _krylov(cfg)
         _check(lib().mgrx_solve(self._h, C.c_void_p(b_ptr), C.c_void_p(x_ptr), C.byref(k), C.byref(rep), 1))
         return self._to_report(rep, hist)
 
@@ -309,6 +324,15 @@ class Hierarchy:
         _check(lib().mgrx_info(self._h, C.byref(m), C.byref(c), fr, 64))
         return {"mgr_levels": m.value, "coarse_amg_levels": c.value,
                 "frelax_amg_levels": [fr[i] for i in range(m.value)]}
+
+    def amg_info(self, which: int = -1) -> dict:
+        """AmgSetupInfo (proj/include/mgrkit/amg.hpp:35-39) of the MGR coarse
+        AMG (which=-1) or of MGR level `which`'s F-relaxation AMG."""
+        nl, fb, tr = C.c_int(), C.c_longlong(), C.c_int()
+        sizes = np.zeros(64, np.int32)
+        _check(lib().mgrx_amg_info(self._h, which, C.byref(nl), _ptr(sizes), 64, C.byref(fb), C.byref(tr)))
+        return {"level_sizes": sizes[:min(nl.value, 64)].tolist(), "interp_fallback_rows": fb.value,
+                "truncated": bool(tr.value)}
 
     def dump(self, path: str):
         """CSR -> (ptr, col, val, shape); int list -> int32 array; vector -> float64 array."""
@@ -421,7 +445,7 @@ class Shard:
         else:
             np.copyto(out, np.asarray(x, dtype=np.float64).reshape(-1))
         rep, hist = Hierarchy._report(history_cap)
-        k = _Krylov(cfg.restart, cfg.max_iters, cfg.rel_tol, cfg.abs_tol)
+        k = _krylov(cfg)
         _check(lib().mgrx_shard_solve(self._h, _ptr(b), _ptr(out), C.byref(k), C.byref(rep), flags))
         return out, Hierarchy._to_report(rep, hist)
 
@@ -429,7 +453,7 @@ class Shard:
                      history_cap: int = 4096) -> SolveReport:
         cfg = cfg or KrylovConfig()
         rep, hist = Hierarchy._report(history_cap)
-        k = _Krylov(cfg.restart, cfg.max_iters, cfg.rel_tol, cfg.abs_tol)
+        k = _krylov(cfg)
         _check(lib().mgrx_shard_solve(self._h, C.c_void_p(b_ptr), C.c_void_p(x_ptr), C.byref(k), C.byref(rep),
                                       1 | (2 if zero_guess else 0)))
         return Hierarchy._to_report(rep, hist)

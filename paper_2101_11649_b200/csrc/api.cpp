@@ -141,7 +141,7 @@ void prepare_probe(mgrx_hier* h, const std::string& w, std::function<void()>& fn
     // v_0..v_k streamed once per pass, v_{k+1} out.
     const int n = h->A.rows;
     const int k = std::stoi(w.substr(8));
-    if (h->ws.n != n) {
+    if (h->ws.n != n || h->ws.m < 30) {
       h->ws.ensure(n, 30, s);
       MGRX_CK(cudaMemsetAsync(h->ws.V.get(), 0, sizeof(double) * static_cast<size_t>(n) * 31, s));
       MGRX_CK(cudaMemsetAsync(h->ws.w.get(), 0, sizeof(double) * n, s));
@@ -152,6 +152,22 @@ void prepare_probe(mgrx_hier* h, const std::string& w, std::function<void()>& fn
     if (!arnoldi_probe(n, k, dbg, *ws, s)) throw InvalidArgument("probe: fused Arnoldi kernel unavailable");
     fn = [=] { arnoldi_probe(n, k, dbg, *ws, s); };
     bytes = 8.0 * n * (2.0 + 2.0 * (k + 1));
+    return;
+  }
+  if (w.rfind("cgs2", 0) == 0) {
+    // low-sync Arnoldi step k (lowsync.cu): cgs2.<k> both sweeps,
+    // cgs2dots.<k> sweep A, cgs2upd.<k> sweep B. Bytes: each sweep reads
+    // V_{0..k-1}, U and w once; sweep B writes v_k and U: 16 n (k+3) per step.
+    const int n = h->A.rows;
+    const size_t dot = w.find('.');
+    const std::string kind = w.substr(0, dot);
+    const int k = std::stoi(w.substr(dot + 1));
+    const int which = kind == "cgs2dots" ? 1 : kind == "cgs2upd" ? 2 : 3;
+    GmresWork* ws = &h->ws;
+    if (!lowsync_probe(n, k, *ws, s, which)) throw InvalidArgument("probe: no low-sync step " + w);
+    fn = [=] { lowsync_probe(n, k, *ws, s, which); };
+    const double sweep = 8.0 * n * (k + 2);
+    bytes = (which & 1 ? sweep : 0.0) + (which & 2 ? sweep + 16.0 * n : 0.0);
     return;
   }
   if (w == "spmv.A") {
@@ -385,6 +401,8 @@ int mgrx_solve(mgrx_hier* h, const double* b, double* x, const mgrx_krylov* cfg,
     k.max_iters = cfg->max_iters;
     k.rel_tol = cfg->rel_tol;
     k.abs_tol = cfg->abs_tol;
+    k.ortho = cfg->ortho;
+    if (k.ortho < 0 || k.ortho > 2) throw InvalidArgument("gmres: unknown orthogonalisation");
     const long long l0 = g_launches;
     const double* db = b;
     double* dx = x;
@@ -399,8 +417,9 @@ int mgrx_solve(mgrx_hier* h, const double* b, double* x, const mgrx_krylov* cfg,
     }
     MgrHier* H = &h->H;
     const DevOp prec = [H](const double* in, double* out, cudaStream_t st) { H->apply_graph(in, out, st); };
+    const DevOp prec_rec = [H](const double* in, double* out, cudaStream_t st) { H->apply(in, out, st); };
     EventTimer t(s);
-    GmresResult r = gmres_device(h->A, db, dx, k, prec, h->ws, s);
+    GmresResult r = gmres_device(h->A, db, dx, k, prec, h->ws, s, prec_rec);
     const double solve_s = t.stop();
     h->H.check(s);
     if (!on_device) {
@@ -431,6 +450,21 @@ int mgrx_info(mgrx_hier* h, int* mgr_levels, int* coarse_amg_levels, int* frelax
       const auto& amg = h->H.levels[l].f_relax.amg;
       frelax_amg_levels[l] = amg ? static_cast<int>(amg->levels.size()) : 0;
     }
+    return MGRX_OK;
+  });
+}
+
+int mgrx_amg_info(mgrx_hier* h, int which, int* nlevels, int* level_sizes, int cap, long long* fallback_rows,
+                  int* truncated) {
+  return guarded([&] {
+    const AmgHier* amg = nullptr;
+    if (which < 0) amg = h->H.coarse_amg.get();
+    else if (which < static_cast<int>(h->H.levels.size())) amg = h->H.levels[which].f_relax.amg.get();
+    if (!amg) throw InvalidArgument("mgrx_amg_info: no AMG hierarchy at " + std::to_string(which));
+    *nlevels = static_cast<int>(amg->level_sizes.size());
+    for (int i = 0; i < *nlevels && i < cap; ++i) level_sizes[i] = amg->level_sizes[i];
+    *fallback_rows = amg->fallback_rows;
+    *truncated = amg->truncated ? 1 : 0;
     return MGRX_OK;
   });
 }
@@ -685,6 +719,8 @@ int mgrx_shard_solve(mgrx_shard* sd, const double* b, double* x, const mgrx_kryl
     k.max_iters = cfg->max_iters;
     k.rel_tol = cfg->rel_tol;
     k.abs_tol = cfg->abs_tol;
+    k.ortho = cfg->ortho;
+    if (k.ortho < 0 || k.ortho > 2) throw InvalidArgument("gmres: unknown orthogonalisation");
     const long long l0 = g_launches;
     const double* db = b;
     double* dx = x;

@@ -65,6 +65,12 @@ void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
   MGRX_CK(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
 }
 
+// Kernel attributes (dynamic shared memory opt-in, cluster flags) and SM
+// counts are per device: one-time setup is keyed by (key, current device),
+// so a second context on another GPU in the same process gets its own.
+bool first_on_device(const void* key);
+int device_sms();  // SM count of the current device (cached per device)
+
 // Process-wide launch counter (the bench reports kernels launched in the
 // timed region; graph replays add their node count).
 extern long long g_launches;

@@ -8,6 +8,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 
 #include "krylov.cuh"
 #include "relax.cuh"
@@ -518,7 +520,10 @@ __device__ __noinline__ void cross_rank(const ArnoldiArgs& a, unsigned phase, do
   __shared__ double m1[kMboxRanks], m2[kMboxRanks];  // this phase's rank partials
   const int T = threadIdx.x;
   const int slot = static_cast<int>(phase % kMboxPhases);
-  const unsigned long long tag = a.epoch + phase + 1;
+  // once this rank has flagged a timeout it publishes the poison tag, so a
+  // peer that is still waiting flags the step too (no rank folds stale values)
+  const bool poisoned = *reinterpret_cast<volatile double*>(a.err) != 0.0;
+  const unsigned long long tag = poisoned ? kMboxPoison : a.epoch + phase + 1;
   if (blockIdx.x == 0 && T < a.nranks) {
     double* dst = a.peers[T] + (static_cast<size_t>(slot) * kMboxRanks + a.rank) * 4;
     dst[0] = t1;
@@ -533,7 +538,11 @@ __device__ __noinline__ void cross_rank(const ArnoldiArgs& a, unsigned phase, do
     bool late = false;
     for (unsigned it = 0;; ++it) {
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(src + 2) : "memory");
-      if (v == tag) break;
+      if (v == tag && !poisoned) break;
+      if (v == kMboxPoison) {
+        late = true;
+        break;
+      }
       // a silent peer: give up after ~2 s (or at once when a previous phase
       // already did) and flag the step; the host discards it
       if ((it & 1023u) == 1023u &&
@@ -547,7 +556,14 @@ __device__ __noinline__ void cross_rank(const ArnoldiArgs& a, unsigned phase, do
     asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(p2) : "l"(src + 1) : "memory");
     m1[T] = p1;
     m2[T] = p2;
-    if (late) *a.err = 1.0;
+    if (late) {
+      *a.err = 1.0;
+      // poison this phase's slot of every peer as well (CTA 0 only)
+      if (blockIdx.x == 0) {
+        double* dst = a.peers[T] + (static_cast<size_t>(slot) * kMboxRanks + a.rank) * 4;
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst + 2), "l"(kMboxPoison) : "memory");
+      }
+    }
   }
   __syncthreads();
   double v1 = m1[0], v2 = m2[0];
@@ -745,21 +761,24 @@ bool arnoldi_fits(K kern, int threads) {
   return occ >= 1;
 }
 
+// Per device (kernel attributes and SM counts are per device).
 const ArnoldiMode& arnoldi_mode() {
-  static const ArnoldiMode m = [] {
-    ArnoldiMode r;
-    if (const char* v = std::getenv("MGRX_ARNOLDI")) r.mode = std::atoi(v);
-    if (const char* v = std::getenv("MGRX_ARNOLDI_U")) r.u = std::atoi(v);
-    if (r.u != 4 && r.u != 6) r.u = 8;
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms != kAB) return r;
+  static std::mutex mu;
+  static std::map<int, ArnoldiMode> modes;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = modes.find(dev);
+  if (it != modes.end()) return it->second;
+  ArnoldiMode r;
+  if (const char* v = std::getenv("MGRX_ARNOLDI")) r.mode = std::atoi(v);
+  if (const char* v = std::getenv("MGRX_ARNOLDI_U")) r.u = std::atoi(v);
+  if (r.u != 4 && r.u != 6) r.u = 8;
+  if (device_sms() == kAB) {
     r.fits1 = arnoldi_fits(k_arnoldi, kAT);
     r.fits2 = arnoldi_fits(r.u == 4 ? k_arnoldi2<4> : r.u == 6 ? k_arnoldi2<6> : k_arnoldi2<8>, kAT2);
-    return r;
-  }();
-  return m;
+  }
+  return modes.emplace(dev, r).first->second;
 }
 
 // MGRX_ARNOLDI_MERGE=0: never merge the pass-1 norm phase with pass 2's
@@ -828,12 +847,10 @@ void arnoldi_sharded(int n, int k, int dbg, const ArnoldiPeers& pe, GmresWork& w
   aa.err = S + m + 3;
   void* args[] = {&aa};
   const ArnoldiMode& md = arnoldi_mode();
-  static const bool attr = [&] {
+  if (first_on_device(reinterpret_cast<const void*>(k_arnoldi2<4, true>))) {
     const int bytes = kAMaxSlots * kAT * static_cast<int>(sizeof(double));
     MGRX_CK(cudaFuncSetAttribute(k_arnoldi2<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    return true;
-  }();
-  (void)attr;
+  }
   (void)md;
   MGRX_CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_arnoldi2<4, true>), dim3(kAB), dim3(kAT2), args,
                                       static_cast<size_t>(slots) * kAT * sizeof(double), s));
@@ -949,10 +966,12 @@ bool self_exchange() {
 }
 
 GmresResult gmres_device(const DCsr& A, const double* b, double* x, const KrylovSpec& cfg,
-                         const DevOp& precond, GmresWork& ws, cudaStream_t s) {
-  StepProf prof;
+                         const DevOp& precond, GmresWork& ws, cudaStream_t s, const DevOp& precond_capture) {
   const int n = A.rows;
   if (cfg.restart < 1) throw InvalidArgument("gmres: restart must be >= 1");
+  if (cfg.ortho != kOrthoMgs && lowsync_supported(n, cfg.restart))
+    return gmres_lowsync(A, b, x, cfg, precond, precond_capture, ws, s);
+  StepProf prof;
   const int m = cfg.restart;
   ws.ensure(n, m, s);
   double* S = ws.scal.get();

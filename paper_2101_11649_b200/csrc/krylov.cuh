@@ -22,6 +22,41 @@ struct GmresResult {
 
 using DevOp = std::function<void(const double* in, double* out, cudaStream_t s)>;
 
+// Low-synchronisation (lagged CGS2) Arnoldi state, device resident
+// (lowsync.cu). flags: stopping reasons of the current restart cycle.
+constexpr int kLsConverged = 1, kLsHappy = 2, kLsNonFinite = 4, kLsCycleEnd = 8;
+constexpr int kLsMaxRestart = 512;
+struct LsState {
+  double bnorm, target;
+  int k;           // next step index of the cycle (= finalised columns + 1)
+  int steps;       // steps done in this cycle
+  int iters_left;  // step budget of this cycle
+  int flags;
+  double gamma, beta;  // last sweep-A normaliser, last preliminary subdiagonal
+  double gt0, gt1;     // tentatively rotated g_k, g_{k+1} of the last step
+};
+
+struct LsWork {
+  int n = 0, m = 0, ldv = 0, G = 0;
+  DVec<double> V, U, part, part2, dbl;
+  DVec<unsigned> ticket;
+  DVec<LsState> st;
+  LsState* hst = nullptr;  // pinned mirror
+  cudaGraphExec_t exec = nullptr;  // one restart cycle (conditional WHILE node)
+  struct Key {
+    const void* w = nullptr;
+    const void* z = nullptr;
+    const void* A = nullptr;
+  } exec_key;
+  long long body_nodes = 0;
+  bool graph_failed = false;
+  void ensure(int n, int m, cudaStream_t s);
+  LsWork() = default;
+  LsWork(const LsWork&) = delete;
+  LsWork& operator=(const LsWork&) = delete;
+  ~LsWork();
+};
+
 struct GmresWork {
   int n = 0, m = 0;
   DVec<double> V, w, r, z, u;
@@ -32,13 +67,24 @@ struct GmresWork {
 
   std::vector<double> hscal;
   double* hpinned = nullptr;
+  LsWork ls;
   void ensure(int n, int m, cudaStream_t s);
   ~GmresWork();
 };
 
-// A x = b with x0 in x; all vectors are device pointers.
+// A x = b with x0 in x; all vectors are device pointers. cfg.ortho selects
+// the orthogonalisation: kOrthoMgs the reference's MGS (bitwise against the
+// oracle), otherwise the lagged CGS2 of lowsync.cu. precond_capture (may be
+// empty): the same operator as precond in a form that can be recorded into
+// a CUDA graph (no graph launches inside).
 GmresResult gmres_device(const DCsr& A, const double* b, double* x, const KrylovSpec& cfg,
-                         const DevOp& precond, GmresWork& ws, cudaStream_t s);
+                         const DevOp& precond, GmresWork& ws, cudaStream_t s,
+                         const DevOp& precond_capture = DevOp());
+GmresResult gmres_lowsync(const DCsr& A, const double* b, double* x, const KrylovSpec& cfg,
+                          const DevOp& precond, const DevOp& precond_capture, GmresWork& ws, cudaStream_t s);
+bool lowsync_supported(int n, int m);
+// Probe: the two sweeps of one low-sync step at index k (which: 1 sweep A, 2 sweep B, 3 both).
+int lowsync_probe(int n, int k, GmresWork& ws, cudaStream_t s, int which);
 
 // One fused MGS step (w -= h*vprev; a.w) for the roofline probe.
 void mgs_probe(int n, double* w, const double* vprev, const double* h, const double* a, GmresWork& ws,
@@ -69,6 +115,9 @@ void basis_combine(int n, int k, const double* V, const double* y, double* u, cu
 // sets S[m + 3] = 1 (the caller falls back / throws).
 constexpr int kMboxRanks = 8, kMboxPhases = 64;
 constexpr int kMboxDoubles = kMboxPhases * kMboxRanks * 4;
+// published instead of a phase tag once a rank has timed out: every peer
+// that reads it flags the step as well
+constexpr unsigned long long kMboxPoison = ~0ull;
 struct ArnoldiPeers {
   int nranks = 1, rank = 0;
   double* mbox = nullptr;

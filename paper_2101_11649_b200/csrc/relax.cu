@@ -993,7 +993,7 @@ void gs_sweep(const DCsr& A, const GsSchedule& sch, const double* d, const doubl
 }
 
 void gs_bind_scratch(GsScratch& scr, cudaStream_t s) {
-  static const bool attrs = [] {
+  if (first_on_device(reinterpret_cast<const void*>(&gs_bind_scratch))) {
     MGRX_CK(cudaFuncSetAttribute(k_gs_small<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmallSmem)));
     MGRX_CK(cudaFuncSetAttribute(k_gs_small<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmallSmem)));
     MGRX_CK(cudaFuncSetAttribute(k_gs_pipe<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kPipeSmem)));
@@ -1007,9 +1007,7 @@ void gs_bind_scratch(GsScratch& scr, cudaStream_t s) {
     MGRX_CK(cudaFuncSetAttribute(k_gs<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     MGRX_CK(cudaFuncSetAttribute(k_gs<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     MGRX_CK(cudaFuncSetAttribute(k_gs<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    return true;
-  }();
-  (void)attrs;
+  }
   if (scr.ticket_err.size() < 2) {
     scr.ticket_err.alloc(2, s);
     scr.ticket_err.zero();

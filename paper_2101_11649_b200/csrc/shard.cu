@@ -580,13 +580,18 @@ ArnoldiPeers Shard::peers_arg() {
 
 void Shard::setup_fused() {
   fused = false;
-  if (const char* e = std::getenv("MGRX_SHARD_FUSED"); e && std::atoi(e) == 0) return;
+  const char* fe = std::getenv("MGRX_SHARD_FUSED");
+  if (fe && std::atoi(fe) == 0) return;
   // one rank: the exchange is the identity (k_fold2 of one partial is the
   // partial), so the single-GPU fused kernel is the same computation
   if (c.size == 1) {
     fused = arnoldi_sharded_ok(spaces.front().own);
     return;
   }
+  // multi-rank in-kernel mailbox exchange: opt-in (MGRX_SHARD_FUSED=1) until
+  // a multi-GPU run has validated it; the default sharded solve is the
+  // low-synchronisation GMRES with two all-gathers per step
+  if (!(fe && std::atoi(fe) == 1)) return;
   // ranks of the local comm share one device: the in-kernel exchange needs
   // every rank's persistent kernel resident at once, i.e. one GPU per rank
   if (c.size < 2 || c.size > kMboxRanks || std::string(comm->kind()) != "nccl") return;

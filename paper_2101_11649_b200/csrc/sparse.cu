@@ -10,6 +10,10 @@
 
 #include "sparse.cuh"
 
+#include <map>
+#include <mutex>
+#include <set>
+
 namespace mgrx {
 
 bool pdl_enabled() {
@@ -21,6 +25,30 @@ bool pdl_enabled() {
 }
 
 long long g_launches = 0;
+
+bool first_on_device(const void* key) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> seen;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  return seen.insert({key, dev}).second;
+}
+
+int device_sms() {
+  static std::mutex mu;
+  static std::map<int, int> sms;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = sms.find(dev);
+  if (it != sms.end()) return it->second;
+  int v = 0;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  if (v <= 0) v = 148;
+  sms[dev] = v;
+  return v;
+}
 
 // ============================================================================
 // primitives
@@ -758,14 +786,11 @@ int staged_geom() {
 }
 template <class Gm, class Epi, class Xs, bool kLong>
 void launch_staged_k(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
-  static bool attr = false;  // per instantiation
-  if (!attr) {
+  if (first_on_device(reinterpret_cast<const void*>(k_spmv_staged<Gm, Epi, Xs, kLong>)))
     MGRX_CK(cudaFuncSetAttribute(k_spmv_staged<Gm, Epi, Xs, kLong>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(Gm::smem)));
-    attr = true;
-  }
   const int per_sm = static_cast<int>(std::min<size_t>(8, 227 * 1024 / Gm::smem));
-  const int grid = std::min(A.nblk, 148 * std::min(per_sm, staged_ctas_per_sm()));
+  const int grid = std::min(A.nblk, device_sms() * std::min(per_sm, staged_ctas_per_sm()));
   launch_pdl(k_spmv_staged<Gm, Epi, Xs, kLong>, grid, Gm::T, Gm::smem, s, A.nblk, A.plan.get(), A.ptr.get(),
              A.col.get(), A.val.get(), x, epi);
   MGRX_LAUNCH_CK();
@@ -783,14 +808,11 @@ void launch_staged(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
 template <class Epi, class Xs>
 void launch_wspec(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
   constexpr size_t smem = 2 * sizeof(StW::Stage) + 32;
-  static bool attr = false;  // per instantiation
-  if (!attr) {
+  if (first_on_device(reinterpret_cast<const void*>(k_spmv_wspec<Epi, Xs>)))
     MGRX_CK(cudaFuncSetAttribute(k_spmv_wspec<Epi, Xs>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
-    attr = true;
-  }
   const int per_sm = static_cast<int>(std::min<size_t>(8, 227 * 1024 / smem));
-  const int grid = std::min(A.nblk, 148 * per_sm);
+  const int grid = std::min(A.nblk, device_sms() * per_sm);
   launch_pdl(k_spmv_wspec<Epi, Xs>, grid, kWsT, smem, s, A.nblk, A.plan.get(), A.ptr.get(), A.col.get(),
              A.val.get(), x, epi);
   MGRX_LAUNCH_CK();

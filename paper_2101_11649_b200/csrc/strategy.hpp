@@ -44,11 +44,17 @@ struct AmgSpec {
   SmootherSpec post{Smoother::hybrid_l1_gs_backward, 1, 1.0, {}, {}, nullptr, false};
 };
 
+// ortho: orthogonalisation of the device GMRES (not part of the reference's
+// KrylovConfig): kOrthoDefault / kOrthoCgs2 the low-synchronisation lagged
+// CGS2 (lowsync.cu), kOrthoMgs the reference's MGS with the conditional
+// re-orthogonalisation (proj/src/krylov.cpp:80-101), bitwise parity mode.
+constexpr int kOrthoDefault = 0, kOrthoMgs = 1, kOrthoCgs2 = 2;
 struct KrylovSpec {
   int restart = 50;
   int max_iters = 500;
   double rel_tol = 1e-7;
   double abs_tol = 0.0;
+  int ortho = kOrthoDefault;
 };
 
 enum class Interp { ideal, jacobi };

@@ -35,6 +35,7 @@ def lib():
         vp = C.c_void_p
         L.ref_last_error.restype = C.c_char_p
         L.ref_set_threads.argtypes = [C.c_int]
+        L.ref_set_dot_order.argtypes = [C.c_int]
         L.ref_spmv.argtypes = [C.c_int, C.c_int, _I32P, _I32P, _F64P, _F64P, _F64P]
         L.ref_setup.argtypes = [C.c_int, _I32P, _I32P, _F64P, _I32P, C.c_int, C.POINTER(C.c_char_p),
                                 vp, C.c_char_p, C.POINTER(vp)]
@@ -48,6 +49,8 @@ def lib():
                                C.POINTER(C.c_int), C.POINTER(C.c_longlong), vp, vp, vp]
         L.ref_info.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_int]
         L.ref_free.argtypes = [vp]
+        L.ref_amg_info.argtypes = [vp, C.c_int, C.POINTER(C.c_int), vp, C.c_int, C.POINTER(C.c_longlong),
+                                   C.POINTER(C.c_int)]
         _lib = L
     return _lib
 
@@ -66,6 +69,16 @@ def _chk(code):
 
 def set_threads(n: int):
     lib().ref_set_threads(n)
+
+
+DOT_ORDERS = {"canonical": 0, "sequential": 1, "eigen_sse2": 2}
+
+
+def set_dot_order(name: str):
+    """Inner-product order of the oracle GMRES: "canonical" (the device's fixed
+    592x256 tree), "sequential" (one accumulator, left to right) or
+    "eigen_sse2" (Eigen's 2-packet SSE2 redux order, restated; unpinned)."""
+    lib().ref_set_dot_order(DOT_ORDERS[name])
 
 
 def spmv(ptr, col, val, x, ncols=None):
@@ -114,6 +127,14 @@ class RefHierarchy:
         lib().ref_info(self._h, C.byref(m), C.byref(c), fr, 64)
         return {"mgr_levels": m.value, "coarse_amg_levels": c.value,
                 "frelax_amg_levels": [fr[i] for i in range(m.value)]}
+
+    def amg_info(self, which=-1):
+        nl, fb, tr = C.c_int(), C.c_longlong(), C.c_int()
+        sizes = np.zeros(64, np.int32)
+        _chk(lib().ref_amg_info(self._h, which, C.byref(nl), C.c_void_p(sizes.ctypes.data), 64, C.byref(fb),
+                                C.byref(tr)))
+        return {"level_sizes": sizes[:min(nl.value, 64)].tolist(), "interp_fallback_rows": fb.value,
+                "truncated": bool(tr.value)}
 
     def dump(self, path):
         kind, rows, cols, nnz = C.c_int(), C.c_int(), C.c_int(), C.c_longlong()

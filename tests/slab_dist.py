@@ -1,4 +1,8 @@
-"""Row-slab distributed MGR-GMRES.
+"""TEST SCAFFOLDING (not the product): a Python/NumPy restatement of the
+row-slab distributed MGR-GMRES, used by the world-size-2
+gloo tests to check the slab algorithm's host logic (partition, halo plans,
+rank-order reductions) on CPU. The product's sharded path is csrc/shard.cu
+(C ABI mgrx_shard_*); it never imports this module.
 
 One process per GPU. The slab-major dof numbering (generators)
 makes every operator of every level a contiguous row block per rank: MGR C/F

@@ -1,5 +1,5 @@
 """Multi-process (world_size 2, gloo, CPU) tests of the row-slab distributed
-solve (paper_2101_11649_b200/dist.py): partition + halo exchange + sharded
+solve (tests/slab_dist.py, a test restatement): partition + halo exchange + sharded
 MGR V-cycle + distributed GMRES against the single-process oracle."""
 import os
 import socket
@@ -34,7 +34,7 @@ def _worker(rank, world, port, q):
         sys.path.insert(0, os.path.join(root, "tests"))
         import json
         import paper_2101_11649_b200 as mx
-        from paper_2101_11649_b200 import dist as D
+        import slab_dist as D
         import refcpu
 
         nx, ny, nz = 6, 5, 8
@@ -91,7 +91,7 @@ def test_sharded_mgr_gmres_matches_oracle(world):
 
 
 def test_slab_ranges_are_contiguous_and_cover():
-    from paper_2101_11649_b200 import dist as D
+    import slab_dist as D
     starts = [0, 10, 20, 30, 40, 50, 60, 70]
     for w in (1, 2, 4, 8):
         rr = D.slab_ranges(80, starts, w)

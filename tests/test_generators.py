@@ -63,3 +63,78 @@ def test_layered_contrast():
     A = sp.csr_matrix((P.val, P.col, P.ptr), shape=(P.n, P.n))
     t = -A[P.partition.labels == 0][:, P.partition.labels == 1].data
     assert t.max() / t.min() > 1e5  # per-layer ln k ~ U(-3,3) plus in-layer sigma 1.5
+
+
+def test_comp_structure():
+    """cfg3/cfg5 generator (BASELINE config 3): 4 unknowns
+    per cell stored as cell-interleaved 4x4 blocks, a 7-point pressure
+    M-matrix with ln T ~ N(0, 2^2), own-cell cross-field couplings only, rho3
+    the strictly cell-local constraint, diagonally dominant density rows,
+    vertical wells of nz elements x 5 dofs numbered after every cell."""
+    nx, ny, nz, wells = 20, 20, 10, 3
+    P = mx.comp_problem(nx, ny, nz, wells=wells)
+    ncell = nx * ny * nz
+    assert P.partition.field_order == ["p", "rho1", "rho2", "rho3", "well"]
+    assert P.n == 4 * ncell + 5 * wells * nz
+    lab = P.partition.labels
+    assert np.array_equal(lab[:4 * ncell], np.tile(np.arange(4), ncell))
+    assert np.all(lab[4 * ncell:] == 4)
+    assert P.meta["well_elements"] == nz and P.meta["dofs_per_well_element"] == 5
+    A = sp.csr_matrix((P.val, P.col, P.ptr), shape=(P.n, P.n)).tocoo()
+    r, c, v = A.row, A.col, A.data
+    cells = (r < 4 * ncell) & (c < 4 * ncell)
+    # cross-field couplings and every rho3 entry stay inside the own cell
+    cross = cells & (lab[r] != lab[c])
+    assert np.all(r[cross] // 4 == c[cross] // 4)
+    rho3 = cells & (lab[r] == 3)
+    assert np.all(r[rho3] // 4 == c[rho3] // 4)
+    # 7-point pressure M-matrix: p-p off-diagonals negative, at most 6 per row
+    pp = cells & (lab[r] == 0) & (lab[c] == 0) & (r != c)
+    assert np.all(v[pp] < 0)
+    assert np.bincount(r[pp] // 4, minlength=ncell).max() == 6
+    lnT = np.log(-v[pp])
+    assert 1.8 < lnT.std() < 2.2 and abs(lnT.mean()) < 0.2
+    d = A.tocsr().diagonal()
+    offpp = np.bincount(r[pp], weights=-v[pp], minlength=P.n)
+    prow = np.arange(0, 4 * ncell, 4)
+    assert np.all(d[prow] >= offpp[prow])
+    # density blocks (same-field entries of the rho1/rho2 rows) strictly diagonally dominant
+    dens = cells & ((lab[r] == 1) | (lab[r] == 2)) & (lab[c] == lab[r]) & (r != c)
+    off = np.bincount(r[dens], weights=np.abs(v[dens]), minlength=P.n)
+    drow = np.where((lab == 1) | (lab == 2))[0]
+    assert np.all(np.abs(d[drow]) > off[drow])
+    # wells couple to well dofs and to their perforated cells' p, rho1, rho2
+    # (never to the rho3 constraint); one perforated cell per element below
+    # the control element (e = 0, the rate-control row with a stored zero
+    # diagonal, like the reference's control rows)
+    wr = r >= 4 * ncell
+    assert np.all((c[wr] >= 4 * ncell) | (lab[c[wr]] <= 2))
+    perf = np.unique(c[wr & (c < 4 * ncell)] // 4)
+    assert perf.size == wells * (nz - 1)
+
+
+def test_frac_structure():
+    """cfg4 generator (BASELINE config 4): 3-D Q1 elasticity on
+    m^3 nodes with the bottom and top node planes fixed, a mid-plane
+    fracture of (m-1)^2 pressure elements whose interior plane nodes are
+    duplicated; node-interleaved displacement dofs with the component as the
+    unknown map; 81 entries on interior displacement rows; symmetric A_uu."""
+    m = 8
+    P = mx.frac_problem(m)
+    assert P.partition.field_order == ["u", "p"]
+    nodes = m * m * (m - 2) + (m - 2) ** 2
+    nfrac = (m - 1) ** 2
+    assert P.n == 3 * nodes + nfrac
+    lab = P.partition.labels
+    assert np.all(lab[:3 * nodes] == 0) and np.all(lab[3 * nodes:] == 1)
+    assert np.array_equal(P.unknown_map[:3 * nodes], np.tile(np.arange(3), nodes))
+    assert np.all(P.unknown_map[3 * nodes:] == 0)
+    A = sp.csr_matrix((P.val, P.col, P.ptr), shape=(P.n, P.n))
+    u = np.arange(3 * nodes)
+    Auu = A[u][:, u]
+    assert abs(Auu - Auu.T).max() == 0.0
+    assert np.all(A.diagonal() > 0)
+    per_row = np.diff(P.ptr)[:3 * nodes]
+    assert per_row.max() == 81 and (per_row == 81).sum() >= 3 * (m - 4) ** 3  # interior: 27 neighbours x 3
+    # full-size point: 64^3 nodes -> 777,357 dofs (DESIGN §7)
+    assert 3 * (64 * 64 * 62 + 62 * 62) + 63 * 63 == 777357

@@ -65,7 +65,7 @@ def test_sharded_apply_and_solve(kind, size):
     zs = _run(shards, lambda s: s.apply(v[s.row_begin:s.row_end]))
     for s, zr in zip(shards, zs):
         assert np.array_equal(zr.view(np.int64), z[s.row_begin:s.row_end].view(np.int64)), (kind, s.row_begin)
-    cfg = mx.KrylovConfig(restart=30, rel_tol=rtol)
+    cfg = mx.KrylovConfig(restart=30, rel_tol=rtol, ortho="mgs")
     x1, r1 = H.solve(P.rhs, None, cfg)
     outs = _run(shards, lambda s: s.solve(P.rhs[s.row_begin:s.row_end], None, cfg))
     reps = [o[1] for o in outs]
@@ -100,7 +100,7 @@ def test_single_rank_shard_equals_global():
     P = mx.mfd_problem(12, 10, 6, "iid")
     H = mx.Hierarchy(mx.Matrix(P.ptr, P.col, P.val), P.partition, mx.load_strategy("mfd_mgr_pi_c1_l1j"))
     S = mx.Shard(H, 0, 1)
-    cfg = mx.KrylovConfig(restart=30, rel_tol=1e-8)
+    cfg = mx.KrylovConfig(restart=30, rel_tol=1e-8, ortho="mgs")
     x1, r1 = H.solve(P.rhs, None, cfg)
     x2, r2 = S.solve(P.rhs, None, cfg)
     assert r2.residual_history == r1.residual_history
@@ -113,7 +113,7 @@ def test_nccl_single_rank():
     P = mx.mfd_problem(10, 10, 5, "iid")
     H = mx.Hierarchy(mx.Matrix(P.ptr, P.col, P.val), P.partition, mx.load_strategy("mfd_mgr_pi_c1_l1j"))
     S = mx.Shard(H, 0, 1, None, nccl_id=mx.nccl_unique_id())
-    cfg = mx.KrylovConfig(restart=30, rel_tol=1e-8)
+    cfg = mx.KrylovConfig(restart=30, rel_tol=1e-8, ortho="mgs")
     x1, r1 = H.solve(P.rhs, None, cfg)
     x2, r2 = S.solve(P.rhs, None, cfg)
     assert r2.residual_history == r1.residual_history
