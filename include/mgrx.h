@@ -185,6 +185,16 @@ MGRX_API int mgrx_local_group_destroy(mgrx_group* g);
  * nccl_id / group when size > 1. */
 MGRX_API int mgrx_shard_create(mgrx_hier* h, int rank, int size, const int* row_starts,
                                const unsigned char* nccl_id, mgrx_group* group, mgrx_shard** out);
+/* Scattered setup (SURVEY §8(e) "build on GPU 0, then scatter"): rank 0
+ * passes the global hierarchy it built (h), every other rank passes NULL and
+ * never holds a global operator. Rank 0 cuts every rank's slabs and halo
+ * plans and sends each rank its plan; small replicated parts (dense coarse
+ * factors, replicated coarse AMG levels) are rebuilt on each rank from their
+ * (small) matrices with the same bit-exact setup. row_starts are required
+ * (size+1 fine-row offsets, the same on every rank). After return rank 0 may
+ * destroy h; the shard does not reference it. Collective over the group. */
+MGRX_API int mgrx_shard_create_scatter(mgrx_ctx* ctx, mgrx_hier* h, int rank, int size, const int* row_starts,
+                                       const unsigned char* nccl_id, mgrx_group* group, mgrx_shard** out);
 MGRX_API int mgrx_shard_rows(mgrx_shard* sd, int* row_begin, int* row_end);
 /* 1 when this shard's GMRES steps use the fused sharded Arnoldi kernel
  * (in-kernel partial exchange over NVLink; enabled after a bitwise

@@ -99,6 +99,7 @@ def lib() -> C.CDLL:
         L.mgrx_local_group_create.argtypes = [C.c_int, C.POINTER(vp)]
         L.mgrx_local_group_destroy.argtypes = [vp]
         L.mgrx_shard_create.argtypes = [vp, C.c_int, C.c_int, vp, C.c_char_p, vp, C.POINTER(vp)]
+        L.mgrx_shard_create_scatter.argtypes = [vp, vp, C.c_int, C.c_int, vp, C.c_char_p, vp, C.POINTER(vp)]
         L.mgrx_shard_rows.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.mgrx_shard_fused.argtypes = [vp, C.POINTER(C.c_int)]
         L.mgrx_shard_apply.argtypes = [vp, vp, vp, C.c_int]
@@ -407,9 +408,15 @@ class Shard:
     owned fine rows [row_begin, row_end); apply / solve on owned slices.
     Collective: every rank of the group makes the same sequence of calls."""
 
-    def __init__(self, H: Hierarchy, rank: int, size: int, row_starts=None, nccl_id: Optional[bytes] = None,
-                 group: Optional[LocalGroup] = None):
-        self.H = H
+    def __init__(self, H: Optional[Hierarchy], rank: int, size: int, row_starts=None,
+                 nccl_id: Optional[bytes] = None, group: Optional[LocalGroup] = None, scatter: bool = False,
+                 ctx: Optional[Context] = None):
+        """scatter=False: every rank passes its replica of the global Hierarchy.
+        scatter=True (mgrx_shard_create_scatter): rank 0 passes the global
+        Hierarchy, the other ranks pass None (and a Context); rank 0 sends
+        every rank its slab plan, no other rank holds a global operator, and
+        rank 0 may drop H afterwards."""
+        self.H = H if not scatter else None
         st = None
         if row_starts is not None:
             st = np.ascontiguousarray(row_starts, dtype=np.int32)
@@ -417,8 +424,17 @@ class Shard:
                 raise MgrxInvalidArgument(INVALID_ARGUMENT, "row_starts must have size+1 entries")
         self._st = st
         self._h = C.c_void_p()
-        _check(lib().mgrx_shard_create(H._h, rank, size, _ptr(st) if st is not None else None,
-                                       nccl_id, group._h if group is not None else None, C.byref(self._h)))
+        g = group._h if group is not None else None
+        if scatter:
+            if st is None:
+                raise MgrxInvalidArgument(INVALID_ARGUMENT, "scatter: row_starts are required")
+            cx = ctx or (H.ctx if H is not None else default_context())
+            self._ctx = cx
+            _check(lib().mgrx_shard_create_scatter(cx._h, H._h if H is not None else None, rank, size, _ptr(st),
+                                                   nccl_id, g, C.byref(self._h)))
+        else:
+            _check(lib().mgrx_shard_create(H._h, rank, size, _ptr(st) if st is not None else None,
+                                           nccl_id, g, C.byref(self._h)))
         b, e = C.c_int(), C.c_int()
         _check(lib().mgrx_shard_rows(self._h, C.byref(b), C.byref(e)))
         self.row_begin, self.row_end = b.value, e.value

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -42,7 +43,8 @@ struct mgrx_group {
 };
 
 struct mgrx_shard {
-  mgrx_hier* h = nullptr;
+  mgrx_ctx* ctx = nullptr;
+  double setup_s = 0.0;    // hierarchy setup (root) + plan / scatter / load
   cudaStream_t stream = nullptr;
   std::unique_ptr<Shard> sh;
   DVec<double> vin, vout;
@@ -654,7 +656,8 @@ int mgrx_shard_create(mgrx_hier* h, int rank, int size, const int* row_starts, c
       cm = make_local_comm(hub, 0);
     }
     auto* sd = new mgrx_shard;
-    sd->h = h;
+    sd->ctx = h->ctx;
+    sd->setup_s = h->setup_s;
     try {
       MGRX_CK(cudaStreamCreateWithFlags(&sd->stream, cudaStreamNonBlocking));
       MGRX_CK(cudaStreamSynchronize(h->ctx->stream));
@@ -663,6 +666,51 @@ int mgrx_shard_create(mgrx_hier* h, int rank, int size, const int* row_starts, c
       const int own = sd->sh->row_end - sd->sh->row_begin;
       sd->vin.alloc(own, sd->stream);
       sd->vout.alloc(own, sd->stream);
+    } catch (...) {
+      delete sd;
+      throw;
+    }
+    *out = sd;
+    return MGRX_OK;
+  });
+}
+
+int mgrx_shard_create_scatter(mgrx_ctx* ctx, mgrx_hier* h, int rank, int size, const int* row_starts,
+                              const unsigned char* nccl_id, mgrx_group* group, mgrx_shard** out) {
+  return guarded([&] {
+    if (!ctx || !out || size < 1 || rank < 0 || rank >= size)
+      throw InvalidArgument("mgrx_shard_create_scatter: bad rank/size");
+    use(ctx);
+    if ((rank == 0) != (h != nullptr))
+      throw InvalidArgument("mgrx_shard_create_scatter: rank 0 (and only rank 0) passes the global hierarchy");
+    if (!row_starts) throw InvalidArgument("mgrx_shard_create_scatter: row starts are required");
+    if ((nccl_id == nullptr) == (group == nullptr) && size > 1)
+      throw InvalidArgument("mgrx_shard_create_scatter: give exactly one of nccl_id and group");
+    const std::vector<int> st(row_starts, row_starts + size + 1);
+    std::unique_ptr<Comm> cm;
+    if (group) {
+      if (group->size != size) throw InvalidArgument("mgrx_shard_create_scatter: group size mismatch");
+      cm = make_local_comm(group->hub, rank);
+    } else if (nccl_id) {
+      cm = make_nccl_comm(nccl_id, rank, size);
+    } else {
+      auto hub = make_local_hub(1);
+      cm = make_local_comm(hub, 0);
+    }
+    auto* sd = new mgrx_shard;
+    sd->ctx = ctx;
+    try {
+      const auto t0 = std::chrono::steady_clock::now();
+      MGRX_CK(cudaStreamCreateWithFlags(&sd->stream, cudaStreamNonBlocking));
+      MGRX_CK(cudaStreamSynchronize(ctx->stream));
+      sd->sh = std::make_unique<Shard>();
+      sd->sh->build_scatter(h ? &h->H : nullptr, h ? &h->A : nullptr, st, std::move(cm), sd->stream);
+      const int own = sd->sh->row_end - sd->sh->row_begin;
+      sd->vin.alloc(own, sd->stream);
+      sd->vout.alloc(own, sd->stream);
+      MGRX_CK(cudaStreamSynchronize(sd->stream));
+      sd->setup_s = (h ? h->setup_s : 0.0) +
+                    std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     } catch (...) {
       delete sd;
       throw;
@@ -690,7 +738,7 @@ int mgrx_shard_fused(mgrx_shard* sd, int* fused) {
 
 int mgrx_shard_apply(mgrx_shard* sd, const double* v, double* z, int on_device) {
   return guarded([&] {
-    use(sd->h->ctx);
+    use(sd->ctx);
     const int n = sd->sh->row_end - sd->sh->row_begin;
     cudaStream_t s = sd->stream;
     if (on_device) {
@@ -710,7 +758,7 @@ int mgrx_shard_solve(mgrx_shard* sd, const double* b, double* x, const mgrx_kryl
   const bool on_device = flags & MGRX_ON_DEVICE;
   const bool zero_guess = flags & MGRX_ZERO_GUESS;
   return guarded([&] {
-    use(sd->h->ctx);
+    use(sd->ctx);
     if (!cfg) throw InvalidArgument("mgrx_shard_solve: null config");
     cudaStream_t s = sd->stream;
     const int n = sd->sh->row_end - sd->sh->row_begin;
@@ -747,7 +795,7 @@ int mgrx_shard_solve(mgrx_shard* sd, const double* b, double* x, const mgrx_kryl
       rep->history_len = static_cast<int>(r.history.size());
       if (rep->history)
         for (int i = 0; i < rep->history_len && i < rep->history_cap; ++i) rep->history[i] = r.history[i];
-      rep->setup_s = sd->h->setup_s;
+      rep->setup_s = sd->setup_s;
       rep->solve_s = solve_s;
       rep->gpu_launches = g_launches - l0;
     }
@@ -757,7 +805,7 @@ int mgrx_shard_solve(mgrx_shard* sd, const double* b, double* x, const mgrx_kryl
 
 int mgrx_shard_destroy(mgrx_shard* sd) {
   return guarded([&] {
-    if (sd) use(sd->h->ctx);
+    if (sd) use(sd->ctx);
     delete sd;
     return MGRX_OK;
   });

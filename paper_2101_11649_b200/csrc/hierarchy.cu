@@ -540,6 +540,7 @@ void AmgHier::setup(const DCsr& A, const AmgSpec& cfg, const std::vector<int>& u
   if (cfg.coarse_size < 1) throw InvalidArgument("amg_setup: coarse_size must be >= 1");
   if (!umap.empty() && static_cast<int>(umap.size()) != A.rows)
     throw InvalidArgument("amg_setup: unknown_map size mismatch");
+  spec = cfg;
   levels.clear();
   level_sizes.clear();
   DCsr Acur = csr_copy(A, s);

@@ -61,6 +61,7 @@ struct AmgLevelD {
 };
 
 struct AmgHier {
+  AmgSpec spec;  // the configuration it was set up with
   std::deque<AmgLevelD> levels;  // deque: smoothers hold pointers to level matrices
   DenseLU coarse;
   std::vector<int> level_sizes;
@@ -79,6 +80,10 @@ struct AmgHier {
  private:
   void vcycle_level(int l, const double* r, double* z, cudaStream_t s);
 };
+
+// spmv plans and the single-CTA tail of a set-up AMG hierarchy (and of its
+// nested smoothers); called once after setup.
+void prepare_amg(AmgHier& h, cudaStream_t s);
 
 struct MgrLevelD {
   DCsr A;

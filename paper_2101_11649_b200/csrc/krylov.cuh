@@ -6,6 +6,7 @@
 #pragma once
 
 #include <functional>
+#include <memory>
 #include <vector>
 
 #include "sparse.cuh"
@@ -39,6 +40,7 @@ struct LsState {
 struct LsWork {
   int n = 0, m = 0, ldv = 0, G = 0;
   DVec<double> V, U, part, part2, dbl;
+  DVec<double> rpart, gath;  // sharded: this rank's sums, all ranks' sums
   DVec<unsigned> ticket;
   DVec<LsState> st;
   LsState* hst = nullptr;  // pinned mirror
@@ -55,6 +57,35 @@ struct LsWork {
   LsWork(const LsWork&) = delete;
   LsWork& operator=(const LsWork&) = delete;
   ~LsWork();
+};
+
+// Host side of one low-sync GMRES over an LsWork (lowsync.cu), shared by the
+// single-GPU solve and the sharded one (shard.cu). The caller runs the
+// preconditioner and the SpMV into w from U(), then step()/step_sharded().
+struct LsArgs;
+class LsDriver {
+ public:
+  using Allgather = std::function<void(const double* in, double* out, int count, cudaStream_t s)>;
+  LsDriver(LsWork& L, int n, int m, double* w);
+  ~LsDriver();
+  double* U() const;  // the next vector (input of M^-1 each step)
+  const LsArgs& args() const;
+  void start_cycle(double bnorm, double target, int iters_left, cudaStream_t s);
+  void step(cudaStream_t s);  // sweep A + sweep B, single GPU
+  // the same with the two reductions completed across ranks: each rank's
+  // sums all-gathered and folded in rank order (every rank gets the same bits)
+  void step_sharded(int nranks, const Allgather& allgather, cudaStream_t s);
+  const LsState& sync_state(cudaStream_t s);
+  // end of a restart cycle: appends its residual estimates to hist, y = the
+  // triangular solve on the rotated H (empty: nothing to add)
+  LsState end_cycle(std::vector<double>& hist, std::vector<double>& y, cudaStream_t s);
+  void combine(const std::vector<double>& y, double* u, cudaStream_t s);  // u = V y (synchronises)
+
+ private:
+  LsWork& L_;
+  int n_, m_;
+  double* w_;
+  std::unique_ptr<LsArgs> args_;
 };
 
 struct GmresWork {

@@ -58,11 +58,6 @@
 #include "relax.cuh"
 
 namespace mgrx {
-namespace {
-
-constexpr int kLT = 256;  // threads per CTA
-constexpr int kLW = kLT / 32;
-constexpr int kLC = 8;    // basis columns per register chunk (16 spills)
 
 struct LsArgs {
   int n, ldv, m, G;
@@ -80,9 +75,17 @@ struct LsArgs {
   double* g;          // rotated rhs, final through index k
   double* coef;       // sweep A -> B: s[0..k), d[0..k] at m.., 1/gamma at 2m+1
   double* hist;       // per-cycle residual estimates (relative)
+  double* rank_part;  // sharded: this rank's folded partials (null: single GPU, fused finish)
   cudaGraphConditionalHandle cond;
   int use_cond;
 };
+
+namespace {
+constexpr int kLT = 256;  // threads per CTA
+constexpr int kLW = kLT / 32;
+constexpr int kLC = 8;    // basis columns per register chunk (16 spills)
+
+
 
 __device__ __forceinline__ unsigned long long pol_last() {
   unsigned long long p;
@@ -211,15 +214,9 @@ __device__ __forceinline__ void dots_chunk(const LsArgs& a, int k, int c0, doubl
 __device__ __forceinline__ double& HR(const LsArgs& a, int i, int j) { return a.Hraw[static_cast<size_t>(j) * (a.m + 1) + i]; }
 __device__ __forceinline__ double& HT(const LsArgs& a, int i, int j) { return a.Hrot[static_cast<size_t>(j) * (a.m + 1) + i]; }
 
-// Last CTA of sweep A: fold the partials (value v: CTAs in index order),
-// finalise column k-1, form the preliminary column k and the sweep-B
-// coefficients.
-__device__ void dots_finish(const LsArgs& a, int k) {
-  extern __shared__ double sm[];  // [2m+2] totals, [m+1] q
-  double* tot = sm;
-  double* q = sm + 2 * a.m + 2;
-  __shared__ double sh_g, sh_e;
-  const int nv = 2 * k + 2;
+// Last CTA of sweep A: fold the per-CTA partials of value v in CTA index
+// order into tot[v] (shared memory).
+__device__ void fold_cta_partials(const LsArgs& a, int nv, double* tot) {
   for (int v = threadIdx.x; v < nv; v += kLT) {
     const double* p = a.part + static_cast<size_t>(v) * a.G;
     double acc = 0.0;
@@ -235,6 +232,13 @@ __device__ void dots_finish(const LsArgs& a, int k) {
     tot[v] = acc;
   }
   __syncthreads();
+}
+
+// From the reduced dots tot[] (s_i at 2i, t_i at 2i+1, alpha at 2k, nu at
+// 2k+1): finalise column k-1, form the preliminary column k and the sweep-B
+// coefficients (one CTA). q: shared scratch of m+1.
+__device__ void coef_math(const LsArgs& a, int k, const double* tot, double* q) {
+  __shared__ double sh_g, sh_e;
   if (threadIdx.x == 0) {
     double ss = 0.0, st = 0.0;
     for (int i = 0; i < k; ++i) {
@@ -271,6 +275,17 @@ __device__ void dots_finish(const LsArgs& a, int k) {
     a.coef[a.m + i] = ti / gam;
   }
   if (threadIdx.x == 0) a.coef[2 * a.m + 1] = 1.0 / gam;
+}
+
+__device__ void dots_finish(const LsArgs& a, int k) {
+  extern __shared__ double sm[];  // [2m+2] totals, [m+1] q
+  double* tot = sm;
+  fold_cta_partials(a, 2 * k + 2, tot);
+  if (a.rank_part) {  // sharded: publish this rank's sums; k_ls_coef finishes
+    for (int v = threadIdx.x; v < 2 * k + 2; v += kLT) a.rank_part[v] = tot[v];
+    return;
+  }
+  coef_math(a, k, tot, sm + 2 * a.m + 2);
 }
 
 // Chunk of nc (1..kLC) columns: one exact instantiation per count; RU keeps
@@ -487,9 +502,34 @@ __global__ void __launch_bounds__(kLT, 1) k_ls_update(LsArgs a) {
   if (threadIdx.x == 0) {
     double b2 = 0.0;
     for (int c = 0; c < a.G; ++c) b2 += __ldcg(a.part2 + c);
-    step_finish(a, k, sqrt(b2));
+    if (a.rank_part) a.rank_part[0] = b2;  // sharded: k_ls_finish completes the step
+    else step_finish(a, k, sqrt(b2));
     a.ticket[1] = 0u;
   }
+}
+
+// Sharded: the ranks' sums (gathered[q * stride + v]) folded in rank order,
+// then the coefficient math (one CTA; every rank computes the same bits).
+__global__ void __launch_bounds__(kLT, 1) k_ls_coef(LsArgs a, const double* __restrict__ gathered, int nranks,
+                                                   int stride) {
+  pdl_enter();
+  extern __shared__ double sm[];
+  double* tot = sm;
+  const int k = a.st->k;
+  for (int v = threadIdx.x; v < 2 * k + 2; v += kLT) {
+    double acc = gathered[v];
+    for (int q = 1; q < nranks; ++q) acc += gathered[static_cast<size_t>(q) * stride + v];
+    tot[v] = acc;
+  }
+  __syncthreads();
+  coef_math(a, k, tot, sm + 2 * a.m + 2);
+}
+
+__global__ void k_ls_finish(LsArgs a, const double* __restrict__ gathered, int nranks, int stride) {
+  pdl_enter();
+  double b2 = gathered[0];
+  for (int q = 1; q < nranks; ++q) b2 += gathered[static_cast<size_t>(q) * stride];
+  step_finish(a, a.st->k, sqrt(b2));
 }
 
 // x-update combination u = V(:, 0..k) y (ld = ldv), j ascending.
@@ -501,13 +541,6 @@ __global__ void k_ls_combine(int n, int ldv, int k, const double* __restrict__ V
   double s = 0.0;
   for (int j = 0; j < k; ++j) s = fma(V[static_cast<size_t>(j) * ldv + i], y[j], s);
   u[i] = s;
-}
-
-int num_sms() {
-  int dev = 0, sms = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return sms > 0 ? sms : 148;
 }
 
 LsArgs make_args(LsWork& L, int n, int m, double* w) {
@@ -559,9 +592,9 @@ void LsWork::ensure(int n_, int m_, cudaStream_t s) {
   n = n_;
   m = m_;
   ldv = (n + 31) / 32 * 32;
-  G = num_sms();
+  G = device_sms();
   V.alloc(static_cast<size_t>(ldv) * (m + 1), s);
-  U.alloc(n, s);
+  U.alloc(n > 0 ? n : 1, s);
   part.alloc(static_cast<size_t>(2 * m + 2) * G, s);
   part2.alloc(G, s);
   ticket.alloc(2, s);
@@ -569,6 +602,8 @@ void LsWork::ensure(int n_, int m_, cudaStream_t s) {
   st.alloc(1, s);
   dbl.alloc(static_cast<size_t>(2 * (m + 1) * m + 3 * m + 1 + 2 * m + 2 + m + 8), s);
   dbl.zero();
+  rpart.alloc(2 * m + 2, s);
+  gath.release();
   if (hst) cudaFreeHost(hst);
   MGRX_CK(cudaMallocHost(&hst, sizeof(LsState)));
   if (exec) cudaGraphExecDestroy(exec);
@@ -581,7 +616,90 @@ LsWork::~LsWork() {
   if (exec) cudaGraphExecDestroy(exec);
 }
 
-bool lowsync_supported(int n, int m) { return n > 0 && m >= 1 && m <= kLsMaxRestart; }
+bool lowsync_supported(int n, int m) { return n >= 0 && m >= 1 && m <= kLsMaxRestart; }
+
+// ---------------------------------------------------------------------------
+// LsDriver: the host side of one low-sync GMRES, shared by the single-GPU
+// solve and the sharded one (shard.cu).
+LsDriver::LsDriver(LsWork& L, int n, int m, double* w) : L_(L), n_(n), m_(m), w_(w) {
+  if (L_.n != n || L_.m != m) throw RuntimeError("LsDriver: work buffers not sized for this solve");
+  args_ = std::make_unique<LsArgs>(make_args(L_, n, m, w));
+}
+LsDriver::~LsDriver() = default;
+double* LsDriver::U() const { return L_.U.get(); }
+const LsArgs& LsDriver::args() const { return *args_; }
+
+void LsDriver::start_cycle(double bnorm, double target, int iters_left, cudaStream_t s) {
+  LsState hs{};
+  hs.bnorm = bnorm;
+  hs.target = target;
+  hs.iters_left = iters_left;
+  *L_.hst = hs;
+  MGRX_CK(cudaMemcpyAsync(L_.st.get(), L_.hst, sizeof(LsState), cudaMemcpyHostToDevice, s));
+}
+
+void LsDriver::step(cudaStream_t s) { launch_step_kernels(*args_, s); }
+
+void LsDriver::step_sharded(int nranks, const Allgather& allgather, cudaStream_t s) {
+  const int stride = 2 * m_ + 2;
+  if (L_.gath.size() < static_cast<size_t>(nranks) * stride) L_.gath.alloc(static_cast<size_t>(nranks) * stride, s);
+  LsArgs a = *args_;
+  a.rank_part = L_.rpart.get();
+  launch_pdl(k_ls_dots, dim3(a.G), dim3(kLT), dots_smem(m_), s, a);
+  allgather(L_.rpart.get(), L_.gath.get(), stride, s);
+  launch_pdl(k_ls_coef, dim3(1), dim3(kLT), dots_smem(m_), s, a, static_cast<const double*>(L_.gath.get()), nranks,
+             stride);
+  launch_pdl(k_ls_update, dim3(a.G), dim3(kLT), update_smem(m_), s, a);
+  allgather(L_.rpart.get(), L_.gath.get(), stride, s);
+  launch_pdl(k_ls_finish, dim3(1), dim3(1), 0, s, a, static_cast<const double*>(L_.gath.get()), nranks, stride);
+  count_launch(4);
+}
+
+const LsState& LsDriver::sync_state(cudaStream_t s) {
+  MGRX_CK(cudaMemcpyAsync(L_.hst, L_.st.get(), sizeof(LsState), cudaMemcpyDeviceToHost, s));
+  MGRX_CK(cudaStreamSynchronize(s));
+  return *L_.hst;
+}
+
+// End of a restart cycle: the cycle's residual estimates (appended to
+// hist) and the reference's triangular solve (krylov.cpp:119-124) on the
+// rotated H (last column: its tentative rotation). Returns the state.
+LsState LsDriver::end_cycle(std::vector<double>& hist, std::vector<double>& y, cudaStream_t s) {
+  const LsState hs = sync_state(s);
+  const int k = hs.steps;
+  const LsArgs& a = *args_;
+  std::vector<double> h(k), Hrot(static_cast<size_t>(m_ + 1) * m_), gv(m_ + 1);
+  if (k > 0) MGRX_CK(cudaMemcpyAsync(h.data(), a.hist, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
+  MGRX_CK(cudaMemcpyAsync(Hrot.data(), a.Hrot, sizeof(double) * Hrot.size(), cudaMemcpyDeviceToHost, s));
+  MGRX_CK(cudaMemcpyAsync(gv.data(), a.g, sizeof(double) * (m_ + 1), cudaMemcpyDeviceToHost, s));
+  MGRX_CK(cudaStreamSynchronize(s));
+  hist.insert(hist.end(), h.begin(), h.end());
+  y.clear();
+  if (k == 0 || (hs.flags & kLsNonFinite)) return hs;
+  gv[k - 1] = hs.gt0;
+  auto R = [&](int i, int j) { return Hrot[static_cast<size_t>(j) * (m_ + 1) + i]; };
+  int keff = k;
+  while (keff > 0 && std::abs(R(keff - 1, keff - 1)) < 1e-300) --keff;
+  y.assign(keff, 0.0);
+  for (int i = keff - 1; i >= 0; --i) {
+    double acc = gv[i];
+    for (int j = i + 1; j < keff; ++j) acc -= R(i, j) * y[j];
+    y[i] = acc / R(i, i);
+  }
+  return hs;
+}
+
+void LsDriver::combine(const std::vector<double>& y, double* u, cudaStream_t s) {
+  const int keff = static_cast<int>(y.size());
+  const LsArgs& a = *args_;
+  MGRX_CK(cudaMemcpyAsync(a.coef, y.data(), sizeof(double) * keff, cudaMemcpyHostToDevice, s));
+  if (n_ > 0) {
+    launch_pdl(k_ls_combine, dim3(blocks_for(n_, 256)), dim3(256), 0, s, n_, L_.ldv, keff,
+               static_cast<const double*>(L_.V.get()), static_cast<const double*>(a.coef), u);
+    count_launch();
+  }
+  MGRX_CK(cudaStreamSynchronize(s));  // y lives on the host
+}
 
 // Right-preconditioned restarted GMRES (proj/src/krylov.cpp:37-147) with the
 // lagged CGS2 Arnoldi above. The restart-cycle work (triangular solve, x
@@ -596,8 +714,8 @@ GmresResult gmres_lowsync(const DCsr& A, const double* b, double* x, const Krylo
   L.ensure(n, m, s);
   double* w = ws.w.get();
   double* z = ws.z.get();
-  double* U = L.U.get();
-  LsArgs a = make_args(L, n, m, w);
+  LsDriver drv(L, n, m, w);
+  double* U = drv.U();
   GmresResult res;
   auto prec = [&](const double* in, double* out) {
     if (precond) precond(in, out, s);
@@ -634,7 +752,7 @@ GmresResult gmres_lowsync(const DCsr& A, const double* b, double* x, const Krylo
       cudaGraphNode_t node;
       MGRX_CK(cudaGraphAddNode(&node, g, nullptr, 0, &np));
       cudaGraph_t body = np.conditional.phGraph_out[0];
-      LsArgs ag = a;
+      LsArgs ag = drv.args();
       ag.cond = h;
       ag.use_cond = 1;
       const long long l0 = g_launches;
@@ -671,8 +789,7 @@ GmresResult gmres_lowsync(const DCsr& A, const double* b, double* x, const Krylo
 
   spmv_residual(A, x, b, nullptr, U, s);  // U = r = b - A x
   double rnorm = std::sqrt(norm2(U));
-  LsState hs{};
-  std::vector<double> hist(m), Hrot, gv;
+  std::vector<double> y;
   while (true) {
     if (!std::isfinite(rnorm)) throw RuntimeError("gmres: residual is non-finite");
     if (rnorm <= target) {
@@ -685,59 +802,25 @@ GmresResult gmres_lowsync(const DCsr& A, const double* b, double* x, const Krylo
       res.final_residual = rnorm / bnorm;
       return res;
     }
-    // cycle state; the cycle starts from U = r (v_0 = r / ||r|| in sweep B)
-    std::memset(&hs, 0, sizeof(hs));
-    hs.bnorm = bnorm;
-    hs.target = target;
-    hs.iters_left = std::min(m, cfg.max_iters - res.iterations);
-    *L.hst = hs;
-    MGRX_CK(cudaMemcpyAsync(L.st.get(), L.hst, sizeof(LsState), cudaMemcpyHostToDevice, s));
+    // the cycle starts from U = r (v_0 = r / ||r|| in sweep B)
+    drv.start_cycle(bnorm, target, std::min(m, cfg.max_iters - res.iterations), s);
     if (use_graph) {
       MGRX_CK(cudaGraphLaunch(L.exec, s));
-      MGRX_CK(cudaMemcpyAsync(L.hst, L.st.get(), sizeof(LsState), cudaMemcpyDeviceToHost, s));
-      MGRX_CK(cudaStreamSynchronize(s));
-      count_launch(L.body_nodes * L.hst->steps);
+      count_launch(L.body_nodes * drv.sync_state(s).steps);
     } else {
-      while (true) {
+      do {
         prec(U, z);
         spmv(A, z, w, s);
-        launch_step_kernels(a, s);
-        MGRX_CK(cudaMemcpyAsync(L.hst, L.st.get(), sizeof(LsState), cudaMemcpyDeviceToHost, s));
-        MGRX_CK(cudaStreamSynchronize(s));
-        if (L.hst->flags & kLsCycleEnd) break;
-      }
+        drv.step(s);
+      } while (!(drv.sync_state(s).flags & kLsCycleEnd));
     }
-    hs = *L.hst;
-    const int k = hs.steps;
-    MGRX_CK(cudaMemcpyAsync(hist.data(), a.hist, sizeof(double) * k, cudaMemcpyDeviceToHost, s));
-    Hrot.resize(static_cast<size_t>(m + 1) * m);
-    gv.resize(m + 1);
-    MGRX_CK(cudaMemcpyAsync(Hrot.data(), a.Hrot, sizeof(double) * Hrot.size(), cudaMemcpyDeviceToHost, s));
-    MGRX_CK(cudaMemcpyAsync(gv.data(), a.g, sizeof(double) * (m + 1), cudaMemcpyDeviceToHost, s));
-    MGRX_CK(cudaStreamSynchronize(s));
+    const LsState hs = drv.end_cycle(res.history, y, s);
     if (hs.flags & kLsNonFinite) throw RuntimeError("gmres: Arnoldi vector is non-finite");
-    for (int i = 0; i < k; ++i) res.history.push_back(hist[i]);
-    res.iterations += k;
-    const bool breakdown = hs.flags & kLsHappy;
-    // triangular solve on the rotated H (last column: tentative rotation)
-    gv[k - 1] = hs.gt0;
-    auto R = [&](int i, int j) { return Hrot[static_cast<size_t>(j) * (m + 1) + i]; };
-    int keff = k;
-    while (keff > 0 && std::abs(R(keff - 1, keff - 1)) < 1e-300) --keff;
-    if (keff > 0) {
-      std::vector<double> y(keff);
-      for (int i = keff - 1; i >= 0; --i) {
-        double acc = gv[i];
-        for (int j = i + 1; j < keff; ++j) acc -= R(i, j) * y[j];
-        y[i] = acc / R(i, i);
-      }
-      MGRX_CK(cudaMemcpyAsync(a.coef, y.data(), sizeof(double) * keff, cudaMemcpyHostToDevice, s));
-      launch_pdl(k_ls_combine, dim3(blocks_for(n, 256)), dim3(256), 0, s, n, L.ldv, keff,
-                 static_cast<const double*>(L.V.get()), static_cast<const double*>(a.coef), ws.u.get());
-      count_launch();
+    res.iterations += hs.steps;
+    if (!y.empty()) {
+      drv.combine(y, ws.u.get(), s);
       prec(ws.u.get(), z);
       vec_add(n, z, x, s);  // x += M^{-1}(V y)
-      MGRX_CK(cudaStreamSynchronize(s));  // y lives on the host stack
     }
     spmv_residual(A, x, b, nullptr, U, s);
     const double tn = std::sqrt(norm2(U));
@@ -748,7 +831,7 @@ GmresResult gmres_lowsync(const DCsr& A, const double* b, double* x, const Krylo
       res.final_residual = tn / bnorm;
       return res;
     }
-    if (breakdown) throw RuntimeError("gmres: Arnoldi breakdown before reaching tolerance");
+    if (hs.flags & kLsHappy) throw RuntimeError("gmres: Arnoldi breakdown before reaching tolerance");
     res.final_residual = tn / bnorm;
     if (res.iterations >= cfg.max_iters) return res;
     rnorm = tn;  // the next cycle starts from this residual (already in U)

@@ -60,95 +60,6 @@ std::vector<T> dl(const DVec<T>& v, size_t n, cudaStream_t s) {
   return h;
 }
 
-// st[q] = number of entries of the ascending list `sub` below p.st[q]
-Part sub_part(const Part& p, const std::vector<int>& sub) {
-  Part o;
-  o.st.resize(p.st.size());
-  for (size_t q = 0; q < p.st.size(); ++q)
-    o.st[q] = static_cast<int>(std::lower_bound(sub.begin(), sub.end(), p.st[q]) - sub.begin());
-  o.st.back() = static_cast<int>(sub.size());
-  return o;
-}
-
-Space make_space(const Part& p, int rank) {
-  Space s;
-  s.part = p;
-  s.own = p.n(rank);
-  s.cap = s.own;
-  return s;
-}
-
-// Slab of global operator G: rows of `rows` owned by `rank`, columns of the
-// space `cols` renumbered [owned | halo]. The send lists are derived from the
-// other ranks' rows of the same (replicated) operator.
-void build_op(SOp& op, const DCsr& G, const Part& rows, Space& cols, int rank, cudaStream_t s) {
-  const int size = static_cast<int>(rows.st.size()) - 1;
-  if (G.rows != rows.total() || G.cols != cols.part.total())
-    throw RuntimeError("sharded solve: operator does not match its index spaces");
-  const std::vector<int> ptr = dl(G.ptr, G.rows + 1, s);
-  const std::vector<int> col = dl(G.col, G.nnz, s);
-  const std::vector<double> val = dl(G.val, G.nnz, s);
-  const int r0 = rows.lo(rank), r1 = rows.hi(rank);
-  const int c0 = cols.part.lo(rank), c1 = cols.part.hi(rank);
-  op.own = c1 - c0;
-  // halo of this rank: sorted unique non-owned columns of its rows
-  std::vector<int> halo;
-  for (int k = ptr[r0]; k < ptr[r1]; ++k)
-    if (col[k] < c0 || col[k] >= c1) halo.push_back(col[k]);
-  std::sort(halo.begin(), halo.end());
-  halo.erase(std::unique(halo.begin(), halo.end()), halo.end());
-  op.nhalo = static_cast<int>(halo.size());
-  cols.need(op.nhalo);
-  // local CSR (entries keep their order: the per-row sum is unchanged)
-  const int m = r1 - r0;
-  std::vector<int> lp(m + 1), lc(ptr[r1] - ptr[r0]);
-  std::vector<double> lv(val.begin() + ptr[r0], val.begin() + ptr[r1]);
-  for (int i = 0; i <= m; ++i) lp[i] = ptr[r0 + i] - ptr[r0];
-  for (int k = ptr[r0]; k < ptr[r1]; ++k) {
-    const int j = col[k];
-    lc[k - ptr[r0]] = (j >= c0 && j < c1)
-                          ? j - c0
-                          : op.own + static_cast<int>(std::lower_bound(halo.begin(), halo.end(), j) - halo.begin());
-  }
-  op.M = DCsr();
-  op.M.rows = m;
-  op.M.cols = op.own + op.nhalo;
-  op.M.nnz = static_cast<int>(lc.size());
-  op.M.ptr.alloc(m + 1, s);
-  op.M.ptr.upload(lp.data(), m + 1);
-  op.M.col.alloc(lc.size() > 0 ? lc.size() : 1, s);
-  op.M.col.upload(lc.data(), lc.size());
-  op.M.val.alloc(lv.size() > 0 ? lv.size() : 1, s);
-  op.M.val.upload(lv.data(), lv.size());
-  // recv segments: halo entries grouped by owner (owners are monotone in j)
-  op.recv.clear();
-  for (int a = 0; a < op.nhalo;) {
-    const int q = cols.part.owner(halo[a]);
-    int b = a;
-    while (b < op.nhalo && halo[b] < cols.part.hi(q)) ++b;
-    op.recv.push_back({q, a, b - a});
-    a = b;
-  }
-  // send segments: for every other rank q, the owned columns its rows read
-  op.send.clear();
-  std::vector<int> sidx;
-  for (int q = 0; q < size; ++q) {
-    if (q == rank) continue;
-    std::vector<int> need;
-    for (int k = ptr[rows.lo(q)]; k < ptr[rows.hi(q)]; ++k)
-      if (col[k] >= c0 && col[k] < c1) need.push_back(col[k] - c0);
-    if (need.empty()) continue;
-    std::sort(need.begin(), need.end());
-    need.erase(std::unique(need.begin(), need.end()), need.end());
-    op.send.push_back({q, static_cast<int>(sidx.size()), static_cast<int>(need.size())});
-    sidx.insert(sidx.end(), need.begin(), need.end());
-  }
-  op.sidx.alloc(sidx.size() > 0 ? sidx.size() : 1, s);
-  op.sidx.upload(sidx.data(), sidx.size());
-  op.sbuf.alloc(sidx.size() > 0 ? sidx.size() : 1, s);
-  op.built = true;
-  spmv_prepare(op.M, s);
-}
 
 // Fill the halo region x[own, own + nhalo) of an extended vector.
 void halo(SOp& op, double* x, ShardCtx& c) {
@@ -208,38 +119,6 @@ void Repl::solve(const double* r, double* z, ShardCtx& c) {
 // ---------------------------------------------------------------------------
 // smoothers
 // ---------------------------------------------------------------------------
-void SRelax::build(const BoundRelax& g, const DCsr& Ag, Space& space, ShardCtx& c) {
-  kind = g.spec.kind;
-  sweeps = g.spec.sweeps;
-  weight = g.spec.weight;
-  sp = &space;
-  n = space.own;
-  const int lo = space.part.lo(c.rank);
-  switch (kind) {
-    case Smoother::jacobi:
-    case Smoother::l1_jacobi:
-      dinv.alloc(n > 0 ? n : 1, c.s);
-      d2d(dinv.get(), g.dinv.get() + lo, n, c.s);
-      if (sweeps > 1) build_op(A, Ag, space.part, space, c.rank, c.s);
-      break;
-    case Smoother::amg_vcycle:
-      amg = std::make_unique<SAmg>();
-      amg->build(*g.amg, space, c);
-      if (sweeps > 1) build_op(A, Ag, space.part, space, c.rank, c.s);
-      break;
-    case Smoother::dense_lu:
-      dense.build(&g.lu, space.part, c.s);
-      break;
-    case Smoother::hybrid_l1_gs_forward:
-    case Smoother::hybrid_l1_gs_backward:
-      throw RuntimeError(
-          "sharded solve: hybrid Gauss-Seidel is a sequential sweep over the whole matrix; use a "
-          "Jacobi-family or AMG smoother");
-    default:
-      throw RuntimeError("sharded solve: smoother kind not supported across slabs");
-  }
-}
-
 void SRelax::alloc(cudaStream_t s) {
   alloc_cap(b0, *sp, s);
   alloc_cap(b1, *sp, s);
@@ -299,6 +178,7 @@ void SRelax::apply(const double* r, const int* rrow, double* z, double* zacc, Sh
 void RepAmg::build(const AmgHier& h, int l, const Part& p, cudaStream_t s) {
   g = &h;
   from = l;
+  at = l;
   part = p;
   const int size = static_cast<int>(p.st.size()) - 1;
   maxc = 1;
@@ -371,61 +251,6 @@ void RepAmg::vcycle(const double* r, double* z, ShardCtx& c) {
   d2d(z, zfull.get() + part.lo(c.rank), own, c.s);
 }
 
-int repl_rows() {
-  static const int m = [] {
-    const char* v = std::getenv("MGRX_SHARD_REPL_ROWS");
-    return v ? std::atoi(v) : 65536;
-  }();
-  return m;
-}
-
-void SAmg::build(const AmgHier& g, Space& fine, ShardCtx& c) {
-  const int nl = static_cast<int>(g.levels.size());
-  std::vector<Space*> sp(nl);
-  sp[0] = &fine;
-  for (int l = 1; l < nl; ++l) {
-    const AmgLevelD& G = g.levels[l - 1];
-    const std::vector<int> C = dl(G.C, G.P.cols, c.s);
-    spaces.push_back(make_space(sub_part(sp[l - 1]->part, C), c.rank));
-    sp[l] = &spaces.back();
-  }
-  // first level that is replicated: small, Jacobi-type smoothing from there
-  // on (the single-GPU smoother path without a gather), more than one rank
-  int from = -1;
-  if (c.size > 1 && repl_rows() > 0) {
-    for (int l = 1; l < nl && from < 0; ++l) {
-      if (g.levels[l].A.rows > repl_rows()) continue;
-      bool ok = true;
-      for (int k = l; k < nl - 1 && ok; ++k) {
-        const BoundRelax* bs[2] = {&g.levels[k].pre, &g.levels[k].post};
-        for (const BoundRelax* b : bs)
-          ok = ok && (b->spec.kind == Smoother::jacobi || b->spec.kind == Smoother::l1_jacobi) &&
-               (b->spec.sweeps <= 1 || b->n <= fold_sweep0_max_rows());
-      }
-      if (ok) from = l;
-    }
-  }
-  for (int l = 0; l < nl; ++l) {
-    L.emplace_back();
-    SAmgLevel& S = L.back();
-    S.sp = sp[l];
-    if (l == from) {
-      rep.build(g, l, sp[l]->part, c.s);
-      break;
-    }
-    if (l == nl - 1) {
-      coarse.build(&g.coarse, sp[l]->part, c.s);
-      break;
-    }
-    const AmgLevelD& G = g.levels[l];
-    build_op(S.A, G.A, sp[l]->part, *sp[l], c.rank, c.s);
-    build_op(S.R, G.R, sp[l + 1]->part, *sp[l], c.rank, c.s);
-    build_op(S.P, G.P, sp[l]->part, *sp[l + 1], c.rank, c.s);
-    S.pre.build(G.pre, G.A, *sp[l], c);
-    S.post.build(G.post, G.A, *sp[l], c);
-  }
-}
-
 void SAmg::alloc(cudaStream_t s) {
   for (size_t l = 0; l < L.size(); ++l) {
     SAmgLevel& S = L[l];
@@ -442,7 +267,7 @@ void SAmg::alloc(cudaStream_t s) {
 // V(1,1) (proj/src/amg.cpp:232-242), with halos before each product.
 void SAmg::level(int l, const double* r, double* z, ShardCtx& c) {
   SAmgLevel& S = L[l];
-  if (l == rep.from) {
+  if (l == rep.at) {
     rep.vcycle(r, z, c);
     return;
   }
@@ -467,95 +292,6 @@ void SAmg::level(int l, const double* r, double* z, ShardCtx& c) {
 // ---------------------------------------------------------------------------
 // MGR
 // ---------------------------------------------------------------------------
-void Shard::build(MgrHier& h, const DCsr& A, const std::vector<int>& fine_starts, std::unique_ptr<Comm> cm,
-                  cudaStream_t stream) {
-  comm = std::move(cm);
-  c.comm = comm.get();
-  c.rank = comm->rank;
-  c.size = comm->size;
-  c.s = stream;
-  H = &h;
-  Ag = &A;
-  Part p0;
-  p0.st = fine_starts;
-  if (static_cast<int>(p0.st.size()) != c.size + 1 || p0.st.front() != 0 || p0.st.back() != A.rows)
-    throw InvalidArgument("sharded solve: row starts must be size+1 offsets from 0 to n");
-  for (int q = 0; q < c.size; ++q)
-    if (p0.st[q + 1] <= p0.st[q]) throw InvalidArgument("sharded solve: every rank needs at least one row");
-  row_begin = p0.lo(c.rank);
-  row_end = p0.hi(c.rank);
-  spaces.push_back(make_space(p0, c.rank));
-  Space* cur = &spaces.back();
-  for (auto& G : h.levels) {
-    levels.emplace_back();
-    SMgrLevel& S = levels.back();
-    S.sl = cur;
-    const int nf = static_cast<int>(G.F.size()), nc = static_cast<int>(G.C.size());
-    const std::vector<int> F = dl(G.F, nf, c.s), C = dl(G.C, nc, c.s);
-    spaces.push_back(make_space(sub_part(cur->part, F), c.rank));
-    S.sf = &spaces.back();
-    spaces.push_back(make_space(sub_part(cur->part, C), c.rank));
-    S.sc = &spaces.back();
-    const int lo = cur->part.lo(c.rank);
-    S.nl = cur->own;
-    S.nf = S.sf->own;
-    S.nc = S.sc->own;
-    std::vector<int> fl(S.nf), cl(S.nc);
-    for (int i = 0; i < S.nf; ++i) fl[i] = F[S.sf->part.lo(c.rank) + i] - lo;
-    for (int i = 0; i < S.nc; ++i) cl[i] = C[S.sc->part.lo(c.rank) + i] - lo;
-    std::vector<int> fp(S.nl, -1);
-    for (int i = 0; i < S.nf; ++i) fp[fl[i]] = i;
-    S.Floc = upload_ints(fl, c.s);
-    S.Cloc = upload_ints(cl, c.s);
-    S.fpos = upload_ints(fp, c.s);
-    S.injection = G.injection;
-    S.general = !G.injection || G.g_relax.has_value();
-    build_op(S.P, G.P, cur->part, *S.sc, c.rank, c.s);
-    if (S.general) {
-      build_op(S.A, G.A, cur->part, *cur, c.rank, c.s);
-      build_op(S.R, G.R, S.sc->part, *cur, c.rank, c.s);
-      if (G.g_relax) {
-        S.g_relax = std::make_unique<SRelax>();
-        S.g_relax->build(*G.g_relax, G.A, *cur, c);
-      }
-    } else {
-      build_op(S.Acf, G.Acf, S.sc->part, *S.sf, c.rank, c.s);
-    }
-    S.f_relax.build(G.f_relax, G.Aff, *S.sf, c);
-    cur = S.sc;
-  }
-  // coarse solver on the last C space
-  if (h.coarse_spec.kind == Coarse::dense_lu) {
-    coarse_lu.build(&h.coarse_lu, cur->part, c.s);
-  } else {
-    coarse_amg = std::make_unique<SAmg>();
-    coarse_amg->build(*h.coarse_amg, *cur, c);
-    coarse_cycles = h.coarse_spec.cycles;
-    if (coarse_cycles > 1) build_op(Acoarse, h.A_coarse, cur->part, *cur, c.rank, c.s);
-  }
-  build_op(Afine, A, spaces.front().part, spaces.front(), c.rank, c.s);
-  // buffers last: every space's halo capacity is known now
-  for (auto& S : levels) {
-    alloc_cap(S.zF, *S.sf, c.s);
-    alloc_cap(S.vF, *S.sf, c.s);
-    alloc_cap(S.rc, *S.sc, c.s);
-    alloc_cap(S.e, *S.sc, c.s);
-    alloc_cap(S.t, *S.sl, c.s);
-    S.f_relax.alloc(c.s);
-    if (S.g_relax) S.g_relax->alloc(c.s);
-  }
-  if (coarse_amg) coarse_amg->alloc(c.s);
-  alloc_cap(ct, *cur, c.s);
-  alloc_cap(cd, *cur, c.s);
-  alloc_cap(xext, spaces.front(), c.s);
-  alloc_cap(zext, spaces.front(), c.s);
-  loc.alloc(2, c.s);
-  loc.zero();
-  gbuf.alloc(2 * c.size, c.s);
-  MGRX_CK(cudaStreamSynchronize(c.s));
-  setup_fused();
-}
-
 namespace {
 // deterministic self-check data from the global row index
 __global__ void k_seed(int n, int row0, int salt, double* v) {
@@ -775,10 +511,104 @@ void Shard::apply(const double* v, double* z) {
 // Right-preconditioned restarted GMRES (proj/src/krylov.cpp:37-147) over the
 // slabs: the control flow of gmres_device's per-projection MGS path, with
 // every inner product reduced across ranks (all-gather + rank-order sum).
-GmresResult Shard::solve(const double* b, double* x, const KrylovSpec& cfg) {
+// Low-synchronisation variant (the default, KrylovSpec::ortho != mgs): the
+// lagged CGS2 step of lowsync.cu on the slabs, its two reductions per step
+// completed across ranks by an all-gather of the rank sums and a rank-order
+// fold (2 collectives per step instead of 2k+4 under MGS).
+GmresResult Shard::solve_lowsync(const double* b, double* x, const KrylovSpec& cfg) {
   const int n = spaces.front().own;
   cudaStream_t s = c.s;
+  const int m = cfg.restart;
+  ws.ensure(n, 1, s);
+  ws.ls.ensure(n, m, s);
+  LsDriver drv(ws.ls, n, m, ws.w.get());
+  double* U = drv.U();
+  double* L = loc.get();
+  const LsDriver::Allgather ag = [this](const double* in, double* out, int count, cudaStream_t st) {
+    c.comm->allgather(in, out, count, st);
+  };
+  auto norm2 = [&](const double* v) {
+    mgs_step(n, const_cast<double*>(v), nullptr, nullptr, nullptr, true, ws, nullptr, nullptr, false, L + 1, s);
+    c.comm->allgather(L, gbuf.get(), 2, s);
+    fold2(c.size, gbuf.get(), nullptr, nullptr, false, ws.scal.get(), s);
+    return read_scalar(ws.scal.get(), s);
+  };
+  double* xe = xext.get();
+  d2d(xe, x, n, s);
+  GmresResult res;
+  auto finish = [&] {
+    d2d(x, xe, n, s);
+    MGRX_CK(cudaStreamSynchronize(s));
+  };
+  const double bb = norm2(b);
+  if (!std::isfinite(bb)) throw RuntimeError("gmres: rhs contains non-finite entries");
+  const double bnorm = std::sqrt(bb);
+  if (bnorm == 0.0) {
+    if (n > 0) MGRX_CK(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
+    MGRX_CK(cudaStreamSynchronize(s));
+    res.converged = true;
+    return res;
+  }
+  const double target = std::max(cfg.rel_tol * bnorm, cfg.abs_tol);
+  halo(Afine, xe, c);
+  spmv_residual(Afine.M, xe, b, nullptr, U, s);  // U = r = b - A x
+  double rnorm = std::sqrt(norm2(U));
+  std::vector<double> y;
+  while (true) {
+    if (!std::isfinite(rnorm)) throw RuntimeError("gmres: residual is non-finite");
+    if (rnorm <= target) {
+      res.converged = true;
+      res.final_residual = rnorm / bnorm;
+      res.history.push_back(res.final_residual);
+      finish();
+      return res;
+    }
+    if (res.iterations >= cfg.max_iters) {
+      res.final_residual = rnorm / bnorm;
+      finish();
+      return res;
+    }
+    drv.start_cycle(bnorm, target, std::min(m, cfg.max_iters - res.iterations), s);
+    do {
+      prec(U, zext.get());
+      halo(Afine, zext.get(), c);
+      spmv(Afine.M, zext.get(), ws.w.get(), s);  // w = A M^{-1} U
+      drv.step_sharded(c.size, ag, s);
+    } while (!(drv.sync_state(s).flags & kLsCycleEnd));
+    const LsState hs = drv.end_cycle(res.history, y, s);
+    if (hs.flags & kLsNonFinite) throw RuntimeError("gmres: Arnoldi vector is non-finite");
+    res.iterations += hs.steps;
+    if (!y.empty()) {
+      drv.combine(y, ws.u.get(), s);
+      prec(ws.u.get(), zext.get());
+      vec_add(n, zext.get(), xe, s);  // x += M^{-1}(V y)
+    }
+    halo(Afine, xe, c);
+    spmv_residual(Afine.M, xe, b, nullptr, U, s);
+    const double tn = std::sqrt(norm2(U));
+    if (!std::isfinite(tn)) throw RuntimeError("gmres: residual is non-finite");
+    res.history.push_back(tn / bnorm);
+    if (tn <= target) {
+      res.converged = true;
+      res.final_residual = tn / bnorm;
+      finish();
+      return res;
+    }
+    if (hs.flags & kLsHappy) throw RuntimeError("gmres: Arnoldi breakdown before reaching tolerance");
+    res.final_residual = tn / bnorm;
+    if (res.iterations >= cfg.max_iters) {
+      finish();
+      return res;
+    }
+    rnorm = tn;
+  }
+}
+
+GmresResult Shard::solve(const double* b, double* x, const KrylovSpec& cfg) {
   if (cfg.restart < 1) throw InvalidArgument("gmres: restart must be >= 1");
+  if (cfg.ortho != kOrthoMgs && lowsync_supported(spaces.front().own, cfg.restart)) return solve_lowsync(b, x, cfg);
+  const int n = spaces.front().own;
+  cudaStream_t s = c.s;
   const int m = cfg.restart;
   ws.ensure(n, m, s);
   double* S = ws.scal.get();

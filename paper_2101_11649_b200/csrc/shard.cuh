@@ -98,7 +98,6 @@ struct SRelax {
   Repl dense;
   Space* sp = nullptr;
   DVec<double> b0, b1, b2, b3;
-  void build(const BoundRelax& g, const DCsr& Ag, Space& space, ShardCtx& c);
   void alloc(cudaStream_t s);
   // z = smoother(r[rrow]) (rrow: local gather indices or null); zacc: += instead
   void apply(const double* r, const int* rrow, double* z, double* zacc, ShardCtx& c);
@@ -120,7 +119,8 @@ struct SAmgLevel {
 // The operations are the single-GPU V-cycle's, so results stay bitwise.
 struct RepAmg {
   const AmgHier* g = nullptr;
-  int from = -1;
+  int from = -1;  // first replicated level of g
+  int at = -1;    // the sharded AMG level it replaces (-1: none)
   Part part;  // partition of level `from`
   int maxc = 1;
   DVec<double> pad, all, rfull, zfull;
@@ -141,8 +141,7 @@ struct SAmg {
   std::deque<Space> spaces;  // spaces[0] unused when the fine space is external
   std::deque<SAmgLevel> L;
   Repl coarse;
-  RepAmg rep;  // rep.from >= 1: levels from rep.from on are replicated
-  void build(const AmgHier& g, Space& fine, ShardCtx& c);
+  RepAmg rep;  // rep.at >= 1: levels from rep.at on are replicated
   void alloc(cudaStream_t s);
   void vcycle(const double* r, double* z, ShardCtx& c) { level(0, r, z, c); }
 
@@ -166,8 +165,6 @@ struct SMgrLevel {
 struct Shard {
   ShardCtx c;
   std::unique_ptr<Comm> comm;
-  MgrHier* H = nullptr;
-  const DCsr* Ag = nullptr;
   std::deque<Space> spaces;  // [0] fine level
   std::deque<SMgrLevel> levels;
   SOp Afine;  // the GMRES operator
@@ -185,13 +182,27 @@ struct Shard {
   double* graph_out = nullptr;
   long long graph_nodes_ = 0;
 
+  // replicated small parts this shard owns (dense coarse factors, the
+  // coarse AMG levels it replicates), built from the plan's small matrices
+  std::deque<DCsr> own_mat;
+  std::deque<DenseLU> own_lu;
+  std::vector<std::unique_ptr<AmgHier>> own_amg;
+
+  // Every rank holds the global hierarchy h (a replica): plan, keep own slab.
   // s: the shard's stream (owned by the caller, outlives the shard)
   void build(MgrHier& h, const DCsr& A, const std::vector<int>& fine_starts, std::unique_ptr<Comm> cm,
              cudaStream_t s);
+  // Only rank 0 holds the global hierarchy (h, A non-null there, null
+  // elsewhere): it plans for every rank and sends each its plan
+  // (shardplan.cu). No global operator ever lives on the other ranks.
+  void build_scatter(MgrHier* h, const DCsr* A, const std::vector<int>& fine_starts, std::unique_ptr<Comm> cm,
+                     cudaStream_t s);
+  void load(const std::vector<unsigned char>& plan);
   ~Shard();
   // z = M^{-1} v on the owned rows (device pointers; z needs no halo room)
   void apply(const double* v, double* z);
   GmresResult solve(const double* b, double* x, const KrylovSpec& cfg);
+  GmresResult solve_lowsync(const double* b, double* x, const KrylovSpec& cfg);
 
   // Fused sharded Arnoldi (krylov.cu arnoldi_sharded): each GMRES step's
   // whole MGS in one kernel per rank, the per-projection rank partials

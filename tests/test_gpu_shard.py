@@ -83,6 +83,98 @@ def test_sharded_apply_and_solve(kind, size):
     g.close()
 
 
+@pytest.mark.parametrize("size", [1, 2, 3])
+@pytest.mark.parametrize("kind", ["mfd", "comp", "frac", "amg_cycles"])
+def test_sharded_lowsync_solve(kind, size):
+    """The default low-synchronisation GMRES on the slabs (two all-gathered
+    reductions per step): every rank reports the same history; against the
+    single-GPU low-sync solve and the single-GPU MGS solve the north_star bar
+    holds (history 1e-10 of the initial residual, iterations +-1) and the
+    assembled solution meets rtol."""
+    P, text, rtol = _problem(kind)
+    H = mx.Hierarchy(mx.Matrix(P.ptr, P.col, P.val), P.partition, text, P.unknown_map)
+    g = mx.LocalGroup(size)
+    starts = mx.slab_row_starts(P, size)
+    shards = [mx.Shard(H, r, size, starts, group=g) for r in range(size)]
+    cfg = mx.KrylovConfig(restart=30, rel_tol=rtol, ortho="cgs2")
+    outs = _run(shards, lambda s: s.solve(P.rhs[s.row_begin:s.row_end], None, cfg))
+    reps = [o[1] for o in outs]
+    assert all(r.converged for r in reps)
+    assert all(r.residual_history == reps[0].residual_history for r in reps)
+    for o in ("cgs2", "mgs"):
+        _, r1 = H.solve(P.rhs, None, mx.KrylovConfig(restart=30, rel_tol=rtol, ortho=o))
+        assert abs(reps[0].iterations - r1.iterations) <= 1, (o, reps[0].iterations, r1.iterations)
+        k = min(10, len(r1.residual_history), len(reps[0].residual_history))
+        h, hr = np.array(reps[0].residual_history[:k]), np.array(r1.residual_history[:k])
+        assert np.all(np.abs(h - hr) <= 1e-10 * np.maximum(np.abs(hr), 1.0)), (o, h, hr)
+    x = np.concatenate([o[0] for o in outs])
+    M = sp.csr_matrix((P.val, P.col, P.ptr), shape=(P.n, P.n))
+    assert np.linalg.norm(P.rhs - M @ x) <= rtol * np.linalg.norm(P.rhs) * (1 + 1e-9)
+    for s in shards:
+        s.close()
+    g.close()
+
+
+@pytest.mark.parametrize("size", [2, 3])
+@pytest.mark.parametrize("kind", ["mfd", "comp", "frac", "global_relax", "amg_cycles"])
+def test_scatter_setup_equals_replicated(kind, size):
+    """mgrx_shard_create_scatter (build on rank 0, scatter):
+    only rank 0 holds the global hierarchy; the other ranks receive their
+    slab plans and rebuild the small replicated parts themselves. The
+    shards apply the preconditioner bitwise like the single GPU, solve
+    bitwise like the replicated-setup shards (MGS and low-sync), and keep
+    working after rank 0 drops the global hierarchy."""
+    import gc
+    P, text, rtol = _problem(kind)
+    H = mx.Hierarchy(mx.Matrix(P.ptr, P.col, P.val), P.partition, text, P.unknown_map)
+    starts = mx.slab_row_starts(P, size)
+    v = np.random.default_rng(7).uniform(-1, 1, P.n)
+    z = H.apply(v)
+    g = mx.LocalGroup(size)
+    shards = _run(list(range(size)), lambda r: mx.Shard(H if r == 0 else None, r, size, starts, group=g,
+                                                        scatter=True, ctx=H.ctx))
+    gr = mx.LocalGroup(size)
+    repl = [mx.Shard(H, r, size, starts, group=gr) for r in range(size)]
+    assert [s.row_begin for s in shards] == list(starts[:-1])
+    zs = _run(shards, lambda s: s.apply(v[s.row_begin:s.row_end]))
+    for s, zr in zip(shards, zs):
+        assert np.array_equal(zr.view(np.int64), z[s.row_begin:s.row_end].view(np.int64)), (kind, s.row_begin)
+    del H
+    gc.collect()
+    for o in ("mgs", "cgs2"):
+        cfg = mx.KrylovConfig(restart=30, rel_tol=rtol, ortho=o)
+        a = _run(shards, lambda s: s.solve(P.rhs[s.row_begin:s.row_end], None, cfg))
+        b = _run(repl, lambda s: s.solve(P.rhs[s.row_begin:s.row_end], None, cfg))
+        assert all(x[1].converged for x in a)
+        assert a[0][1].residual_history == b[0][1].residual_history, o
+        xa, xb = np.concatenate([x[0] for x in a]), np.concatenate([x[0] for x in b])
+        assert np.array_equal(xa.view(np.int64), xb.view(np.int64)), o
+    for s in shards + repl:
+        s.close()
+    g.close()
+    gr.close()
+
+
+def test_scatter_setup_errors_reach_every_rank():
+    """A strategy the slabs cannot run (one-range hybrid Gauss-Seidel) fails
+    on rank 0's planner; every rank gets the message instead of waiting."""
+    P = mx.mfd_problem(6, 5, 4, "iid")
+    H = mx.Hierarchy(mx.Matrix(P.ptr, P.col, P.val), P.partition, mx.load_strategy("mfd_mgr_pi_c1"))
+    g = mx.LocalGroup(2)
+    st = mx.slab_row_starts(P, 2)
+
+    def mk(r):
+        try:
+            mx.Shard(H if r == 0 else None, r, 2, st, group=g, scatter=True, ctx=H.ctx)
+        except mx.MgrxError as e:
+            return str(e)
+        return "no error"
+    msgs = _run([0, 1], mk)
+    assert all("hybrid Gauss-Seidel is a sequential sweep" in m for m in msgs), msgs
+    with pytest.raises(mx.MgrxInvalidArgument, match="rank 0"):
+        mx.Shard(None, 0, 1, [0, P.n], scatter=True, ctx=H.ctx)
+
+
 def test_sharded_rejects_sequential_gs():
     P = mx.mfd_problem(6, 5, 4, "iid")
     H = mx.Hierarchy(mx.Matrix(P.ptr, P.col, P.val), P.partition, mx.load_strategy("mfd_mgr_pi_c1"))
