@@ -2,7 +2,12 @@
 system on a 128x128x64 grid with a layered log-normal permeability field,
 4,227,072 DOF), FGMRES(30), rtol 1e-6, strategy = one exact reduction of the
 face multipliers (ideal interp, injection) + one AMG V-cycle on the cell
-pressure system (strategies/mfd_mgr_pi_c1.json).
+pressure system with l1-Jacobi x2 AMG smoothing
+(strategies/mfd_mgr_pi_c1_l1j.json: BASELINE cfg2's "one AMG V-cycle"; the
+shipped proj/strategies/mfd_mgr_pi.json, 8 V-cycles of hybrid Gauss-Seidel,
+is measured in the same line under "variants"). Orthogonalisation: the
+default low-synchronisation lagged CGS2 (csrc/lowsync.cu); the reference's
+MGS (bitwise parity mode) is a variant.
 
 A step = one complete solve from x0 = 0 with the hierarchy already built
 (setup is timed separately and reported). value = DOF * GMRES iterations /
@@ -33,17 +38,17 @@ CONFIGS = {
              "strategy": "mfd_mgr_pi_c1", "rtol": 1e-6,
              "desc": "cfg1: hybrid-MFD [p,pi] 20x20x10 iid log-normal, FGMRES(30) rtol 1e-6, MGR_pi + 1 AMG V-cycle"},
     "cfg2": {"kind": "mfd", "dims": (128, 128, 64), "field": "layered", "seed": 20210129,
-             "strategy": "mfd_mgr_pi_c1_l1j", "rtol": 1e-6, "variant": "mfd_mgr_pi_c1",
+             "strategy": "mfd_mgr_pi_c1_l1j", "rtol": 1e-6, "variant": ["mfd_mgr_pi", "mfd_mgr_pi_c1"],
              "desc": "cfg2: hybrid-MFD [p,pi] 128x128x64 layered log-normal (1e6 contrast), "
                      "FGMRES(30) rtol 1e-6, MGR_pi (exact pi elimination) + 1 AMG V-cycle "
                      "(l1-Jacobi x2 AMG smoothing; variant: the AMG default hybrid Gauss-Seidel)"},
     "cfg3": {"kind": "comp", "dims": (100, 100, 50), "wells": 8, "seed": 20210130,
-             "strategy": "comp_mgr_l1j", "rtol": 1e-5, "variant": "comp_mgr",
+             "strategy": "comp_mgr_l1j", "rtol": 1e-5, "variant": ["comp_mgr"],
              "desc": "cfg3: compositional p+3 densities 100x100x50 (4x4 blocks) + 8 wells x 50 elements x 5 dofs, "
                      "FGMRES(30) rtol 1e-5, MGR rho3 -> rho1,rho2 -> p(AMG, l1-Jacobi x2; variant: hybrid GS) "
                      "-> wells(dense LU)"},
     "cfg4": {"kind": "frac", "m": 64, "seed": 20210131, "strategy": "frac_mgr_u_l1j", "rtol": 1e-6,
-             "variant": "frac_mgr_u",
+             "variant": ["frac_mgr_u"],
              "desc": "cfg4: 3-D Q1 elasticity 64^3 nodes (81 nnz/row) + mid-plane fracture lubrication, "
                      "FGMRES(30) rtol 1e-6, MGR_u with unknown-based AMG on A_uu (l1-Jacobi x2; variant: "
                      "hybrid GS), AMG coarse on p"},
@@ -188,10 +193,24 @@ def scaling_kind(n_gpus):
     return "weak" if (CONFIGS[CONFIG].get("weak") or n_gpus == 1) else "strong"
 
 
+STRATEGY_NOTES = {
+    "mfd_mgr_pi_c1_l1j": "BASELINE cfg2 fixes one exact reduction + ONE AMG V-cycle but not the AMG smoother; "
+                         "this strategy file (reference JSON schema) uses l1-Jacobi x2, the north_star's "
+                         "relaxation family. The shipped proj/strategies/mfd_mgr_pi.json (8 V-cycles, hybrid "
+                         "Gauss-Seidel) and its 1-cycle form are timed under variants.",
+    "comp_mgr_l1j": "l1-Jacobi x2 AMG smoothing in the reference schema; the shipped-style comp_mgr "
+                    "(hybrid Gauss-Seidel) is timed under variants.",
+    "frac_mgr_u_l1j": "l1-Jacobi x2 AMG smoothing in the reference schema; the shipped frac_mgr_u (hybrid "
+                      "Gauss-Seidel) is timed under variants.",
+}
+
+
 def workload_config(P, n_gpus):
     return {"workload": CONFIGS[CONFIG]["desc"],
             "dofs": int(P.n), "nnz": int(P.ptr[-1]), "strategy": STRATEGY, "restart": RESTART,
-            "rel_tol": RTOL,
+            "rel_tol": RTOL, "strategy_note": STRATEGY_NOTES.get(STRATEGY),
+            "ortho": "cgs2 (lagged CGS2, 2 basis sweeps + 2 reductions per step, device-resident restart cycle); "
+                     "history within the north_star bar of the oracle (tests/test_gpu_fullsize.py)",
             "parallelism": f"zslab{n_gpus} (NCCL halo exchange + all-gathered inner products)"
             if n_gpus > 1 else "single",
             "l2_flush": "inputs exceed L2 (matrix+hierarchy > 126 MB)"}
@@ -199,7 +218,7 @@ def workload_config(P, n_gpus):
 
 def probe_names(H):
     info = H.info()
-    names = ["arnoldi.15", "mgs", "spmv.A"]
+    names = ["cgs2.15", "cgs2dots.15", "cgs2upd.15", "arnoldi.15", "spmv.A"]
     if info["mgr_levels"]:
         names += ["mgr.0.rres", "mgr.0.prolong"]
     for k in range(max(info["coarse_amg_levels"] - 1, 0)):
@@ -294,7 +313,8 @@ def run_sharded(args):
             from solve_model import SolveModel
             peak, peak_kind = peaks()
             mb = SolveModel(H, mx.load_strategy(STRATEGY)).solve_bytes(int(P.ptr[-1]), P.n,
-                                                                       int(round(its / args.steps)), RESTART)
+                                                                       int(round(its / args.steps)), RESTART,
+                                                                       ortho="cgs2")
             ts = t_max / args.steps
             solve_roof = {"bound": "hbm", "model_bytes_per_solve": mb["bytes"],
                           "achieved": mb["bytes"] / ts / 1e9, "peak": peak * world, "unit": "GB/s",
@@ -483,41 +503,52 @@ def main():
         from solve_model import SolveModel
         sm = SolveModel(H, mx.load_strategy(STRATEGY))
         its_solve = int(round(its / args.steps))
-        mb = sm.solve_bytes(int(P.ptr[-1]), P.n, its_solve, RESTART)
+        mb = sm.solve_bytes(int(P.ptr[-1]), P.n, its_solve, RESTART, ortho="cgs2")
         t_solve = ms * 1e-3 / args.steps
         solve_roof = {"bound": "hbm", "model_bytes_per_solve": mb["bytes"],
                       "achieved": mb["bytes"] / t_solve / 1e9, "peak": peak, "unit": "GB/s",
                       "frac": mb["bytes"] / t_solve / 1e9 / peak,
                       "precond_bytes_per_apply": mb["precond_bytes_per_apply"],
                       "spmv_bytes": mb["spmv_bytes"], "restart_cycles": mb["restart_cycles"],
-                      "model": "SURVEY 8(d) compulsory traffic per operation (tools/solve_model.py), "
-                               "MGS at 24n(k+1)+32n per step"}
+                      "model": "SURVEY 8(d) compulsory traffic per operation (tools/solve_model.py); "
+                               "low-sync orthogonalisation at 16n(k+3) per step"}
     except Exception as e:  # the model is reporting, never a reason to lose the line
         solve_roof = {"error": f"{type(e).__name__}: {e}"}
 
     variants = {}
-    vname = CONFIGS[CONFIG].get("variant")
-    if vname and not args.strategy and not args.no_variant:
-        Hv = mx.Hierarchy(A, P.partition, mx.load_strategy(vname), P.unknown_map)
-        step_v = lambda: (x.zero_(), torch.cuda.synchronize(), Hv.solve_device(b.data_ptr(), x.data_ptr(), cfg))[2]
-        step_v()
+
+    def time_solves(Hx, cfgx, reps):
+        stepx = lambda: (x.zero_(), torch.cuda.synchronize(), Hx.solve_device(b.data_ptr(), x.data_ptr(), cfgx))[2]
+        stepx()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
-        rv = [step_v() for _ in range(max(1, args.steps // 2))]
+        rv = [stepx() for _ in range(reps)]
         ev1.record()
         torch.cuda.synchronize()
-        msv = ev0.elapsed_time(ev1) / len(rv)
-        itv = sum(r.iterations for r in rv) / len(rv)
-        variants[vname] = {"value": P.n * itv / (msv * 1e-3), "unit": UNIT, "ms_per_step": msv,
-                           "iterations_per_solve": itv,
-                           "smoother": "hybrid_l1_gs (exact sequential Gauss-Seidel, sync-free sweep)"}
-        if "amg.0.pre" in probe_names(Hv):
-            gs_ms, gs_by = Hv.time_kernel("amg.0.pre", reps=5)
-            variants[vname]["dominant_kernel"] = {
-                "name": "k_gs (fine coarse-AMG level, forward sweep)", "avg_ms": gs_ms,
-                "achieved_GBps": gs_by / (gs_ms * 1e-3) / 1e9, "frac": gs_by / (gs_ms * 1e-3) / 1e9 / peak,
-                "bound": "latency (dependency chain of the sequential sweep)"}
-        del Hv
+        msx = ev0.elapsed_time(ev1) / len(rv)
+        itx = sum(r.iterations for r in rv) / len(rv)
+        return {"value": P.n * itx / (msx * 1e-3), "unit": UNIT, "ms_per_step": msx, "iterations_per_solve": itx}
+
+    if not args.no_variant:
+        # the reference's MGS orthogonalisation (bitwise parity mode), same strategy
+        variants["ortho_mgs"] = {**time_solves(H, mx.KrylovConfig(restart=RESTART, max_iters=500, rel_tol=RTOL,
+                                                                   ortho="mgs"), max(1, args.steps // 2)),
+                                 "strategy": STRATEGY, "ortho": "mgs (reference MGS, bitwise vs the oracle)"}
+    vnames = CONFIGS[CONFIG].get("variant") or []
+    if not args.strategy and not args.no_variant:
+        for vname in vnames:
+            Hv = mx.Hierarchy(A, P.partition, mx.load_strategy(vname), P.unknown_map)
+            reps = 1 if vname == "mfd_mgr_pi" else max(1, args.steps // 2)
+            variants[vname] = {**time_solves(Hv, cfg, reps), "strategy": vname,
+                               "smoother": "hybrid_l1_gs (AMG default; exact sequential Gauss-Seidel, sync-free sweep)",
+                               "shipped": vname in ("mfd_mgr_pi", "comp_mgr", "frac_mgr_u")}
+            if "amg.0.pre" in probe_names(Hv):
+                gs_ms, gs_by = Hv.time_kernel("amg.0.pre", reps=5)
+                variants[vname]["dominant_kernel"] = {
+                    "name": "k_gs (fine coarse-AMG level, forward sweep)", "avg_ms": gs_ms,
+                    "achieved_GBps": gs_by / (gs_ms * 1e-3) / 1e9, "frac": gs_by / (gs_ms * 1e-3) / 1e9 / peak,
+                    "bound": "latency (dependency chain of the sequential sweep)"}
+            del Hv
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1

@@ -92,6 +92,9 @@ MGRX_API const char* mgrx_last_error(void);
 /* devices: CUDA ordinals; this build drives devices[0] (one process per GPU). */
 MGRX_API int mgrx_create(const int* devices, int ndev, mgrx_ctx** out);
 MGRX_API int mgrx_destroy(mgrx_ctx* ctx);
+/* Device memory of the context's GPU held by libmgrx (stream-ordered pool):
+ * bytes in use now, reserved by the pool, and the in-use high-water mark. */
+MGRX_API int mgrx_device_memory(mgrx_ctx* ctx, long long* used, long long* reserved, long long* high);
 
 /* CSR with sorted, in-range columns and finite values (validate()). host
  * pointers; copied to HBM. */

@@ -99,6 +99,8 @@ def lib() -> C.CDLL:
         L.mgrx_local_group_create.argtypes = [C.c_int, C.POINTER(vp)]
         L.mgrx_local_group_destroy.argtypes = [vp]
         L.mgrx_shard_create.argtypes = [vp, C.c_int, C.c_int, vp, C.c_char_p, vp, C.POINTER(vp)]
+        L.mgrx_device_memory.argtypes = [vp, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong),
+                                         C.POINTER(C.c_longlong)]
         L.mgrx_shard_create_scatter.argtypes = [vp, vp, C.c_int, C.c_int, vp, C.c_char_p, vp, C.POINTER(vp)]
         L.mgrx_shard_rows.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.mgrx_shard_fused.argtypes = [vp, C.POINTER(C.c_int)]
@@ -130,6 +132,13 @@ class Context:
         dev = (C.c_int * 1)(device)
         _check(lib().mgrx_create(dev, 1, C.byref(self._h)))
         self.device = device
+
+    def memory(self) -> dict:
+        """libmgrx's device memory on this GPU (stream-ordered pool): bytes in
+        use, reserved, and the in-use high-water mark."""
+        u, r, h = C.c_longlong(), C.c_longlong(), C.c_longlong()
+        _check(lib().mgrx_device_memory(self._h, C.byref(u), C.byref(r), C.byref(h)))
+        return {"used": u.value, "reserved": r.value, "high": h.value}
 
     def close(self):
         if self._h:

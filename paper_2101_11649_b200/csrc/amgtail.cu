@@ -238,7 +238,7 @@ bool build_tail_blob(const std::vector<TailLevelHost>& lv, int nc, const std::ve
 }
 
 void prepare_amg_tail(const TailDesc& d) {
-  MGRX_CK(cudaFuncSetAttribute(k_amg_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, d.total_bytes));
+  ensure_smem(reinterpret_cast<const void*>(k_amg_tail), static_cast<size_t>(d.total_bytes));
 }
 
 void launch_amg_tail(const TailDesc& d, const unsigned char* blob, const double* r, double* z, cudaStream_t s) {

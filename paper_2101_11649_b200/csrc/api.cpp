@@ -263,6 +263,24 @@ int mgrx_create(const int* devices, int ndev, mgrx_ctx** out) {
   });
 }
 
+int mgrx_device_memory(mgrx_ctx* ctx, long long* used, long long* reserved, long long* high) {
+  return guarded([&] {
+    if (!ctx) throw InvalidArgument("mgrx_device_memory: null context");
+    use(ctx);
+    MGRX_CK(cudaStreamSynchronize(ctx->stream));
+    cudaMemPool_t pool;
+    MGRX_CK(cudaDeviceGetDefaultMemPool(&pool, ctx->device));
+    uint64_t u = 0, r = 0, h = 0;
+    MGRX_CK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &u));
+    MGRX_CK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &r));
+    MGRX_CK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &h));
+    if (used) *used = static_cast<long long>(u);
+    if (reserved) *reserved = static_cast<long long>(r);
+    if (high) *high = static_cast<long long>(h);
+    return MGRX_OK;
+  });
+}
+
 int mgrx_destroy(mgrx_ctx* ctx) {
   return guarded([&] {
     if (ctx) {

@@ -289,7 +289,7 @@ DCsr dense_solve_columns(const DenseLU& f, const DCsr& B, cudaStream_t s) {
     const DCsr Bt = transpose(B, s);
     const size_t sm = 2 * sizeof(double) * n;
     if (sm > 48 * 1024)
-      MGRX_CK(cudaFuncSetAttribute(k_dense_columns, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+      ensure_smem(reinterpret_cast<const void*>(k_dense_columns), static_cast<size_t>(static_cast<int>(sm)));
     k_dense_columns<<<m, kDT, sm, s>>>(n, f.lu.get(), f.perm.get(), Bt.ptr.get(), Bt.col.get(), Bt.val.get(),
                                        Xd.get());
     MGRX_LAUNCH_CK();

@@ -62,7 +62,11 @@ void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
   at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  MGRX_CK(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+  if (e != cudaSuccess)
+    throw RuntimeError(std::string("CUDA error: ") + cudaGetErrorString(e) + " (launch grid " +
+                       std::to_string(grid.x) + " block " + std::to_string(block.x) + " smem " + std::to_string(smem) +
+                       ")");
 }
 
 // Kernel attributes (dynamic shared memory opt-in, cluster flags) and SM
@@ -70,6 +74,10 @@ void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
 // so a second context on another GPU in the same process gets its own.
 bool first_on_device(const void* key);
 int device_sms();  // SM count of the current device (cached per device)
+// Raise kernel `kern`'s dynamic shared memory limit on the current device to
+// at least `bytes` (never lowers it: several hierarchies in one process size
+// the same kernel differently, and the attribute is per kernel, not per launch).
+void ensure_smem(const void* kern, size_t bytes);
 
 // Process-wide launch counter (the bench reports kernels launched in the
 // timed region; graph replays add their node count).

@@ -415,7 +415,7 @@ void prepare_panel_solve(int n) {
   size_t sm = 0;
   PanelKern k = panel_variant(n, sm);
   if (sm > 48 * 1024)
-    MGRX_CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+    ensure_smem(reinterpret_cast<const void*>(k), static_cast<size_t>(static_cast<int>(sm)));
 }
 void launch_panel_solve(int grid, int n, const int* bst, const long long* boff, const int* rows, const double* lu,
                         const int* perm, int n1, const double* b, double* x, cudaStream_t s) {
@@ -612,8 +612,7 @@ void build_slabs(DenseLU& f, cudaStream_t s) {
   const int ns = nmax;
   const size_t smem = sizeof(double) * (static_cast<size_t>(ns) * 32 + ns + 2);
   if (smem > 48 * 1024)
-    MGRX_CK(cudaFuncSetAttribute(k_lu_solve_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)));
+    ensure_smem(reinterpret_cast<const void*>(k_lu_solve_cluster), static_cast<size_t>(static_cast<int>(smem)));
   f.slab.alloc(static_cast<size_t>(f.nb) * C * ns * 32, s);
   const long long total = static_cast<long long>(f.nb) * C * ns * 32;
   const int grid = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 16));
@@ -746,12 +745,12 @@ void dense_factor(const DCsr& A, DenseLU& out, cudaStream_t s, double pivot_tol,
   if (n <= kWarpLuMax) {
     const int smw = static_cast<int>(sizeof(double) * n * n);
     if (smw > 48 * 1024)
-      MGRX_CK(cudaFuncSetAttribute(k_lu_solve_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, smw));
+      ensure_smem(reinterpret_cast<const void*>(k_lu_solve_warp), static_cast<size_t>(smw));
   }
   const size_t sm = sizeof(double) * n;
   if (sm > 200 * 1024) throw RuntimeError("dense LU solve: system too large for shared memory");
   if (sm > 48 * 1024)
-    MGRX_CK(cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+    ensure_smem(reinterpret_cast<const void*>(k_lu_solve), static_cast<size_t>(static_cast<int>(sm)));
   prepare_panel_solve(n);
   build_slabs(out, s);
   const int b = read_scalar(bad.get(), s);

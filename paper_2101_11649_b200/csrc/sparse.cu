@@ -35,6 +35,19 @@ bool first_on_device(const void* key) {
   return seen.insert({key, dev}).second;
 }
 
+void ensure_smem(const void* kern, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> lim;
+  if (bytes <= 48 * 1024) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& cur = lim[{kern, dev}];
+  if (bytes <= cur) return;
+  MGRX_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+  cur = bytes;
+}
+
 int device_sms() {
   static std::mutex mu;
   static std::map<int, int> sms;

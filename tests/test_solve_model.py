@@ -52,6 +52,13 @@ def test_mfd_model_terms():
     out = sm.solve_bytes(int(P.ptr[-1]), P.n, 35, 30)
     assert out["restart_cycles"] == 2
     assert out["bytes"] > 35 * (sm.m_prec + _spmv(int(P.ptr[-1]), P.n, P.n))
+    # low-sync orthogonalisation: 16 n (k+3) per step instead of 24 n (k+1) + 32 n,
+    # and no v0 scaling pass per cycle
+    ls = sm.solve_bytes(int(P.ptr[-1]), P.n, 35, 30, ortho="cgs2")
+    n = P.n
+    mgs_orth = sum(24.0 * n * (k + 1) + 32.0 * n for k in list(range(30)) + list(range(5)))
+    ls_orth = sum(16.0 * n * (k + 3) for k in list(range(30)) + list(range(5)))
+    assert np.isclose(out["bytes"] - ls["bytes"], mgs_orth - ls_orth + 2 * 16.0 * n)
 
 
 def test_comp_and_frac_models_run():

@@ -20,9 +20,14 @@ for this library, the CPU oracle and a reader recomputing it:
                          + 16|F|); other R kinds: residual + R SpMV + P-add
 * dense LU solve:        8 s^2 + 24 s per diagonal block s (block diagonal
                          coarse systems: the connected components)
-* GMRES step k:          SpMV(A) + M^-1 + MGS(k) = 24 n (k+1) + 32 n
+* GMRES step k:          SpMV(A) + M^-1 + orthogonalisation:
+                         MGS (ortho "mgs", SURVEY §8(d)): 24 n (k+1) + 32 n;
+                         lagged CGS2 (ortho "cgs2", lowsync.cu): two sweeps
+                         each reading V_0..V_{k-1}, U and w, the second
+                         writing v_k and U: 16 n (k+3)
 * per restart cycle:     initial residual + norm + scale (SpMV + 8n + 8n
-                         + 16n), V y (8 n k + 16 n), M^-1, x += z (24 n)
+                         + 16n; cgs2: no scale, r is U), V y (8 n k + 16 n),
+                         M^-1, x += z (24 n)
 
 Used by bench.py (`solve_roofline`). Walks the hierarchy through the public
 dump API (sizes, plus the level operator pattern for nnz(A_CF))."""
@@ -141,17 +146,18 @@ class SolveModel:
         return total
 
     # -- GMRES ----------------------------------------------------------
-    def solve_bytes(self, A_nnz: int, n: int, iterations: int, restart: int) -> dict:
+    def solve_bytes(self, A_nnz: int, n: int, iterations: int, restart: int, ortho: str = "mgs") -> dict:
         spmv_a = _spmv(A_nnz, n, n)
         steps, cycles, left = 0.0, 0, iterations
         while left > 0:
             ks = min(left, restart)
             for k in range(ks):
-                steps += spmv_a + self.m_prec + 24.0 * n * (k + 1) + 32.0 * n
+                orth = 16.0 * n * (k + 3) if ortho == "cgs2" else 24.0 * n * (k + 1) + 32.0 * n
+                steps += spmv_a + self.m_prec + orth
             cycles += 1
-            steps += spmv_a + 8.0 * n + 8.0 * n + 16.0 * n  # r0 = b - A x, norm, v0
+            steps += spmv_a + 8.0 * n + 8.0 * n + (0.0 if ortho == "cgs2" else 16.0 * n)  # r0, norm, v0
             steps += 8.0 * n * ks + 16.0 * n + self.m_prec + 24.0 * n  # x += M^-1 V y
             left -= ks
         steps += spmv_a + 8.0 * n + 8.0 * n  # final true residual
         return {"bytes": steps, "precond_bytes_per_apply": self.m_prec, "spmv_bytes": spmv_a,
-                "restart_cycles": cycles}
+                "restart_cycles": cycles, "ortho": ortho}
