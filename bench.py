@@ -227,11 +227,12 @@ def probe_names(H):
 
 
 def run_sharded(args):
-    """N > 1 (torchrun, one rank per GPU): every rank builds the same
-    hierarchy on its GPU, keeps its z-slab (mgrx_shard_create over NCCL) and
-    runs the sharded solve; gloo carries only the NCCL id and the max-over-
-    ranks timing. value = global DOF x iterations / (max over ranks of the
-    device-timed solve)."""
+    """N > 1 (one rank per GPU): rank 0 builds the global hierarchy on its GPU
+    and scatters every rank its slab plan (mgrx_shard_create_scatter over
+    NCCL); no other rank holds a global operator, and rank 0 drops the
+    global hierarchy once the shards exist. gloo carries only the NCCL id
+    and the max-over-ranks timing. value = global DOF x iterations / (max
+    over ranks of the device-timed solve)."""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -242,25 +243,45 @@ def run_sharded(args):
     os.environ.setdefault("MASTER_PORT", "29533")
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(local)
-    P = make_problem(world)
+    P = make_problem(world)  # host bundle (rhs slices, row starts); device setup on rank 0 only
     ctx = mx.Context(local)
-    A = mx.Matrix(P.ptr, P.col, P.val, ctx=ctx)
-    t0 = time.perf_counter()
-    H = mx.Hierarchy(A, P.partition, mx.load_strategy(STRATEGY), P.unknown_map)
-    setup_wall = time.perf_counter() - t0
+    H, setup_wall, solve_model = None, 0.0, None
+    if rank == 0:
+        A = mx.Matrix(P.ptr, P.col, P.val, ctx=ctx)
+        t0 = time.perf_counter()
+        H = mx.Hierarchy(A, P.partition, mx.load_strategy(STRATEGY), P.unknown_map)
+        setup_wall = time.perf_counter() - t0
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            from solve_model import SolveModel
+            solve_model = SolveModel(H, mx.load_strategy(STRATEGY))
+        except Exception as e:
+            solve_model = e
+        hinfo = H.info()
     obj = [mx.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     starts = mx.slab_row_starts(P, world)
-    S = mx.Shard(H, rank, world, starts, nccl_id=obj[0])
+    t0 = time.perf_counter()
+    S = mx.Shard(H, rank, world, starts, nccl_id=obj[0], scatter=True, ctx=ctx)
+    scatter_wall = time.perf_counter() - t0
+    if rank == 0:
+        if not isinstance(solve_model, Exception):
+            solve_model.H = None  # the model keeps only sizes
+        del H, A  # the shards do not reference the global hierarchy
+    import gc
+    gc.collect()
+    lo, hi = S.row_begin, S.row_end
     # NCCL communicator of this rank is up: log it and count the ranks that got there
     print(f"[bench rank {rank}/{world}] NCCL communicator ready on cuda:{local} "
-          f"(rows {S.row_begin}..{S.row_end}, fused Arnoldi exchange {bool(getattr(S, 'fused', False))})",
-          file=sys.stderr, flush=True)
+          f"(rows {lo}..{hi}, scattered setup {scatter_wall:.2f}s)", file=sys.stderr, flush=True)
     ready = torch.ones(1)
     dist.all_reduce(ready)
     nccl_ranks = int(ready.item())
     assert nccl_ranks == world, (nccl_ranks, world)
-    lo, hi = S.row_begin, S.row_end
+    mem = ctx.memory()
+    memt = torch.tensor([float(mem["used"]), float(mem["high"])], dtype=torch.float64)
+    mems = [torch.zeros(2, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(mems, memt)
     cfg = mx.KrylovConfig(restart=RESTART, max_iters=500, rel_tol=RTOL)
     dev = torch.device("cuda", local)
     b = torch.from_numpy(np.ascontiguousarray(P.rhs[lo:hi])).to(dev)
@@ -309,12 +330,10 @@ def run_sharded(args):
         # whole-job roofline: the single-GPU byte model of the global solve
         # (halo traffic excluded) over N GPUs' HBM for the max-over-ranks time
         try:
-            sys.path.insert(0, os.path.join(ROOT, "tools"))
-            from solve_model import SolveModel
+            if isinstance(solve_model, Exception):
+                raise solve_model
             peak, peak_kind = peaks()
-            mb = SolveModel(H, mx.load_strategy(STRATEGY)).solve_bytes(int(P.ptr[-1]), P.n,
-                                                                       int(round(its / args.steps)), RESTART,
-                                                                       ortho="cgs2")
+            mb = solve_model.solve_bytes(int(P.ptr[-1]), P.n, int(round(its / args.steps)), RESTART, ortho="cgs2")
             ts = t_max / args.steps
             solve_roof = {"bound": "hbm", "model_bytes_per_solve": mb["bytes"],
                           "achieved": mb["bytes"] / ts / 1e9, "peak": peak * world, "unit": "GB/s",
@@ -329,7 +348,11 @@ def run_sharded(args):
                 "scaling": scaling_kind(world), "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {**workload_config(P, world), "row_starts": [int(v) for v in starts]},
                 "iterations_per_solve": its / args.steps, "solve_time_s": t_max / args.steps,
-                "setup_wall_s": setup_wall, "hierarchy": H.info(),
+                "setup_wall_s": setup_wall, "scatter_wall_s": scatter_wall, "hierarchy": hinfo,
+                "setup": "rank 0 builds the global hierarchy and scatters slab plans (mgrx_shard_create_scatter); "
+                         "no other rank holds a global operator",
+                "device_mem_used_bytes_per_rank": [int(m[0].item()) for m in mems],
+                "device_mem_high_bytes_per_rank": [int(m[1].item()) for m in mems],
                 "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(nb.item()),
                         "d2h_bytes_per_step": int(nb.item()),
                         "path": "Shard.solve -> mgrx_shard_solve (C ABI) per rank, pinned host slices"},

@@ -436,8 +436,15 @@ int mgrx_solve(mgrx_hier* h, const double* b, double* x, const mgrx_krylov* cfg,
       MGRX_CK(cudaMemsetAsync(dx, 0, sizeof(double) * n, s));
     }
     MgrHier* H = &h->H;
-    const DevOp prec = [H](const double* in, double* out, cudaStream_t st) { H->apply_graph(in, out, st); };
-    const DevOp prec_rec = [H](const double* in, double* out, cudaStream_t st) { H->apply(in, out, st); };
+    // the bitwise parity mode (MGS) keeps the exact dense substitutions; the
+    // default low-sync solve applies dense coarse blocks via their inverses
+    const bool exact = k.ortho == kOrthoMgs;
+    const DevOp prec = [H, exact](const double* in, double* out, cudaStream_t st) {
+      H->apply_graph(in, out, st, exact);
+    };
+    const DevOp prec_rec = [H, exact](const double* in, double* out, cudaStream_t st) {
+      H->apply(in, out, st, exact);
+    };
     EventTimer t(s);
     GmresResult r = gmres_device(h->A, db, dx, k, prec, h->ws, s, prec_rec);
     const double solve_s = t.stop();

@@ -729,6 +729,7 @@ void dense_factor(const DCsr& A, DenseLU& out, cudaStream_t s, double pivot_tol,
       const int b = read_scalar(bad.get(), s);
       // the dense algorithm reports the first singular pivot in row order
       if (b != INT_MAX) throw RuntimeError("dense LU: matrix numerically singular (pivot " + std::to_string(b) + ")");
+      dense_build_inverse(out, s);
       return;
     }
   }
@@ -755,10 +756,133 @@ void dense_factor(const DCsr& A, DenseLU& out, cudaStream_t s, double pivot_tol,
   build_slabs(out, s);
   const int b = read_scalar(bad.get(), s);
   if (b >= 0) throw RuntimeError("dense LU: matrix numerically singular (pivot " + std::to_string(b) + ")");
+  dense_build_inverse(out, s);
 }
 
-void dense_solve(const DenseLU& f, const double* b, double* x, cudaStream_t s) {
+namespace {
+constexpr int kInvMax = 1024;   // rows per block for the explicit inverse
+constexpr long long kInvEntries = 16ll << 20;
+
+// Column j of block b's inverse = the LU solve of e_j (unit-lower forward,
+// upper backward substitution), one warp per column, the column held in
+// registers (lane l owns rows l, l+32, ...).
+__global__ void __launch_bounds__(256) k_lu_inverse(int nb, int n1, const int* __restrict__ bst,
+                                                    const long long* __restrict__ boff, const double* __restrict__ lu,
+                                                    const int* __restrict__ perm_all,
+                                                    const long long* __restrict__ ioff, double* __restrict__ inv) {
+  constexpr int kQ = kInvMax / 32;
+  const int b = blockIdx.y;
+  const int s = nb > 1 ? bst[b + 1] - bst[b] : n1;
+  const int j = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int l = threadIdx.x & 31;
+  if (j >= s) return;
+  const double* LU = lu + (nb > 1 ? boff[b] : 0);
+  const int* perm = perm_all + (nb > 1 ? bst[b] : 0);
+  double y[kQ];
+#pragma unroll
+  for (int q = 0; q < kQ; ++q) {
+    const int i = l + 32 * q;
+    y[q] = (i < s && perm[i] == j) ? 1.0 : 0.0;
+  }
+  for (int k = 0; k < s; ++k) {  // L y = P e_j
+    double v = 0.0;
+#pragma unroll
+    for (int q = 0; q < kQ; ++q)
+      if (q == (k >> 5)) v = y[q];
+    const double yk = __shfl_sync(0xffffffffu, v, k & 31);
+    const double* col = LU + static_cast<size_t>(k) * s;
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+      const int i = l + 32 * q;
+      if (i > k && i < s) y[q] = fma(-col[i], yk, y[q]);
+    }
+  }
+  for (int k = s - 1; k >= 0; --k) {  // U x = y
+    const double* col = LU + static_cast<size_t>(k) * s;
+    double v = 0.0;
+#pragma unroll
+    for (int q = 0; q < kQ; ++q)
+      if (q == (k >> 5)) v = y[q];
+    const double xk = __shfl_sync(0xffffffffu, v, k & 31) / col[k];
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+      const int i = l + 32 * q;
+      if (i == k) y[q] = xk;
+      else if (i < k) y[q] = fma(-col[i], xk, y[q]);
+    }
+  }
+  double* out = inv + ioff[b];
+#pragma unroll
+  for (int q = 0; q < kQ; ++q) {
+    const int i = l + 32 * q;
+    if (i < s) out[static_cast<size_t>(i) * s + j] = y[q];
+  }
+}
+
+// x[rows[p]] = sum_j inv_b(i, j) b[rows[bst_b + j]], warp per position p.
+__global__ void __launch_bounds__(256) k_inv_apply(int n, int nb, const int* __restrict__ bst,
+                                                   const int* __restrict__ rows, const int* __restrict__ pblk,
+                                                   const long long* __restrict__ ioff,
+                                                   const double* __restrict__ inv, const double* __restrict__ bv,
+                                                   double* __restrict__ x) {
+  pdl_enter();
+  const int p = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int l = threadIdx.x & 31;
+  if (p >= n) return;
+  const int b = nb > 1 ? pblk[p] : 0;
+  const int b0 = nb > 1 ? bst[b] : 0;
+  const int s = nb > 1 ? bst[b + 1] - b0 : n;
+  const int i = p - b0;
+  const double* row = inv + ioff[b] + static_cast<size_t>(i) * s;
+  double acc = 0.0;
+  for (int j = l; j < s; j += 32) acc = fma(__ldg(row + j), __ldg(bv + (rows ? __ldg(rows + b0 + j) : b0 + j)), acc);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (l == 0) x[rows ? rows[p] : p] = acc;
+}
+}  // namespace
+
+void dense_build_inverse(DenseLU& f, cudaStream_t s) {
+  f.has_inv = false;
+  if (f.n <= 0) return;
+  const int nb = f.nb;
+  std::vector<int> bst(nb + 1, 0);
+  if (nb > 1) bst = f.bst.download(nb + 1);
+  else bst[1] = f.n;
+  std::vector<long long> io(nb + 1, 0);
+  std::vector<int> pb(f.n);
+  int maxs = 0;
+  for (int b = 0; b < nb; ++b) {
+    const int sb = bst[b + 1] - bst[b];
+    maxs = std::max(maxs, sb);
+    io[b + 1] = io[b] + static_cast<long long>(sb) * sb;
+    for (int p = bst[b]; p < bst[b + 1]; ++p) pb[p] = b;
+  }
+  if (maxs > kInvMax || io[nb] > kInvEntries) return;
+  f.ioff.alloc(nb + 1, s);
+  f.ioff.upload(io.data(), nb + 1);
+  f.pblk.alloc(f.n, s);
+  f.pblk.upload(pb.data(), f.n);
+  f.inv.alloc(static_cast<size_t>(io[nb]), s);
+  const dim3 grid((maxs + 7) / 8, nb);
+  if (nb > 1)
+    k_lu_inverse<<<grid, 256, 0, s>>>(nb, f.n, f.bst.get(), f.boff.get(), f.blu.get(), f.perm.get(), f.ioff.get(),
+                                      f.inv.get());
+  else
+    k_lu_inverse<<<grid, 256, 0, s>>>(1, f.n, nullptr, nullptr, f.lu.get(), f.perm.get(), f.ioff.get(), f.inv.get());
+  MGRX_LAUNCH_CK();
+  count_launch();
+  f.has_inv = true;
+}
+
+void dense_solve(const DenseLU& f, const double* b, double* x, cudaStream_t s, bool exact) {
   if (f.n == 0) return;
+  if (!exact && f.has_inv) {
+    launch_pdl(k_inv_apply, dim3((f.n + 7) / 8), dim3(256), 0, s, f.n, f.nb, f.nb > 1 ? f.bst.get() : nullptr,
+               f.nb > 1 ? f.rows.get() : nullptr, f.nb > 1 ? f.pblk.get() : nullptr, f.ioff.get(), f.inv.get(), b, x);
+    count_launch();
+    return;
+  }
   if (f.ccl > 0) {
     launch_cluster_solve(f, b, x, s);
     return;

@@ -24,6 +24,16 @@ struct DenseLU {
   // slab[((b * ccl + c) * slab_n + j) * 32 + r] = M_b(32c + r, j); ccl = 0: off
   int ccl = 0, slab_n = 0;
   DVec<double> slab;
+  // explicit inverse of every diagonal block (blocks <= 1024 rows, <= 16M
+  // entries in all): inv row-major per block at ioff[b], pblk = block of each
+  // position of `rows`. Used by dense_solve(..., exact = false): a warp-per-
+  // row GEMV instead of the dependent triangular sweeps. The reference's LU
+  // solve is tolerance-level (Eigen's blocked order);
+  // exact = true keeps the unblocked substitution (bitwise vs the oracle).
+  bool has_inv = false;
+  DVec<double> inv;
+  DVec<long long> ioff;
+  DVec<int> pblk;
 };
 
 // Densify CSR A and factor it (per connected component when A is block
@@ -33,7 +43,10 @@ struct DenseLU {
 // allow_blocks = false keeps the single dense factor (callers that read lu).
 void dense_factor(const DCsr& A, DenseLU& out, cudaStream_t s, double pivot_tol = 1e-300,
                   bool allow_blocks = true);
-// x = A^{-1} b (x may alias nothing).
-void dense_solve(const DenseLU& f, const double* b, double* x, cudaStream_t s);
+// Build DenseLU::inv from the factors (no-op when the blocks are too large).
+void dense_build_inverse(DenseLU& f, cudaStream_t s);
+// x = A^{-1} b (x may alias nothing). exact = false and f.has_inv: the
+// explicit-inverse GEMV (tolerance-level; see DenseLU::inv).
+void dense_solve(const DenseLU& f, const double* b, double* x, cudaStream_t s, bool exact = true);
 
 }  // namespace mgrx

@@ -903,7 +903,7 @@ void MgrHier::setup(const DCsr& A, const std::vector<int>& labels, const std::ve
 
 void MgrHier::coarse_solve(const double* v, double* z, cudaStream_t s) {
   if (coarse_spec.kind == Coarse::dense_lu) {
-    dense_solve(coarse_lu, v, z, s);
+    dense_solve(coarse_lu, v, z, s, exact_dense_);
     return;
   }
   // z = V(v); z += V(v - A_c z) for the remaining cycles (mgr.cpp:181-186)
@@ -915,7 +915,11 @@ void MgrHier::coarse_solve(const double* v, double* z, cudaStream_t s) {
   }
 }
 
-void MgrHier::apply(const double* v, double* z, cudaStream_t s) { apply_level(0, v, z, s); }
+void MgrHier::apply(const double* v, double* z, cudaStream_t s, bool exact) {
+  exact_dense_ = exact;
+  apply_level(0, v, z, s);
+  exact_dense_ = true;
+}
 
 bool split_prolong_enabled() {
   static const bool on = [] {
@@ -931,23 +935,23 @@ void MgrHier::prolong(int l, const double* e, const double* zF, double* z, cudaS
   else spmv_prolong(L.P, e, L.fpos.get(), zF, z, s);
 }
 
-void MgrHier::apply_graph(const double* v, double* z, cudaStream_t s) {
+void MgrHier::apply_graph(const double* v, double* z, cudaStream_t s, bool exact) {
   static const bool enabled = [] {
     const char* e = std::getenv("MGRX_GRAPHS");
     return !(e && e[0] == '0');
   }();
   if (!enabled) {
-    apply(v, z, s);
+    apply(v, z, s, exact);
     return;
   }
-  auto it = graphs_.find({v, z});
+  auto it = graphs_.find({v, z, exact});
   if (it == graphs_.end()) {
     Captured c;
     const long long l0 = g_launches;
     cudaGraph_t g;
     MGRX_CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     try {
-      apply(v, z, s);
+      apply(v, z, s, exact);
     } catch (...) {
       cudaStreamEndCapture(s, &g);
       throw;
@@ -957,7 +961,7 @@ void MgrHier::apply_graph(const double* v, double* z, cudaStream_t s) {
     MGRX_CK(cudaGraphDestroy(g));
     c.nodes = g_launches - l0;
     g_launches = l0;
-    it = graphs_.emplace(std::make_pair(v, z), c).first;
+    it = graphs_.emplace(std::make_tuple(v, z, exact), c).first;
   }
   MGRX_CK(cudaGraphLaunch(it->second.exec, s));
   count_launch(it->second.nodes);

@@ -9,6 +9,7 @@
 #include <memory>
 #include <optional>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "amgtail.cuh"
@@ -107,11 +108,13 @@ struct MgrHier {
 
   void setup(const DCsr& A, const std::vector<int>& labels, const std::vector<std::string>& fields,
              const std::vector<int>* umap, const Strategy& strat, cudaStream_t s);
-  void apply(const double* v, double* z, cudaStream_t s);
+  // exact = false: dense coarse solves through their explicit inverses
+  // (tolerance-level; the default solve); exact = true: the bitwise path
+  void apply(const double* v, double* z, cudaStream_t s, bool exact = true);
   // z = [0 + zF; 0] + P e of level l (split form when available)
   void prolong(int l, const double* e, const double* zF, double* z, cudaStream_t s);
-  // Same, replayed from a CUDA graph captured once per (v, z) address pair.
-  void apply_graph(const double* v, double* z, cudaStream_t s);
+  // Same, replayed from a CUDA graph captured once per (v, z, exact).
+  void apply_graph(const double* v, double* z, cudaStream_t s, bool exact = true);
   void check(cudaStream_t s);
   ~MgrHier();
 
@@ -120,7 +123,8 @@ struct MgrHier {
     cudaGraphExec_t exec = nullptr;
     long long nodes = 0;
   };
-  std::map<std::pair<const double*, double*>, Captured> graphs_;
+  std::map<std::tuple<const double*, double*, bool>, Captured> graphs_;
+  bool exact_dense_ = true;
   void apply_level(int l, const double* v, double* z, cudaStream_t s);
   void coarse_solve(const double* v, double* z, cudaStream_t s);
 };

@@ -112,7 +112,7 @@ void Repl::solve(const double* r, double* z, ShardCtx& c) {
   d2d(pad.get(), r, own, c.s);
   c.comm->allgather(pad.get(), all.get(), maxc, c.s);
   pack(part.total(), map.get(), all.get(), full.get(), c.s);
-  dense_solve(*lu, full.get(), sol.get(), c.s);
+  dense_solve(*lu, full.get(), sol.get(), c.s, c.exact);
   d2d(z, sol.get() + part.lo(c.rank), own, c.s);
 }
 
@@ -481,7 +481,7 @@ void Shard::prec(const double* v, double* z) {
     apply_level(0, v, z);
     return;
   }
-  if (!graph || graph_in != v || graph_out != z) {
+  if (!graph || graph_in != v || graph_out != z || graph_exact != c.exact) {
     if (graph) cudaGraphExecDestroy(graph);
     graph = nullptr;
     cudaGraph_t g;
@@ -494,6 +494,7 @@ void Shard::prec(const double* v, double* z) {
     cudaGraphDestroy(g);
     graph_in = v;
     graph_out = z;
+    graph_exact = c.exact;
     g_launches = before;
   }
   MGRX_CK(cudaGraphLaunch(graph, c.s));
@@ -501,6 +502,7 @@ void Shard::prec(const double* v, double* z) {
 }
 
 void Shard::apply(const double* v, double* z) {
+  c.exact = true;
   const int n = spaces.front().own;
   // z may lack halo room: run into zext and copy out
   prec(v, zext.get());
@@ -519,6 +521,7 @@ GmresResult Shard::solve_lowsync(const double* b, double* x, const KrylovSpec& c
   const int n = spaces.front().own;
   cudaStream_t s = c.s;
   const int m = cfg.restart;
+  c.exact = false;  // dense blocks through their inverses (tolerance-level)
   ws.ensure(n, 1, s);
   ws.ls.ensure(n, m, s);
   LsDriver drv(ws.ls, n, m, ws.w.get());
@@ -607,6 +610,7 @@ GmresResult Shard::solve_lowsync(const double* b, double* x, const KrylovSpec& c
 GmresResult Shard::solve(const double* b, double* x, const KrylovSpec& cfg) {
   if (cfg.restart < 1) throw InvalidArgument("gmres: restart must be >= 1");
   if (cfg.ortho != kOrthoMgs && lowsync_supported(spaces.front().own, cfg.restart)) return solve_lowsync(b, x, cfg);
+  c.exact = true;
   const int n = spaces.front().own;
   cudaStream_t s = c.s;
   const int m = cfg.restart;

@@ -71,6 +71,7 @@ struct ShardCtx {
   Comm* comm = nullptr;
   cudaStream_t s = nullptr;
   int rank = 0, size = 1;
+  bool exact = true;  // false: replicated dense solves through their inverses (low-sync solve)
 };
 
 // Replicated dense solve: all-gather the distributed vector, solve on every
@@ -180,6 +181,7 @@ struct Shard {
   cudaGraphExec_t graph = nullptr;
   const double* graph_in = nullptr;
   double* graph_out = nullptr;
+  bool graph_exact = true;
   long long graph_nodes_ = 0;
 
   // replicated small parts this shard owns (dense coarse factors, the

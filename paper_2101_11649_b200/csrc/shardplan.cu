@@ -134,12 +134,6 @@ DVec<int> upload_ints(const std::vector<int>& v, cudaStream_t s) {
 
 void alloc_cap(DVec<double>& v, const Space& sp, cudaStream_t s) { v.alloc(sp.cap > 0 ? sp.cap : 1, s); }
 
-struct HostCsr {
-  int rows = 0, cols = 0;
-  std::vector<int> ptr, col;
-  std::vector<double> val;
-};
-
 // One rank's slab of an operator (rows of `rows` owned by the rank, columns
 // of `cols` renumbered [owned | halo]; entries keep their order, so every
 // row sum is the single-GPU one). recv / send: (peer, offset, count) triples.
@@ -260,13 +254,7 @@ struct Planner {
   const HostCsr& host(const DCsr& M) {
     auto it = mats.find(&M);
     if (it != mats.end()) return it->second;
-    HostCsr c;
-    c.rows = M.rows;
-    c.cols = M.cols;
-    c.ptr = dl(M.ptr, M.rows + 1, s);
-    c.col = dl(M.col, M.nnz, s);
-    c.val = dl(M.val, M.nnz, s);
-    return mats.emplace(&M, std::move(c)).first->second;
+    return mats.emplace(&M, to_host(M, s)).first->second;
   }
   void part_all(const Part& p) {
     for (PlanW& w : W) w.vec(p.st);

@@ -39,3 +39,4 @@ for k in (0, 3, 8, 15, 29):
             print(e)
 P = mx.comp_problem(100, 100, 50, wells=8, seed=20210130); run(P, "comp_mgr_l1j", 1e-5)
 P = mx.frac_problem(64, seed=20210131); run(P, "frac_mgr_u_l1j", 1e-6)
+P = mx.comp_problem(128, 128, 64, wells=16, seed=20210134); run(P, "comp_mgr_l1j", 1e-5)
