@@ -199,6 +199,10 @@ MGRX_API int mgrx_shard_create(mgrx_hier* h, int rank, int size, const int* row_
 MGRX_API int mgrx_shard_create_scatter(mgrx_ctx* ctx, mgrx_hier* h, int rank, int size, const int* row_starts,
                                        const unsigned char* nccl_id, mgrx_group* group, mgrx_shard** out);
 MGRX_API int mgrx_shard_rows(mgrx_shard* sd, int* row_begin, int* row_end);
+/* Device bytes allocated while building the hierarchy / this rank's shard
+ * (the setup footprint; the GMRES basis is allocated at the first solve). */
+MGRX_API int mgrx_hier_bytes(mgrx_hier* h, long long* bytes);
+MGRX_API int mgrx_shard_bytes(mgrx_shard* sd, long long* bytes);
 /* 1 when this shard's GMRES steps use the fused sharded Arnoldi kernel
  * (in-kernel partial exchange over NVLink; enabled after a bitwise
  * self-check on every rank), 0 for the all-gather path. No reference

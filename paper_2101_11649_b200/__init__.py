@@ -101,6 +101,8 @@ def lib() -> C.CDLL:
         L.mgrx_shard_create.argtypes = [vp, C.c_int, C.c_int, vp, C.c_char_p, vp, C.POINTER(vp)]
         L.mgrx_device_memory.argtypes = [vp, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong),
                                          C.POINTER(C.c_longlong)]
+        L.mgrx_hier_bytes.argtypes = [vp, C.POINTER(C.c_longlong)]
+        L.mgrx_shard_bytes.argtypes = [vp, C.POINTER(C.c_longlong)]
         L.mgrx_shard_create_scatter.argtypes = [vp, vp, C.c_int, C.c_int, vp, C.c_char_p, vp, C.POINTER(vp)]
         L.mgrx_shard_rows.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
         L.mgrx_shard_fused.argtypes = [vp, C.POINTER(C.c_int)]
@@ -335,6 +337,12 @@ class Hierarchy:
         return {"mgr_levels": m.value, "coarse_amg_levels": c.value,
                 "frelax_amg_levels": [fr[i] for i in range(m.value)]}
 
+    def device_bytes(self) -> int:
+        """Device bytes the setup allocated (matrix copy + hierarchy)."""
+        v = C.c_longlong()
+        _check(lib().mgrx_hier_bytes(self._h, C.byref(v)))
+        return v.value
+
     def amg_info(self, which: int = -1) -> dict:
         """AmgSetupInfo (proj/include/mgrkit/amg.hpp:35-39) of the MGR coarse
         AMG (which=-1) or of MGR level `which`'s F-relaxation AMG."""
@@ -451,6 +459,13 @@ class Shard:
         f = C.c_int()
         _check(lib().mgrx_shard_fused(self._h, C.byref(f)))
         self.fused = bool(f.value)  # fused sharded Arnoldi in use (one GPU per rank)
+
+    def device_bytes(self) -> int:
+        """Device bytes of this rank's shard (slabs, halo plans, replicated
+        small parts, work vectors), as allocated by the creating thread."""
+        v = C.c_longlong()
+        _check(lib().mgrx_shard_bytes(self._h, C.byref(v)))
+        return v.value
 
     def apply(self, v: np.ndarray) -> np.ndarray:
         v = np.ascontiguousarray(v, dtype=np.float64)

@@ -310,6 +310,9 @@ def main(argv=None):
                 return NO_CONVERGE
             return OK
         if a.cmd == "study":
+            # proj/tools/mgr_main.cpp:344-400: sizes outer, strategies inner;
+            # study.csv = report rows + "growth,<strategy>,<max/min>" lines;
+            # study.json = {"rows": [...], "growth": {strategy: ratio or null}}
             sizes = []
             for tok in a.sizes.split(","):
                 try:
@@ -317,24 +320,38 @@ def main(argv=None):
                 except ValueError:
                     raise UsageError(f"--sizes entry '{tok}' is not an integer")
             if len(sizes) < 2:
-                raise UsageError("--sizes needs at least two sizes")
+                raise UsageError("--sizes needs at least two refinements")
+            strategies = [t for t in a.strategies.split(",") if t]
+            if not strategies:
+                raise UsageError("--strategies needs at least one entry")
             rows = []
-            for strat in a.strategies.split(","):
-                its = []
-                for nsz in sizes:
-                    P = {"mfd": lambda k: mx.mfd_problem(k, k, k, "iid"),
-                         "comp": lambda k: mx.comp_problem(k, k, k, wells=2),
-                         "frac": lambda k: mx.frac_problem(k)}[a.problem](nsz)
+            for nsz in sizes:
+                P = {"mfd": lambda k: mx.mfd_problem(k, k, k, "iid"),
+                     "comp": lambda k: mx.comp_problem(k, k, k, wells=2),
+                     "frac": lambda k: mx.frac_problem(k)}[a.problem](nsz)
+                for strat in strategies:
                     _, row = run_solve(P, resolve_strategy(strat, P), strat, a.tol, a.restart, a.max_iters)
                     row["size"] = nsz
                     rows.append(row)
-                    its.append(row["iterations"])
-                growth = max(its) / max(min(its), 1)
-                print(f"{strat}: iterations {its} growth {growth:.2f}")
+            csv = CSV_HEADER + "\n" + "".join(csv_row(r) + "\n" for r in rows)
+            growth, all_conv = {}, True
+            for strat in strategies:
+                rs = [r for r in rows if r["strategy"] == strat]
+                if not all(r["converged"] for r in rs):
+                    csv += f"growth,{strat},unconverged\n"
+                    growth[strat] = None
+                    all_conv = False
+                    continue
+                its = [r["iterations"] for r in rs]
+                growth[strat] = max(its) / max(min(its), 1)
+                csv += f"growth,{strat},{growth[strat]:.4f}\n"
             os.makedirs(a.out, exist_ok=True)
+            with open(os.path.join(a.out, "study.csv"), "w") as f:
+                f.write(csv)
             with open(os.path.join(a.out, "study.json"), "w") as f:
-                json.dump(rows, f, indent=2)
-            return OK if all(r["converged"] for r in rows) else NO_CONVERGE
+                json.dump({"rows": rows, "growth": growth}, f, indent=2)
+            print(csv, end="")
+            return OK if all_conv else NO_CONVERGE
         return USAGE
     except UsageError as e:
         print(f"error: {e}", file=sys.stderr)

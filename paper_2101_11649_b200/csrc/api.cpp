@@ -32,6 +32,7 @@ struct mgrx_hier {
   MgrHier H;
   GmresWork ws;
   double setup_s = 0.0;
+  long long bytes = 0;     // device bytes allocated by the setup (thread counter)
   DVec<double> vin, vout;  // staging for host-pointer calls
   DVec<double> px, py, pz;  // roofline-probe operands
   DVec<char> flushbuf;      // probe: L2 flush before each timed launch
@@ -45,6 +46,7 @@ struct mgrx_group {
 struct mgrx_shard {
   mgrx_ctx* ctx = nullptr;
   double setup_s = 0.0;    // hierarchy setup (root) + plan / scatter / load
+  long long bytes = 0;     // device bytes of this rank's shard (built on this thread)
   cudaStream_t stream = nullptr;
   std::unique_ptr<Shard> sh;
   DVec<double> vin, vout;
@@ -366,6 +368,7 @@ int mgrx_setup(mgrx_ctx* ctx, mgrx_mat* A, const int* labels, int nfields, const
     if (unknown_map) umap.assign(unknown_map, unknown_map + n);
     auto h = std::make_unique<mgrx_hier>();
     h->ctx = ctx;
+    const long long b0 = thread_device_bytes();
     EventTimer t(s);
     h->A = csr_copy(A->A, s);
     h->H.setup(h->A, lab, fields, unknown_map ? &umap : nullptr, strat, s);
@@ -373,6 +376,7 @@ int mgrx_setup(mgrx_ctx* ctx, mgrx_mat* A, const int* labels, int nfields, const
     h->setup_s = t.stop();
     h->vin.alloc(n > 0 ? n : 1, s);
     h->vout.alloc(n > 0 ? n : 1, s);
+    h->bytes = thread_device_bytes() - b0;
     *out = h.release();
     return MGRX_OK;
   });
@@ -683,6 +687,7 @@ int mgrx_shard_create(mgrx_hier* h, int rank, int size, const int* row_starts, c
     auto* sd = new mgrx_shard;
     sd->ctx = h->ctx;
     sd->setup_s = h->setup_s;
+    const long long b0 = thread_device_bytes();
     try {
       MGRX_CK(cudaStreamCreateWithFlags(&sd->stream, cudaStreamNonBlocking));
       MGRX_CK(cudaStreamSynchronize(h->ctx->stream));
@@ -691,6 +696,7 @@ int mgrx_shard_create(mgrx_hier* h, int rank, int size, const int* row_starts, c
       const int own = sd->sh->row_end - sd->sh->row_begin;
       sd->vin.alloc(own, sd->stream);
       sd->vout.alloc(own, sd->stream);
+      sd->bytes = thread_device_bytes() - b0;
     } catch (...) {
       delete sd;
       throw;
@@ -724,6 +730,7 @@ int mgrx_shard_create_scatter(mgrx_ctx* ctx, mgrx_hier* h, int rank, int size, c
     }
     auto* sd = new mgrx_shard;
     sd->ctx = ctx;
+    const long long b0 = thread_device_bytes();
     try {
       const auto t0 = std::chrono::steady_clock::now();
       MGRX_CK(cudaStreamCreateWithFlags(&sd->stream, cudaStreamNonBlocking));
@@ -736,11 +743,28 @@ int mgrx_shard_create_scatter(mgrx_ctx* ctx, mgrx_hier* h, int rank, int size, c
       MGRX_CK(cudaStreamSynchronize(sd->stream));
       sd->setup_s = (h ? h->setup_s : 0.0) +
                     std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      sd->bytes = thread_device_bytes() - b0;
     } catch (...) {
       delete sd;
       throw;
     }
     *out = sd;
+    return MGRX_OK;
+  });
+}
+
+int mgrx_hier_bytes(mgrx_hier* h, long long* bytes) {
+  return guarded([&] {
+    if (!h || !bytes) throw InvalidArgument("mgrx_hier_bytes: null argument");
+    *bytes = h->bytes;
+    return MGRX_OK;
+  });
+}
+
+int mgrx_shard_bytes(mgrx_shard* sd, long long* bytes) {
+  return guarded([&] {
+    if (!sd || !bytes) throw InvalidArgument("mgrx_shard_bytes: null argument");
+    *bytes = sd->bytes;
     return MGRX_OK;
   });
 }

@@ -84,6 +84,11 @@ void ensure_smem(const void* kern, size_t bytes);
 extern long long g_launches;
 inline void count_launch(long long k = 1) { g_launches += k; }
 
+// Device bytes held by DVec allocations made on the calling thread (frees
+// are credited to the allocating thread's counter too). Lets a rank that is
+// a thread (local groups) measure the footprint of what it built.
+long long& thread_device_bytes();
+
 // Stream-ordered device buffer (cudaMallocAsync on the owning stream).
 template <class T>
 class DVec {
@@ -107,12 +112,20 @@ class DVec {
     n_ = n;
     s_ = s;
     // +32 bytes: bulk (TMA) copies round slices out to 16-byte multiples
-    if (n_) MGRX_CK(cudaMallocAsync(reinterpret_cast<void**>(&p_), n_ * sizeof(T) + 32, s_));
+    if (n_) {
+      MGRX_CK(cudaMallocAsync(reinterpret_cast<void**>(&p_), n_ * sizeof(T) + 32, s_));
+      ctr_ = &thread_device_bytes();
+      *ctr_ += static_cast<long long>(n_ * sizeof(T) + 32);
+    }
   }
   void release() {
-    if (p_) cudaFreeAsync(p_, s_);
+    if (p_) {
+      cudaFreeAsync(p_, s_);
+      if (ctr_) *ctr_ -= static_cast<long long>(n_ * sizeof(T) + 32);
+    }
     p_ = nullptr;
     n_ = 0;
+    ctr_ = nullptr;
   }
   void zero() {
     if (n_) MGRX_CK(cudaMemsetAsync(p_, 0, n_ * sizeof(T), s_));
@@ -137,12 +150,14 @@ class DVec {
     std::swap(p_, o.p_);
     std::swap(n_, o.n_);
     std::swap(s_, o.s_);
+    std::swap(ctr_, o.ctr_);
   }
 
  private:
   T* p_ = nullptr;
   size_t n_ = 0;
   cudaStream_t s_ = nullptr;
+  long long* ctr_ = nullptr;  // the allocating thread's byte counter
 };
 
 inline int blocks_for(int64_t n, int threads) {

@@ -550,6 +550,104 @@ __global__ void __launch_bounds__(kPipeThreads)
   }
 }
 
+// Block-partitioned sweep from zero (dep-only entries). A CTA takes the next
+// row block (processing order) from a ticket counter, so every block it
+// waits on was taken earlier by a running CTA (deadlock-free). The block's
+// rows are swept in local dependency-level order with its iterate in shared
+// memory (xs, indexed by row - lo), chunks of steps double-buffered by
+// cp.async exactly as in k_gs_small. Entries flagged kCrossBit depend on an
+// earlier block: the value is polled from xnew (pre-filled with the pending
+// pattern; published with one relaxed 64-bit store). Per row: the
+// reference's operations in its order (bitwise equal).
+constexpr int kCrossBit = 1 << 30;
+__global__ void __launch_bounds__(kPipeThreads)
+    k_gs_blk(int nblk, const int* __restrict__ blk_lo, const int* __restrict__ blk_chunk,
+             int nsteps, const int* __restrict__ steps, const int* __restrict__ chunks,
+             const int* __restrict__ order, const int* __restrict__ sptr, const int* __restrict__ scol,
+             const double* __restrict__ sval, const double* __restrict__ sd, const double* __restrict__ bp,
+             double* xnew, double* zadd, int* tk) {
+  extern __shared__ __align__(16) unsigned char blk_raw[];
+  SmallBuf* buf = reinterpret_cast<SmallBuf*>(blk_raw);
+  double* xs = reinterpret_cast<double*>(blk_raw + 2 * sizeof(SmallBuf));
+  const int tid = threadIdx.x;
+  __shared__ int bidx;
+  auto SP = [&](int q) { return steps[q]; };
+  auto SE = [&](int q) { return steps[nsteps + 1 + q]; };
+  auto issue = [&](int c, SmallBuf& B) {
+    const int sa = chunks[c], sb = chunks[c + 1];
+    const int p0 = SP(sa), p1 = SP(sb);
+    const int nr = p1 - p0;
+    const int e0 = SE(sa), e1 = SE(sb);
+    for (int q = tid; q < nr; q += kPipeThreads) {
+      cpa4(&B.ord[q], order + p0 + q);
+      cpa8(&B.sd[q], sd + p0 + q);
+      cpa8(&B.bp[q], bp + p0 + q);
+    }
+    for (int q = tid; q <= nr; q += kPipeThreads) cpa4(&B.ptr[q], sptr + p0 + q);
+    for (int q = tid; q < e1 - e0; q += kPipeThreads) {
+      cpa4(&B.col[q], scol + e0 + q);
+      cpa8(&B.val[q], sval + e0 + q);
+    }
+    cpa_commit();
+  };
+  while (true) {
+    if (tid == 0) bidx = atomicAdd(tk, 1);
+    __syncthreads();
+    const int bk = bidx;
+    if (bk >= nblk) return;
+    const int lo = blk_lo[bk];
+    const int c0 = blk_chunk[bk], c1 = blk_chunk[bk + 1];
+    issue(c0, buf[0]);
+    for (int c = c0; c < c1; ++c) {
+      SmallBuf& B = buf[(c - c0) & 1];
+      if (c + 1 < c1) issue(c + 1, buf[(c + 1 - c0) & 1]);
+      else cpa_commit();
+      cpa_wait1();
+      __syncthreads();
+      const int cbase = SP(chunks[c]);
+      for (int st = chunks[c]; st < chunks[c + 1]; ++st) {
+        const int qa = SP(st) - cbase, qb = SP(st + 1) - cbase;
+        const int e0 = B.ptr[0];
+        for (int q = qa + tid; q < qb; q += kPipeThreads) {
+          const int i = B.ord[q];
+          double s = B.bp[q];
+          const int k1 = B.ptr[q + 1] - e0;
+          auto xval = [&](int cc) -> double {
+            if (!(cc & kCrossBit)) return xs[cc];
+            const double* p = xnew + (cc & ~kCrossBit);
+            double v = ld_relaxed(p);
+            long long spins = 0;
+            while (pending_value(v)) {
+              if (++spins > kSpinLimit) {
+                atomicExch(tk + 1, 1);
+                return 0.0;
+              }
+              __nanosleep(32);
+              v = ld_relaxed(p);
+            }
+            return v;
+          };
+          int k = B.ptr[q] - e0;
+          for (; k + 4 <= k1; k += 4) {
+            const int cc0 = B.col[k], cc1 = B.col[k + 1], cc2 = B.col[k + 2], cc3 = B.col[k + 3];
+            const double x0 = xval(cc0), x1 = xval(cc1), x2 = xval(cc2), x3 = xval(cc3);
+            const double p0 = __dmul_rn(B.val[k], x0), p1 = __dmul_rn(B.val[k + 1], x1);
+            const double p2 = __dmul_rn(B.val[k + 2], x2), p3 = __dmul_rn(B.val[k + 3], x3);
+            s = __dsub_rn(__dsub_rn(__dsub_rn(__dsub_rn(s, p0), p1), p2), p3);
+          }
+          for (; k < k1; ++k) s = __dsub_rn(s, __dmul_rn(B.val[k], xval(B.col[k])));
+          const double v = __dadd_rn(0.0, __ddiv_rn(s, B.sd[q]));
+          xs[i - lo] = v;
+          st_relaxed(xnew + i, v);
+          if (zadd) zadd[i] = __dadd_rn(zadd[i], v);
+        }
+        __syncthreads();
+      }
+    }
+    __syncthreads();  // buffers and xs are reused by the next block
+  }
+}
+
 // Group consecutive sweep steps into chunks of <= rows_cap rows / ent_cap
 // entries (st: step row boundaries, ptr: the sweep CSR's row pointer).
 std::vector<int> small_chunks(const std::vector<int>& st, const std::vector<int>& ptr, int rows_cap, int ent_cap) {
@@ -731,6 +829,138 @@ void trace_end(Trace& tr, const char* dir, const GsSchedule& sch, int n, cudaStr
   }
 }
 
+int gs_blk_rows() {
+  static const int v = [] {
+    const char* e = std::getenv("MGRX_GS_BLK_ROWS");
+    const int r = e ? std::atoi(e) : kSmallN;
+    return r <= 0 ? 0 : std::min(r, kSmallN);
+  }();
+  return v;
+}
+
+// Block plan of the block-partitioned sweep (see k_gs_blk and GsSchedule).
+bool build_block_plan(const DCsr& A, bool forward, const double* d, const int* owner, GsSchedule& out,
+                      cudaStream_t s) {
+  const int n = A.rows;
+  const int B = gs_blk_rows();
+  if (B <= 0 || n <= B) return false;
+  const HostCsr h = to_host(A, s);
+  std::vector<int> own;
+  if (owner) {
+    own.resize(n);
+    MGRX_CK(cudaMemcpyAsync(own.data(), owner, sizeof(int) * n, cudaMemcpyDeviceToHost, s));
+  }
+  std::vector<double> dh(n);
+  MGRX_CK(cudaMemcpyAsync(dh.data(), d, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+  MGRX_CK(cudaStreamSynchronize(s));
+  auto dep = [&](int i, int j) {
+    return (forward ? j < i : j > i) && (own.empty() || own[j] == own[i]);
+  };
+  const int nb = (n + B - 1) / B;
+  std::vector<int> lev(n, 0);
+  std::vector<int> pos_row, sp{0}, sc;
+  std::vector<double> sv, sdv;
+  std::vector<int> steps{0}, step_e, chunks{0}, blo, bch;
+  step_e.push_back(0);
+  for (int t = 0; t < nb; ++t) {
+    const int b = forward ? t : nb - 1 - t;
+    const int lo = b * B, hi = std::min(n, lo + B);
+    int maxl = 0;
+    for (int u = 0; u < hi - lo; ++u) {
+      const int i = forward ? lo + u : hi - 1 - u;
+      int m = 0;
+      for (int k = h.ptr[i]; k < h.ptr[i + 1]; ++k) {
+        const int j = h.col[k];
+        if (dep(i, j) && j >= lo && j < hi) m = std::max(m, lev[j] + 1);
+      }
+      lev[i] = m;
+      maxl = std::max(maxl, m);
+    }
+    // rows by (local level, row index)
+    std::vector<int> cnt(maxl + 2, 0);
+    for (int i = lo; i < hi; ++i) ++cnt[lev[i] + 1];
+    for (int l = 0; l <= maxl; ++l) cnt[l + 1] += cnt[l];
+    std::vector<int> rows(hi - lo);
+    {
+      std::vector<int> at(cnt.begin(), cnt.end() - 1);
+      for (int i = lo; i < hi; ++i) rows[at[lev[i]]++] = i;
+    }
+    blo.push_back(lo);
+    bch.push_back(static_cast<int>(chunks.size()) - 1);
+    const int pbase = static_cast<int>(pos_row.size());
+    for (int i : rows) {
+      pos_row.push_back(i);
+      sdv.push_back(dh[i]);
+      for (int k = h.ptr[i]; k < h.ptr[i + 1]; ++k) {
+        const int j = h.col[k];
+        if (!dep(i, j)) continue;
+        sc.push_back((j >= lo && j < hi) ? j - lo : (j | kCrossBit));
+        sv.push_back(h.val[k]);
+      }
+      if (static_cast<int>(sc.size()) - sp.back() > kSmallEnt) return false;
+      sp.push_back(static_cast<int>(sc.size()));
+    }
+    // steps: runs of one local level within the buffer caps; chunks: runs
+    // of consecutive steps within the same caps
+    const int first_step = static_cast<int>(steps.size()) - 1;
+    for (int l = 0; l <= maxl; ++l) {
+      int p = pbase + cnt[l];
+      const int pe = pbase + cnt[l + 1];
+      while (p < pe) {
+        int q = p;
+        while (q < pe && q - p < kSmallRows && sp[q + 1] - sp[p] <= kSmallEnt) ++q;
+        if (q == p) ++q;
+        steps.push_back(q);
+        step_e.push_back(sp[q]);
+        p = q;
+      }
+    }
+    const int last_step = static_cast<int>(steps.size()) - 1;
+    int a = first_step;
+    while (a < last_step) {
+      int c = a + 1;
+      while (c < last_step && steps[c + 1] - steps[a] <= kSmallRows && sp[steps[c + 1]] - sp[steps[a]] <= kSmallEnt)
+        ++c;
+      chunks.push_back(c);
+      a = c;
+    }
+  }
+  bch.push_back(static_cast<int>(chunks.size()) - 1);
+  out.nblk = nb;
+  out.blk_lo.alloc(nb, s);
+  out.blk_lo.upload(blo.data(), nb);
+  out.blk_chunk.alloc(nb + 1, s);
+  out.blk_chunk.upload(bch.data(), nb + 1);
+  out.border.alloc(n, s);
+  out.border.upload(pos_row.data(), n);
+  out.bsptr.alloc(n + 1, s);
+  out.bsptr.upload(sp.data(), n + 1);
+  const size_t ne = sc.size();
+  out.bscol.alloc(ne > 0 ? ne : 1, s);
+  out.bscol.upload(sc.data(), ne);
+  out.bsval.alloc(ne > 0 ? ne : 1, s);
+  out.bsval.upload(sv.data(), ne);
+  out.bsd.alloc(n, s);
+  out.bsd.upload(sdv.data(), n);
+  out.bbp.alloc(n, s);
+  out.nbsteps = static_cast<int>(steps.size()) - 1;
+  std::vector<int> stv(steps);
+  stv.insert(stv.end(), step_e.begin(), step_e.end());
+  out.bsteps.alloc(stv.size(), s);
+  out.bsteps.upload(stv.data(), stv.size());
+  out.nbchunks = static_cast<int>(chunks.size()) - 1;
+  out.bchunks.alloc(chunks.size(), s);
+  out.bchunks.upload(chunks.data(), chunks.size());
+  MGRX_CK(cudaStreamSynchronize(s));
+  if (const char* v = std::getenv("MGRX_VERBOSE"); v && v[0] == '1') {
+    int maxdepth = 0;
+    for (int i = 0; i < n; ++i) maxdepth = std::max(maxdepth, lev[i] + 1);
+    std::fprintf(stderr, "[mgrx] gs block plan: n=%d blocks=%d rows/block<=%d max local depth %d steps %d chunks %d\n",
+                 n, nb, B, maxdepth, out.nbsteps, out.nbchunks);
+  }
+  return true;
+}
+
 void gs_schedule(const DCsr& A, bool forward, const double* d, bool full, GsSchedule& out,
                  cudaStream_t s, const int* owner) {
   const int n = A.rows;
@@ -838,6 +1068,8 @@ void gs_schedule(const DCsr& A, bool forward, const double* d, bool full, GsSche
       out.small = 1;
     }
   }
+  out.blk = 0;
+  if (n > kSmallN && mode == 0 && !out.small) out.blk = build_block_plan(A, forward, d, owner, out, s) ? 1 : 0;
   if (mode == 2) {
     const std::vector<int> dp = out.dptr.download(n + 1);
     bool ok = true;
@@ -894,6 +1126,19 @@ void gs_sweep(const DCsr& A, const GsSchedule& sch, const double* d, const doubl
       k_gs_small<false><<<1, kPipeThreads, kSmallSmem, s>>>(sch.ndsteps, sch.dsteps.get(), sch.ndchunks,
                                                             sch.dchunks.get(), sch.order.get(), sp, sc, sv,
                                                             sch.sd.get(), sch.bp.get(), xold, xnew, zadd);
+    MGRX_LAUNCH_CK();
+    count_launch(2);
+    return;
+  }
+  if (sch.blk && !full_sweep) {
+    MGRX_CK(cudaMemsetAsync(scr.ticket_err.get(), 0, sizeof(int), s));
+    MGRX_CK(cudaMemsetAsync(xnew, 0xff, sizeof(double) * n, s));
+    k_gather_d<<<blocks_for(n, 256), 256, 0, s>>>(n, sch.border.get(), b, const_cast<double*>(sch.bbp.get()));
+    const int grid = std::min(sch.nblk, device_sms());
+    k_gs_blk<<<grid, kPipeThreads, kSmallSmem, s>>>(sch.nblk, sch.blk_lo.get(), sch.blk_chunk.get(), sch.nbsteps,
+                                                     sch.bsteps.get(), sch.bchunks.get(), sch.border.get(),
+                                                     sch.bsptr.get(), sch.bscol.get(), sch.bsval.get(),
+                                                     sch.bsd.get(), sch.bbp.get(), xnew, zadd, scr.ticket_err.get());
     MGRX_LAUNCH_CK();
     count_launch(2);
     return;
@@ -996,6 +1241,7 @@ void gs_bind_scratch(GsScratch& scr, cudaStream_t s) {
   if (first_on_device(reinterpret_cast<const void*>(&gs_bind_scratch))) {
     MGRX_CK(cudaFuncSetAttribute(k_gs_small<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmallSmem)));
     MGRX_CK(cudaFuncSetAttribute(k_gs_small<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmallSmem)));
+    MGRX_CK(cudaFuncSetAttribute(k_gs_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmallSmem)));
     MGRX_CK(cudaFuncSetAttribute(k_gs_pipe<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kPipeSmem)));
     MGRX_CK(cudaFuncSetAttribute(k_gs_pipe<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kPipeSmem)));
     MGRX_CK(cudaFuncSetAttribute(k_gs_lv<false, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));

@@ -42,6 +42,18 @@ struct GsSchedule {
   DVec<int> dchunks, fchunks;
   int ndchunks = 0, nfchunks = 0;
   DVec<double> bp;                 // rhs gathered into sweep order (pipelined sweep)
+  // Block-partitioned sweep (default for n > 12288, sweeps from zero): the
+  // rows are cut into contiguous blocks of <= 12288 (processed in sweep
+  // direction); one CTA sweeps a block with its part of the iterate in
+  // shared memory, rows in local dependency-level order, so a dependency
+  // inside the block costs a barrier; dependencies on earlier blocks are
+  // polled from global memory (the value is its own ready flag).
+  int blk = 0, nblk = 0;
+  DVec<int> blk_lo, blk_chunk;     // per block in processing order: first row, first chunk (nblk + 1)
+  DVec<int> border, bsptr, bscol;  // positions in (block, local level) order; dep-only sweep CSR
+  DVec<double> bsval, bsd, bbp;    // entry values, d and rhs in that order
+  DVec<int> bsteps, bchunks;       // steps (positions, then entry offsets), chunks (step ranges)
+  int nbsteps = 0, nbchunks = 0;
 };
 // owner (nullable): range id per row for a multi-range hybrid partition;
 // dependencies are then only the earlier rows of the row's own range.

@@ -26,6 +26,13 @@ bool pdl_enabled() {
 
 long long g_launches = 0;
 
+long long& thread_device_bytes() {
+  // heap-allocated and never freed: a DVec released after its allocating
+  // thread has exited still finds its counter
+  thread_local long long* c = new long long(0);
+  return *c;
+}
+
 bool first_on_device(const void* key) {
   static std::mutex mu;
   static std::set<std::pair<const void*, int>> seen;

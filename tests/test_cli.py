@@ -61,3 +61,25 @@ def test_cli_solve_on_gpu(tmp_path):
     assert rep["converged"] and rep["true_residual"] <= 1e-6 and rep["dofs"] == 16800
     x = cli.mm_read_vector(str(tmp_path / "o" / "x.mtx"))
     assert x.size == 16800
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("problem,sizes,strategies,tol,ceiling", [
+    ("mfd", "8,16,32", "mfd_mgr_pi,mfd_mgr_pi_c1_l1j", 1e-7, 30),   # SPEC.md:750 criterion 6 (TPFA, MGR_pi)
+    ("comp", "8,12,16", "comp_mgr,comp_mgr_l1j", 1e-6, 40),           # criterion 7 (2 wells)
+    ("frac", "8,12,16", "frac_mgr_u,frac_mgr_u_l1j", 1e-6, 60),      # criterion 8 (MGR_U, ratio <= 1.5)
+])
+def test_cli_study_mesh_independence_on_gpu(tmp_path, problem, sizes, strategies, tol, ceiling):
+    """The `study` mirror (proj/tools/mgr_main.cpp:344-400) on the GPU path: every
+    refinement converges, iteration counts stay under the SPEC ceilings and the
+    max/min growth ratio per strategy is <= 1.5."""
+    rc = cli.main(["study", "--problem", problem, "--sizes", sizes, "--strategies", strategies, "--tol", str(tol),
+                   "--restart", "30", "--out", str(tmp_path)])
+    assert rc == 0
+    out = json.loads((tmp_path / "study.json").read_text())
+    assert len(out["rows"]) == len(sizes.split(",")) * len(strategies.split(","))
+    for r in out["rows"]:
+        assert r["converged"] and r["iterations"] <= ceiling, r
+    for s, g in out["growth"].items():
+        assert g is not None and g <= 1.5, (s, g, [r["iterations"] for r in out["rows"] if r["strategy"] == s])
+    assert (tmp_path / "study.csv").read_text().count("growth,") == len(strategies.split(","))

@@ -136,6 +136,10 @@ def test_scatter_setup_equals_replicated(kind, size):
     gr = mx.LocalGroup(size)
     repl = [mx.Shard(H, r, size, starts, group=gr) for r in range(size)]
     assert [s.row_begin for s in shards] == list(starts[:-1])
+    # each rank's footprint is its slab (plus small replicated coarse parts)
+    assert all(s.device_bytes() > 0 for s in shards)
+    if kind in ("mfd", "comp", "frac"):
+        assert all(s.device_bytes() < H.device_bytes() for s in shards), [s.device_bytes() for s in shards]
     zs = _run(shards, lambda s: s.apply(v[s.row_begin:s.row_end]))
     for s, zr in zip(shards, zs):
         assert np.array_equal(zr.view(np.int64), z[s.row_begin:s.row_end].view(np.int64)), (kind, s.row_begin)
