@@ -485,39 +485,41 @@ def main():
             probes[name] = {"avg_ms": ms_k, "bytes": by, "GBps": by / (ms_k * 1e-3) / 1e9}
         except mx.MgrxError as e:
             probes[name] = {"error": str(e)}
-    # roofline object: the fused Arnoldi step (k_arnoldi2: both MGS passes of
-    # one GMRES step in one persistent launch), the largest single kernel (35%
-    # of cfg2 solve kernel time in 73 launches, profiles/r01/launch_shares.txt);
-    # the staged SpMV function k_spmv_staged has 40% spread over ~1,200
-    # launches on ~15 matrices and is reported beside it (dominant_by_share,
-    # with its largest instance, the fine operator). arnoldi.15 is the step at
-    # the mean Krylov index of a 30-step restart cycle. For other strategies
-    # take the probe with the largest time.
+    # roofline object: the dominant kernel by time share of one timed solve.
+    # profiles/r02/launch_shares_cfg2.txt: k_spmv_staged 47% (1,217 launches
+    # on the fine operator, the AMG levels 0-2 and the transfers), k_ls_update
+    # 14%, k_ls_dots 12% (73 launches each) -- k_spmv_staged also leads cfg3-5.
+    # It is measured on its largest instance, the fine operator (spmv.A: the
+    # GMRES SpMV, same plan and kernel as the AMG level-0 passes); the two
+    # low-sync Arnoldi sweeps are reported beside it at the mean Krylov index
+    # of a 30-step cycle (k = 15). Other strategies: the probe with the
+    # largest time.
     share = {k: v["avg_ms"] for k, v in probes.items() if "avg_ms" in v}
-    if "l1j" in STRATEGY:
-        dom = "arnoldi.15" if "avg_ms" in probes.get("arnoldi.15", {}) else "mgs"
+    if "l1j" in STRATEGY and "avg_ms" in probes.get("spmv.A", {}):
+        dom = "spmv.A"
     else:
         dom = max((k for k in share), key=lambda k: share[k])
     d = probes[dom]
-    traffic = None
+    traffic, shares = None, None
     try:
-        with open(os.path.join(ROOT, "profiles", "r01", "roofline_traffic.json")) as f:
-            tr = json.load(f)
-        if tr.get("config") == CONFIG and dom in tr.get("kernels", {}):
-            traffic = tr["kernels"][dom]["dram_bytes_per_launch"]
+        with open(os.path.join(ROOT, "profiles", "r02", "roofline_traffic.json")) as f:
+            tr = json.load(f).get(CONFIG, {})
+        traffic = tr.get("kernels", {}).get(dom, {}).get("dram_bytes_per_launch")
+        shares = tr.get("launch_shares")
     except Exception:
         pass
-    by_share = None
-    if "avg_ms" in probes.get("spmv.A", {}):
-        sa = probes["spmv.A"]
-        by_share = {"kernel": "k_spmv_staged (all staged SpMV launches: fine operator, AMG levels 0-2, "
-                              "restriction; ~40% of cfg2 solve kernel time)",
-                    "largest_instance": "spmv.A (fine operator)", "achieved": sa["GBps"], "peak": peak,
-                    "frac": sa["GBps"] / peak}
-    roof = {"bound": "hbm", "kernel": dom, "achieved": d["GBps"], "peak": peak, "unit": "GB/s",
+    arn = {}
+    for nm, kern in (("cgs2dots.15", "k_ls_dots"), ("cgs2upd.15", "k_ls_update"), ("cgs2.15", "both sweeps")):
+        if "avg_ms" in probes.get(nm, {}):
+            arn[kern] = {"probe": nm, "achieved": probes[nm]["GBps"], "frac": probes[nm]["GBps"] / peak,
+                         "algorithmic_bytes": probes[nm]["bytes"], "avg_ms": probes[nm]["avg_ms"]}
+    roof = {"bound": "hbm", "kernel": "k_spmv_staged" if dom == "spmv.A" else dom,
+            "instance": "spmv.A (fine operator; GMRES SpMV)" if dom == "spmv.A" else dom,
+            "achieved": d["GBps"], "peak": peak, "unit": "GB/s",
             "frac": d["GBps"] / peak, "traffic": traffic, "algorithmic_bytes": d["bytes"],
-            "peak_source": peak_kind, "dominant_by_share": by_share, "kernels": probes,
-            "probe_method": "CUDA events on the library stream over 20 back-to-back launches (inputs in HBM; the L2 may retain part of a working set near its 126 MB size)"}
+            "peak_source": peak_kind, "launch_shares": shares, "arnoldi_low_sync": arn, "kernels": probes,
+            "probe_method": "CUDA events on the library stream over 20 back-to-back launches (inputs in HBM; "
+                            "the L2 may retain part of a working set near its 126 MB size)"}
 
     # whole-solve roofline: SURVEY §8(d) compulsory-traffic bytes of one solve
     # (tools/solve_model.py, from the hierarchy's sizes) over the timed solve

@@ -857,6 +857,27 @@ bool build_block_plan(const DCsr& A, bool forward, const double* d, const int* o
     return (forward ? j < i : j > i) && (own.empty() || own[j] == own[i]);
   };
   const int nb = (n + B - 1) / B;
+  // MGRX_GS_BLK_ORDER=local: rows of a block by their block-local level
+  // (intra-block dependencies only); default: by their global dependency
+  // level, so every block walks the levels in the sweep's global order and
+  // a block never waits on a later step of an earlier block
+  static const bool local_order = [] {
+    const char* e = std::getenv("MGRX_GS_BLK_ORDER");
+    return e && e[0] == 'l';
+  }();
+  std::vector<int> glev;
+  if (!local_order) {
+    glev.assign(n, 0);
+    for (int u = 0; u < n; ++u) {
+      const int i = forward ? u : n - 1 - u;
+      int m = 0;
+      for (int k = h.ptr[i]; k < h.ptr[i + 1]; ++k) {
+        const int j = h.col[k];
+        if (dep(i, j)) m = std::max(m, glev[j] + 1);
+      }
+      glev[i] = m;
+    }
+  }
   std::vector<int> lev(n, 0);
   std::vector<int> pos_row, sp{0}, sc;
   std::vector<double> sv, sdv;
@@ -869,9 +890,13 @@ bool build_block_plan(const DCsr& A, bool forward, const double* d, const int* o
     for (int u = 0; u < hi - lo; ++u) {
       const int i = forward ? lo + u : hi - 1 - u;
       int m = 0;
-      for (int k = h.ptr[i]; k < h.ptr[i + 1]; ++k) {
-        const int j = h.col[k];
-        if (dep(i, j) && j >= lo && j < hi) m = std::max(m, lev[j] + 1);
+      if (!local_order) {
+        m = glev[i];
+      } else {
+        for (int k = h.ptr[i]; k < h.ptr[i + 1]; ++k) {
+          const int j = h.col[k];
+          if (dep(i, j) && j >= lo && j < hi) m = std::max(m, lev[j] + 1);
+        }
       }
       lev[i] = m;
       maxl = std::max(maxl, m);
@@ -1069,7 +1094,43 @@ void gs_schedule(const DCsr& A, bool forward, const double* d, bool full, GsSche
     }
   }
   out.blk = 0;
-  if (n > kSmallN && mode == 0 && !out.small) out.blk = build_block_plan(A, forward, d, owner, out, s) ? 1 : 0;
+  if (n > kSmallN && mode == 0 && !out.small && build_block_plan(A, forward, d, owner, out, s)) {
+    // keep the block-partitioned sweep only where it times faster than the
+    // sync-free one (it wins on structured levels whose row blocks carry
+    // their dependency chains, loses on coarse levels whose blocks couple at
+    // every dependency level): best of two timed sweeps each, from zero
+    GsScratch scr;
+    gs_bind_scratch(scr, s);
+    DVec<double> bb(n, s), xx(n, s);
+    std::vector<double> ones(n, 1.0);
+    bb.upload(ones.data(), n);
+    cudaEvent_t e0, e1;
+    MGRX_CK(cudaEventCreate(&e0));
+    MGRX_CK(cudaEventCreate(&e1));
+    auto time_mode = [&](int blk) {
+      out.blk = blk;
+      float best = 1e30f;
+      for (int r = 0; r < 3; ++r) {
+        MGRX_CK(cudaEventRecord(e0, s));
+        gs_sweep(A, out, d, bb.get(), nullptr, xx.get(), nullptr, forward, scr, s);
+        MGRX_CK(cudaEventRecord(e1, s));
+        MGRX_CK(cudaEventSynchronize(e1));
+        float ms = 0.0f;
+        MGRX_CK(cudaEventElapsedTime(&ms, e0, e1));
+        if (r > 0) best = std::min(best, ms);
+      }
+      return best;
+    };
+    const float tb = time_mode(1), tf = time_mode(0);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    gs_check(scr, s);
+    out.blk = tb < tf ? 1 : 0;
+    if (const char* v = std::getenv("MGRX_VERBOSE"); v && v[0] == '1')
+      std::fprintf(stderr, "[mgrx] gs sweep n=%d: block %.1f us, sync-free %.1f us -> %s\n", n, tb * 1e3, tf * 1e3,
+                   out.blk ? "block" : "sync-free");
+    if (std::getenv("MGRX_GS_BLK_FORCE")) out.blk = 1;
+  }
   if (mode == 2) {
     const std::vector<int> dp = out.dptr.download(n + 1);
     bool ok = true;

@@ -418,13 +418,14 @@ def test_alternative_gs_sweeps_are_bit_exact(mode):
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
 
 
-@pytest.mark.parametrize("env", [{}, {"MGRX_GS_BLK_ROWS": "4096"}, {"MGRX_GS_BLK_ROWS": "0"}],
-                         ids=["block12288", "block4096", "syncfree"])
+@pytest.mark.parametrize("env", [{}, {"MGRX_GS_BLK_FORCE": "1"}, {"MGRX_GS_BLK_ROWS": "4096", "MGRX_GS_BLK_FORCE": "1"},
+                                 {"MGRX_GS_BLK_ORDER": "local", "MGRX_GS_BLK_FORCE": "1"}, {"MGRX_GS_BLK_ROWS": "0"}],
+                         ids=["autotuned", "block12288", "block4096", "blocklocal", "syncfree"])
 def test_gauss_seidel_block_sweep_bit_exact(env):
     """The block-partitioned Gauss-Seidel sweep (rows cut into contiguous
     blocks, one CTA per block with its iterate in shared memory, cross-block
-    dependencies polled; the default for levels > 12288 rows) and the
-    sync-free sweep (MGRX_GS_BLK_ROWS=0) reproduce the oracle bitwise: one
+    dependencies polled; chosen per level at setup when it times faster) and
+    the sync-free sweep (MGRX_GS_BLK_ROWS=0) reproduce the oracle bitwise: one
     preconditioner application and the whole MGS-mode residual history, on a
     system whose coarse AMG levels are large enough (196,608 / ~70K rows)."""
     import subprocess
