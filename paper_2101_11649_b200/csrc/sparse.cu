@@ -839,9 +839,92 @@ void launch_wspec(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
   count_launch();
 }
 
+// BSR SpMV (b x b blocks, b <= 4): a CTA takes one chunk of block rows
+// (<= kBsrBlocks blocks, bounds precomputed), forms every product of the
+// chunk in shared memory at its CSR position (coalesced block-value loads,
+// one x load per block column triple), then one thread per row sums its
+// products left to right, i.e. the serial loop's arithmetic over the same
+// entries (bitwise equal to the CSR kernels). Bytes per entry: 8 + 4/b^2
+// instead of 12.
+constexpr int kBsrThreads = 256;
+constexpr int kBsrProducts = 4608;  // products per chunk (36 KB of shared memory)
+constexpr int kBsrMaxRows = 192;    // rows per chunk
+template <int B>
+constexpr int bsr_blocks() { return kBsrProducts / (B * B); }
+
+template <int B, class Epi, class Xs>
+__global__ void __launch_bounds__(kBsrThreads) k_spmv_bsr(int nchunk, const int* __restrict__ bplan,
+                                                          const int* __restrict__ bptr, const int* __restrict__ bcol,
+                                                          const double* __restrict__ bval, Xs x, Epi epi) {
+  pdl_enter();
+  __shared__ double prod[kBsrProducts];
+  __shared__ int sbp[kBsrMaxRows / B + 2];  // chunk block-row pointers (relative)
+  const int t = threadIdx.x;
+  for (int ch = blockIdx.x; ch < nchunk; ch += gridDim.x) {
+    const int br0 = bplan[ch], br1 = bplan[ch + 1];
+    const int nbr = br1 - br0;
+    const int g0 = bptr[br0];
+    for (int q = t; q <= nbr; q += kBsrThreads) sbp[q] = bptr[br0 + q] - g0;
+    __syncthreads();
+    const int nb = sbp[nbr];
+    for (int q = t; q < nb; q += kBsrThreads) {
+      // block row of block q (binary search in the chunk's pointers)
+      int lo = 0, hi = nbr;
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (sbp[mid] <= q) lo = mid;
+        else hi = mid;
+      }
+      const int m = sbp[lo + 1] - sbp[lo];  // blocks in this block row
+      const int kq = q - sbp[lo];           // position of the block in the row
+      const int c0 = __ldg(bcol + g0 + q) * B;
+      double xv[B];
+#pragma unroll
+      for (int c = 0; c < B; ++c) xv[c] = x(c0 + c);
+      const double* v = bval + static_cast<size_t>(g0 + q) * (B * B);
+      // row r of block row lo starts at sbp[lo]*B*B + r*m*B in the chunk's CSR order
+#pragma unroll
+      for (int r = 0; r < B; ++r)
+#pragma unroll
+        for (int c = 0; c < B; ++c)
+          prod[sbp[lo] * B * B + r * m * B + kq * B + c] = __dmul_rn(__ldcs(v + r * B + c), xv[c]);
+    }
+    __syncthreads();
+    for (int rr = t; rr < nbr * B; rr += kBsrThreads) {
+      const int lb = rr / B, r = rr - lb * B;
+      const int m = sbp[lb + 1] - sbp[lb];
+      const double* p = prod + sbp[lb] * B * B + r * m * B;
+      double sum = 0.0;
+      for (int e = 0; e < m * B; ++e) sum = __dadd_rn(sum, p[e]);
+      epi((br0 + lb) * B + r, sum);
+    }
+    __syncthreads();
+  }
+}
+
+template <class Epi, class Xs>
+void launch_bsr(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
+  const int grid = std::min(A.nbchunk, device_sms() * 8);
+  if (A.bsr == 3)
+    launch_pdl(k_spmv_bsr<3, Epi, Xs>, grid, kBsrThreads, 0, s, A.nbchunk, A.bplan.get(), A.bptr.get(),
+               A.bcol.get(), A.bval.get(), x, epi);
+  else if (A.bsr == 2)
+    launch_pdl(k_spmv_bsr<2, Epi, Xs>, grid, kBsrThreads, 0, s, A.nbchunk, A.bplan.get(), A.bptr.get(),
+               A.bcol.get(), A.bval.get(), x, epi);
+  else
+    launch_pdl(k_spmv_bsr<4, Epi, Xs>, grid, kBsrThreads, 0, s, A.nbchunk, A.bplan.get(), A.bptr.get(),
+               A.bcol.get(), A.bval.get(), x, epi);
+  MGRX_LAUNCH_CK();
+  count_launch();
+}
+
 template <class Epi, class Xs = XPlain>
 void launch_spmv(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
   if (A.rows == 0) return;
+  if (A.bsr > 0) {
+    launch_bsr(A, x, epi, s);
+    return;
+  }
   if (A.nblk > 0 && A.plan_kind == 1) {
     launch_wspec(A, x, epi, s);
     return;
@@ -929,7 +1012,152 @@ std::vector<int> block_plan(const std::vector<int>& p, int rows, int max_rows, i
   return rs;
 }
 
+// BSR(b) copy of A when every block row holds full aligned b x b blocks with
+// one column pattern (e.g. the 3-D elasticity displacement block, 3 x 3);
+// false otherwise.
+bool build_bsr(DCsr& A, int b, cudaStream_t s) {
+  if (A.rows % b || A.cols % b || A.rows == 0) return false;
+  const std::vector<int> p = A.ptr.download(A.rows + 1);
+  const std::vector<int> c = A.col.download(A.nnz);
+  const int nbr = A.rows / b;
+  std::vector<int> bptr(nbr + 1, 0), bcol;
+  bcol.reserve(A.nnz / (b * b) + 1);
+  for (int R = 0; R < nbr; ++R) {
+    const int r0 = R * b;
+    const int len = p[r0 + 1] - p[r0];
+    if (len % b) return false;
+    for (int r = 1; r < b; ++r)
+      if (p[r0 + r + 1] - p[r0 + r] != len) return false;
+    for (int k = 0; k < len; k += b) {
+      const int c0 = c[p[r0] + k];
+      if (c0 % b) return false;
+      for (int r = 0; r < b; ++r)
+        for (int q = 0; q < b; ++q)
+          if (c[p[r0 + r] + k + q] != c0 + q) return false;
+      bcol.push_back(c0 / b);
+    }
+    bptr[R + 1] = static_cast<int>(bcol.size());
+  }
+  // values block-major, row-major inside a block
+  const std::vector<double> v = A.val.download(A.nnz);
+  std::vector<double> bv(static_cast<size_t>(bcol.size()) * b * b);
+  for (int R = 0; R < nbr; ++R)
+    for (int k = 0; k < bptr[R + 1] - bptr[R]; ++k)
+      for (int r = 0; r < b; ++r)
+        for (int q = 0; q < b; ++q)
+          bv[(static_cast<size_t>(bptr[R] + k) * b + r) * b + q] = v[p[R * b + r] + k * b + q];
+  // chunks: <= kBsrProducts products, <= kBsrMaxRows rows
+  const int maxblk = kBsrProducts / (b * b);
+  std::vector<int> plan{0};
+  int R = 0;
+  while (R < nbr) {
+    if (bptr[R + 1] - bptr[R] > maxblk) return false;
+    int Q = R + 1;
+    while (Q < nbr && (Q + 1 - R) * b <= kBsrMaxRows && bptr[Q + 1] - bptr[R] <= maxblk) ++Q;
+    plan.push_back(Q);
+    R = Q;
+  }
+  A.bptr.alloc(nbr + 1, s);
+  A.bptr.upload(bptr.data(), nbr + 1);
+  A.bcol.alloc(bcol.size() > 0 ? bcol.size() : 1, s);
+  A.bcol.upload(bcol.data(), bcol.size());
+  A.bval.alloc(bv.size() > 0 ? bv.size() : 1, s);
+  A.bval.upload(bv.data(), bv.size());
+  A.nbchunk = static_cast<int>(plan.size()) - 1;
+  A.bplan.alloc(plan.size(), s);
+  A.bplan.upload(plan.data(), plan.size());
+  return true;
+}
+
+int bsr_mode() {
+  // MGRX_SPMV_BSR: 0 off, 1 (default) chosen per matrix by the setup
+  // timing, 2 forced whenever the block structure is there
+  static const int m = [] {
+    const char* v = std::getenv("MGRX_SPMV_BSR");
+    return v ? std::atoi(v) : 1;
+  }();
+  return m;
+}
+
+// Try BSR(3) then BSR(2) on a prepared matrix; keep it when it times faster
+// than the CSR choice (>= 3%) or when forced.
+void bsr_try(DCsr& A, cudaStream_t s) {
+  A.bsr = 0;
+  if (!bsr_mode() || A.rows < staged_min_rows() || static_cast<long long>(A.nnz) < 4LL * A.rows) return;
+  int b = 0;
+  for (int cand : {3, 2})
+    if (build_bsr(A, cand, s)) {
+      b = cand;
+      break;
+    }
+  if (!b) return;
+  DVec<double> xs(A.cols, s), ys(A.rows, s);
+  xs.zero();
+  cudaEvent_t e0, e1;
+  MGRX_CK(cudaEventCreate(&e0));
+  MGRX_CK(cudaEventCreate(&e1));
+  auto time = [&](int mode) {
+    A.bsr = mode;
+    spmv(A, xs.get(), ys.get(), s);
+    MGRX_CK(cudaEventRecord(e0, s));
+    for (int k = 0; k < 10; ++k) spmv(A, xs.get(), ys.get(), s);
+    MGRX_CK(cudaEventRecord(e1, s));
+    MGRX_CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    MGRX_CK(cudaEventElapsedTime(&ms, e0, e1));
+    return ms;
+  };
+  float tc = 1e30f, tb = 1e30f;
+  const char* pf = std::getenv("MGRX_SPMV_PLAN_FILE");
+  bool replayed = false;
+  if (pf)
+    if (FILE* f = std::fopen(pf, "r")) {
+      int r, c, z;
+      char what[16];
+      while (std::fscanf(f, "%d %d %d %15s", &r, &c, &z, what) == 4)
+        if (r == A.rows && c == A.cols && z == A.nnz && (!std::strcmp(what, "bsr") || !std::strcmp(what, "csr"))) {
+          replayed = true;
+          tb = what[0] == 'b' ? 1.f : 2.f;
+          tc = what[0] == 'b' ? 2.f : 1.f;
+        }
+      std::fclose(f);
+    }
+  if (!replayed) {
+    for (int trial = 0; trial < 3; ++trial) {
+      tc = std::min(tc, time(0));
+      tb = std::min(tb, time(b));
+    }
+    if (pf)
+      if (FILE* f = std::fopen(pf, "a")) {
+        std::fprintf(f, "%d %d %d %s\n", A.rows, A.cols, A.nnz, tb < 0.97f * tc ? "bsr" : "csr");
+        std::fclose(f);
+      }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const bool keep = bsr_mode() == 2 || tb < 0.97f * tc;
+  if (const char* v = std::getenv("MGRX_VERBOSE"); v && v[0] == '1')
+    std::fprintf(stderr, "spmv_prepare rows %d nnz %d: csr %.1f us bsr(%d) %.1f us -> %s\n", A.rows, A.nnz,
+                 100.f * tc, b, 100.f * tb, keep ? "bsr" : "csr");
+  A.bsr = keep ? b : 0;
+  if (!keep) {
+    A.bptr.release();
+    A.bcol.release();
+    A.bval.release();
+    A.bplan.release();
+    A.nbchunk = 0;
+  }
+}
+
+void spmv_prepare_csr(DCsr& A, cudaStream_t s);
+
 void spmv_prepare(DCsr& A, cudaStream_t s) {
+  A.bsr = 0;
+  spmv_prepare_csr(A, s);
+  bsr_try(A, s);
+}
+
+void spmv_prepare_csr(DCsr& A, cudaStream_t s) {
   A.nblk = 0;
   A.plan_kind = 0;
   A.plan.release();
@@ -1005,7 +1233,7 @@ void spmv_prepare(DCsr& A, cudaStream_t s) {
       int r, c, z;
       char what[16];
       while (std::fscanf(f, "%d %d %d %15s", &r, &c, &z, what) == 4)
-        if (r == A.rows && c == A.cols && z == A.nnz) {
+        if (r == A.rows && c == A.cols && z == A.nnz && std::strcmp(what, "bsr") && std::strcmp(what, "csr")) {
           replayed = true;
           // "wspec_staged": the specialised plan plus the staged one for the
           // products the specialised kernel does not serve

@@ -25,6 +25,15 @@ struct DCsr {
   // the specialised kernel overlaps with the sums): nblk_w == 0: none
   int nblk_w = 0;
   DVec<int> plan_w;
+  // BSR copy (spmv_prepare, when every block row of b rows holds full,
+  // aligned b x b blocks with identical column patterns, and it times
+  // faster): bptr per block row, bcol per block (block column), bval b*b
+  // values per block, row-major inside the block -- the same entries in the
+  // same per-row order as the CSR, so row sums are bitwise equal. bplan:
+  // first block row of each CTA chunk (nbchunk + 1). bsr == 0: none.
+  int bsr = 0, nbchunk = 0;
+  DVec<int> bptr, bcol, bplan;
+  DVec<double> bval;
   bool empty() const { return rows == 0; }
 };
 
