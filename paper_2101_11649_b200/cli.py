@@ -327,7 +327,7 @@ def main(argv=None):
             rows = []
             for nsz in sizes:
                 P = {"mfd": lambda k: mx.mfd_problem(k, k, k, "iid"),
-                     "comp": lambda k: mx.comp_problem(k, k, k, wells=2),
+                     "comp": lambda k: mx.comp_problem(k, k, k, wells=2, sigma_t=1.0),  # reference default perm_sigma 1
                      "frac": lambda k: mx.frac_problem(k)}[a.problem](nsz)
                 for strat in strategies:
                     _, row = run_solve(P, resolve_strategy(strat, P), strat, a.tol, a.restart, a.max_iters)

@@ -409,7 +409,8 @@ Shard::~Shard() {
     if (comm) comm->unmap_peers(peer_mbox);
     cudaFree(mbox);
   }
-  if (graph) cudaGraphExecDestroy(graph);
+  for (auto& kv : graphs_)
+    if (kv.second.first) cudaGraphExecDestroy(kv.second.first);
   // buffers are freed on c.s by their destructors; the stream is destroyed
   // after them by the owning API object (mgrx_shard_destroy)
   if (c.s) cudaStreamSynchronize(c.s);
@@ -481,24 +482,25 @@ void Shard::prec(const double* v, double* z) {
     apply_level(0, v, z);
     return;
   }
-  if (!graph || graph_in != v || graph_out != z || graph_exact != c.exact) {
-    if (graph) cudaGraphExecDestroy(graph);
-    graph = nullptr;
+  // one captured graph per (input, output, dense mode): the solve alternates
+  // M^-1 U (every step) and M^-1 (V y) (once per cycle)
+  const auto key = std::make_tuple(v, z, c.exact);
+  auto it = graphs_.find(key);
+  if (it == graphs_.end()) {
     cudaGraph_t g;
+    cudaGraphExec_t ex = nullptr;
     MGRX_CK(cudaStreamBeginCapture(c.s, cudaStreamCaptureModeThreadLocal));
     const long long before = g_launches;
     apply_level(0, v, z);
-    graph_nodes_ = g_launches - before;
+    const long long nodes = g_launches - before;
     MGRX_CK(cudaStreamEndCapture(c.s, &g));
-    MGRX_CK(cudaGraphInstantiate(&graph, g, 0));
+    MGRX_CK(cudaGraphInstantiate(&ex, g, 0));
     cudaGraphDestroy(g);
-    graph_in = v;
-    graph_out = z;
-    graph_exact = c.exact;
     g_launches = before;
+    it = graphs_.emplace(key, std::make_pair(ex, nodes)).first;
   }
-  MGRX_CK(cudaGraphLaunch(graph, c.s));
-  count_launch(graph_nodes_);
+  MGRX_CK(cudaGraphLaunch(it->second.first, c.s));
+  count_launch(it->second.second);
 }
 
 void Shard::apply(const double* v, double* z) {

@@ -26,6 +26,8 @@
 #pragma once
 
 #include <deque>
+#include <map>
+#include <tuple>
 #include <memory>
 #include <vector>
 
@@ -178,11 +180,7 @@ struct Shard {
   GmresWork ws;
   DVec<double> xext, zext, loc, gbuf;
   int row_begin = 0, row_end = 0;
-  cudaGraphExec_t graph = nullptr;
-  const double* graph_in = nullptr;
-  double* graph_out = nullptr;
-  bool graph_exact = true;
-  long long graph_nodes_ = 0;
+  std::map<std::tuple<const double*, double*, bool>, std::pair<cudaGraphExec_t, long long>> graphs_;
 
   // replicated small parts this shard owns (dense coarse factors, the
   // coarse AMG levels it replicates), built from the plan's small matrices
