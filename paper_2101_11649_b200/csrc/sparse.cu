@@ -902,6 +902,48 @@ __global__ void __launch_bounds__(kBsrThreads) k_spmv_bsr(int nchunk, const int*
   }
 }
 
+// SELL-32 SpMV: a warp per slice of 32 rows, a lane per row; the slice's
+// entries are column-major, so every load of a warp is one coalesced run
+// (128 B of columns, 256 B of values); each lane sums its row left to right
+// (the serial loop's arithmetic), 4 entries' loads in flight at a time.
+template <class Epi, class Xs>
+__global__ void __launch_bounds__(256) k_spmv_sell(int nslice, const int* __restrict__ soff,
+                                                   const int* __restrict__ sperm, const int* __restrict__ slen,
+                                                   const int* __restrict__ scol, const double* __restrict__ sval,
+                                                   int rows, Xs x, Epi epi) {
+  pdl_enter();
+  const int l = threadIdx.x & 31;
+  for (int sl = blockIdx.x * 8 + (threadIdx.x >> 5); sl < nslice; sl += gridDim.x * 8) {
+    const int slot = sl * 32 + l;
+    const int r = __ldg(sperm + slot);
+    const int len = __ldg(slen + slot);
+    const int* c = scol + __ldg(soff + sl) + l;
+    const double* v = sval + __ldg(soff + sl) + l;
+    double sum = 0.0;
+    int k = 0;
+    for (; k + 4 <= len; k += 4) {
+      const int c0 = __ldcs(c + 32 * k), c1 = __ldcs(c + 32 * (k + 1)), c2 = __ldcs(c + 32 * (k + 2)),
+                c3 = __ldcs(c + 32 * (k + 3));
+      const double a0 = __ldcs(v + 32 * k), a1 = __ldcs(v + 32 * (k + 1)), a2 = __ldcs(v + 32 * (k + 2)),
+                   a3 = __ldcs(v + 32 * (k + 3));
+      const double p0 = __dmul_rn(a0, x(c0)), p1 = __dmul_rn(a1, x(c1));
+      const double p2 = __dmul_rn(a2, x(c2)), p3 = __dmul_rn(a3, x(c3));
+      sum = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(sum, p0), p1), p2), p3);
+    }
+    for (; k < len; ++k) sum = __dadd_rn(sum, __dmul_rn(__ldcs(v + 32 * k), x(__ldcs(c + 32 * k))));
+    if (r < rows) epi(r, sum);
+  }
+}
+
+template <class Epi, class Xs>
+void launch_sell(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
+  const int grid = std::min((A.nslice + 7) / 8, device_sms() * 8);
+  launch_pdl(k_spmv_sell<Epi, Xs>, grid, 256, 0, s, A.nslice, A.soff.get(), A.sperm.get(), A.slen.get(),
+             A.scol.get(), A.sval.get(), A.rows, x, epi);
+  MGRX_LAUNCH_CK();
+  count_launch();
+}
+
 template <class Epi, class Xs>
 void launch_bsr(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
   const int grid = std::min(A.nbchunk, device_sms() * 8);
@@ -923,6 +965,10 @@ void launch_spmv(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
   if (A.rows == 0) return;
   if (A.bsr > 0) {
     launch_bsr(A, x, epi, s);
+    return;
+  }
+  if (A.nslice > 0) {
+    launch_sell(A, x, epi, s);
     return;
   }
   if (A.nblk > 0 && A.plan_kind == 1) {
@@ -1149,12 +1195,138 @@ void bsr_try(DCsr& A, cudaStream_t s) {
   }
 }
 
+// SELL-32 with rows length-sorted (descending, stable) inside windows of
+// 256 rows; padding slots carry length 0 (their lane sums nothing and writes
+// nothing: sperm = rows).
+bool build_sell(DCsr& A, cudaStream_t s) {
+  constexpr int kWin = 256;
+  const int n = A.rows;
+  const std::vector<int> p = A.ptr.download(n + 1);
+  const std::vector<int> c = A.col.download(A.nnz);
+  const std::vector<double> v = A.val.download(A.nnz);
+  const int nslice = (n + 31) / 32;
+  std::vector<int> perm(static_cast<size_t>(nslice) * 32, n), len(static_cast<size_t>(nslice) * 32, 0);
+  for (int w0 = 0; w0 < n; w0 += kWin) {
+    const int w1 = std::min(n, w0 + kWin);
+    std::vector<int> rs(w1 - w0);
+    for (int i = w0; i < w1; ++i) rs[i - w0] = i;
+    std::stable_sort(rs.begin(), rs.end(), [&](int a, int b) { return p[a + 1] - p[a] > p[b + 1] - p[b]; });
+    for (int q = 0; q < w1 - w0; ++q) {
+      perm[w0 + q] = rs[q];
+      len[w0 + q] = p[rs[q] + 1] - p[rs[q]];
+    }
+  }
+  std::vector<int> off(nslice + 1, 0);
+  for (int sl = 0; sl < nslice; ++sl) {
+    int w = 0;
+    for (int l = 0; l < 32; ++l) w = std::max(w, len[sl * 32 + l]);
+    off[sl + 1] = off[sl] + 32 * w;
+  }
+  if (off[nslice] > 2LL * A.nnz + 64LL * nslice) return false;  // padding too large
+  std::vector<int> sc(off[nslice], 0);
+  std::vector<double> sv(off[nslice], 0.0);
+  for (int sl = 0; sl < nslice; ++sl)
+    for (int l = 0; l < 32; ++l) {
+      const int slot = sl * 32 + l;
+      if (len[slot] == 0) continue;
+      const int r = perm[slot];
+      for (int k = 0; k < len[slot]; ++k) {
+        sc[off[sl] + 32 * k + l] = c[p[r] + k];
+        sv[off[sl] + 32 * k + l] = v[p[r] + k];
+      }
+    }
+  A.nslice = nslice;
+  A.soff.alloc(nslice + 1, s);
+  A.soff.upload(off.data(), nslice + 1);
+  A.sperm.alloc(perm.size(), s);
+  A.sperm.upload(perm.data(), perm.size());
+  A.slen.alloc(len.size(), s);
+  A.slen.upload(len.data(), len.size());
+  A.scol.alloc(sc.size() > 0 ? sc.size() : 1, s);
+  A.scol.upload(sc.data(), sc.size());
+  A.sval.alloc(sv.size() > 0 ? sv.size() : 1, s);
+  A.sval.upload(sv.data(), sv.size());
+  return true;
+}
+
+// MGRX_SPMV_SELL: 0 off, 1 (default) per matrix by timing, 2 forced.
+void sell_try(DCsr& A, cudaStream_t s) {
+  static const int mode = [] {
+    const char* e = std::getenv("MGRX_SPMV_SELL");
+    return e ? std::atoi(e) : 1;
+  }();
+  A.nslice = 0;
+  if (!mode || A.bsr || A.rows < 65536) return;
+  const double avg = static_cast<double>(A.nnz) / A.rows;
+  if (mode == 1 && (avg < 6.0 || avg > 48.0)) return;
+  if (!build_sell(A, s)) return;
+  DVec<double> xs(A.cols > 0 ? A.cols : 1, s), ys(A.rows, s);
+  xs.zero();
+  cudaEvent_t e0, e1;
+  MGRX_CK(cudaEventCreate(&e0));
+  MGRX_CK(cudaEventCreate(&e1));
+  const int ns = A.nslice;
+  auto time = [&](bool sell) {
+    A.nslice = sell ? ns : 0;
+    spmv(A, xs.get(), ys.get(), s);
+    MGRX_CK(cudaEventRecord(e0, s));
+    for (int k = 0; k < 10; ++k) spmv(A, xs.get(), ys.get(), s);
+    MGRX_CK(cudaEventRecord(e1, s));
+    MGRX_CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    MGRX_CK(cudaEventElapsedTime(&ms, e0, e1));
+    return ms;
+  };
+  float tc = 1e30f, tl = 1e30f;
+  const char* pf = std::getenv("MGRX_SPMV_PLAN_FILE");
+  bool replayed = false;
+  if (pf)
+    if (FILE* f = std::fopen(pf, "r")) {
+      int r, c, z;
+      char what[16];
+      while (std::fscanf(f, "%d %d %d %15s", &r, &c, &z, what) == 4)
+        if (r == A.rows && c == A.cols && z == A.nnz && (!std::strcmp(what, "sell") || !std::strcmp(what, "nosell"))) {
+          replayed = true;
+          tl = what[0] == 's' ? 1.f : 2.f;
+          tc = what[0] == 's' ? 2.f : 1.f;
+        }
+      std::fclose(f);
+    }
+  if (!replayed) {
+    for (int trial = 0; trial < 3; ++trial) {
+      tc = std::min(tc, time(false));
+      tl = std::min(tl, time(true));
+    }
+    if (pf)
+      if (FILE* f = std::fopen(pf, "a")) {
+        std::fprintf(f, "%d %d %d %s\n", A.rows, A.cols, A.nnz, tl < 0.97f * tc ? "sell" : "nosell");
+        std::fclose(f);
+      }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const bool keep = mode == 2 || tl < 0.97f * tc;
+  if (const char* v = std::getenv("MGRX_VERBOSE"); v && v[0] == '1')
+    std::fprintf(stderr, "spmv_prepare rows %d nnz %d: current %.1f us sell %.1f us -> %s\n", A.rows, A.nnz,
+                 100.f * tc, 100.f * tl, keep ? "sell" : "keep");
+  A.nslice = keep ? ns : 0;
+  if (!keep) {
+    A.soff.release();
+    A.sperm.release();
+    A.slen.release();
+    A.scol.release();
+    A.sval.release();
+  }
+}
+
 void spmv_prepare_csr(DCsr& A, cudaStream_t s);
 
 void spmv_prepare(DCsr& A, cudaStream_t s) {
   A.bsr = 0;
+  A.nslice = 0;
   spmv_prepare_csr(A, s);
   bsr_try(A, s);
+  sell_try(A, s);
 }
 
 void spmv_prepare_csr(DCsr& A, cudaStream_t s) {
@@ -1233,7 +1405,8 @@ void spmv_prepare_csr(DCsr& A, cudaStream_t s) {
       int r, c, z;
       char what[16];
       while (std::fscanf(f, "%d %d %d %15s", &r, &c, &z, what) == 4)
-        if (r == A.rows && c == A.cols && z == A.nnz && std::strcmp(what, "bsr") && std::strcmp(what, "csr")) {
+        if (r == A.rows && c == A.cols && z == A.nnz && std::strcmp(what, "bsr") && std::strcmp(what, "csr") &&
+            std::strcmp(what, "sell") && std::strcmp(what, "nosell")) {
           replayed = true;
           // "wspec_staged": the specialised plan plus the staged one for the
           // products the specialised kernel does not serve

@@ -34,6 +34,14 @@ struct DCsr {
   int bsr = 0, nbchunk = 0;
   DVec<int> bptr, bcol, bplan;
   DVec<double> bval;
+  // SELL-32 copy (medium rows; chosen per matrix by the setup timing): rows
+  // length-sorted inside windows of 256, slices of 32 rows stored column-
+  // major (slot k of lane l at soff[slice] + 32 k + l), each row's entries in
+  // its CSR order; sperm = original row of a slot, slen = its length.
+  // nslice == 0: none.
+  int nslice = 0;
+  DVec<int> soff, sperm, slen, scol;
+  DVec<double> sval;
   bool empty() const { return rows == 0; }
 };
 

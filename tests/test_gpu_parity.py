@@ -481,8 +481,9 @@ def test_gauss_seidel_block_sweep_bit_exact(env):
 
 
 @pytest.mark.parametrize("env", [{"MGRX_ARNOLDI": "0"}, {"MGRX_ARNOLDI": "1"}, {"MGRX_ARNOLDI_MERGE": "0"},
-                                 {"MGRX_SPMV_STAGED": "2"}, {"MGRX_SPMV_STAGED": "0"}],
-                         ids=["mgs", "arnoldi", "unmerged", "staged", "direct"])
+                                 {"MGRX_SPMV_STAGED": "2"}, {"MGRX_SPMV_STAGED": "0"}, {"MGRX_SPMV_SELL": "2"},
+                                 {"MGRX_SPMV_SELL": "0", "MGRX_SPMV_BSR": "0"}],
+                         ids=["mgs", "arnoldi", "unmerged", "staged", "direct", "sell", "nosell"])
 def test_solve_paths_are_bit_exact(env):
     """Every device path choice reproduces the oracle's residual history and
     solution bitwise on a system large enough (n > 5 * 151552) that every
