@@ -61,6 +61,7 @@ namespace mgrx {
 
 struct LsArgs {
   int n, ldv, m, G;
+  int G2;             // sweep B grid (2 CTAs per SM)
   double* V;          // basis, column-major, leading dimension ldv
   double* U;          // next vector (in: U_k, out: U_{k+1})
   const double* w;    // A M^-1 U_k
@@ -111,10 +112,10 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 // This CTA's row pairs [pb, pe) (a fixed partition of the n/2 pairs); the
 // odd last row (n odd) belongs to the last CTA.
-__device__ __forceinline__ void cta_pairs(const LsArgs& a, long long& pb, long long& pe) {
+__device__ __forceinline__ void cta_pairs(const LsArgs& a, long long& pb, long long& pe, int G) {
   const long long np = a.n / 2;
-  pb = np * blockIdx.x / a.G;
-  pe = np * (blockIdx.x + 1) / a.G;
+  pb = np * blockIdx.x / G;
+  pe = np * (blockIdx.x + 1) / G;
 }
 
 // Sweep A over basis columns [c0, c0 + nc) (nc <= NC; NC == 0: alpha and nu
@@ -156,7 +157,7 @@ __device__ __forceinline__ void dots_group(const LsArgs& a, const double* Vc, lo
 template <int NC, int RU, bool kFirst>
 __device__ __forceinline__ void dots_chunk(const LsArgs& a, int k, int c0, double* red) {
   long long pb, pe;
-  cta_pairs(a, pb, pe);
+  cta_pairs(a, pb, pe, a.G);
   const unsigned long long pl = pol_last(), pf = pol_first();
   double s[NC > 0 ? NC : 1], t[NC > 0 ? NC : 1], al = 0.0, nu = 0.0;
 #pragma unroll
@@ -452,13 +453,13 @@ __device__ __forceinline__ void upd_rows(const LsArgs& a, int k, const double* c
 template <int RU>
 __device__ __forceinline__ void update_rows(const LsArgs& a, int k, const double* cf, double& acc2) {
   long long pb, pe;
-  cta_pairs(a, pb, pe);
+  cta_pairs(a, pb, pe, a.G2);
   const unsigned long long pf = pol_first();
   long long p = pb + threadIdx.x;
   for (; p + static_cast<long long>(RU - 1) * kLT < pe; p += static_cast<long long>(kLT) * RU)
     upd_rows<RU>(a, k, cf, p, acc2, pf);
   for (; p < pe; p += kLT) upd_rows<1>(a, k, cf, p, acc2, pf);
-  if ((a.n & 1) && blockIdx.x == a.G - 1 && threadIdx.x == 0) {  // odd last row
+  if ((a.n & 1) && blockIdx.x == a.G2 - 1 && threadIdx.x == 0) {  // odd last row
     const double ig = cf[2 * a.m + 1], dk = cf[a.m + k];
     const int i = a.n - 1;
     double v = a.U[i], ww = a.w[i] * ig;
@@ -475,7 +476,7 @@ __device__ __forceinline__ void update_rows(const LsArgs& a, int k, const double
   }
 }
 
-__global__ void __launch_bounds__(kLT, 1) k_ls_update(LsArgs a) {
+__global__ void __launch_bounds__(kLT, 2) k_ls_update(LsArgs a) {
   pdl_enter();
   extern __shared__ double cf[];  // coef copy: 2m+2
   const int k = a.st->k;
@@ -494,14 +495,14 @@ __global__ void __launch_bounds__(kLT, 1) k_ls_update(LsArgs a) {
     for (int q = 1; q < kLW; ++q) v += red[q];
     a.part2[blockIdx.x] = v;
     __threadfence();
-    last = atomicAdd(&a.ticket[1], 1u) == static_cast<unsigned>(a.G) - 1;
+    last = atomicAdd(&a.ticket[1], 1u) == static_cast<unsigned>(a.G2) - 1;
   }
   __syncthreads();
   if (!last) return;
   __threadfence();
   if (threadIdx.x == 0) {
     double b2 = 0.0;
-    for (int c = 0; c < a.G; ++c) b2 += __ldcg(a.part2 + c);
+    for (int c = 0; c < a.G2; ++c) b2 += __ldcg(a.part2 + c);
     if (a.rank_part) a.rank_part[0] = b2;  // sharded: k_ls_finish completes the step
     else step_finish(a, k, sqrt(b2));
     a.ticket[1] = 0u;
@@ -549,6 +550,7 @@ LsArgs make_args(LsWork& L, int n, int m, double* w) {
   a.ldv = L.ldv;
   a.m = m;
   a.G = L.G;
+  a.G2 = 2 * L.G;
   a.V = L.V.get();
   a.U = L.U.get();
   a.w = w;
@@ -573,7 +575,7 @@ size_t update_smem(int m) { return sizeof(double) * (2 * m + 2); }
 void launch_step_kernels(const LsArgs& a, cudaStream_t s) {
   launch_pdl(k_ls_dots, dim3(a.G), dim3(kLT), dots_smem(a.m), s, a);
   count_launch();
-  launch_pdl(k_ls_update, dim3(a.G), dim3(kLT), update_smem(a.m), s, a);
+  launch_pdl(k_ls_update, dim3(a.G2), dim3(kLT), update_smem(a.m), s, a);
   count_launch();
 }
 
@@ -596,7 +598,7 @@ void LsWork::ensure(int n_, int m_, cudaStream_t s) {
   V.alloc(static_cast<size_t>(ldv) * (m + 1), s);
   U.alloc(n > 0 ? n : 1, s);
   part.alloc(static_cast<size_t>(2 * m + 2) * G, s);
-  part2.alloc(G, s);
+  part2.alloc(2 * G, s);
   ticket.alloc(2, s);
   ticket.zero();
   st.alloc(1, s);
@@ -649,7 +651,7 @@ void LsDriver::step_sharded(int nranks, const Allgather& allgather, cudaStream_t
   allgather(L_.rpart.get(), L_.gath.get(), stride, s);
   launch_pdl(k_ls_coef, dim3(1), dim3(kLT), dots_smem(m_), s, a, static_cast<const double*>(L_.gath.get()), nranks,
              stride);
-  launch_pdl(k_ls_update, dim3(a.G), dim3(kLT), update_smem(m_), s, a);
+  launch_pdl(k_ls_update, dim3(a.G2), dim3(kLT), update_smem(m_), s, a);
   allgather(L_.rpart.get(), L_.gath.get(), stride, s);
   launch_pdl(k_ls_finish, dim3(1), dim3(1), 0, s, a, static_cast<const double*>(L_.gath.get()), nranks, stride);
   count_launch(4);
@@ -858,7 +860,7 @@ int lowsync_probe(int n, int k, GmresWork& ws, cudaStream_t s, int which) {
     count_launch();
   }
   if (which & 2) {
-    launch_pdl(k_ls_update, dim3(a.G), dim3(kLT), update_smem(m), s, a);
+    launch_pdl(k_ls_update, dim3(a.G2), dim3(kLT), update_smem(m), s, a);
     count_launch();
   }
   return 1;

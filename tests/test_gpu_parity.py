@@ -596,3 +596,40 @@ def test_sharded_arnoldi_mailbox_exchange_single_gpu():
     out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
                          env={**__import__("os").environ, "MGRX_ARNOLDI_SELFXCHG": "1"}, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
+
+
+@pytest.mark.gpu
+def test_repeat_determinism_of_synchronising_kernels():
+    """compute-sanitizer is closed on the GPU pool, so races are hunted by
+    repetition: every kernel family with inter-CTA synchronisation (the
+    low-sync sweeps' last-CTA election and conditional graph, the fused MGS
+    grid barrier, the sync-free / block-partitioned / single-CTA Gauss-
+    Seidel polling, the cluster dense solve, the AMG tail) reruns 25 times
+    and must give the same bits every time (a race shows up as a flipped bit
+    or a hang long before it shows up in a tolerance)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, '.');"
+        "import paper_2101_11649_b200 as mx\n"
+        "cases = [(mx.mfd_problem(32, 32, 24, 'layered'), 'mfd_mgr_pi_c1', 1e-6),"
+        "         (mx.mfd_problem(24, 20, 12, 'iid'), 'mfd_mgr_pi_c1_l1j', 1e-8),"
+        "         (mx.comp_problem(12, 10, 6, wells=2), 'comp_mgr', 1e-6)]\n"
+        "for P, name, tol in cases:\n"
+        "    H = mx.Hierarchy(mx.Matrix(P.ptr, P.col, P.val), P.partition, mx.load_strategy(name), P.unknown_map)\n"
+        "    v = np.random.default_rng(1).uniform(-1, 1, P.n)\n"
+        "    z0 = H.apply(v).view(np.int64)\n"
+        "    ref = {}\n"
+        "    for it in range(25):\n"
+        "        assert np.array_equal(H.apply(v).view(np.int64), z0), (name, it)\n"
+        "        for o in ('cgs2', 'mgs'):\n"
+        "            x, rep = H.solve(P.rhs, cfg=mx.KrylovConfig(restart=30, rel_tol=tol, ortho=o))\n"
+        "            key = (x.view(np.int64).tobytes(), tuple(rep.residual_history))\n"
+        "            assert ref.setdefault(o, key) == key, (name, o, it)\n"
+        "print('ok')")
+    root = make_golden.ROOT
+    for env in ({}, {"MGRX_GS_BLK_FORCE": "1", "MGRX_GS_BLK_ROWS": "4096"}):
+        out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                             env={**os.environ, **env}, timeout=900)
+        assert out.returncode == 0 and "ok" in out.stdout, (env, out.stderr[-3000:])
