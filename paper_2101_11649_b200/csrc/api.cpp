@@ -174,6 +174,16 @@ void prepare_probe(mgrx_hier* h, const std::string& w, std::function<void()>& fn
     bytes = (which & 1 ? sweep : 0.0) + (which & 2 ? sweep + 16.0 * n : 0.0);
     return;
   }
+  if (w == "precond" || w == "precond.inexact") {
+    // one whole MGR application z = M^-1 v through its replayed CUDA graph
+    // (the solve's default mode applies dense coarse blocks through their
+    // inverses: "precond.inexact"); bytes: the caller's model (solve_model.py)
+    MgrHier* HH = &h->H;
+    const bool exact = w == "precond";
+    fn = [=] { HH->apply_graph(x, y, s, exact); };
+    bytes = 0.0;
+    return;
+  }
   if (w == "spmv.A") {
     const DCsr* A = &h->A;
     fn = [=] { spmv(*A, x, y, s); };
@@ -597,7 +607,7 @@ int mgrx_time_kernel(mgrx_hier* h, const char* which, int reps, double* avg_ms, 
     // Default: launches back to back (the L2 keeps whatever of the previous
     // launch's inputs fits in 126 MB: kernels whose working set is near the L2
     // size read part of it from L2). MGRX_PROBE_FLUSH=1: each timed launch
-    // starts from a cold L2 (256 MB written before it, outside its event
+    // starts from a cold L2 (256 MB read before it, outside its event
     // pair; the per-launch events then include ~5 us of launch latency).
     static const bool flush = [] {
       const char* e = std::getenv("MGRX_PROBE_FLUSH");
@@ -609,13 +619,16 @@ int mgrx_time_kernel(mgrx_hier* h, const char* which, int reps, double* avg_ms, 
       *avg_ms = t.stop() * 1e3 / (reps > 0 ? reps : 1);
     } else {
       constexpr size_t kFlush = 256ull << 20;
-      if (h->flushbuf.size() < kFlush) h->flushbuf.alloc(kFlush, s);
+      if (h->flushbuf.size() < kFlush) {
+        h->flushbuf.alloc(kFlush, s);
+        h->flushbuf.zero();
+      }
       cudaEvent_t e0, e1;
       MGRX_CK(cudaEventCreate(&e0));
       MGRX_CK(cudaEventCreate(&e1));
       double tot = 0.0;
       for (int i = 0; i < reps; ++i) {
-        MGRX_CK(cudaMemsetAsync(h->flushbuf.get(), i & 0xff, kFlush, s));
+        l2_flush_read(h->flushbuf.get(), kFlush, s);
         MGRX_CK(cudaEventRecord(e0, s));
         fn();
         MGRX_CK(cudaEventRecord(e1, s));

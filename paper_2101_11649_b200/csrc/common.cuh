@@ -32,22 +32,33 @@ struct RuntimeError : std::runtime_error {
 #define MGRX_LAUNCH_CK() MGRX_CK(cudaGetLastError())
 
 // Programmatic dependent launch (PDL): solve-path kernels are launched with
-// the programmatic-serialization attribute and begin with pdl_enter(), which
-// waits until the previous grid has completed and its writes are visible.
-// Every memory access comes after the wait, so stream order is preserved;
-// what overlaps is the launch processing between dependent kernels. An
-// early launch_dependents trigger (MGRX_PDL_TRIGGER=1) measured slower at
-// cfg2 (74.8 vs 72.6 ms per solve; no PDL: 73.0): resident waiting CTAs
-// crowd the running grid.
-#ifndef MGRX_PDL_TRIGGER
-#define MGRX_PDL_TRIGGER 0
+// the programmatic-serialization attribute. griddepcontrol.wait (pdl_wait)
+// blocks until the previous grid has completed and its writes are visible
+// (it acquires: tools/pdl_l1_test.cu finds no stale L1-cached reads behind
+// it). Every access to data a previous kernel may have written comes after
+// the wait, so stream order is preserved; what overlaps by default is only
+// the launch processing between dependent kernels.
+// MGRX_PDL_MODE (compile time) adds early launches, both MEASURED SLOWER and
+// therefore off (cfg2 solve, round 2: 54.0 ms without; bit 0 alone 64.2 ms;
+// bit 1 alone 57.3 ms; both 62.4 ms): CTAs of an early-launched grid are
+// placed greedily on whichever SMs free up first, so the dependent grid
+// starts unevenly spread over the SMs and its slowest SM sets its time.
+//   bit 0: kernels signal launch_dependents at entry;
+//   bit 1: the staged SpMV kernels issue their first stages' bulk copies
+//          (matrix data: setup-time constants) before the wait and signal
+//          their dependents when a CTA starts its last block.
+#ifndef MGRX_PDL_MODE
+#define MGRX_PDL_MODE 0
 #endif
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_signal() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_enter() {
-#if MGRX_PDL_TRIGGER
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#if MGRX_PDL_MODE & 1
+  pdl_signal();
 #endif
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  pdl_wait();
 }
+constexpr bool kPdlStagedEarly = (MGRX_PDL_MODE & 2) != 0;
 bool pdl_enabled();
 
 template <class... KArgs, class... Args>

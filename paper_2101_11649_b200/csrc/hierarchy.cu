@@ -389,7 +389,8 @@ bool BoundRelax::z0_fusable() const {
   // (short rows only: on the long-row levels of cfg4 the extra epilogue
   // traffic of the sum-bound staged kernel measured slower)
   return on && (spec.kind == Smoother::jacobi || spec.kind == Smoother::l1_jacobi) && spec.sweeps >= 2 &&
-         n > fold_sweep0_max_rows() && A && static_cast<long long>(A->nnz) <= 24LL * A->rows;
+         (n > fold_sweep0_max_rows() || (A && A->xt_nblk > 0)) && A &&
+         static_cast<long long>(A->nnz) <= 24LL * A->rows;
 }
 
 void BoundRelax::jacobi_sweeps(const double* rc, const int* rrow, double* z, double* zacc, cudaStream_t st,
@@ -405,7 +406,9 @@ void BoundRelax::jacobi_sweeps(const double* rc, const int* rrow, double* z, dou
   // <= 64K rows faster, the 1M / 366K-row levels 15-20% slower).
   const double* cur = nullptr;
   double* bufs[2] = {w1.get(), w2.get()};
-  if (n > fold_sweep0_max_rows()) {
+  // (levels served by the x-window SpMV keep sweep 0 apart too: that kernel
+  // stages plain x vectors, not an iterate formed on the fly)
+  if (n > fold_sweep0_max_rows() || A->xt_nblk > 0) {
     if (!have_z0) jacobi0(n, spec.weight, dinv.get(), rc, rrow, w2.get(), st);
     cur = w2.get();
     bufs[1] = w0.get();  // w2 holds sweep 0; w0 is free (no gather when jacobi)

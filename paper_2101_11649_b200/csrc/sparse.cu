@@ -391,8 +391,9 @@ struct StGeom {
   static constexpr int T = kR, R = kR, E = kE;
   struct Stage {
     int rp[kR + 8];
-    int col[kE + 8];
+    int col[kE + 8];  // column indices, or the block's offset dictionary (pattern-coded plans)
     double val[kE + 4];
+    unsigned char pat[kR + 16];  // pattern id per row (pattern-coded plans)
   };
   static constexpr int kStages = 2;
   static constexpr size_t smem = kStages * sizeof(Stage) + 16 * kStages;
@@ -409,13 +410,23 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 __constant__ int c_two_phase_min = 48;
 __device__ __forceinline__ int two_phase_min() { return c_two_phase_min; }
 
-template <class Gm, class Epi, class Xs, bool kLong>
+// Pattern-coded plan operands (kPat instantiation; null otherwise).
+struct PatArgs {
+  const int* meta;            // per block {dictionary start, W}
+  const int* dict;            // offsets col - row
+  const unsigned char* prow;  // pattern id per row, 256 bytes per block
+};
+
+template <class Gm, class Epi, class Xs, bool kLong, bool kPat = false>
 __global__ void __launch_bounds__(Gm::T) k_spmv_staged(int nblk, const int* __restrict__ plan,
                                                        const int* __restrict__ ptr, const int* __restrict__ col,
-                                                       const double* __restrict__ val, Xs x, Epi epi) {
-  pdl_enter();
+                                                       const double* __restrict__ val, Xs x, Epi epi,
+                                                       PatArgs pa = PatArgs{}) {
+  static_assert(!(kLong && kPat), "pattern-coded plans serve the short-row kernel");
+  if (!kPdlStagedEarly) pdl_enter();
   using Stage = typename Gm::Stage;
   constexpr int kStages = Gm::kStages;
+  static_assert(kStages == 2, "the plan prefetch below runs two blocks ahead");
   extern __shared__ __align__(128) unsigned char st_raw[];
   Stage* stg = reinterpret_cast<Stage*>(st_raw);
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(st_raw + kStages * sizeof(Stage));
@@ -427,9 +438,30 @@ __global__ void __launch_bounds__(Gm::T) k_spmv_staged(int nblk, const int* __re
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  auto issue = [&](int b, int s) {
-    const int r0 = prow[b], r1 = prow[b + 1];
-    const int p0 = pnnz[b], p1 = pnnz[b + 1];
+  // Plan entries of a block. They are loaded two blocks ahead and the
+  // epilogue's row operands one block ahead, so that neither global-load
+  // latency sits between two consecutive blocks of a CTA.
+  struct PlanE {
+    int r0, r1, p0, p1, d0, d1, w;
+  };
+  auto ldp = [&](int b) {
+    PlanE e{0, 0, 0, 0, 0, 0, 0};
+    if (b < nblk) {
+      e.r0 = prow[b];
+      e.r1 = prow[b + 1];
+      e.p0 = pnnz[b];
+      e.p1 = pnnz[b + 1];
+      if constexpr (kPat) {
+        e.d0 = pa.meta[2 * b];
+        e.w = pa.meta[2 * b + 1];
+        e.d1 = pa.meta[2 * b + 2];
+      }
+    }
+    return e;
+  };
+  auto issue = [&](const PlanE& e, int s) {
+    const int r0 = e.r0, r1 = e.r1;
+    const int p0 = e.p0, p1 = e.p1;
     const int ra = r0 & ~3, pa4 = p0 & ~3, pa2 = p0 & ~1;
     const unsigned brp = ((r1 + 1 - ra + 3) & ~3) * 4u;
     const unsigned bc = p1 > p0 ? ((p1 - pa4 + 3) & ~3) * 4u : 0u;
@@ -451,20 +483,66 @@ __global__ void __launch_bounds__(Gm::T) k_spmv_staged(int nblk, const int* __re
                    : "memory");
     }
   };
+  // pattern-coded plan: the block's dictionary and pattern ids instead of its
+  // column indices
+  auto issue_pat = [&](const PlanE& e, int b, int s) {
+    const int r0 = e.r0, r1 = e.r1;
+    const int p0 = e.p0, p1 = e.p1;
+    const int ra = r0 & ~3, pa2 = p0 & ~1;
+    const int d0 = e.d0, d1 = e.d1;
+    const unsigned brp = ((r1 + 1 - ra + 3) & ~3) * 4u;
+    const unsigned bd = static_cast<unsigned>(d1 - d0) * 4u;
+    const unsigned bp = static_cast<unsigned>((r1 - r0 + 15) & ~15);
+    const unsigned bv = p1 > p0 ? ((p1 - pa2 + 1) & ~1) * 8u : 0u;
+    const unsigned mb = smem_u32(bar + s);
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(mb), "r"(brp + bd + bp + bv) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(stg[s].rp)),
+                 "l"(ptr + ra), "r"(brp), "r"(mb)
+                 : "memory");
+    if (bp)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(stg[s].pat)),
+                   "l"(pa.prow + static_cast<size_t>(b) * 256), "r"(bp), "r"(mb)
+                   : "memory");
+    if (bd)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(stg[s].col)),
+                   "l"(pa.dict + d0), "r"(bd), "r"(mb)
+                   : "memory");
+    if (bv)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(stg[s].val)),
+                   "l"(val + pa2), "r"(bv), "r"(mb)
+                   : "memory");
+  };
+  auto issue_any = [&](const PlanE& e, int b, int s) {
+    if constexpr (kPat) issue_pat(e, b, s);
+    else issue(e, s);
+  };
   const int G = gridDim.x;
-  if (t == 0)
-    for (int s = 0; s < kStages; ++s)
-      if (blockIdx.x + s * G < nblk) issue(blockIdx.x + s * G, s);
+  PlanE cur = ldp(blockIdx.x), nxt = ldp(blockIdx.x + G);
+  if (t == 0) {
+    issue_any(cur, blockIdx.x, 0);
+    if (blockIdx.x + G < nblk) issue_any(nxt, blockIdx.x + G, 1);
+  }
+  // the plan and the matrix are setup-time constants: the first stages are in
+  // flight before the previous kernel's results are waited for
+  if (kPdlStagedEarly) pdl_wait();
+  decltype(epi.load(0)) pre{};
+  if (cur.r0 + t < cur.r1) pre = epi.load(cur.r0 + t);
   unsigned phase = 0;  // bit s: parity of stage s
   int it = 0;
   for (int b = blockIdx.x; b < nblk; b += G, ++it) {
+    if (kPdlStagedEarly && b + G >= nblk) pdl_signal();  // last block of this CTA
     const int s = it % kStages;
-    const int r0 = prow[b], r1 = prow[b + 1];
-    const int p0 = pnnz[b];
+    const PlanE nn = ldp(b + 2 * G);  // needed at the end of this block (next copy) and two blocks on
+    // next block's row operands of the epilogue (its plan entries arrived a block ago)
+    decltype(epi.load(0)) pre_n{};
+    if (nxt.r0 + t < nxt.r1) pre_n = epi.load(nxt.r0 + t);
+    const int r0 = cur.r0, r1 = cur.r1;
+    const int p0 = cur.p0, p1 = cur.p1;
     const int r = r0 + t;
-    // row operands of the epilogue: independent of the stage, issue first
-    decltype(epi.load(0)) pre{};
-    if (r < r1) pre = epi.load(r);
     const unsigned mb = smem_u32(bar + s);
     const unsigned par = (phase >> s) & 1u;
     unsigned done = 0;
@@ -478,8 +556,24 @@ __global__ void __launch_bounds__(Gm::T) k_spmv_staged(int nblk, const int* __re
     phase ^= 1u << s;
     Stage& S = stg[s];
     const int ra = r0 & ~3, pa4 = p0 & ~3, pa2 = p0 & ~1;
-    const int p1 = pnnz[b + 1];
-    if (!kLong && p1 - p0 > 48 * (r1 - r0)) {
+    if constexpr (kPat) {
+      if (r < r1) {
+        const int lo = S.rp[r - ra], hi = S.rp[r + 1 - ra];
+        // offsets of this row's pattern; column = row + offset
+        const int* D = S.col + static_cast<int>(S.pat[t]) * cur.w - lo;
+        double sum = 0.0;
+        int k = lo;
+        for (; k + 4 <= hi; k += 4) {
+          const int c0 = r + D[k], c1 = r + D[k + 1], c2 = r + D[k + 2], c3 = r + D[k + 3];
+          const double x0 = x(c0), x1 = x(c1), x2 = x(c2), x3 = x(c3);
+          const double q0 = __dmul_rn(S.val[k - pa2], x0), q1 = __dmul_rn(S.val[k + 1 - pa2], x1);
+          const double q2 = __dmul_rn(S.val[k + 2 - pa2], x2), q3 = __dmul_rn(S.val[k + 3 - pa2], x3);
+          sum = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(sum, q0), q1), q2), q3);
+        }
+        for (; k < hi; ++k) sum = __dadd_rn(sum, __dmul_rn(S.val[k - pa2], x(r + D[k])));
+        epi.store(r, sum, pre);
+      }
+    } else if (!kLong && p1 - p0 > 48 * (r1 - r0)) {
       // (short-row matrices: rare long blocks, simple strided product pass)
 #pragma unroll 8
       for (int q = p0 + t; q < p1; q += Gm::T) S.val[q - pa2] = __dmul_rn(S.val[q - pa2], x(S.col[q - pa4]));
@@ -529,7 +623,266 @@ __global__ void __launch_bounds__(Gm::T) k_spmv_staged(int nblk, const int* __re
       epi.store(r, sum, pre);
     }
     __syncthreads();  // stage s consumed
-    if (t == 0 && b + kStages * G < nblk) issue(b + kStages * G, s);
+    if (t == 0 && b + kStages * G < nblk) issue_any(nn, b + kStages * G, s);
+    cur = nxt;
+    nxt = nn;
+    pre = pre_n;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// x-window staged SpMV for irregular medium-row operators (the coarse AMG
+// levels: 18-30 entries per row, columns scattered over a few z-planes). The
+// thread-per-row staged kernel above gathers x through L1: the lanes of a
+// warp touch ~32 different 128-byte lines per instruction and the kernel is
+// bound by L1 tag lookups (one line per cycle per SM: 0.57 of HBM on the
+// cfg2 level-1 operator). Here the x entries a row block needs arrive the same
+// way its matrix entries do: the block's lines of x, precomputed at setup as
+// a few runs of consecutive lines, are bulk-copied into a shared-memory
+// window, and the entries address that window with 16-bit local columns.
+// Row sums are the serial loop's (left to right), bitwise equal.
+// Geometry: kR rows (= row threads) / kE entries / kL window lines per block,
+// kS stages per CTA; one extra warp issues the copies.
+__constant__ int c_xt_dbg = 0;  // MGRX_XT_DBG: timing experiments (1: window as one copy)
+constexpr int kXtRuns = 32;     // runs per block: one per lane of the copy warp
+constexpr int kXtDirect = -2;   // block meta "tail" value: no window, global columns
+template <int kR_, int kE_, int kL_, int kS_>
+struct XtGeom {
+  static constexpr int R = kR_, E = kE_, L = kL_, S = kS_, T = kR_ + 32;
+  struct Stage {
+    int rp[R + 8];
+    unsigned short col[E + 16];
+    double val[E + 4];
+    double win[L * 16];
+  };
+  static constexpr size_t smem = S * sizeof(Stage) + 32 * S;
+};
+using XtA = XtGeom<256, 2048, 120, 2>;  // 3 CTAs / SM
+using XtB = XtGeom<128, 1024, 88, 2>;   // 5 CTAs / SM
+using XtC = XtGeom<256, 2048, 120, 3>;  // XtA's blocks, 3 stages, 2 CTAs / SM
+
+// The copy warp: for each of the CTA's blocks it waits until the stage is
+// free, then its lanes issue the block's copies in parallel (one x run per
+// lane, the matrix slices by lanes 0-2); the next block's plan entries are
+// already in its registers. The row warps own one row per thread; their plan
+// entries and epilogue operands are loaded one block ahead, so a block's
+// critical path is the stage wait and the shared-memory row sum only.
+template <class Gm, class Epi>
+__global__ void __launch_bounds__(Gm::T) k_spmv_xtile(int nblk, const int* __restrict__ plan,
+                                                      const int* __restrict__ ptr,
+                                                      const unsigned short* __restrict__ lcol,
+                                                      const double* __restrict__ val, const int* __restrict__ runs,
+                                                      const int* __restrict__ meta, const int* __restrict__ gcol,
+                                                      const double* __restrict__ x, int xcols, Epi epi) {
+  using Stage = typename Gm::Stage;
+  constexpr int kS = Gm::S;
+  extern __shared__ __align__(128) unsigned char st_raw[];
+  Stage* stg = reinterpret_cast<Stage*>(st_raw);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(st_raw + kS * sizeof(Stage));
+  unsigned long long* empty = full + kS;
+  const int t = threadIdx.x;
+  const int* prow = plan;
+  const int* pnnz = plan + nblk + 1;
+  if (t == 0) {
+    for (int s = 0; s < kS; ++s) {
+      asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_u32(full + s)));
+      asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_u32(empty + s)), "r"(Gm::R / 32));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int G = gridDim.x;
+  auto wait = [](unsigned mb, unsigned par) {
+    unsigned done = 0;
+    do {
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done)
+                   : "r"(mb), "r"(par)
+                   : "memory");
+    } while (!done);
+  };
+  if (t >= Gm::R) {
+    // ---- copy warp
+    const int l = t - Gm::R;
+    struct Desc {
+      int r0, r1, p0, p1, l0, nl, tail;
+    };
+    auto load_desc = [&](int b) {  // plan entries of a block (all setup data)
+      Desc d;
+      d.r0 = prow[b];
+      d.r1 = prow[b + 1];
+      d.p0 = pnnz[b];
+      d.p1 = pnnz[b + 1];
+      const int q0 = meta[2 * b], q1 = meta[2 * b + 2];
+      d.tail = meta[2 * b + 1];
+      d.l0 = 0;
+      d.nl = 0;
+      if (q0 + l < q1) {
+        d.l0 = runs[2 * (q0 + l)];
+        d.nl = runs[2 * (q0 + l) + 1];
+      }
+      return d;
+    };
+    Desc d{};
+    if (blockIdx.x < nblk) d = load_desc(blockIdx.x);
+    pdl_enter();  // x is the previous kernel's
+    int it = 0;
+    for (int b = blockIdx.x; b < nblk; b += G, ++it) {
+      const int s = it % kS;
+      Desc nx{};
+      if (b + G < nblk) nx = load_desc(b + G);  // in flight while this block's stage is awaited
+      if (it >= kS) wait(smem_u32(empty + s), ((it / kS) - 1) & 1u);
+      const unsigned mb = smem_u32(full + s);
+      Stage& S = stg[s];
+      // window slot of this lane's run: exclusive prefix sum of the run lengths
+      int slot = d.nl;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, slot, o);
+        if (l >= o) slot += v;
+      }
+      slot -= d.nl;
+      // whole 16-byte pieces inside x only (an odd last element is the tail slot)
+      const int e1 = min((d.l0 + d.nl) * 16, xcols & ~1);
+      unsigned nb = d.nl > 0 && e1 > d.l0 * 16 ? static_cast<unsigned>(e1 - d.l0 * 16) * 8u : 0u;
+      if (c_xt_dbg & 4) nb = 0u;  // timing experiment: no window copies
+      if (c_xt_dbg == 1) {
+        // timing experiment (wrong results): the block's window bytes as ONE copy
+        unsigned tot = nb;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        const int first = __shfl_sync(0xffffffffu, d.l0, 0);
+        const long long start = min(static_cast<long long>(first) * 16, max(0LL, (xcols & ~1) - static_cast<long long>(tot / 8)));
+        nb = l == 0 ? tot : 0u;
+        if (nb)
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                           smem_u32(S.win)),
+                       "l"(x + (start & ~1LL)), "r"(nb), "r"(mb)
+                       : "memory");
+      } else if (nb)
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(S.win + slot * 16)),
+                     "l"(x + static_cast<size_t>(d.l0) * 16), "r"(nb), "r"(mb)
+                     : "memory");
+      const int ra = d.r0 & ~3, pa8 = d.p0 & ~7, pa2 = d.p0 & ~1;
+      const unsigned brp = ((d.r1 + 1 - ra + 3) & ~3) * 4u;
+      unsigned bc = d.p1 > d.p0 && d.tail != kXtDirect ? ((d.p1 - pa8 + 7) & ~7) * 2u : 0u;
+      unsigned bv = d.p1 > d.p0 ? ((d.p1 - pa2 + 1) & ~1) * 8u : 0u;
+      if (c_xt_dbg & 8) bc = bv = 0u;  // timing experiment: no matrix copies
+      if (l == 0) {
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(S.rp)),
+                     "l"(ptr + ra), "r"(brp), "r"(mb)
+                     : "memory");
+      } else if (l == 1 && bc) {
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(S.col)),
+                     "l"(lcol + pa8), "r"(bc), "r"(mb)
+                     : "memory");
+      } else if (l == 2 && bv) {
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(S.val)),
+                     "l"(val + pa2), "r"(bv), "r"(mb)
+                     : "memory");
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) nb += __shfl_xor_sync(0xffffffffu, nb, o);
+      if (l == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(mb), "r"(nb + brp + bc + bv)
+                     : "memory");
+      d = nx;
+    }
+    return;
+  }
+  // ---- row warps
+  struct Blk {
+    int r0, r1, p0, tail;
+  };
+  auto load_blk = [&](int b) {
+    return b < nblk ? Blk{prow[b], prow[b + 1], pnnz[b], meta[2 * b + 1]} : Blk{0, 0, 0, -1};
+  };
+  // plan entries two blocks ahead, epilogue operands one block ahead
+  Blk cur = load_blk(blockIdx.x), nxt = load_blk(blockIdx.x + G);
+  pdl_enter();
+  decltype(epi.load(0)) pre{};
+  if (cur.r0 + t < cur.r1) pre = epi.load(cur.r0 + t);
+  int it = 0;
+  for (int b = blockIdx.x; b < nblk; b += G, ++it) {
+    const int s = it % kS;
+    const Blk nn = load_blk(b + 2 * G);
+    decltype(epi.load(0)) pre_n{};
+    if (nxt.r0 + t < nxt.r1) pre_n = epi.load(nxt.r0 + t);
+    const int r0 = cur.r0, r1 = cur.r1, p0 = cur.p0, tail = cur.tail;
+    const int r = r0 + t;
+    double xt = 0.0;  // x[xcols - 1] when xcols is odd and the block needs it (tail = its window slot)
+    if (tail >= 0 && t == 0) xt = x[xcols - 1];
+    wait(smem_u32(full + s), (it / kS) & 1u);
+    Stage& S = stg[s];
+    if (tail >= 0) {  // block-uniform
+      if (t == 0) S.win[tail] = xt;
+      asm volatile("bar.sync 1, %0;" ::"r"(Gm::R) : "memory");
+    }
+    const int ra = r0 & ~3, pa8 = p0 & ~7, pa2 = p0 & ~1;
+    double sum = 0.0;
+    if (tail == kXtDirect) {
+      // a block whose rows reach past the window caps (few, by construction
+      // one row each): global column indices, x gathered directly
+      if (r < r1) {
+        const int lo = S.rp[r - ra], hi = S.rp[r + 1 - ra];
+        for (int k = lo; k < hi; ++k) sum = __dadd_rn(sum, __dmul_rn(S.val[k - pa2], __ldg(x + __ldg(gcol + k))));
+      }
+    } else if (r < r1 && !(c_xt_dbg & 2)) {
+      const int lo = S.rp[r - ra], hi = S.rp[r + 1 - ra];
+      // products of 4 entries at a time, the next 4 entries' operands loaded
+      // (local column, then window value and matrix value) before the current
+      // 4 products join the row's in-order sum
+      const unsigned short* cp = S.col - pa8;
+      const double* vp = S.val - pa2;
+      auto ld4 = [&](int k, double (&xv)[4], double (&av)[4]) {
+        const int c0 = cp[k], c1 = cp[k + 1], c2 = cp[k + 2], c3 = cp[k + 3];
+        xv[0] = S.win[c0], xv[1] = S.win[c1], xv[2] = S.win[c2], xv[3] = S.win[c3];
+        av[0] = vp[k], av[1] = vp[k + 1], av[2] = vp[k + 2], av[3] = vp[k + 3];
+      };
+      auto add4 = [&](const double (&xv)[4], const double (&av)[4]) {
+        const double q0 = __dmul_rn(av[0], xv[0]), q1 = __dmul_rn(av[1], xv[1]);
+        const double q2 = __dmul_rn(av[2], xv[2]), q3 = __dmul_rn(av[3], xv[3]);
+        sum = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(sum, q0), q1), q2), q3);
+      };
+      double xa[4], aa[4], xb[4], ab[4];
+      int k = lo;
+      if (k + 4 <= hi) ld4(k, xa, aa);
+      while (k + 8 <= hi) {
+        ld4(k + 4, xb, ab);
+        add4(xa, aa);
+        k += 4;
+        if (k + 8 <= hi) {
+          ld4(k + 4, xa, aa);
+          add4(xb, ab);
+          k += 4;
+        } else {
+          add4(xb, ab);
+          k += 4;
+          goto tail;
+        }
+      }
+      if (k + 4 <= hi) {
+        add4(xa, aa);
+        k += 4;
+      }
+    tail:
+      for (; k < hi; ++k) sum = __dadd_rn(sum, __dmul_rn(vp[k], S.win[cp[k]]));
+    }
+    // this warp is done with stage s (the tail slot was written by a thread:
+    // order it before the copy warp's next bulk copy into the window)
+    __syncwarp();
+    if ((t & 31) == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(smem_u32(empty + s)) : "memory");
+    }
+    if (r < r1) epi.store(r, sum, pre);
+    cur = nxt;
+    nxt = nn;
+    pre = pre_n;
   }
 }
 
@@ -552,7 +905,7 @@ template <class Epi, class Xs>
 __global__ void __launch_bounds__(kWsT) k_spmv_wspec(int nblk, const int* __restrict__ plan,
                                                      const int* __restrict__ ptr, const int* __restrict__ col,
                                                      const double* __restrict__ val, Xs x, Epi epi) {
-  pdl_enter();
+  if (!kPdlStagedEarly) pdl_enter();
   using Stage = StW::Stage;
   extern __shared__ __align__(128) unsigned char st_raw[];
   Stage* stg = reinterpret_cast<Stage*>(st_raw);
@@ -593,6 +946,7 @@ __global__ void __launch_bounds__(kWsT) k_spmv_wspec(int nblk, const int* __rest
   if (t == 0)
     for (int s = 0; s < 2; ++s)
       if (blockIdx.x + s * G < nblk) issue(blockIdx.x + s * G, s);
+  if (kPdlStagedEarly) pdl_wait();
   if (t >= kWsSumT) {
     // product warps
     constexpr int kPT = kWsT - kWsSumT;
@@ -631,6 +985,7 @@ __global__ void __launch_bounds__(kWsT) k_spmv_wspec(int nblk, const int* __rest
     // sum warps: one lane per row
     int it = 0;
     for (int b = blockIdx.x; b < nblk; b += G, ++it) {
+      if (kPdlStagedEarly && b + G >= nblk) pdl_signal();
       const int s = it & 1;
       const int r0 = prow[b], r1 = prow[b + 1];
       const int r = r0 + t;
@@ -812,7 +1167,7 @@ void launch_staged_k(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
   const int per_sm = static_cast<int>(std::min<size_t>(8, 227 * 1024 / Gm::smem));
   const int grid = std::min(A.nblk, device_sms() * std::min(per_sm, staged_ctas_per_sm()));
   launch_pdl(k_spmv_staged<Gm, Epi, Xs, kLong>, grid, Gm::T, Gm::smem, s, A.nblk, A.plan.get(), A.ptr.get(),
-             A.col.get(), A.val.get(), x, epi);
+             A.col.get(), A.val.get(), x, epi, PatArgs{});
   MGRX_LAUNCH_CK();
   count_launch();
 }
@@ -820,8 +1175,21 @@ void launch_staged_k(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
 // product pass (a separate instantiation keeps the common kernel's
 // registers free of the batch arrays).
 template <class Gm, class Epi, class Xs>
+void launch_staged_pat(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
+  auto* kern = k_spmv_staged<Gm, Epi, Xs, false, true>;
+  if (first_on_device(reinterpret_cast<const void*>(kern)))
+    MGRX_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Gm::smem)));
+  const int per_sm = static_cast<int>(std::min<size_t>(8, 227 * 1024 / Gm::smem));
+  const int grid = std::min(A.nblk, device_sms() * std::min(per_sm, staged_ctas_per_sm()));
+  launch_pdl(kern, grid, Gm::T, Gm::smem, s, A.nblk, A.plan.get(), A.ptr.get(), A.col.get(), A.val.get(), x, epi,
+             PatArgs{A.pmeta.get(), A.pdict.get(), A.prow.get()});
+  MGRX_LAUNCH_CK();
+  count_launch();
+}
+template <class Gm, class Epi, class Xs>
 void launch_staged(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
-  if (static_cast<long long>(A.nnz) > 24LL * A.rows) launch_staged_k<Gm, Epi, Xs, true>(A, x, epi, s);
+  if (A.pat) launch_staged_pat<Gm>(A, x, epi, s);
+  else if (static_cast<long long>(A.nnz) > 24LL * A.rows) launch_staged_k<Gm, Epi, Xs, true>(A, x, epi, s);
   else launch_staged_k<Gm, Epi, Xs, false>(A, x, epi, s);
 }
 
@@ -837,6 +1205,30 @@ void launch_wspec(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
              A.val.get(), x, epi);
   MGRX_LAUNCH_CK();
   count_launch();
+}
+
+template <class Gm, class Epi>
+void launch_xtile_g(const DCsr& A, const double* x, Epi epi, cudaStream_t s) {
+  auto* kern = k_spmv_xtile<Gm, Epi>;
+  if (first_on_device(reinterpret_cast<const void*>(kern))) {
+    MGRX_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Gm::smem)));
+    if (const char* e = std::getenv("MGRX_XT_DBG")) {
+      const int v = std::atoi(e);
+      MGRX_CK(cudaMemcpyToSymbol(c_xt_dbg, &v, sizeof v));
+    }
+  }
+  const int per_sm = static_cast<int>(227 * 1024 / (Gm::smem + 1024));
+  const int grid = std::min(A.xt_nblk, device_sms() * per_sm);
+  launch_pdl(kern, grid, Gm::T, Gm::smem, s, A.xt_nblk, A.xt_plan.get(), A.ptr.get(), A.xt_col.get(), A.val.get(),
+             A.xt_runs.get(), A.xt_meta.get(), A.col.get(), x, A.cols, epi);
+  MGRX_LAUNCH_CK();
+  count_launch();
+}
+template <class Epi>
+void launch_xtile(const DCsr& A, const double* x, Epi epi, cudaStream_t s) {
+  if (A.xt_geom == 1) launch_xtile_g<XtB>(A, x, epi, s);
+  else if (A.xt_geom == 2) launch_xtile_g<XtC>(A, x, epi, s);
+  else launch_xtile_g<XtA>(A, x, epi, s);
 }
 
 // BSR SpMV (b x b blocks, b <= 4): a CTA takes one chunk of block rows
@@ -967,6 +1359,13 @@ void launch_spmv(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
     launch_bsr(A, x, epi, s);
     return;
   }
+  if constexpr (std::is_same_v<Xs, XPlain>) {
+    // x-window plan: plain x vectors on a 16-byte boundary (bulk-copy source)
+    if (A.xt_nblk > 0 && (reinterpret_cast<uintptr_t>(x.x) & 15) == 0) {
+      launch_xtile(A, x.x, epi, s);
+      return;
+    }
+  }
   if (A.nslice > 0) {
     launch_sell(A, x, epi, s);
     return;
@@ -1037,6 +1436,62 @@ bool wspec_enabled() {
     return !v || std::atoi(v) != 0;
   }();
   return on;
+}
+
+// Setup timing of one SpMV candidate (ms per 10 launches). In the solve every
+// operator is read cold — a V-cycle moves ~1.5 GB between two uses of the same
+// matrix, twelve times the L2 — so each timed launch starts from a flushed L2
+// (256 MB read before it, outside its event pair). MGRX_TUNE_COLD=0: ten
+// launches back to back (operators under ~100 MB then stream from L2, which
+// flatters formats that trade HBM bytes for on-chip work).
+namespace {
+__global__ void k_flush_read(const double* __restrict__ p, size_t n, double* sink) {
+  double a = 0.0;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    a += p[i];
+  if (a == 1.2345e300) *sink = a;  // never: keeps the loads
+}
+}  // namespace
+
+// Replace the L2's contents with clean lines of `buf` (a read-only sweep: a
+// memset would leave the L2 full of dirty lines whose write-backs then compete
+// with the timed kernel, which the solve's mostly read-only streams do not).
+void l2_flush_read(const void* buf, size_t bytes, cudaStream_t s) {
+  k_flush_read<<<device_sms() * 8, 256, 0, s>>>(static_cast<const double*>(buf), bytes / 8,
+                                                const_cast<double*>(static_cast<const double*>(buf)));
+  MGRX_LAUNCH_CK();
+}
+
+float tune_time(const DCsr& A, const double* x, double* y, cudaStream_t s, cudaEvent_t e0, cudaEvent_t e1) {
+  static const bool cold = [] {
+    const char* v = std::getenv("MGRX_TUNE_COLD");
+    return !v || std::atoi(v) != 0;
+  }();
+  spmv(A, x, y, s);  // warm (kernel attributes, instruction cache)
+  float ms = 0.f;
+  if (!cold) {
+    MGRX_CK(cudaEventRecord(e0, s));
+    for (int k = 0; k < 10; ++k) spmv(A, x, y, s);
+    MGRX_CK(cudaEventRecord(e1, s));
+    MGRX_CK(cudaEventSynchronize(e1));
+    MGRX_CK(cudaEventElapsedTime(&ms, e0, e1));
+    return ms;
+  }
+  constexpr size_t kFlush = 256ull << 20;
+  DVec<char> fl(kFlush, s);
+  MGRX_CK(cudaMemsetAsync(fl.get(), 0, kFlush, s));
+  float tot = 0.f;
+  for (int k = 0; k < 5; ++k) {
+    l2_flush_read(fl.get(), kFlush, s);
+    MGRX_CK(cudaEventRecord(e0, s));
+    spmv(A, x, y, s);
+    MGRX_CK(cudaEventRecord(e1, s));
+    MGRX_CK(cudaEventSynchronize(e1));
+    MGRX_CK(cudaEventElapsedTime(&ms, e0, e1));
+    tot += ms;
+  }
+  return 2.f * tot;
 }
 
 // Row blocks of <= max_rows rows / <= max_e entries: the nb+1 first rows then
@@ -1144,13 +1599,7 @@ void bsr_try(DCsr& A, cudaStream_t s) {
   MGRX_CK(cudaEventCreate(&e1));
   auto time = [&](int mode) {
     A.bsr = mode;
-    spmv(A, xs.get(), ys.get(), s);
-    MGRX_CK(cudaEventRecord(e0, s));
-    for (int k = 0; k < 10; ++k) spmv(A, xs.get(), ys.get(), s);
-    MGRX_CK(cudaEventRecord(e1, s));
-    MGRX_CK(cudaEventSynchronize(e1));
-    float ms = 0.f;
-    MGRX_CK(cudaEventElapsedTime(&ms, e0, e1));
+    const float ms = tune_time(A, xs.get(), ys.get(), s, e0, e1);
     return ms;
   };
   float tc = 1e30f, tb = 1e30f;
@@ -1268,13 +1717,7 @@ void sell_try(DCsr& A, cudaStream_t s) {
   const int ns = A.nslice;
   auto time = [&](bool sell) {
     A.nslice = sell ? ns : 0;
-    spmv(A, xs.get(), ys.get(), s);
-    MGRX_CK(cudaEventRecord(e0, s));
-    for (int k = 0; k < 10; ++k) spmv(A, xs.get(), ys.get(), s);
-    MGRX_CK(cudaEventRecord(e1, s));
-    MGRX_CK(cudaEventSynchronize(e1));
-    float ms = 0.f;
-    MGRX_CK(cudaEventElapsedTime(&ms, e0, e1));
+    const float ms = tune_time(A, xs.get(), ys.get(), s, e0, e1);
     return ms;
   };
   float tc = 1e30f, tl = 1e30f;
@@ -1321,18 +1764,288 @@ void sell_try(DCsr& A, cudaStream_t s) {
 
 void spmv_prepare_csr(DCsr& A, cudaStream_t s);
 
+// x-window plan (k_spmv_xtile): greedy row blocks under the row / entry /
+// line caps, each block's lines as runs, 16-bit local columns.
+bool build_xtile(DCsr& A, int geom, cudaStream_t s) {
+  const int kXtRows = geom == 1 ? XtB::R : XtA::R, kXtE = geom == 1 ? XtB::E : XtA::E,
+            kXtLines = geom == 1 ? XtB::L : XtA::L;
+  const int n = A.rows;
+  if (n == 0 || A.nnz == 0) return false;
+  const std::vector<int> p = A.ptr.download(n + 1);
+  const std::vector<int> c = A.col.download(A.nnz);
+  const int nlines = (A.cols + 15) / 16;
+  std::vector<int> slot_of(nlines, -1);
+  std::vector<int> rs{0}, ns{0}, runs, meta, lines;
+  std::vector<unsigned short> lc(static_cast<size_t>(A.nnz) + 16, 0);
+  int r = 0, ndirect = 0;
+  while (r < n) {
+    if (p[r + 1] - p[r] > kXtE) return false;
+    lines.clear();
+    int q = r;
+    // grow the block row by row while it stays under the caps
+    while (q < n && q - r < kXtRows && p[q + 1] - p[r] <= kXtE) {
+      const size_t before = lines.size();
+      for (int k = p[q]; k < p[q + 1]; ++k) {
+        const int ln = c[k] >> 4;
+        if (slot_of[ln] < 0) {
+          slot_of[ln] = 0;
+          lines.push_back(ln);
+        }
+      }
+      if (static_cast<int>(lines.size()) > kXtLines) {
+        for (size_t i = before; i < lines.size(); ++i) slot_of[lines[i]] = -1;
+        lines.resize(before);
+        break;
+      }
+      ++q;
+    }
+    bool direct = false;
+    if (q == r) {  // one row alone exceeds the window: a block of its own with global columns
+      direct = true;
+      q = r + 1;
+    }
+    std::sort(lines.begin(), lines.end());
+    // runs of consecutive lines; too many runs: shorten the block
+    while (!direct) {
+      int nr = lines.empty() ? 0 : 1;
+      for (size_t i = 1; i < lines.size(); ++i) nr += lines[i] != lines[i - 1] + 1;
+      if (nr <= kXtRuns) break;
+      for (int ln : lines) slot_of[ln] = -1;
+      lines.clear();
+      q = r + std::max(1, (q - r) / 2);
+      for (int k = p[r]; k < p[q]; ++k) {
+        const int ln = c[k] >> 4;
+        if (slot_of[ln] < 0) {
+          slot_of[ln] = 0;
+          lines.push_back(ln);
+        }
+      }
+      std::sort(lines.begin(), lines.end());
+      if (q - r == 1) {
+        int nr1 = lines.empty() ? 0 : 1;
+        for (size_t i = 1; i < lines.size(); ++i) nr1 += lines[i] != lines[i - 1] + 1;
+        if (nr1 > kXtRuns) direct = true;
+      }
+    }
+    meta.push_back(static_cast<int>(runs.size() / 2));
+    if (direct) {
+      for (int ln : lines) slot_of[ln] = -1;
+      lines.clear();
+      ++ndirect;
+    }
+    int tail = direct ? kXtDirect : -1;
+    for (size_t i = 0; i < lines.size(); ++i) {
+      slot_of[lines[i]] = static_cast<int>(i);
+      if (i == 0 || lines[i] != lines[i - 1] + 1) {
+        runs.push_back(lines[i]);
+        runs.push_back(1);
+      } else {
+        ++runs.back();
+      }
+      if ((A.cols & 1) && lines[i] == (A.cols - 1) >> 4) tail = static_cast<int>(i) * 16 + ((A.cols - 1) & 15);
+    }
+    meta.push_back(tail);
+    if (!direct)
+      for (int k = p[r]; k < p[q]; ++k) lc[k] = static_cast<unsigned short>(slot_of[c[k] >> 4] * 16 + (c[k] & 15));
+    for (int ln : lines) slot_of[ln] = -1;
+    rs.push_back(q);
+    ns.push_back(p[q]);
+    r = q;
+  }
+  const int nb = static_cast<int>(rs.size()) - 1;
+  if (ndirect > nb / 2) return false;  // not a windowable operator
+  meta.push_back(static_cast<int>(runs.size() / 2));
+  meta.push_back(-1);
+  rs.insert(rs.end(), ns.begin(), ns.end());
+  A.xt_plan.alloc(rs.size(), s);
+  A.xt_plan.upload(rs.data(), rs.size());
+  A.xt_runs.alloc(runs.size() + 2, s);
+  A.xt_runs.upload(runs.data(), runs.size());
+  A.xt_meta.alloc(meta.size(), s);
+  A.xt_meta.upload(meta.data(), meta.size());
+  A.xt_col.alloc(lc.size(), s);
+  A.xt_col.upload(lc.data(), lc.size());
+  A.xt_nblk = nb;
+  A.xt_geom = geom;
+  return true;
+}
+
+// MGRX_SPMV_XT: 0 off, 1 (default) per matrix by timing, 2 forced wherever a
+// plan exists.
+void xtile_try(DCsr& A, cudaStream_t s) {
+  static const int mode = [] {
+    const char* e = std::getenv("MGRX_SPMV_XT");
+    return e ? std::atoi(e) : 1;
+  }();
+  static const int force_geom = [] {  // MGRX_SPMV_XT_GEOM: 0 / 1 only that geometry
+    const char* e = std::getenv("MGRX_SPMV_XT_GEOM");
+    return e ? std::atoi(e) : -1;
+  }();
+  A.xt_nblk = 0;
+  if (!mode || A.bsr || A.rows < staged_min_rows()) return;
+  // (one thread per row: rows averaging > 48 entries keep the block-wide
+  // product-pass kernels)
+  if (mode == 1 && static_cast<long long>(A.nnz) > 48LL * A.rows) return;
+  DVec<double> xs(A.cols > 0 ? A.cols : 1, s), ys(A.rows, s);
+  xs.zero();
+  cudaEvent_t e0, e1;
+  MGRX_CK(cudaEventCreate(&e0));
+  MGRX_CK(cudaEventCreate(&e1));
+  struct Cand {
+    int geom = 0, nb = 0;
+    DVec<int> plan, runs, meta;
+    DVec<unsigned short> col;
+    float t = 1e30f;
+  };
+  auto stash = [&](Cand& c) {
+    c.geom = A.xt_geom;
+    c.nb = A.xt_nblk;
+    c.plan = std::move(A.xt_plan);
+    c.runs = std::move(A.xt_runs);
+    c.meta = std::move(A.xt_meta);
+    c.col = std::move(A.xt_col);
+    A.xt_nblk = 0;
+  };
+  auto install = [&](Cand& c) {
+    A.xt_geom = c.geom;
+    A.xt_nblk = c.nb;
+    A.xt_plan = std::move(c.plan);
+    A.xt_runs = std::move(c.runs);
+    A.xt_meta = std::move(c.meta);
+    A.xt_col = std::move(c.col);
+  };
+  // decisions of an earlier run (MGRX_SPMV_PLAN_FILE): xtile0 / xtile1 / noxtile
+  const char* pf = std::getenv("MGRX_SPMV_PLAN_FILE");
+  int replay = -2;
+  if (pf)
+    if (FILE* f = std::fopen(pf, "r")) {
+      int r, c, z;
+      char what[16];
+      while (std::fscanf(f, "%d %d %d %15s", &r, &c, &z, what) == 4)
+        if (r == A.rows && c == A.cols && z == A.nnz) {
+          if (!std::strcmp(what, "xtile0")) replay = 0;
+          if (!std::strcmp(what, "xtile1")) replay = 1;
+          if (!std::strcmp(what, "xtile2")) replay = 2;
+          if (!std::strcmp(what, "noxtile")) replay = -1;
+        }
+      std::fclose(f);
+    }
+  Cand best;
+  float tc = 1e30f;
+  if (replay == -2) tc = std::min(tune_time(A, xs.get(), ys.get(), s, e0, e1), tune_time(A, xs.get(), ys.get(), s, e0, e1));
+  for (int g = 0; g < 3; ++g) {
+    if (force_geom >= 0 && g != force_geom) continue;
+    if (replay != -2 && replay != g) continue;
+    if (!build_xtile(A, g, s)) continue;
+    Cand c;
+    if (replay == -2)
+      for (int trial = 0; trial < 3; ++trial) c.t = std::min(c.t, tune_time(A, xs.get(), ys.get(), s, e0, e1));
+    else c.t = 0.f;
+    if (const char* v = std::getenv("MGRX_VERBOSE"); v && v[0] == '1')
+      std::fprintf(stderr, "spmv_prepare rows %d nnz %d: current %.1f us xtile geometry %d (%d blocks) %.1f us\n",
+                   A.rows, A.nnz, 100.f * tc, g, A.xt_nblk, 100.f * c.t);
+    stash(c);
+    if (c.t < best.t || best.nb == 0) best = std::move(c);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const bool keep = best.nb > 0 && (mode == 2 || replay >= 0 || best.t < 0.97f * tc);
+  if (pf && replay == -2)
+    if (FILE* f = std::fopen(pf, "a")) {
+      std::fprintf(f, "%d %d %d %s\n", A.rows, A.cols, A.nnz, !keep ? "noxtile" : best.geom == 2 ? "xtile2" : best.geom ? "xtile1" : "xtile0");
+      std::fclose(f);
+    }
+  if (keep) {
+    install(best);
+    if (const char* v = std::getenv("MGRX_VERBOSE"); v && v[0] == '1')
+      std::fprintf(stderr, "spmv_prepare rows %d nnz %d -> xtile geometry %d\n", A.rows, A.nnz, A.xt_geom);
+  }
+}
+
+// MGRX_SPMV_PAT: 0 off, 1 (default) pattern-coded columns where they time
+// faster, 2 forced wherever the structure is there.
+int pat_mode() {
+  static const int m = [] {
+    const char* v = std::getenv("MGRX_SPMV_PAT");
+    return v ? std::atoi(v) : 1;
+  }();
+  return m;
+}
+
+// Pattern-coded columns for the staged plan `h` (nb blocks) of A: per block,
+// the distinct offset patterns (col - row) of its rows. Built only when the
+// dictionaries are small next to the column indices they replace (stencil-
+// like operators); false otherwise.
+bool build_patterns(DCsr& A, const std::vector<int>& p, const std::vector<int>& h, int nb, int max_e,
+                    cudaStream_t s) {
+  if (nb <= 0 || A.nnz == 0 || static_cast<long long>(A.nnz) > 24LL * A.rows) return false;
+  const std::vector<int> c = A.col.download(A.nnz);
+  std::vector<int> meta(2 * static_cast<size_t>(nb) + 2, 0), dict;
+  std::vector<unsigned char> prow(static_cast<size_t>(nb) * 256, 0);
+  std::vector<int> order;
+  for (int b = 0; b < nb; ++b) {
+    const int r0 = h[b], r1 = h[b + 1];
+    if (r1 - r0 > 256) return false;
+    const int p0 = p[r0], p1 = p[r1];
+    if (p1 - p0 > 48 * (r1 - r0)) return false;  // the block-wide product pass reads column indices
+    int W = 0;
+    for (int r = r0; r < r1; ++r) W = std::max(W, p[r + 1] - p[r]);
+    // rows sorted by (length, offsets): equal patterns become neighbours
+    order.resize(r1 - r0);
+    for (int i = 0; i < r1 - r0; ++i) order[i] = r0 + i;
+    auto less = [&](int a, int bb) {
+      const int la = p[a + 1] - p[a], lb = p[bb + 1] - p[bb];
+      if (la != lb) return la < lb;
+      for (int k = 0; k < la; ++k) {
+        const int da = c[p[a] + k] - a, db = c[p[bb] + k] - bb;
+        if (da != db) return da < db;
+      }
+      return false;
+    };
+    std::sort(order.begin(), order.end(), less);
+    meta[2 * b] = static_cast<int>(dict.size());
+    meta[2 * b + 1] = W;
+    int npat = 0;
+    for (size_t i = 0; i < order.size(); ++i) {
+      const int r = order[i];
+      if (i == 0 || less(order[i - 1], r)) {
+        if (npat == 256 || static_cast<long long>(npat + 1) * W > max_e) return false;
+        for (int k = 0; k < W; ++k) dict.push_back(k < p[r + 1] - p[r] ? c[p[r] + k] - r : 0);
+        ++npat;
+      }
+      prow[static_cast<size_t>(b) * 256 + (r - r0)] = static_cast<unsigned char>(npat - 1);
+    }
+    while (dict.size() % 4) dict.push_back(0);
+    if (dict.size() > static_cast<size_t>(A.nnz) / 3) return false;  // not stencil-like: no bytes saved
+  }
+  meta[2 * static_cast<size_t>(nb)] = static_cast<int>(dict.size());
+  A.pdict.alloc(dict.size() + 4, s);
+  A.pdict.upload(dict.data(), dict.size());
+  A.pmeta.alloc(meta.size(), s);
+  A.pmeta.upload(meta.data(), meta.size());
+  A.prow.alloc(prow.size(), s);
+  A.prow.upload(prow.data(), prow.size());
+  return true;
+}
+
 void spmv_prepare(DCsr& A, cudaStream_t s) {
   A.bsr = 0;
   A.nslice = 0;
+  A.xt_nblk = 0;
   spmv_prepare_csr(A, s);
   bsr_try(A, s);
   sell_try(A, s);
+  xtile_try(A, s);
 }
 
 void spmv_prepare_csr(DCsr& A, cudaStream_t s) {
   A.nblk = 0;
   A.plan_kind = 0;
   A.plan.release();
+  A.pat = 0;
+  A.pdict.release();
+  A.pmeta.release();
+  A.prow.release();
   if (A.rows < staged_min_rows()) return;
   const int kStRows = staged_geom() == 0 ? StA::R : StB::R;
   const int kStE = staged_geom() == 0 ? StA::E : StB::E;
@@ -1350,19 +2063,16 @@ void spmv_prepare_csr(DCsr& A, cudaStream_t s) {
   cudaEvent_t e0, e1;
   MGRX_CK(cudaEventCreate(&e0));
   MGRX_CK(cudaEventCreate(&e1));
-  auto time = [&](bool staged) {
+  const bool has_pat = pat_mode() && build_patterns(A, p, h, nb, kStE, s);
+  auto time = [&](bool staged, bool patc = false) {
     A.nblk = staged ? nb : 0;
     A.plan_kind = 0;
+    A.pat = patc ? 1 : 0;
     A.plan = DVec<int>();
     if (staged) A.plan = std::move(plan);
-    spmv(A, xs.get(), ys.get(), s);  // warm
-    MGRX_CK(cudaEventRecord(e0, s));
-    for (int k = 0; k < 10; ++k) spmv(A, xs.get(), ys.get(), s);
-    MGRX_CK(cudaEventRecord(e1, s));
-    MGRX_CK(cudaEventSynchronize(e1));
-    float ms = 0.f;
-    MGRX_CK(cudaEventElapsedTime(&ms, e0, e1));
+    const float ms = tune_time(A, xs.get(), ys.get(), s, e0, e1);
     if (staged) plan = std::move(A.plan);
+    A.pat = 0;
     return ms;
   };
   // best of three trials each, interleaved (robust to clock / neighbour noise).
@@ -1386,18 +2096,12 @@ void spmv_prepare_csr(DCsr& A, cudaStream_t s) {
     A.nblk = nbw;
     A.plan_kind = 1;
     A.plan = std::move(planw);
-    spmv(A, xs.get(), ys.get(), s);  // warm
-    MGRX_CK(cudaEventRecord(e0, s));
-    for (int k = 0; k < 10; ++k) spmv(A, xs.get(), ys.get(), s);
-    MGRX_CK(cudaEventRecord(e1, s));
-    MGRX_CK(cudaEventSynchronize(e1));
-    float ms = 0.f;
-    MGRX_CK(cudaEventElapsedTime(&ms, e0, e1));
+    const float ms = tune_time(A, xs.get(), ys.get(), s, e0, e1);
     planw = std::move(A.plan);
     A.plan_kind = 0;
     return ms;
   };
-  float td = 1e30f, ts = 1e30f, tw = 1e30f;
+  float td = 1e30f, ts = 1e30f, tw = 1e30f, tp = 1e30f;
   const char* pf = std::getenv("MGRX_SPMV_PLAN_FILE");
   bool replayed = false;
   if (pf) {
@@ -1414,6 +2118,7 @@ void spmv_prepare_csr(DCsr& A, cudaStream_t s) {
           ts = st ? 1.f : 2.f;
           td = st ? 2.f : 1.f;
           tw = ws ? 0.5f : 1e30f;
+          tp = has_pat && std::strstr(what, "_pat") ? 0.25f : 1e30f;
         }
       std::fclose(f);
     }
@@ -1422,13 +2127,16 @@ void spmv_prepare_csr(DCsr& A, cudaStream_t s) {
     for (int trial = 0; trial < 5; ++trial) {
       td = std::min(td, time(false));
       ts = std::min(ts, time(true));
+      if (has_pat) tp = std::min(tp, time(true, true));
       if (nbw > 0) tw = std::min(tw, time_w());
     }
     if (pf)
       if (FILE* f = std::fopen(pf, "a")) {
         const float tb = ts < 0.97f * td ? ts : td;
+        const bool usep = has_pat && (pat_mode() == 2 || tp < 0.97f * std::min(ts, td));
         std::fprintf(f, "%d %d %d %s\n", A.rows, A.cols, A.nnz,
-                     tw < 0.97f * tb ? (ts < 0.97f * td ? "wspec_staged" : "wspec")
+                     usep                ? "staged_pat"
+                     : tw < 0.97f * tb ? (ts < 0.97f * td ? "wspec_staged" : "wspec")
                      : ts < 0.97f * td ? "staged"
                                        : "direct");
         std::fclose(f);
@@ -1442,6 +2150,17 @@ void spmv_prepare_csr(DCsr& A, cudaStream_t s) {
   A.nblk = 0;
   A.plan_kind = 0;
   A.nblk_w = 0;
+  if (has_pat && (pat_mode() == 2 || tp < 0.97f * std::min(ts, td))) {
+    if (const char* v = std::getenv("MGRX_VERBOSE"); v && v[0] == '1')
+      std::fprintf(stderr, "spmv_prepare rows %d: pattern-coded staged %.1f us -> staged_pat\n", A.rows, 100.f * tp);
+    A.plan = std::move(plan);
+    A.nblk = nb;
+    A.pat = 1;
+    return;
+  }
+  A.pdict.release();
+  A.pmeta.release();
+  A.prow.release();
   const float tbest = (ts < 0.97f * td || staged_force()) ? ts : td;
   if (nbw > 0 && wspec_jacobi_only()) {
     // the specialised kernel serves the Jacobi sweeps; the others keep the

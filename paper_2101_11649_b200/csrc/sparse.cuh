@@ -42,6 +42,30 @@ struct DCsr {
   int nslice = 0;
   DVec<int> soff, sperm, slen, scol;
   DVec<double> sval;
+  // Pattern-coded columns of the staged plan (spmv_prepare; stencil-like
+  // operators): inside a row block, rows whose column offsets col - row agree
+  // share one dictionary entry. Per block: pmeta = {first dictionary int
+  // (multiple of 4), dictionary row width W}; the block's dictionary holds
+  // npat x W offsets (pdict), prow one byte per row (pattern id; blocks are
+  // strided by 256 bytes). The kernel reads 8 B per entry + 1 B per row
+  // instead of 12 B per entry; the entries and their order are the CSR's, so
+  // row sums are bitwise equal. pat == 0: none.
+  int pat = 0;
+  DVec<int> pdict, pmeta;
+  DVec<unsigned char> prow;
+  // x-window plan (spmv_prepare; irregular medium-row operators, e.g. the
+  // coarse AMG levels): row blocks of <= 256 rows / 2048 entries whose
+  // columns fall into <= kXtLines 128-byte lines of x. A block's lines are
+  // bulk-copied into shared memory as runs of consecutive lines (xt_runs:
+  // {first line, line count} pairs, xt_meta per block: {first run, tail slot
+  // or -1}); entries address the window through 16-bit local columns
+  // (xt_col: slot * 16 + col % 16, same order as col). The row sums run
+  // entirely out of shared memory: no scattered L1 gathers, 10 B per entry.
+  // xt_nblk == 0: none. xt_plan: nblk+1 first rows, nblk+1 first entries.
+  int xt_nblk = 0;
+  int xt_geom = 0;  // 0: 256 rows / 2048 entries / 120 lines x 2 stages; 1: 128 / 1024 / 88 x 2 stages; 2: geometry 0's blocks x 3 stages
+  DVec<int> xt_plan, xt_runs, xt_meta;
+  DVec<unsigned short> xt_col;
   bool empty() const { return rows == 0; }
 };
 
@@ -62,6 +86,9 @@ DCsr csr_from_device(int rows, int cols, const int* ptr, const int* col, const d
                      cudaStream_t s);
 void csr_validate(const DCsr& A, cudaStream_t s);
 DCsr csr_copy(const DCsr& A, cudaStream_t s);
+
+// Evict the L2 by reading `bytes` of `buf` (clean lines; timing helpers).
+void l2_flush_read(const void* buf, size_t bytes, cudaStream_t s);
 
 // ---- SpMV family (solve path) ---------------------------------------------
 // Build the block plan of the bulk-copy-staged SpMV for a solve-path matrix

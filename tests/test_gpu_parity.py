@@ -278,6 +278,100 @@ def test_staged_spmv_bit_exact():
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
 
 
+def test_pattern_coded_spmv_bit_exact():
+    """Pattern-coded columns of the staged SpMV (forced, MGRX_SPMV_PAT=2): a
+    truncated 7-point stencil with defect rows and empty rows, the hybrid-MFD
+    operator (y-dependent offsets), and an irregular matrix that must fall
+    back to plain column indices."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
+        "import paper_2101_11649_b200 as mx, refcpu;"
+        "rng = np.random.default_rng(5)\n"
+        "nx, ny, nz = 37, 29, 23; n = nx * ny * nz\n"
+        "rows = []\n"
+        "for i in range(n):\n"
+        "    x, y, z = i % nx, (i // nx) % ny, i // (nx * ny)\n"
+        "    c = [i]\n"
+        "    if x > 0: c.append(i - 1)\n"
+        "    if x < nx - 1: c.append(i + 1)\n"
+        "    if y > 0: c.append(i - nx)\n"
+        "    if y < ny - 1: c.append(i + nx)\n"
+        "    if z > 0: c.append(i - nx * ny)\n"
+        "    if z < nz - 1: c.append(i + nx * ny)\n"
+        "    if i % 997 == 0: c = []\n"
+        "    if i % 1013 == 5: c = list(rng.choice(n, size=11, replace=False))\n"
+        "    rows.append(np.sort(np.array(c, np.int32)))\n"
+        "ptr = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int32)\n"
+        "col = np.concatenate(rows).astype(np.int32)\n"
+        "val = rng.standard_normal(ptr[-1]); x = rng.standard_normal(n)\n"
+        "y = mx.Matrix(ptr, col, val).spmv(x); yr = refcpu.spmv(ptr, col, val, x)\n"
+        "assert np.array_equal(y.view(np.int64), yr.view(np.int64)), 'stencil'\n"
+        "P = mx.mfd_problem(24, 20, 12, 'layered')\n"
+        "x = rng.standard_normal(P.n)\n"
+        "y = mx.Matrix(P.ptr, P.col, P.val).spmv(x); yr = refcpu.spmv(P.ptr, P.col, P.val, x)\n"
+        "assert np.array_equal(y.view(np.int64), yr.view(np.int64)), 'mfd'\n"
+        "n = 50021; lens = rng.integers(0, 9, n)\n"
+        "ptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)\n"
+        "col = np.concatenate([np.sort(rng.choice(n, size=l, replace=False)) for l in lens]).astype(np.int32)\n"
+        "val = rng.standard_normal(ptr[-1]); x = rng.standard_normal(n)\n"
+        "y = mx.Matrix(ptr, col, val).spmv(x); yr = refcpu.spmv(ptr, col, val, x)\n"
+        "assert np.array_equal(y.view(np.int64), yr.view(np.int64)), 'irregular'\n"
+        "print('ok')")
+    root = make_golden.ROOT
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                         env={**__import__("os").environ, "MGRX_SPMV_STAGED": "2", "MGRX_SPMV_PAT": "2",
+                              "MGRX_SPMV_SELL": "0", "MGRX_VERBOSE": "1"}, timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+    # the two structured operators took the pattern-coded plan, the irregular one did not
+    assert out.stderr.count("-> staged_pat") == 2, out.stderr[-2000:]
+
+
+def test_xwindow_spmv_bit_exact():
+    """x-window staged SpMV (forced, MGRX_SPMV_XT=2): an irregular banded
+    operator with odd column count (tail slot), empty rows and a few
+    far-reaching rows; a rectangular one; and a fully random matrix whose blocks
+    are cut down by the line / run caps."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
+        "import paper_2101_11649_b200 as mx, refcpu;"
+        "rng = np.random.default_rng(17)\n"
+        "def banded(n, m):\n"
+        "    rows = []\n"
+        "    for i in range(n):\n"
+        "        j = i * m // n\n"
+        "        k = rng.integers(5, 26)\n"
+        "        cand = np.concatenate([np.arange(j - 40, j + 41), np.arange(j - 5040, j - 4960), np.arange(j + 4960, j + 5040)])\n"
+        "        cand = cand[(cand >= 0) & (cand < m)]\n"
+        "        c = rng.choice(cand, size=min(k, len(cand)), replace=False)\n"
+        "        if i % 501 == 0: c = c[:0]\n"
+        "        if i % 733 == 1: c = np.concatenate([c, rng.choice(m, size=30, replace=False)])\n"
+        "        if i >= n - 3: c = np.concatenate([c, [m - 1, m - 2]])\n"
+        "        rows.append(np.unique(c).astype(np.int32))\n"
+        "    ptr = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int32)\n"
+        "    return ptr, np.concatenate(rows).astype(np.int32)\n"
+        "for n, m in ((60001, 60001), (30000, 45001)):\n"
+        "    ptr, col = banded(n, m)\n"
+        "    val = rng.standard_normal(ptr[-1]); x = rng.standard_normal(m)\n"
+        "    y = mx.Matrix(ptr, col, val, shape=(n, m)).spmv(x); yr = refcpu.spmv(ptr, col, val, x, ncols=m)\n"
+        "    assert np.array_equal(y.view(np.int64), yr.view(np.int64)), (n, m)\n"
+        "n = 20011; lens = rng.integers(0, 19, n)\n"
+        "ptr = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)\n"
+        "col = np.concatenate([np.sort(rng.choice(n, size=l, replace=False)) for l in lens]).astype(np.int32)\n"
+        "val = rng.standard_normal(ptr[-1]); x = rng.standard_normal(n)\n"
+        "y = mx.Matrix(ptr, col, val).spmv(x); yr = refcpu.spmv(ptr, col, val, x)\n"
+        "assert np.array_equal(y.view(np.int64), yr.view(np.int64)), 'random'\n"
+        "print('ok')")
+    root = make_golden.ROOT
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                         env={**__import__("os").environ, "MGRX_SPMV_XT": "2", "MGRX_VERBOSE": "1"}, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+    assert out.stderr.count("-> xtile") == 3, out.stderr[-2000:]
+
+
 def test_zero_rhs_and_errors():
     P = mx.mfd_problem(4, 4, 3, "iid")
     A = mx.Matrix(P.ptr, P.col, P.val)
