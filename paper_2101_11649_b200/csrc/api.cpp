@@ -383,6 +383,7 @@ int mgrx_setup(mgrx_ctx* ctx, mgrx_mat* A, const int* labels, int nfields, const
     h->A = csr_copy(A->A, s);
     h->H.setup(h->A, lab, fields, unknown_map ? &umap : nullptr, strat, s);
     spmv_prepare(h->A, s);
+    h->H.tune_spmv(s);
     h->setup_s = t.stop();
     h->vin.alloc(n > 0 ? n : 1, s);
     h->vout.alloc(n > 0 ? n : 1, s);

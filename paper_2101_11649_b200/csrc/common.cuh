@@ -61,6 +61,34 @@ __device__ __forceinline__ void pdl_enter() {
 constexpr bool kPdlStagedEarly = (MGRX_PDL_MODE & 2) != 0;
 bool pdl_enabled();
 
+// Under MGRX_PDL_MODE bit 1 only launches flagged `early` (persistent grids
+// that fill every SM to their shared-memory limit, so their CTAs cannot pile
+// up on the first SMs that drain) may start before the previous grid has
+// completed; everything else is then launched fully serialised.
+struct PdlEarly {
+  bool ok;
+};
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args);
+template <class... KArgs, class... Args>
+void launch_pdl(PdlEarly early, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() && (!kPdlStagedEarly || early.ok) ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+  if (e != cudaSuccess)
+    throw RuntimeError(std::string("CUDA error: ") + cudaGetErrorString(e) + " (launch grid " +
+                       std::to_string(grid.x) + " block " + std::to_string(block.x) + " smem " + std::to_string(smem) +
+                       ")");
+}
 template <class... KArgs, class... Args>
 void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg{};
@@ -70,7 +98,7 @@ void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() && !kPdlStagedEarly ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);

@@ -11,6 +11,8 @@
 #include "coarsen.cuh"
 #include "hierarchy.cuh"
 
+#include <functional>
+
 namespace mgrx {
 namespace {
 
@@ -968,6 +970,81 @@ void MgrHier::apply_graph(const double* v, double* z, cudaStream_t s, bool exact
   }
   MGRX_CK(cudaGraphLaunch(it->second.exec, s));
   count_launch(it->second.nodes);
+}
+
+void MgrHier::tune_spmv(cudaStream_t s) {
+  static const bool on = [] {
+    const char* e = std::getenv("MGRX_TUNE_INSITU");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (!on || n == 0 || std::getenv("MGRX_SPMV_PLAN_FILE")) return;  // (a plan file replays recorded choices)
+  std::vector<DCsr*> cands;
+  auto add = [&](DCsr& M) {
+    if (M.xt_plan_nblk > 0) cands.push_back(&M);
+  };
+  std::function<void(AmgHier*)> add_amg = [&](AmgHier* a) {
+    if (!a) return;
+    for (auto& L : a->levels) {
+      add(L.A);
+      add(L.P);
+      add(L.R);
+    }
+  };
+  for (auto& L : levels) {
+    for (DCsr* M : {&L.A, &L.P, &L.R, &L.Acf, &L.Aff}) add(*M);
+    add_amg(L.f_relax.amg.get());
+    if (L.g_relax) add_amg(L.g_relax->amg.get());
+  }
+  add(A_coarse);
+  add_amg(coarse_amg.get());
+  if (cands.empty()) return;
+  std::sort(cands.begin(), cands.end(), [](const DCsr* a, const DCsr* b) { return a->nnz > b->nnz; });
+  DVec<double> v(n, s), z(n, s);
+  v.zero();
+  cudaEvent_t e0, e1;
+  MGRX_CK(cudaEventCreate(&e0));
+  MGRX_CK(cudaEventCreate(&e1));
+  const long long l0 = g_launches;
+  int reps = 3;
+  auto time = [&] {
+    float best = 1e30f;
+    for (int rep = 0; rep < reps; ++rep) {
+      MGRX_CK(cudaEventRecord(e0, s));
+      apply(v.get(), z.get(), s, false);
+      MGRX_CK(cudaEventRecord(e1, s));
+      MGRX_CK(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      MGRX_CK(cudaEventElapsedTime(&ms, e0, e1));
+      best = std::min(best, ms);
+    }
+    return best;
+  };
+  apply(v.get(), z.get(), s, false);  // warm
+  float cur = time();
+  // (sweep-bound strategies, e.g. exact Gauss-Seidel: one repetition, or no
+  // pass at all when an application takes tens of milliseconds)
+  if (cur > 5.f) reps = 1;
+  if (cur > 30.f) cands.clear();
+  const bool verbose = [] {
+    const char* e = std::getenv("MGRX_VERBOSE");
+    return e && e[0] == '1';
+  }();
+  for (DCsr* M : cands) {
+    const int was = M->xt_nblk;
+    M->xt_nblk = was ? 0 : M->xt_plan_nblk;
+    const float t = time();
+    if (verbose)
+      std::fprintf(stderr, "tune_spmv rows %d nnz %d: x-window %s %.1f us, %s %.1f us\n", M->rows, M->nnz,
+                   was ? "on" : "off", 1e3f * cur, was ? "off" : "on", 1e3f * t);
+    if (t < 0.995f * cur) cur = t;
+    else M->xt_nblk = was;
+  }
+  for (DCsr* M : cands)
+    if (M->xt_nblk == 0) spmv_drop_xtile(*M);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  g_launches = l0;
+  check(s);
 }
 
 MgrHier::~MgrHier() {

@@ -115,6 +115,10 @@ struct MgrHier {
   void prolong(int l, const double* e, const double* zF, double* z, cudaStream_t s);
   // Same, replayed from a CUDA graph captured once per (v, z, exact).
   void apply_graph(const double* v, double* z, cudaStream_t s, bool exact = true);
+  // In-situ choice of the x-window SpMV per operator: each candidate plan is
+  // switched on / off by timing whole applications (every operator is then
+  // read as cold as in the solve, with its real epilogues and neighbours).
+  void tune_spmv(cudaStream_t s);
   void check(cudaStream_t s);
   ~MgrHier();
 

@@ -10,6 +10,8 @@
 
 #include "sparse.cuh"
 
+#include <thread>
+
 #include <map>
 #include <mutex>
 #include <set>
@@ -646,9 +648,9 @@ __global__ void __launch_bounds__(Gm::T) k_spmv_staged(int nblk, const int* __re
 __constant__ int c_xt_dbg = 0;  // MGRX_XT_DBG: timing experiments (1: window as one copy)
 constexpr int kXtRuns = 32;     // runs per block: one per lane of the copy warp
 constexpr int kXtDirect = -2;   // block meta "tail" value: no window, global columns
-template <int kR_, int kE_, int kL_, int kS_>
+template <int kR_, int kE_, int kL_, int kS_, int kCtas_>
 struct XtGeom {
-  static constexpr int R = kR_, E = kE_, L = kL_, S = kS_, T = kR_ + 32;
+  static constexpr int R = kR_, E = kE_, L = kL_, S = kS_, T = kR_ + 32, CTAS = kCtas_;
   struct Stage {
     int rp[R + 8];
     unsigned short col[E + 16];
@@ -657,9 +659,14 @@ struct XtGeom {
   };
   static constexpr size_t smem = S * sizeof(Stage) + 32 * S;
 };
-using XtA = XtGeom<256, 2048, 120, 2>;  // 3 CTAs / SM
-using XtB = XtGeom<128, 1024, 88, 2>;   // 5 CTAs / SM
-using XtC = XtGeom<256, 2048, 120, 3>;  // XtA's blocks, 3 stages, 2 CTAs / SM
+using XtA = XtGeom<256, 2048, 120, 2, 3>;  // 3 CTAs / SM
+using XtB = XtGeom<128, 1024, 88, 2, 5>;   // 5 CTAs / SM
+using XtC = XtGeom<256, 2048, 120, 3, 2>;  // XtA's blocks, 3 stages, 2 CTAs / SM
+using XtD = XtGeom<128, 1024, 88, 3, 3>;   // XtB's blocks, 3 stages, 3 CTAs / SM
+using XtE = XtGeom<128, 1024, 88, 4, 2>;   // XtB's blocks, 4 stages, 2 CTAs / SM
+using XtF = XtGeom<64, 512, 48, 4, 5>;     // 64 rows / 512 entries / 48 lines, 4 stages, 5 CTAs / SM
+constexpr int kXtGeoms = 6;
+constexpr int kXtTuned = 1;  // geometries the setup timing tries by default (the others measured slower everywhere)
 
 // The copy warp: for each of the CTA's blocks it waits until the stage is
 // free, then its lanes issue the block's copies in parallel (one x run per
@@ -668,7 +675,7 @@ using XtC = XtGeom<256, 2048, 120, 3>;  // XtA's blocks, 3 stages, 2 CTAs / SM
 // entries and epilogue operands are loaded one block ahead, so a block's
 // critical path is the stage wait and the shared-memory row sum only.
 template <class Gm, class Epi>
-__global__ void __launch_bounds__(Gm::T) k_spmv_xtile(int nblk, const int* __restrict__ plan,
+__global__ void __launch_bounds__(Gm::T, Gm::CTAS) k_spmv_xtile(int nblk, const int* __restrict__ plan,
                                                       const int* __restrict__ ptr,
                                                       const unsigned short* __restrict__ lcol,
                                                       const double* __restrict__ val, const int* __restrict__ runs,
@@ -707,30 +714,30 @@ __global__ void __launch_bounds__(Gm::T) k_spmv_xtile(int nblk, const int* __res
     struct Desc {
       int r0, r1, p0, p1, l0, nl, tail;
     };
-    auto load_desc = [&](int b) {  // plan entries of a block (all setup data)
-      Desc d;
-      d.r0 = prow[b];
-      d.r1 = prow[b + 1];
-      d.p0 = pnnz[b];
-      d.p1 = pnnz[b + 1];
-      const int q0 = meta[2 * b], q1 = meta[2 * b + 2];
-      d.tail = meta[2 * b + 1];
-      d.l0 = 0;
-      d.nl = 0;
-      if (q0 + l < q1) {
-        d.l0 = runs[2 * (q0 + l)];
-        d.nl = runs[2 * (q0 + l) + 1];
+    // Plan entries of a block (all setup data): independent loads — a
+    // block's runs sit at a fixed stride (lane l's run at slot 32 b + l,
+    // line count 0 when unused) — fetched two blocks ahead, so their (cold:
+    // HBM) latency never sits between two copies of this warp.
+    auto load_desc = [&](int b) {
+      Desc d{0, 0, 0, 0, 0, 0, -1};
+      if (b < nblk) {
+        d.r0 = prow[b];
+        d.r1 = prow[b + 1];
+        d.p0 = pnnz[b];
+        d.p1 = pnnz[b + 1];
+        d.tail = meta[2 * b + 1];
+        const int2 rn = reinterpret_cast<const int2*>(runs)[static_cast<size_t>(b) * kXtRuns + l];
+        d.l0 = rn.x;
+        d.nl = rn.y;
       }
       return d;
     };
-    Desc d{};
-    if (blockIdx.x < nblk) d = load_desc(blockIdx.x);
+    Desc d = load_desc(blockIdx.x), nx = load_desc(blockIdx.x + G);
     pdl_enter();  // x is the previous kernel's
     int it = 0;
     for (int b = blockIdx.x; b < nblk; b += G, ++it) {
       const int s = it % kS;
-      Desc nx{};
-      if (b + G < nblk) nx = load_desc(b + G);  // in flight while this block's stage is awaited
+      const Desc nn = load_desc(b + 2 * G);
       if (it >= kS) wait(smem_u32(empty + s), ((it / kS) - 1) & 1u);
       const unsigned mb = smem_u32(full + s);
       Stage& S = stg[s];
@@ -791,15 +798,16 @@ __global__ void __launch_bounds__(Gm::T) k_spmv_xtile(int nblk, const int* __res
         asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(mb), "r"(nb + brp + bc + bv)
                      : "memory");
       d = nx;
+      nx = nn;
     }
     return;
   }
   // ---- row warps
   struct Blk {
-    int r0, r1, p0, tail;
+    int r0, r1, p0, p1, tail;
   };
   auto load_blk = [&](int b) {
-    return b < nblk ? Blk{prow[b], prow[b + 1], pnnz[b], meta[2 * b + 1]} : Blk{0, 0, 0, -1};
+    return b < nblk ? Blk{prow[b], prow[b + 1], pnnz[b], pnnz[b + 1], meta[2 * b + 1]} : Blk{0, 0, 0, 0, -1};
   };
   // plan entries two blocks ahead, epilogue operands one block ahead
   Blk cur = load_blk(blockIdx.x), nxt = load_blk(blockIdx.x + G);
@@ -1166,8 +1174,8 @@ void launch_staged_k(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
                                  static_cast<int>(Gm::smem)));
   const int per_sm = static_cast<int>(std::min<size_t>(8, 227 * 1024 / Gm::smem));
   const int grid = std::min(A.nblk, device_sms() * std::min(per_sm, staged_ctas_per_sm()));
-  launch_pdl(k_spmv_staged<Gm, Epi, Xs, kLong>, grid, Gm::T, Gm::smem, s, A.nblk, A.plan.get(), A.ptr.get(),
-             A.col.get(), A.val.get(), x, epi, PatArgs{});
+  launch_pdl(PdlEarly{grid == device_sms() * per_sm}, k_spmv_staged<Gm, Epi, Xs, kLong>, grid, Gm::T, Gm::smem, s,
+             A.nblk, A.plan.get(), A.ptr.get(), A.col.get(), A.val.get(), x, epi, PatArgs{});
   MGRX_LAUNCH_CK();
   count_launch();
 }
@@ -1226,9 +1234,14 @@ void launch_xtile_g(const DCsr& A, const double* x, Epi epi, cudaStream_t s) {
 }
 template <class Epi>
 void launch_xtile(const DCsr& A, const double* x, Epi epi, cudaStream_t s) {
-  if (A.xt_geom == 1) launch_xtile_g<XtB>(A, x, epi, s);
-  else if (A.xt_geom == 2) launch_xtile_g<XtC>(A, x, epi, s);
-  else launch_xtile_g<XtA>(A, x, epi, s);
+  switch (A.xt_geom) {
+    case 1: launch_xtile_g<XtB>(A, x, epi, s); break;
+    case 2: launch_xtile_g<XtC>(A, x, epi, s); break;
+    case 3: launch_xtile_g<XtD>(A, x, epi, s); break;
+    case 4: launch_xtile_g<XtE>(A, x, epi, s); break;
+    case 5: launch_xtile_g<XtF>(A, x, epi, s); break;
+    default: launch_xtile_g<XtA>(A, x, epi, s); break;
+  }
 }
 
 // BSR SpMV (b x b blocks, b <= 4): a CTA takes one chunk of block rows
@@ -1482,7 +1495,7 @@ float tune_time(const DCsr& A, const double* x, double* y, cudaStream_t s, cudaE
   DVec<char> fl(kFlush, s);
   MGRX_CK(cudaMemsetAsync(fl.get(), 0, kFlush, s));
   float tot = 0.f;
-  for (int k = 0; k < 5; ++k) {
+  for (int k = 0; k < 3; ++k) {
     l2_flush_read(fl.get(), kFlush, s);
     MGRX_CK(cudaEventRecord(e0, s));
     spmv(A, x, y, s);
@@ -1491,7 +1504,7 @@ float tune_time(const DCsr& A, const double* x, double* y, cudaStream_t s, cudaE
     MGRX_CK(cudaEventElapsedTime(&ms, e0, e1));
     tot += ms;
   }
-  return 2.f * tot;
+  return tot * (10.f / 3.f);
 }
 
 // Row blocks of <= max_rows rows / <= max_e entries: the nb+1 first rows then
@@ -1767,94 +1780,136 @@ void spmv_prepare_csr(DCsr& A, cudaStream_t s);
 // x-window plan (k_spmv_xtile): greedy row blocks under the row / entry /
 // line caps, each block's lines as runs, 16-bit local columns.
 bool build_xtile(DCsr& A, int geom, cudaStream_t s) {
-  const int kXtRows = geom == 1 ? XtB::R : XtA::R, kXtE = geom == 1 ? XtB::E : XtA::E,
-            kXtLines = geom == 1 ? XtB::L : XtA::L;
+  const bool gb = geom == 1 || geom == 3 || geom == 4, gf = geom == 5;
+  const int kXtRows = gf ? XtF::R : gb ? XtB::R : XtA::R, kXtE = gf ? XtF::E : gb ? XtB::E : XtA::E,
+            kXtLines = gf ? XtF::L : gb ? XtB::L : XtA::L;
   const int n = A.rows;
   if (n == 0 || A.nnz == 0) return false;
   const std::vector<int> p = A.ptr.download(n + 1);
   const std::vector<int> c = A.col.download(A.nnz);
   const int nlines = (A.cols + 15) / 16;
-  std::vector<int> slot_of(nlines, -1);
-  std::vector<int> rs{0}, ns{0}, runs, meta, lines;
   std::vector<unsigned short> lc(static_cast<size_t>(A.nnz) + 16, 0);
-  int r = 0, ndirect = 0;
-  while (r < n) {
-    if (p[r + 1] - p[r] > kXtE) return false;
-    lines.clear();
-    int q = r;
-    // grow the block row by row while it stays under the caps
-    while (q < n && q - r < kXtRows && p[q + 1] - p[r] <= kXtE) {
-      const size_t before = lines.size();
-      for (int k = p[q]; k < p[q + 1]; ++k) {
-        const int ln = c[k] >> 4;
-        if (slot_of[ln] < 0) {
-          slot_of[ln] = 0;
-          lines.push_back(ln);
-        }
+  // Row chunks are planned independently (host threads; a chunk boundary is
+  // a block boundary), then concatenated in row order.
+  struct Part {
+    std::vector<int> rs, ns, runs, meta;
+    int ndirect = 0;
+    bool ok = true;
+  };
+  auto plan_rows = [&](int ra, int rb, Part& out) {
+    std::vector<int> slot_of(nlines, -1), lines;
+    std::vector<int>&rs = out.rs, &ns = out.ns, &runs = out.runs, &meta = out.meta;
+    int& ndirect = out.ndirect;
+    const int n = rb;  // rows of this chunk end here
+    int r = ra;
+    while (r < n) {
+      if (p[r + 1] - p[r] > kXtE) {
+        out.ok = false;
+        return;
       }
-      if (static_cast<int>(lines.size()) > kXtLines) {
-        for (size_t i = before; i < lines.size(); ++i) slot_of[lines[i]] = -1;
-        lines.resize(before);
-        break;
-      }
-      ++q;
-    }
-    bool direct = false;
-    if (q == r) {  // one row alone exceeds the window: a block of its own with global columns
-      direct = true;
-      q = r + 1;
-    }
-    std::sort(lines.begin(), lines.end());
-    // runs of consecutive lines; too many runs: shorten the block
-    while (!direct) {
-      int nr = lines.empty() ? 0 : 1;
-      for (size_t i = 1; i < lines.size(); ++i) nr += lines[i] != lines[i - 1] + 1;
-      if (nr <= kXtRuns) break;
-      for (int ln : lines) slot_of[ln] = -1;
       lines.clear();
-      q = r + std::max(1, (q - r) / 2);
-      for (int k = p[r]; k < p[q]; ++k) {
-        const int ln = c[k] >> 4;
-        if (slot_of[ln] < 0) {
-          slot_of[ln] = 0;
-          lines.push_back(ln);
+      int q = r;
+      // grow the block row by row while it stays under the caps
+      while (q < n && q - r < kXtRows && p[q + 1] - p[r] <= kXtE) {
+        const size_t before = lines.size();
+        for (int k = p[q]; k < p[q + 1]; ++k) {
+          const int ln = c[k] >> 4;
+          if (slot_of[ln] < 0) {
+            slot_of[ln] = 0;
+            lines.push_back(ln);
+          }
         }
+        if (static_cast<int>(lines.size()) > kXtLines) {
+          for (size_t i = before; i < lines.size(); ++i) slot_of[lines[i]] = -1;
+          lines.resize(before);
+          break;
+        }
+        ++q;
+      }
+      bool direct = false;
+      if (q == r) {  // one row alone exceeds the window: a block of its own with global columns
+        direct = true;
+        q = r + 1;
       }
       std::sort(lines.begin(), lines.end());
-      if (q - r == 1) {
-        int nr1 = lines.empty() ? 0 : 1;
-        for (size_t i = 1; i < lines.size(); ++i) nr1 += lines[i] != lines[i - 1] + 1;
-        if (nr1 > kXtRuns) direct = true;
+      // runs of consecutive lines; too many runs: shorten the block
+      while (!direct) {
+        int nr = lines.empty() ? 0 : 1;
+        for (size_t i = 1; i < lines.size(); ++i) nr += lines[i] != lines[i - 1] + 1;
+        if (nr <= kXtRuns) break;
+        for (int ln : lines) slot_of[ln] = -1;
+        lines.clear();
+        q = r + std::max(1, (q - r) / 2);
+        for (int k = p[r]; k < p[q]; ++k) {
+          const int ln = c[k] >> 4;
+          if (slot_of[ln] < 0) {
+            slot_of[ln] = 0;
+            lines.push_back(ln);
+          }
+        }
+        std::sort(lines.begin(), lines.end());
+        if (q - r == 1) {
+          int nr1 = lines.empty() ? 0 : 1;
+          for (size_t i = 1; i < lines.size(); ++i) nr1 += lines[i] != lines[i - 1] + 1;
+          if (nr1 > kXtRuns) direct = true;
+        }
       }
-    }
-    meta.push_back(static_cast<int>(runs.size() / 2));
-    if (direct) {
+      meta.push_back(0);  // (unused)
+      const size_t run0 = runs.size();
+      if (direct) {
+        for (int ln : lines) slot_of[ln] = -1;
+        lines.clear();
+        ++ndirect;
+      }
+      int tail = direct ? kXtDirect : -1;
+      for (size_t i = 0; i < lines.size(); ++i) {
+        slot_of[lines[i]] = static_cast<int>(i);
+        if (i == 0 || lines[i] != lines[i - 1] + 1) {
+          runs.push_back(lines[i]);
+          runs.push_back(1);
+        } else {
+          ++runs.back();
+        }
+        if ((A.cols & 1) && lines[i] == (A.cols - 1) >> 4) tail = static_cast<int>(i) * 16 + ((A.cols - 1) & 15);
+      }
+      meta.push_back(tail);
+      runs.resize(run0 + 2 * kXtRuns, 0);  // fixed stride: kXtRuns {first line, count} slots per block
+      if (!direct)
+        for (int k = p[r]; k < p[q]; ++k) lc[k] = static_cast<unsigned short>(slot_of[c[k] >> 4] * 16 + (c[k] & 15));
       for (int ln : lines) slot_of[ln] = -1;
-      lines.clear();
-      ++ndirect;
+      rs.push_back(q);
+      ns.push_back(p[q]);
+      r = q;
     }
-    int tail = direct ? kXtDirect : -1;
-    for (size_t i = 0; i < lines.size(); ++i) {
-      slot_of[lines[i]] = static_cast<int>(i);
-      if (i == 0 || lines[i] != lines[i - 1] + 1) {
-        runs.push_back(lines[i]);
-        runs.push_back(1);
-      } else {
-        ++runs.back();
-      }
-      if ((A.cols & 1) && lines[i] == (A.cols - 1) >> 4) tail = static_cast<int>(i) * 16 + ((A.cols - 1) & 15);
-    }
-    meta.push_back(tail);
-    if (!direct)
-      for (int k = p[r]; k < p[q]; ++k) lc[k] = static_cast<unsigned short>(slot_of[c[k] >> 4] * 16 + (c[k] & 15));
-    for (int ln : lines) slot_of[ln] = -1;
-    rs.push_back(q);
-    ns.push_back(p[q]);
-    r = q;
+  };
+  const int nthr = A.nnz < (1 << 20) ? 1 : static_cast<int>(std::min(8u, std::max(1u, std::thread::hardware_concurrency())));
+  std::vector<Part> parts(nthr);
+  std::vector<int> cut(nthr + 1, n);
+  cut[0] = 0;
+  for (int t = 1; t < nthr; ++t)  // chunk boundaries at equal entry counts
+    cut[t] = static_cast<int>(std::lower_bound(p.begin(), p.end(), static_cast<int>(static_cast<long long>(A.nnz) * t / nthr)) -
+                              p.begin());
+  for (int t = 1; t <= nthr; ++t) cut[t] = std::max(cut[t], cut[t - 1]);
+  cut[nthr] = n;
+  {
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nthr; ++t) pool.emplace_back([&, t] { plan_rows(cut[t], cut[t + 1], parts[t]); });
+    plan_rows(cut[0], cut[1], parts[0]);
+    for (auto& th : pool) th.join();
+  }
+  std::vector<int> rs{0}, ns{0}, runs, meta;
+  int ndirect = 0;
+  for (auto& pt : parts) {
+    if (!pt.ok) return false;
+    rs.insert(rs.end(), pt.rs.begin(), pt.rs.end());
+    ns.insert(ns.end(), pt.ns.begin(), pt.ns.end());
+    runs.insert(runs.end(), pt.runs.begin(), pt.runs.end());
+    meta.insert(meta.end(), pt.meta.begin(), pt.meta.end());
+    ndirect += pt.ndirect;
   }
   const int nb = static_cast<int>(rs.size()) - 1;
   if (ndirect > nb / 2) return false;  // not a windowable operator
-  meta.push_back(static_cast<int>(runs.size() / 2));
+  meta.push_back(0);
   meta.push_back(-1);
   rs.insert(rs.end(), ns.begin(), ns.end());
   A.xt_plan.alloc(rs.size(), s);
@@ -1882,10 +1937,13 @@ void xtile_try(DCsr& A, cudaStream_t s) {
     return e ? std::atoi(e) : -1;
   }();
   A.xt_nblk = 0;
+  A.xt_plan_nblk = 0;
   if (!mode || A.bsr || A.rows < staged_min_rows()) return;
   // (one thread per row: rows averaging > 48 entries keep the block-wide
-  // product-pass kernels)
-  if (mode == 1 && static_cast<long long>(A.nnz) > 48LL * A.rows) return;
+  // product-pass kernels; under 6 entries per row the window costs more than
+  // the gathers it replaces)
+  if (mode == 1 && (static_cast<long long>(A.nnz) > 48LL * A.rows || static_cast<long long>(A.nnz) < 6LL * A.rows))
+    return;
   DVec<double> xs(A.cols > 0 ? A.cols : 1, s), ys(A.rows, s);
   xs.zero();
   cudaEvent_t e0, e1;
@@ -1923,23 +1981,22 @@ void xtile_try(DCsr& A, cudaStream_t s) {
       char what[16];
       while (std::fscanf(f, "%d %d %d %15s", &r, &c, &z, what) == 4)
         if (r == A.rows && c == A.cols && z == A.nnz) {
-          if (!std::strcmp(what, "xtile0")) replay = 0;
-          if (!std::strcmp(what, "xtile1")) replay = 1;
-          if (!std::strcmp(what, "xtile2")) replay = 2;
+          if (!std::strncmp(what, "xtile", 5) && what[5] >= '0' && what[5] < '0' + kXtGeoms) replay = what[5] - '0';
           if (!std::strcmp(what, "noxtile")) replay = -1;
         }
       std::fclose(f);
     }
   Cand best;
   float tc = 1e30f;
-  if (replay == -2) tc = std::min(tune_time(A, xs.get(), ys.get(), s, e0, e1), tune_time(A, xs.get(), ys.get(), s, e0, e1));
-  for (int g = 0; g < 3; ++g) {
-    if (force_geom >= 0 && g != force_geom) continue;
+  if (replay == -2)
+    for (int trial = 0; trial < 2; ++trial) tc = std::min(tc, tune_time(A, xs.get(), ys.get(), s, e0, e1));
+  for (int g = 0; g < kXtGeoms; ++g) {
+    if (force_geom >= 0 ? g != force_geom : (replay == -2 && g >= kXtTuned)) continue;
     if (replay != -2 && replay != g) continue;
     if (!build_xtile(A, g, s)) continue;
     Cand c;
     if (replay == -2)
-      for (int trial = 0; trial < 3; ++trial) c.t = std::min(c.t, tune_time(A, xs.get(), ys.get(), s, e0, e1));
+      for (int trial = 0; trial < 2; ++trial) c.t = std::min(c.t, tune_time(A, xs.get(), ys.get(), s, e0, e1));
     else c.t = 0.f;
     if (const char* v = std::getenv("MGRX_VERBOSE"); v && v[0] == '1')
       std::fprintf(stderr, "spmv_prepare rows %d nnz %d: current %.1f us xtile geometry %d (%d blocks) %.1f us\n",
@@ -1949,17 +2006,33 @@ void xtile_try(DCsr& A, cudaStream_t s) {
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  // Kept as a candidate unless clearly slower alone; switched on when clearly
+  // faster. Inside a hierarchy the in-situ pass has the last word.
+  const bool cand = best.nb > 0 && (mode == 2 || replay >= 0 || best.t < 1.10f * tc);
   const bool keep = best.nb > 0 && (mode == 2 || replay >= 0 || best.t < 0.97f * tc);
   if (pf && replay == -2)
     if (FILE* f = std::fopen(pf, "a")) {
-      std::fprintf(f, "%d %d %d %s\n", A.rows, A.cols, A.nnz, !keep ? "noxtile" : best.geom == 2 ? "xtile2" : best.geom ? "xtile1" : "xtile0");
+      if (keep) std::fprintf(f, "%d %d %d xtile%d\n", A.rows, A.cols, A.nnz, best.geom);
+      else std::fprintf(f, "%d %d %d noxtile\n", A.rows, A.cols, A.nnz);
       std::fclose(f);
     }
-  if (keep) {
+  if (cand) {
     install(best);
+    A.xt_plan_nblk = A.xt_nblk;
+    if (!keep) A.xt_nblk = 0;
     if (const char* v = std::getenv("MGRX_VERBOSE"); v && v[0] == '1')
-      std::fprintf(stderr, "spmv_prepare rows %d nnz %d -> xtile geometry %d\n", A.rows, A.nnz, A.xt_geom);
+      std::fprintf(stderr, "spmv_prepare rows %d nnz %d -> xtile geometry %d%s\n", A.rows, A.nnz, A.xt_geom,
+                   keep ? "" : " (candidate, off)");
   }
+}
+
+void spmv_drop_xtile(DCsr& A) {
+  A.xt_nblk = 0;
+  A.xt_plan_nblk = 0;
+  A.xt_plan.release();
+  A.xt_runs.release();
+  A.xt_meta.release();
+  A.xt_col.release();
 }
 
 // MGRX_SPMV_PAT: 0 off, 1 (default) pattern-coded columns where they time
@@ -2124,7 +2197,7 @@ void spmv_prepare_csr(DCsr& A, cudaStream_t s) {
     }
   }
   if (!replayed) {
-    for (int trial = 0; trial < 5; ++trial) {
+    for (int trial = 0; trial < 3; ++trial) {
       td = std::min(td, time(false));
       ts = std::min(ts, time(true));
       if (has_pat) tp = std::min(tp, time(true, true));

@@ -57,12 +57,16 @@ struct DCsr {
   // coarse AMG levels): row blocks of <= 256 rows / 2048 entries whose
   // columns fall into <= kXtLines 128-byte lines of x. A block's lines are
   // bulk-copied into shared memory as runs of consecutive lines (xt_runs:
-  // {first line, line count} pairs, xt_meta per block: {first run, tail slot
-  // or -1}); entries address the window through 16-bit local columns
+  // 32 {first line, line count} slots per block, xt_meta per block: {0, tail
+  // slot or -1 or -2 = no window}); entries address the window through 16-bit local columns
   // (xt_col: slot * 16 + col % 16, same order as col). The row sums run
   // entirely out of shared memory: no scattered L1 gathers, 10 B per entry.
   // xt_nblk == 0: none. xt_plan: nblk+1 first rows, nblk+1 first entries.
   int xt_nblk = 0;
+  // a built plan the per-matrix timing did not rule out; the hierarchy's
+  // in-situ pass (MgrHier::tune_spmv) switches xt_nblk between 0 and this by
+  // timing whole preconditioner applications
+  int xt_plan_nblk = 0;
   int xt_geom = 0;  // 0: 256 rows / 2048 entries / 120 lines x 2 stages; 1: 128 / 1024 / 88 x 2 stages; 2: geometry 0's blocks x 3 stages
   DVec<int> xt_plan, xt_runs, xt_meta;
   DVec<unsigned short> xt_col;
@@ -96,6 +100,8 @@ void l2_flush_read(const void* buf, size_t bytes, cudaStream_t s);
 // matrices without a plan use the direct kernels. Host-
 // synchronising: call at setup, never inside a captured region.
 void spmv_prepare(DCsr& A, cudaStream_t s);
+// Drop an x-window plan that the in-situ pass switched off.
+void spmv_drop_xtile(DCsr& A);
 // y = A x                                (Eigen y = A*x: 0 + row sum)
 void spmv(const DCsr& A, const double* x, double* y, cudaStream_t s);
 // y = b - A x ; if brow != null, b is gathered: b[brow[r]]

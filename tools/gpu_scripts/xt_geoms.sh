@@ -1,0 +1,8 @@
+#!/bin/bash
+export PYTHONUNBUFFERED=1
+for g in 0 1 2 3 4 5; do
+echo "== geom $g warm"; MGRX_SPMV_XT_GEOM=$g MGRX_SPMV_XT=2 timeout 600 python tools/probe_spmv.py amg.1.resid amg.1.pre amg.0.resid amg.2.resid spmv.A 2>&1 | grep avg20
+echo "== geom $g cold"; MGRX_PROBE_FLUSH=1 MGRX_SPMV_XT_GEOM=$g MGRX_SPMV_XT=2 timeout 600 python tools/probe_spmv.py amg.1.resid amg.1.pre amg.0.resid amg.2.resid spmv.A 2>&1 | grep avg20
+done
+echo "== noxt warm"; MGRX_SPMV_XT=0 timeout 600 python tools/probe_spmv.py amg.1.resid amg.1.pre amg.0.resid amg.2.resid spmv.A 2>&1 | grep avg20
+echo "== noxt cold"; MGRX_PROBE_FLUSH=1 MGRX_SPMV_XT=0 timeout 600 python tools/probe_spmv.py amg.1.resid amg.1.pre amg.0.resid amg.2.resid spmv.A 2>&1 | grep avg20
