@@ -11,6 +11,7 @@
 #include "coarsen.cuh"
 #include "hierarchy.cuh"
 
+#include <cstring>
 #include <functional>
 
 namespace mgrx {
@@ -598,6 +599,21 @@ void AmgHier::vcycle(const double* r, double* z, cudaStream_t s) { vcycle_level(
 
 void AmgHier::vcycle_level(int l, const double* r, double* z, cudaStream_t s) {
   AmgLevelD& L = levels[l];
+  // timing experiment (wrong results): MGRX_VCYCLE_CUT=k replaces the cycle
+  // from level k down by z = 0, so the in-situ cost of the levels >= k shows
+  // as the difference of two "precond" probes
+  static const int cut = [] {
+    const char* e = std::getenv("MGRX_VCYCLE_CUT");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (cut >= 0 && l >= cut) {
+    MGRX_CK(cudaMemsetAsync(z, 0, sizeof(double) * L.A.rows, s));
+    return;
+  }
+  if (l == ctail) {
+    launch_amg_ctail(ctail_desc, ctail_lay, ctail_blob.get(), r, z, s);
+    return;
+  }
   if (l == tail) {
     launch_amg_tail(tail_desc, tail_blob.get(), r, z, s);
     return;
@@ -645,10 +661,82 @@ void prepare_amg(AmgHier& h, cudaStream_t s) {
   h.build_tail(s);
 }
 
+TailLevelHost tail_level_host(const AmgLevelD& L);
+
 // Choose the first level (>= 1) from which the rest of the V-cycle fits in
 // one CTA's shared memory (Jacobi / l1-Jacobi smoothing, single-block
 // coarsest LU) and pack it (MGRX_AMG_TAIL=0: off).
 void AmgHier::build_tail(cudaStream_t s) {
+  build_single_tail(s);
+  // Cluster tail: from the first level of <= kCtMaxRows rows, when that is
+  // above the single-CTA tail (MGRX_AMG_CTAIL=0: off).
+  ctail = -1;
+  // Off by default: bitwise equal (GPU parity suite with MGRX_AMG_CTAIL=1) but
+  // measured SLOWER at cfg2 -- levels 4-6 take 91 us in the cluster kernel
+  // against 46 us as launches + single-CTA tail (preconditioner 403 -> 457 us;
+  // from level 3: 500 us). In-kernel timers: 1.3-3.6 us per published vector
+  // (16 x 16 distributed-shared-memory pushes + rendezvous), 3-4.5 us per
+  // 857-row product on 16 SMs, 23 us around the one-warp dense solve.
+  static const bool con = [] {
+    const char* v = std::getenv("MGRX_AMG_CTAIL");
+    return v && std::atoi(v) != 0;
+  }();
+  const int nl = static_cast<int>(levels.size());
+  if (!con || nl < 3 || coarse.nb != 1 || coarse.n <= 0 || coarse.n > 256) return;
+  auto jac = [](const BoundRelax& b) {
+    return (b.spec.kind == Smoother::jacobi || b.spec.kind == Smoother::l1_jacobi) && b.spec.sweeps >= 1;
+  };
+  for (int t = std::max(1, nl - 1 - kTailMaxLevels); t <= nl - 2; ++t) {
+    if (tail >= 0 && t >= tail) return;  // the single-CTA tail already starts here
+    static const int max_rows = [] {  // MGRX_CTAIL_MAXROWS: largest level the cluster tail starts at
+      const char* v = std::getenv("MGRX_CTAIL_MAXROWS");
+      return v ? std::min(std::atoi(v), kCtMaxRows) : kCtMaxRows;
+    }();
+    if (levels[t].A.rows > max_rows) continue;
+    bool ok = true;
+    for (int l = t; l < nl - 1 && ok; ++l) ok = jac(levels[l].pre) && jac(levels[l].post);
+    if (!ok) continue;
+    std::vector<TailLevelHost> lv;
+    for (int l = t; l < nl - 1; ++l) lv.push_back(tail_level_host(levels[l]));
+    const int nc = coarse.n;
+    const std::vector<double> lu = coarse.lu.download(static_cast<size_t>(nc) * nc);
+    const std::vector<int> perm = coarse.perm.download(nc);
+    std::vector<unsigned char> blob;
+    if (!build_ctail_blob(lv, nc, lu, perm, ctail_desc, blob, ctail_lay)) continue;
+    ctail_blob.alloc(blob.size(), s);
+    ctail_blob.upload(blob.data(), blob.size());
+    prepare_amg_ctail(ctail_lay);
+    ctail = t;
+    if (const char* v = std::getenv("MGRX_VERBOSE"); v && v[0] == '1')
+      std::fprintf(stderr, "[mgrx] amg cluster tail from level %d of %d (%d shared bytes per CTA, %zu blob bytes)\n", t,
+                   nl, ctail_lay.total, blob.size());
+    return;
+  }
+}
+
+TailLevelHost tail_level_host(const AmgLevelD& L) {
+  TailLevelHost h;
+  h.m = L.A.rows;
+  h.mc = L.R.rows;
+  h.a_ptr = L.A.ptr.download(L.A.rows + 1);
+  h.a_col = L.A.col.download(L.A.nnz);
+  h.a_val = L.A.val.download(L.A.nnz);
+  h.r_ptr = L.R.ptr.download(L.R.rows + 1);
+  h.r_col = L.R.col.download(L.R.nnz);
+  h.r_val = L.R.val.download(L.R.nnz);
+  h.p_ptr = L.P.ptr.download(L.P.rows + 1);
+  h.p_col = L.P.col.download(L.P.nnz);
+  h.p_val = L.P.val.download(L.P.nnz);
+  h.dpre = L.pre.dinv.download(L.A.rows);
+  h.dpost = L.post.dinv.download(L.A.rows);
+  h.pre_sweeps = L.pre.spec.sweeps;
+  h.post_sweeps = L.post.spec.sweeps;
+  h.pre_w = L.pre.spec.weight;
+  h.post_w = L.post.spec.weight;
+  return h;
+}
+
+void AmgHier::build_single_tail(cudaStream_t s) {
   tail = -1;
   static const bool on = [] {
     const char* v = std::getenv("MGRX_AMG_TAIL");
@@ -977,7 +1065,8 @@ void MgrHier::tune_spmv(cudaStream_t s) {
     const char* e = std::getenv("MGRX_TUNE_INSITU");
     return !e || std::atoi(e) != 0;
   }();
-  if (!on || n == 0 || std::getenv("MGRX_SPMV_PLAN_FILE")) return;  // (a plan file replays recorded choices)
+  if (!on || n == 0) return;
+  const char* pf = std::getenv("MGRX_SPMV_PLAN_FILE");
   std::vector<DCsr*> cands;
   auto add = [&](DCsr& M) {
     if (M.xt_plan_nblk > 0) cands.push_back(&M);
@@ -998,7 +1087,32 @@ void MgrHier::tune_spmv(cudaStream_t s) {
   add(A_coarse);
   add_amg(coarse_amg.get());
   if (cands.empty()) return;
-  std::sort(cands.begin(), cands.end(), [](const DCsr* a, const DCsr* b) { return a->nnz > b->nnz; });
+  std::stable_sort(cands.begin(), cands.end(), [](const DCsr* a, const DCsr* b) { return a->nnz > b->nnz; });
+  // decisions recorded by an earlier run (so that a profiler sees the production choices)
+  if (pf)
+    if (FILE* f = std::fopen(pf, "r")) {
+      // (the xt_on / xt_off lines are in candidate order: operators of equal
+      // size, e.g. the coarse system and its copy as AMG level 0, stay apart)
+      std::vector<int> dec(cands.size(), -1);
+      int r, c, z;
+      char what[16];
+      size_t i = 0;
+      while (std::fscanf(f, "%d %d %d %15s", &r, &c, &z, what) == 4) {
+        const bool on_line = !std::strcmp(what, "xt_on"), off_line = !std::strcmp(what, "xt_off");
+        if (!on_line && !off_line) continue;
+        if (i < cands.size() && r == cands[i]->rows && c == cands[i]->cols && z == cands[i]->nnz)
+          dec[i] = on_line ? 1 : 0;
+        ++i;
+      }
+      std::fclose(f);
+      if (std::find(dec.begin(), dec.end(), -1) == dec.end()) {
+        for (size_t i = 0; i < cands.size(); ++i) {
+          cands[i]->xt_nblk = dec[i] ? cands[i]->xt_plan_nblk : 0;
+          if (!dec[i]) spmv_drop_xtile(*cands[i]);
+        }
+        return;
+      }
+    }
   DVec<double> v(n, s), z(n, s);
   v.zero();
   cudaEvent_t e0, e1;
@@ -1039,6 +1153,11 @@ void MgrHier::tune_spmv(cudaStream_t s) {
     if (t < 0.995f * cur) cur = t;
     else M->xt_nblk = was;
   }
+  if (pf)
+    if (FILE* f = std::fopen(pf, "a")) {
+      for (DCsr* M : cands) std::fprintf(f, "%d %d %d %s\n", M->rows, M->cols, M->nnz, M->xt_nblk ? "xt_on" : "xt_off");
+      std::fclose(f);
+    }
   for (DCsr* M : cands)
     if (M->xt_nblk == 0) spmv_drop_xtile(*M);
   cudaEventDestroy(e0);

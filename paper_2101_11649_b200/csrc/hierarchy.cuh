@@ -72,11 +72,18 @@ struct AmgHier {
   int tail = -1;
   TailDesc tail_desc;
   DVec<unsigned char> tail_blob;
+  // cluster tail (amgtail.cuh): levels >= ctail run as one 16-CTA cluster
+  // kernel (chosen when it starts above the single-CTA tail); -1: off
+  int ctail = -1;
+  TailDesc ctail_desc;
+  DVec<unsigned char> ctail_blob;
+  CtLayout ctail_lay;
 
   void setup(const DCsr& A, const AmgSpec& cfg, const std::vector<int>& umap, cudaStream_t s);
   void vcycle(const double* r, double* z, cudaStream_t s);
   int fine_size() const { return levels.empty() ? 0 : levels.front().A.rows; }
   void build_tail(cudaStream_t s);
+  void build_single_tail(cudaStream_t s);
 
  private:
   void vcycle_level(int l, const double* r, double* z, cudaStream_t s);

@@ -345,8 +345,17 @@ __global__ void __launch_bounds__(kWarps * 32) k_spmv_wpr(int rows, const int* _
       prod[w][l] = q < hi ? __dmul_rn(__ldg(val + q), x(__ldg(col + q))) : 0.0;
       __syncwarp();
       if (l == 0) {
+        // (8 products loaded at a time: the chain waits on additions only)
         const int m = min(32, hi - c0);
-        for (int t = 0; t < m; ++t) sum = __dadd_rn(sum, prod[w][t]);
+        int t = 0;
+        for (; t + 8 <= m; t += 8) {
+          double q[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) q[u] = prod[w][t + u];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) sum = __dadd_rn(sum, q[u]);
+        }
+        for (; t < m; ++t) sum = __dadd_rn(sum, prod[w][t]);
       }
       __syncwarp();
     }
@@ -2012,7 +2021,7 @@ void xtile_try(DCsr& A, cudaStream_t s) {
   const bool keep = best.nb > 0 && (mode == 2 || replay >= 0 || best.t < 0.97f * tc);
   if (pf && replay == -2)
     if (FILE* f = std::fopen(pf, "a")) {
-      if (keep) std::fprintf(f, "%d %d %d xtile%d\n", A.rows, A.cols, A.nnz, best.geom);
+      if (cand) std::fprintf(f, "%d %d %d xtile%d\n", A.rows, A.cols, A.nnz, best.geom);
       else std::fprintf(f, "%d %d %d noxtile\n", A.rows, A.cols, A.nnz);
       std::fclose(f);
     }
@@ -2183,7 +2192,8 @@ void spmv_prepare_csr(DCsr& A, cudaStream_t s) {
       char what[16];
       while (std::fscanf(f, "%d %d %d %15s", &r, &c, &z, what) == 4)
         if (r == A.rows && c == A.cols && z == A.nnz && std::strcmp(what, "bsr") && std::strcmp(what, "csr") &&
-            std::strcmp(what, "sell") && std::strcmp(what, "nosell")) {
+            std::strcmp(what, "sell") && std::strcmp(what, "nosell") && std::strncmp(what, "xt", 2) &&
+            std::strcmp(what, "noxtile")) {
           replayed = true;
           // "wspec_staged": the specialised plan plus the staged one for the
           // products the specialised kernel does not serve

@@ -662,6 +662,11 @@ def test_amg_tail_kernel_bit_exact():
                          env={**__import__("os").environ, "MGRX_VERBOSE": "1"}, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
     assert out.stderr.count("amg tail from level") >= 2, out.stderr[-3000:]
+    # the cluster tail (off by default: measured slower) runs the same cases bitwise
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                         env={**__import__("os").environ, "MGRX_VERBOSE": "1", "MGRX_AMG_CTAIL": "1"}, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
+    assert out.stderr.count("amg cluster tail from level") >= 1, out.stderr[-3000:]
 
 
 @pytest.mark.gpu
