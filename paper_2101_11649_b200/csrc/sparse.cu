@@ -657,6 +657,7 @@ __global__ void __launch_bounds__(Gm::T) k_spmv_staged(int nblk, const int* __re
 __constant__ int c_xt_dbg = 0;  // MGRX_XT_DBG: timing experiments (1: window as one copy)
 constexpr int kXtRuns = 32;     // runs per block: one per lane of the copy warp
 constexpr int kXtDirect = -2;   // block meta "tail" value: no window, global columns
+constexpr int kXtTwoPhase = 48; // block average row length above which products are formed block-wide
 template <int kR_, int kE_, int kL_, int kS_, int kCtas_>
 struct XtGeom {
   static constexpr int R = kR_, E = kE_, L = kL_, S = kS_, T = kR_ + 32, CTAS = kCtas_;
@@ -847,6 +848,42 @@ __global__ void __launch_bounds__(Gm::T, Gm::CTAS) k_spmv_xtile(int nblk, const 
       if (r < r1) {
         const int lo = S.rp[r - ra], hi = S.rp[r + 1 - ra];
         for (int k = lo; k < hi; ++k) sum = __dadd_rn(sum, __dmul_rn(S.val[k - pa2], __ldg(x + __ldg(gcol + k))));
+      }
+    } else if (cur.p1 - p0 > kXtTwoPhase * (r1 - r0)) {
+      // Long rows (block-uniform test): the row threads form the block's
+      // products in place — consecutive entries per warp, so column and value
+      // reads are conflict-free and every window read of the batch is in
+      // flight at once — then each row sums its products left to right.
+      constexpr int kU = (Gm::E + Gm::R - 1) / Gm::R;
+      const unsigned short* cp = S.col - pa8;
+      double* vp = S.val - pa2;
+      const int p1 = cur.p1;
+      {
+        int c[kU];
+        double xv[kU], av[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) c[u] = p0 + t + u * Gm::R < p1 ? cp[p0 + t + u * Gm::R] : 0;
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          xv[u] = S.win[c[u]];
+          av[u] = p0 + t + u * Gm::R < p1 ? vp[p0 + t + u * Gm::R] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+          if (p0 + t + u * Gm::R < p1) vp[p0 + t + u * Gm::R] = __dmul_rn(av[u], xv[u]);
+      }
+      asm volatile("bar.sync 2, %0;" ::"r"(Gm::R) : "memory");
+      if (r < r1) {
+        const int lo = S.rp[r - ra], hi = S.rp[r + 1 - ra];
+        int k = lo;
+        for (; k + 8 <= hi; k += 8) {
+          double q[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) q[u] = vp[k + u];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) sum = __dadd_rn(sum, q[u]);
+        }
+        for (; k < hi; ++k) sum = __dadd_rn(sum, vp[k]);
       }
     } else if (r < r1 && !(c_xt_dbg & 2)) {
       const int lo = S.rp[r - ra], hi = S.rp[r + 1 - ra];
@@ -1948,9 +1985,10 @@ void xtile_try(DCsr& A, cudaStream_t s) {
   A.xt_nblk = 0;
   A.xt_plan_nblk = 0;
   if (!mode || A.bsr || A.rows < staged_min_rows()) return;
-  // (one thread per row: rows averaging > 48 entries keep the block-wide
-  // product-pass kernels; under 6 entries per row the window costs more than
-  // the gathers it replaces)
+  // (under 6 entries per row the window costs more than the gathers it replaces,
+  // and on matrices averaging > 48 entries per row the block-wide product-pass
+  // kernels win: cfg4's 78-per-row operator measured 120 us per application
+  // slower through the window (in-situ pass), so no plan is built there)
   if (mode == 1 && (static_cast<long long>(A.nnz) > 48LL * A.rows || static_cast<long long>(A.nnz) < 6LL * A.rows))
     return;
   DVec<double> xs(A.cols > 0 ? A.cols : 1, s), ys(A.rows, s);
