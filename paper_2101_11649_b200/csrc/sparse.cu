@@ -421,6 +421,26 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 __constant__ int c_two_phase_min = 48;
 __device__ __forceinline__ int two_phase_min() { return c_two_phase_min; }
 
+// Plan entries of each CTA's first block as a launch parameter (constant
+// bank): the first bulk copies of a kernel are issued at once instead of
+// after a (cold: HBM) round trip to the plan arrays, ~1.5 us earlier per launch.
+// n == 0: not provided (grid larger than kHeadMax), the plan is read from memory.
+constexpr int kHeadMax = 640;
+struct PlanHead {
+  int n;
+  int e[kHeadMax][8];  // {r0, r1, p0, p1, d0, d1, w, tail}
+};
+inline void fill_head(PlanHead& h, const std::vector<int>& src, int grid) {
+  static const bool on = [] {  // MGRX_PLAN_HEAD=0: always read the plan from memory
+    const char* e = std::getenv("MGRX_PLAN_HEAD");
+    return !e || std::atoi(e) != 0;
+  }();
+  h.n = 0;
+  if (!on || grid > kHeadMax || static_cast<int>(src.size()) < 8 * grid) return;
+  h.n = grid;
+  std::memcpy(h.e, src.data(), sizeof(int) * 8 * static_cast<size_t>(grid));
+}
+
 // Pattern-coded plan operands (kPat instantiation; null otherwise).
 struct PatArgs {
   const int* meta;            // per block {dictionary start, W}
@@ -431,8 +451,8 @@ struct PatArgs {
 template <class Gm, class Epi, class Xs, bool kLong, bool kPat = false>
 __global__ void __launch_bounds__(Gm::T) k_spmv_staged(int nblk, const int* __restrict__ plan,
                                                        const int* __restrict__ ptr, const int* __restrict__ col,
-                                                       const double* __restrict__ val, Xs x, Epi epi,
-                                                       PatArgs pa = PatArgs{}) {
+                                                       const double* __restrict__ val, Xs x, Epi epi, PatArgs pa,
+                                                       const __grid_constant__ PlanHead head) {
   static_assert(!(kLong && kPat), "pattern-coded plans serve the short-row kernel");
   if (!kPdlStagedEarly) pdl_enter();
   using Stage = typename Gm::Stage;
@@ -532,7 +552,14 @@ __global__ void __launch_bounds__(Gm::T) k_spmv_staged(int nblk, const int* __re
     else issue(e, s);
   };
   const int G = gridDim.x;
-  PlanE cur = ldp(blockIdx.x), nxt = ldp(blockIdx.x + G);
+  PlanE cur;
+  if (head.n) {
+    const int* e = head.e[blockIdx.x];
+    cur = PlanE{e[0], e[1], e[2], e[3], e[4], e[5], e[6]};
+  } else {
+    cur = ldp(blockIdx.x);
+  }
+  PlanE nxt = ldp(blockIdx.x + G);
   if (t == 0) {
     issue_any(cur, blockIdx.x, 0);
     if (blockIdx.x + G < nblk) issue_any(nxt, blockIdx.x + G, 1);
@@ -690,7 +717,8 @@ __global__ void __launch_bounds__(Gm::T, Gm::CTAS) k_spmv_xtile(int nblk, const 
                                                       const unsigned short* __restrict__ lcol,
                                                       const double* __restrict__ val, const int* __restrict__ runs,
                                                       const int* __restrict__ meta, const int* __restrict__ gcol,
-                                                      const double* __restrict__ x, int xcols, Epi epi) {
+                                                      const double* __restrict__ x, int xcols, Epi epi,
+                                                      const __grid_constant__ PlanHead head) {
   using Stage = typename Gm::Stage;
   constexpr int kS = Gm::S;
   extern __shared__ __align__(128) unsigned char st_raw[];
@@ -743,6 +771,10 @@ __global__ void __launch_bounds__(Gm::T, Gm::CTAS) k_spmv_xtile(int nblk, const 
       return d;
     };
     Desc d = load_desc(blockIdx.x), nx = load_desc(blockIdx.x + G);
+    if (head.n) {  // first block: scalars from the launch parameters (the runs still come from memory)
+      const int* e = head.e[blockIdx.x];
+      d.r0 = e[0], d.r1 = e[1], d.p0 = e[2], d.p1 = e[3], d.tail = e[7];
+    }
     pdl_enter();  // x is the previous kernel's
     int it = 0;
     for (int b = blockIdx.x; b < nblk; b += G, ++it) {
@@ -751,6 +783,30 @@ __global__ void __launch_bounds__(Gm::T, Gm::CTAS) k_spmv_xtile(int nblk, const 
       if (it >= kS) wait(smem_u32(empty + s), ((it / kS) - 1) & 1u);
       const unsigned mb = smem_u32(full + s);
       Stage& S = stg[s];
+      // the matrix slices first: their plan entries are at hand (launch parameters
+      // for a CTA's first block, prefetched registers later), the runs may still be
+      // in flight
+      const int ra = d.r0 & ~3, pa8 = d.p0 & ~7, pa2 = d.p0 & ~1;
+      const unsigned brp = ((d.r1 + 1 - ra + 3) & ~3) * 4u;
+      unsigned bc = d.p1 > d.p0 && d.tail != kXtDirect ? ((d.p1 - pa8 + 7) & ~7) * 2u : 0u;
+      unsigned bv = d.p1 > d.p0 ? ((d.p1 - pa2 + 1) & ~1) * 8u : 0u;
+      if (c_xt_dbg & 8) bc = bv = 0u;  // timing experiment: no matrix copies
+      if (l == 0) {
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(S.rp)),
+                     "l"(ptr + ra), "r"(brp), "r"(mb)
+                     : "memory");
+      } else if (l == 1 && bc) {
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(S.col)),
+                     "l"(lcol + pa8), "r"(bc), "r"(mb)
+                     : "memory");
+      } else if (l == 2 && bv) {
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(S.val)),
+                     "l"(val + pa2), "r"(bv), "r"(mb)
+                     : "memory");
+      }
       // window slot of this lane's run: exclusive prefix sum of the run lengths
       int slot = d.nl;
 #pragma unroll
@@ -781,27 +837,6 @@ __global__ void __launch_bounds__(Gm::T, Gm::CTAS) k_spmv_xtile(int nblk, const 
                          smem_u32(S.win + slot * 16)),
                      "l"(x + static_cast<size_t>(d.l0) * 16), "r"(nb), "r"(mb)
                      : "memory");
-      const int ra = d.r0 & ~3, pa8 = d.p0 & ~7, pa2 = d.p0 & ~1;
-      const unsigned brp = ((d.r1 + 1 - ra + 3) & ~3) * 4u;
-      unsigned bc = d.p1 > d.p0 && d.tail != kXtDirect ? ((d.p1 - pa8 + 7) & ~7) * 2u : 0u;
-      unsigned bv = d.p1 > d.p0 ? ((d.p1 - pa2 + 1) & ~1) * 8u : 0u;
-      if (c_xt_dbg & 8) bc = bv = 0u;  // timing experiment: no matrix copies
-      if (l == 0) {
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         smem_u32(S.rp)),
-                     "l"(ptr + ra), "r"(brp), "r"(mb)
-                     : "memory");
-      } else if (l == 1 && bc) {
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         smem_u32(S.col)),
-                     "l"(lcol + pa8), "r"(bc), "r"(mb)
-                     : "memory");
-      } else if (l == 2 && bv) {
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         smem_u32(S.val)),
-                     "l"(val + pa2), "r"(bv), "r"(mb)
-                     : "memory");
-      }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) nb += __shfl_xor_sync(0xffffffffu, nb, o);
       if (l == 0)
@@ -821,6 +856,10 @@ __global__ void __launch_bounds__(Gm::T, Gm::CTAS) k_spmv_xtile(int nblk, const 
   };
   // plan entries two blocks ahead, epilogue operands one block ahead
   Blk cur = load_blk(blockIdx.x), nxt = load_blk(blockIdx.x + G);
+  if (head.n) {
+    const int* e = head.e[blockIdx.x];
+    cur = Blk{e[0], e[1], e[2], e[3], e[7]};
+  }
   pdl_enter();
   decltype(epi.load(0)) pre{};
   if (cur.r0 + t < cur.r1) pre = epi.load(cur.r0 + t);
@@ -1220,8 +1259,10 @@ void launch_staged_k(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
                                  static_cast<int>(Gm::smem)));
   const int per_sm = static_cast<int>(std::min<size_t>(8, 227 * 1024 / Gm::smem));
   const int grid = std::min(A.nblk, device_sms() * std::min(per_sm, staged_ctas_per_sm()));
+  PlanHead hd;
+  fill_head(hd, A.head, grid);
   launch_pdl(PdlEarly{grid == device_sms() * per_sm}, k_spmv_staged<Gm, Epi, Xs, kLong>, grid, Gm::T, Gm::smem, s,
-             A.nblk, A.plan.get(), A.ptr.get(), A.col.get(), A.val.get(), x, epi, PatArgs{});
+             A.nblk, A.plan.get(), A.ptr.get(), A.col.get(), A.val.get(), x, epi, PatArgs{}, hd);
   MGRX_LAUNCH_CK();
   count_launch();
 }
@@ -1235,8 +1276,10 @@ void launch_staged_pat(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
     MGRX_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(Gm::smem)));
   const int per_sm = static_cast<int>(std::min<size_t>(8, 227 * 1024 / Gm::smem));
   const int grid = std::min(A.nblk, device_sms() * std::min(per_sm, staged_ctas_per_sm()));
+  PlanHead hd;
+  fill_head(hd, A.head, grid);
   launch_pdl(kern, grid, Gm::T, Gm::smem, s, A.nblk, A.plan.get(), A.ptr.get(), A.col.get(), A.val.get(), x, epi,
-             PatArgs{A.pmeta.get(), A.pdict.get(), A.prow.get()});
+             PatArgs{A.pmeta.get(), A.pdict.get(), A.prow.get()}, hd);
   MGRX_LAUNCH_CK();
   count_launch();
 }
@@ -1273,8 +1316,10 @@ void launch_xtile_g(const DCsr& A, const double* x, Epi epi, cudaStream_t s) {
   }
   const int per_sm = static_cast<int>(227 * 1024 / (Gm::smem + 1024));
   const int grid = std::min(A.xt_nblk, device_sms() * per_sm);
+  PlanHead hd;
+  fill_head(hd, A.xt_head, grid);
   launch_pdl(kern, grid, Gm::T, Gm::smem, s, A.xt_nblk, A.xt_plan.get(), A.ptr.get(), A.xt_col.get(), A.val.get(),
-             A.xt_runs.get(), A.xt_meta.get(), A.col.get(), x, A.cols, epi);
+             A.xt_runs.get(), A.xt_meta.get(), A.col.get(), x, A.cols, epi, hd);
   MGRX_LAUNCH_CK();
   count_launch();
 }
@@ -1968,6 +2013,15 @@ bool build_xtile(DCsr& A, int geom, cudaStream_t s) {
   A.xt_col.upload(lc.data(), lc.size());
   A.xt_nblk = nb;
   A.xt_geom = geom;
+  A.xt_head.assign(8 * static_cast<size_t>(std::min(nb, kHeadMax)), 0);
+  for (int b = 0; b < std::min(nb, kHeadMax); ++b) {
+    int* e = A.xt_head.data() + 8 * static_cast<size_t>(b);
+    e[0] = rs[b];
+    e[1] = rs[b + 1];
+    e[2] = rs[nb + 1 + b];
+    e[3] = rs[nb + 2 + b];
+    e[7] = meta[2 * b + 1];
+  }
   return true;
 }
 
@@ -2000,6 +2054,7 @@ void xtile_try(DCsr& A, cudaStream_t s) {
     int geom = 0, nb = 0;
     DVec<int> plan, runs, meta;
     DVec<unsigned short> col;
+    std::vector<int> head;
     float t = 1e30f;
   };
   auto stash = [&](Cand& c) {
@@ -2009,6 +2064,7 @@ void xtile_try(DCsr& A, cudaStream_t s) {
     c.runs = std::move(A.xt_runs);
     c.meta = std::move(A.xt_meta);
     c.col = std::move(A.xt_col);
+    c.head = std::move(A.xt_head);
     A.xt_nblk = 0;
   };
   auto install = [&](Cand& c) {
@@ -2018,6 +2074,7 @@ void xtile_try(DCsr& A, cudaStream_t s) {
     A.xt_runs = std::move(c.runs);
     A.xt_meta = std::move(c.meta);
     A.xt_col = std::move(c.col);
+    A.xt_head = std::move(c.head);
   };
   // decisions of an earlier run (MGRX_SPMV_PLAN_FILE): xtile0 / xtile1 / noxtile
   const char* pf = std::getenv("MGRX_SPMV_PLAN_FILE");
@@ -2080,6 +2137,7 @@ void spmv_drop_xtile(DCsr& A) {
   A.xt_runs.release();
   A.xt_meta.release();
   A.xt_col.release();
+  A.xt_head.clear();
 }
 
 // MGRX_SPMV_PAT: 0 off, 1 (default) pattern-coded columns where they time
@@ -2096,8 +2154,26 @@ int pat_mode() {
 // the distinct offset patterns (col - row) of its rows. Built only when the
 // dictionaries are small next to the column indices they replace (stencil-
 // like operators); false otherwise.
+// Host copy of the first blocks' plan entries (launch-parameter head).
+void set_plan_head(DCsr& A, const std::vector<int>& h, int nb, const std::vector<int>* pmeta) {
+  const int m = std::min(nb, kHeadMax);
+  A.head.assign(8 * static_cast<size_t>(m), 0);
+  for (int b = 0; b < m; ++b) {
+    int* e = A.head.data() + 8 * static_cast<size_t>(b);
+    e[0] = h[b];
+    e[1] = h[b + 1];
+    e[2] = h[nb + 1 + b];
+    e[3] = h[nb + 2 + b];
+    if (pmeta) {
+      e[4] = (*pmeta)[2 * b];
+      e[5] = (*pmeta)[2 * b + 2];
+      e[6] = (*pmeta)[2 * b + 1];
+    }
+  }
+}
+
 bool build_patterns(DCsr& A, const std::vector<int>& p, const std::vector<int>& h, int nb, int max_e,
-                    cudaStream_t s) {
+                    cudaStream_t s, std::vector<int>& meta_out) {
   if (nb <= 0 || A.nnz == 0 || static_cast<long long>(A.nnz) > 24LL * A.rows) return false;
   const std::vector<int> c = A.col.download(A.nnz);
   std::vector<int> meta(2 * static_cast<size_t>(nb) + 2, 0), dict;
@@ -2145,6 +2221,7 @@ bool build_patterns(DCsr& A, const std::vector<int>& p, const std::vector<int>& 
   A.pmeta.upload(meta.data(), meta.size());
   A.prow.alloc(prow.size(), s);
   A.prow.upload(prow.data(), prow.size());
+  meta_out = meta;
   return true;
 }
 
@@ -2183,13 +2260,17 @@ void spmv_prepare_csr(DCsr& A, cudaStream_t s) {
   cudaEvent_t e0, e1;
   MGRX_CK(cudaEventCreate(&e0));
   MGRX_CK(cudaEventCreate(&e1));
-  const bool has_pat = pat_mode() && build_patterns(A, p, h, nb, kStE, s);
+  std::vector<int> pat_meta;
+  const bool has_pat = pat_mode() && build_patterns(A, p, h, nb, kStE, s, pat_meta);
+  A.head.clear();
   auto time = [&](bool staged, bool patc = false) {
     A.nblk = staged ? nb : 0;
     A.plan_kind = 0;
     A.pat = patc ? 1 : 0;
     A.plan = DVec<int>();
     if (staged) A.plan = std::move(plan);
+    if (staged) set_plan_head(A, h, nb, patc ? &pat_meta : nullptr);
+    else A.head.clear();
     const float ms = tune_time(A, xs.get(), ys.get(), s, e0, e1);
     if (staged) plan = std::move(A.plan);
     A.pat = 0;
@@ -2277,8 +2358,10 @@ void spmv_prepare_csr(DCsr& A, cudaStream_t s) {
     A.plan = std::move(plan);
     A.nblk = nb;
     A.pat = 1;
+    set_plan_head(A, h, nb, &pat_meta);
     return;
   }
+  A.head.clear();
   A.pdict.release();
   A.pmeta.release();
   A.prow.release();
@@ -2291,6 +2374,7 @@ void spmv_prepare_csr(DCsr& A, cudaStream_t s) {
     if (ts < 0.97f * td || staged_force()) {
       A.plan = std::move(plan);
       A.nblk = nb;
+      set_plan_head(A, h, nb, nullptr);
     }
   } else if (nbw > 0 && tw < 0.97f * tbest) {
     if (const char* v = std::getenv("MGRX_VERBOSE"); v && v[0] == '1')
@@ -2301,6 +2385,7 @@ void spmv_prepare_csr(DCsr& A, cudaStream_t s) {
   } else if (ts < 0.97f * td || staged_force()) {
     A.plan = std::move(plan);
     A.nblk = nb;
+    set_plan_head(A, h, nb, nullptr);
   }
 }
 

@@ -70,6 +70,11 @@ struct DCsr {
   int xt_geom = 0;  // 0: 256 rows / 2048 entries / 120 lines x 2 stages; 1: 128 / 1024 / 88 x 2 stages; 2: geometry 0's blocks x 3 stages
   DVec<int> xt_plan, xt_runs, xt_meta;
   DVec<unsigned short> xt_col;
+  // Plan entries of the first block of every CTA (host copies, passed to the
+  // staged / x-window kernels as launch parameters so that a CTA's first copy
+  // is issued without a global-memory round trip): 8 ints per block
+  // {r0, r1, p0, p1, d0, d1, w, tail}.
+  std::vector<int> head, xt_head;
   bool empty() const { return rows == 0; }
 };
 
