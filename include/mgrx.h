@@ -139,6 +139,13 @@ MGRX_API int mgrx_solve(mgrx_hier* h, const double* b, double* x, const mgrx_kry
 MGRX_API int mgrx_amg_info(mgrx_hier* h, int which, int* nlevels, int* level_sizes, int cap,
                            long long* fallback_rows, int* truncated);
 
+/* Negative control (proj/src/verify.cpp:105-134, `mgrkit verify
+ * --corrupt-transfer`, proj/tests/test_acceptance.cpp:25-30): scales the
+ * interpolation P of MGR level `level` by `factor` in place (the reference
+ * uses 1.01), so that an exactness check that must then fail can prove it
+ * notices. The hierarchy stays usable; there is no undo. */
+MGRX_API int mgrx_corrupt_transfer(mgrx_hier* h, int level, double factor);
+
 /* Parity dumps. path grammar:
  *   mgr.<l>.{A,P,R,F,C,frelax.dinv}   mgr.coarse.A
  *   mgr.<l>.frelax.amg.<k>.{A,P,R,C,F,l1d,dinv,umap}   mgr.coarse.amg.<k>.{...}

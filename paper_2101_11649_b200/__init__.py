@@ -93,6 +93,7 @@ def lib() -> C.CDLL:
         L.mgrx_info.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_int]
         L.mgrx_amg_info.argtypes = [vp, C.c_int, C.POINTER(C.c_int), vp, C.c_int, C.POINTER(C.c_longlong),
                                     C.POINTER(C.c_int)]
+        L.mgrx_corrupt_transfer.argtypes = [vp, C.c_int, C.c_double]
         L.mgrx_time_kernel.argtypes = [vp, C.c_char_p, C.c_int, C.POINTER(C.c_double),
                                        C.POINTER(C.c_double)]
         L.mgrx_nccl_unique_id.argtypes = [C.c_char_p]
@@ -351,6 +352,11 @@ class Hierarchy:
         _check(lib().mgrx_amg_info(self._h, which, C.byref(nl), _ptr(sizes), 64, C.byref(fb), C.byref(tr)))
         return {"level_sizes": sizes[:min(nl.value, 64)].tolist(), "interp_fallback_rows": fb.value,
                 "truncated": bool(tr.value)}
+
+    def corrupt_transfer(self, level: int = 0, factor: float = 1.01) -> None:
+        """Negative control of proj/src/verify.cpp:115 (`verify
+        --corrupt-transfer`): scale P of MGR level `level` in place."""
+        _check(lib().mgrx_corrupt_transfer(self._h, int(level), float(factor)))
 
     def dump(self, path: str):
         """CSR -> (ptr, col, val, shape); int list -> int32 array; vector -> float64 array."""

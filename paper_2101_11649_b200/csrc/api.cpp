@@ -511,6 +511,18 @@ int mgrx_amg_info(mgrx_hier* h, int which, int* nlevels, int* level_sizes, int c
   });
 }
 
+int mgrx_corrupt_transfer(mgrx_hier* h, int level, double factor) {
+  return guarded([&] {
+    use(h->ctx);
+    h->H.corrupt_transfer(level, factor, h->ctx->stream);
+    // the recorded restart cycle embeds the clean preconditioner
+    if (h->ws.ls.exec) cudaGraphExecDestroy(h->ws.ls.exec);
+    h->ws.ls.exec = nullptr;
+    h->ws.ls.exec_key = {};
+    return MGRX_OK;
+  });
+}
+
 int mgrx_dump(mgrx_hier* h, const char* path_c, int* kind, int* rows, int* cols, long long* nnz, int* ptr,
               int* col, double* val) {
   return guarded([&] {

@@ -3,8 +3,10 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -30,6 +32,21 @@ struct RuntimeError : std::runtime_error {
   } while (0)
 
 #define MGRX_LAUNCH_CK() MGRX_CK(cudaGetLastError())
+
+// NVTX range (header-only NVTX v3; a no-op unless a tool is attached) around
+// a phase: setup / application of each MGR and AMG level, the GMRES solve
+// (SURVEY §5 tracing). Inside a graph capture the range brackets the capture.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  NvtxRange(const char* what, int level) {
+    char buf[48];
+    snprintf(buf, sizeof buf, "%s.%d", what, level);
+    nvtxRangePushA(buf);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Programmatic dependent launch (PDL): solve-path kernels are launched with
 // the programmatic-serialization attribute. griddepcontrol.wait (pdl_wait)

@@ -10,6 +10,7 @@
 
 #include "coarsen.cuh"
 #include "hierarchy.cuh"
+#include "krylov.cuh"
 
 #include <cstring>
 #include <functional>
@@ -540,6 +541,7 @@ LevelBuild build_level_interp(const DCsr& A, double theta, const std::vector<int
 }  // namespace
 
 void AmgHier::setup(const DCsr& A, const AmgSpec& cfg, const std::vector<int>& umap, cudaStream_t s) {
+  NvtxRange nvtx("mgrx.amg_setup");
   if (A.rows != A.cols) throw InvalidArgument("amg_setup: matrix must be square");
   if (!(cfg.strength_theta > 0.0 && cfg.strength_theta < 1.0))
     throw InvalidArgument("amg_setup: strength_theta must lie in (0,1)");
@@ -555,6 +557,7 @@ void AmgHier::setup(const DCsr& A, const AmgSpec& cfg, const std::vector<int>& u
     const int n = Acur.rows;
     level_sizes.push_back(n);
     levels.emplace_back();
+    NvtxRange nvtx_level("mgrx.amg_setup.level", static_cast<int>(levels.size()) - 1);
     AmgLevelD& L = levels.back();
     L.umap = map;
     const bool last = static_cast<int>(levels.size()) >= cfg.max_levels;
@@ -598,6 +601,7 @@ void AmgHier::setup(const DCsr& A, const AmgSpec& cfg, const std::vector<int>& u
 void AmgHier::vcycle(const double* r, double* z, cudaStream_t s) { vcycle_level(0, r, z, s); }
 
 void AmgHier::vcycle_level(int l, const double* r, double* z, cudaStream_t s) {
+  NvtxRange nvtx("mgrx.amg.level", l);
   AmgLevelD& L = levels[l];
   // timing experiment (wrong results): MGRX_VCYCLE_CUT=k replaces the cycle
   // from level k down by z = 0, so the in-situ cost of the levels >= k shows
@@ -797,6 +801,7 @@ void AmgHier::build_single_tail(cudaStream_t s) {
 
 void MgrHier::setup(const DCsr& A, const std::vector<int>& labels, const std::vector<std::string>& fields,
                     const std::vector<int>* umap_in, const Strategy& strat, cudaStream_t s) {
+  NvtxRange nvtx("mgrx.mgr_setup");
   if (A.rows != A.cols) throw InvalidArgument("mgr_setup: matrix must be square");
   if (static_cast<int>(labels.size()) != A.rows)
     throw InvalidArgument("mgr_setup: partition size does not match the matrix");
@@ -830,6 +835,7 @@ void MgrHier::setup(const DCsr& A, const std::vector<int>& labels, const std::ve
 
   for (const auto& spec : strat.levels) {
     levels.emplace_back();
+    NvtxRange nvtx_level("mgrx.mgr_setup.level", static_cast<int>(levels.size()) - 1);
     MgrLevelD& L = levels.back();
     L.A = std::move(Acur);
     const int nl = L.A.rows;
@@ -1171,11 +1177,28 @@ MgrHier::~MgrHier() {
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
 }
 
+void MgrHier::corrupt_transfer(int l, double factor, cudaStream_t s) {
+  if (l < 0 || l >= static_cast<int>(levels.size()))
+    throw InvalidArgument("corrupt_transfer: no MGR level " + std::to_string(l));
+  MgrLevelD& L = levels[l];
+  if (L.P.nnz > 0) vec_scale(L.P.nnz, L.P.val.get(), factor, L.P.val.get(), s);
+  // plans that carry their own copy of the values would keep the clean P
+  L.P.bsr = 0;
+  L.P.nslice = 0;
+  L.pplan.w = 0;
+  MGRX_CK(cudaStreamSynchronize(s));
+  for (auto& kv : graphs_)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  graphs_.clear();
+}
+
 void MgrHier::apply_level(int l, const double* v, double* z, cudaStream_t s) {
   if (l == static_cast<int>(levels.size())) {
+    NvtxRange nvtx("mgrx.mgr.coarse_solve");
     coarse_solve(v, z, s);
     return;
   }
+  NvtxRange nvtx("mgrx.mgr.level", l);
   MgrLevelD& L = levels[l];
   const int nf = static_cast<int>(L.F.size()), nc = static_cast<int>(L.C.size());
   if (L.injection && !L.g_relax) {

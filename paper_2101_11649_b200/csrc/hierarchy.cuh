@@ -126,6 +126,10 @@ struct MgrHier {
   // switched on / off by timing whole applications (every operator is then
   // read as cold as in the solve, with its real epilogues and neighbours).
   void tune_spmv(cudaStream_t s);
+  // Negative control (proj/src/verify.cpp:115, `--corrupt-transfer`): P of
+  // MGR level l scaled by `factor` in place; value-holding SpMV copies of P
+  // and captured application graphs are dropped so every path sees it.
+  void corrupt_transfer(int l, double factor, cudaStream_t s);
   void check(cudaStream_t s);
   ~MgrHier();
 

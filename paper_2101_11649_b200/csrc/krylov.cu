@@ -971,6 +971,7 @@ GmresResult gmres_device(const DCsr& A, const double* b, double* x, const Krylov
   if (cfg.restart < 1) throw InvalidArgument("gmres: restart must be >= 1");
   if (cfg.ortho != kOrthoMgs && lowsync_supported(n, cfg.restart))
     return gmres_lowsync(A, b, x, cfg, precond, precond_capture, ws, s);
+  NvtxRange nvtx("mgrx.gmres.mgs");
   StepProf prof;
   const int m = cfg.restart;
   ws.ensure(n, m, s);

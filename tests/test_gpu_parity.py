@@ -732,3 +732,47 @@ def test_repeat_determinism_of_synchronising_kernels():
         out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
                              env={**os.environ, **env}, timeout=900)
         assert out.returncode == 0 and "ok" in out.stdout, (env, out.stderr[-3000:])
+
+
+def _csr_matvec(ptr, col, val, x):
+    y = np.zeros(ptr.size - 1)
+    np.add.at(y, np.repeat(np.arange(ptr.size - 1), np.diff(ptr)), val * x[col])
+    return y
+
+
+@pytest.mark.parametrize("ortho", ["mgs", "cgs2"])
+def test_corrupt_transfer_negative_control(ortho):
+    """check_mgr_exactness (proj/src/verify.cpp:105-134) and its negative
+    control (`verify --corrupt-transfer`, proj/tests/test_acceptance.cpp:25-30):
+    an exact two-level MGR (ideal interpolation, dense LU on A_FF and on the
+    coarse system) is a direct solver, so GMRES converges in ONE iteration to
+    1e-12; with P scaled by 1.01 (mgrx_corrupt_transfer) that must fail."""
+    strat = json.dumps({"levels": [{"f_fields": ["f"], "interp": "ideal", "restrict": "injection",
+                                    "f_relax": {"kind": "dense_lu", "sweeps": 1}}],
+                        "coarse": {"kind": "dense_lu"}})
+    rng = np.random.default_rng(4711)
+    cfg = mx.KrylovConfig(rel_tol=1e-12, max_iters=10, ortho=ortho)
+    caught = 0
+    for trial in range(12):
+        n = int(rng.integers(20, 201))
+        ptr, col, val = make_golden.rows_to_csr(make_golden.random_sdd(n, 1000 + trial))
+        lab = (rng.uniform(size=n) < 0.5).astype(np.int32)
+        lab[0], lab[1] = 0, 1  # both classes present
+        part = mx.DofPartition(["f", "c"], lab)
+        b = rng.uniform(-1, 1, n)
+        H = mx.Hierarchy(mx.Matrix(ptr, col, val), part, strat)
+        x, rep = H.solve(b, cfg=cfg)
+        resid = np.linalg.norm(b - _csr_matvec(ptr, col, val, x)) / np.linalg.norm(b)
+        assert rep.converged and rep.iterations == 1 and resid <= 1e-12, (trial, n, rep.iterations, resid)
+        H.corrupt_transfer(0, 1.01)
+        x2, rep2 = H.solve(b, cfg=cfg)
+        resid2 = np.linalg.norm(b - _csr_matvec(ptr, col, val, x2)) / np.linalg.norm(b)
+        if not (rep2.converged and rep2.iterations == 1 and resid2 <= 1e-12):
+            caught += 1
+        # the preconditioner application sees the corrupted P as well
+        z_bad = H.apply(b)
+        H2 = mx.Hierarchy(mx.Matrix(ptr, col, val), part, strat)
+        assert not np.array_equal(z_bad, H2.apply(b))
+    assert caught == 12
+    with pytest.raises(mx.MgrxInvalidArgument, match="no MGR level 3"):
+        H.corrupt_transfer(3, 1.01)
