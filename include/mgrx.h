@@ -105,8 +105,14 @@ MGRX_API int mgrx_matrix_csr_device(mgrx_ctx* ctx, int rows, int cols, const int
                            const int* d_colidx, const double* d_values, mgrx_mat** out);
 MGRX_API int mgrx_matrix_destroy(mgrx_mat* m);
 
-/* y = A x. on_device != 0: x, y are device pointers. */
-MGRX_API int mgrx_spmv(mgrx_mat* m, const double* x, double* y, int on_device);
+/* y = A x. flags: bit 0 (MGRX_ON_DEVICE, value 1) x, y are device pointers;
+ * bit 2 (MGRX_TEAM_SUMS, value 4) allow the matrix's team-sum kernel, if the
+ * setup timing chose one (rows summed by a lane team with fused multiply-adds
+ * and a shuffle tree: tolerance-level, what the default solve runs).
+ * Without it the row sums are the reference's left-to-right sums (Eigen's
+ * y = A*x), bitwise. */
+#define MGRX_TEAM_SUMS 4
+MGRX_API int mgrx_spmv(mgrx_mat* m, const double* x, double* y, int flags);
 
 /* Build the MGR hierarchy on the GPU. labels[i] in [0, nfields) names
  * field_names[labels[i]] (DofPartition, proj/include/mgrkit/mgr.hpp:20-28).

@@ -191,12 +191,14 @@ class Matrix:
                                             C.c_void_p(d_col), C.c_void_p(d_val), C.byref(self._h)))
         return self
 
-    def spmv(self, x: np.ndarray) -> np.ndarray:
+    def spmv(self, x: np.ndarray, team_sums: bool = False) -> np.ndarray:
+        """y = A x. team_sums: allow the tolerance-level team-sum kernel the
+        default solve uses (MGRX_TEAM_SUMS); otherwise bitwise row sums."""
         x = np.ascontiguousarray(x, dtype=np.float64)
         if x.size != self.shape[1]:
             raise MgrxInvalidArgument(INVALID_ARGUMENT, "spmv: dimension mismatch")
         y = np.empty(self.shape[0], dtype=np.float64)
-        _check(lib().mgrx_spmv(self._h, _ptr(x), _ptr(y), 0))
+        _check(lib().mgrx_spmv(self._h, _ptr(x), _ptr(y), 4 if team_sums else 0))
         return y
 
     def spmv_device(self, x_ptr: int, y_ptr: int):

@@ -342,10 +342,12 @@ int mgrx_matrix_destroy(mgrx_mat* m) {
   });
 }
 
-int mgrx_spmv(mgrx_mat* m, const double* x, double* y, int on_device) {
+int mgrx_spmv(mgrx_mat* m, const double* x, double* y, int flags) {
   return guarded([&] {
     use(m->ctx);
     cudaStream_t s = m->ctx->stream;
+    const bool on_device = (flags & MGRX_ON_DEVICE) != 0;
+    TeamSums team_sums((flags & MGRX_TEAM_SUMS) != 0);
     if (on_device) {
       spmv(m->A, x, y, s);
       MGRX_CK(cudaStreamSynchronize(s));
@@ -616,6 +618,13 @@ int mgrx_time_kernel(mgrx_hier* h, const char* which, int reps, double* avg_ms, 
     double b = 0.0;
     const std::string w(which);
     prepare_probe(h, w, fn, b, s);
+    // probes time the kernels of the default (tolerance-level) solve;
+    // MGRX_PROBE_EXACT=1: the bitwise kernels
+    static const bool probe_exact = [] {
+      const char* e = std::getenv("MGRX_PROBE_EXACT");
+      return e && e[0] == '1';
+    }();
+    TeamSums team_sums(!probe_exact);
     for (int i = 0; i < 3; ++i) fn();  // warm-up
     // Default: launches back to back (the L2 keeps whatever of the previous
     // launch's inputs fits in 126 MB: kernels whose working set is near the L2

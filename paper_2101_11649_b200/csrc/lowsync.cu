@@ -710,6 +710,7 @@ void LsDriver::combine(const std::vector<double>& y, double* u, cudaStream_t s) 
 GmresResult gmres_lowsync(const DCsr& A, const double* b, double* x, const KrylovSpec& cfg, const DevOp& precond,
                           const DevOp& precond_capture, GmresWork& ws, cudaStream_t s) {
   NvtxRange nvtx("mgrx.gmres.cgs2");
+  TeamSums team_sums(true);  // tolerance-level solve: SpMVs may use their team-sum kernels
   const int n = A.rows;
   const int m = cfg.restart;
   ws.ensure(n, 1, s);  // w, z, r, u, reduction scratch (MGS basis not needed)

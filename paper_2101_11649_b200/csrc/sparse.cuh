@@ -75,7 +75,27 @@ struct DCsr {
   // is issued without a global-memory round trip): 8 ints per block
   // {r0, r1, p0, p1, d0, d1, w, tail}.
   std::vector<int> head, xt_head;
+  // Team-sum SpMV of the tolerance-level solve (k_spmv_vec; lanes per row,
+  // chosen per matrix by the setup timing). 0: none. Only consulted while a
+  // TeamSums scope is active (the default solve); the bitwise paths never
+  // take it.
+  int vec = 0;
   bool empty() const { return rows == 0; }
+};
+
+// Scope in which SpMVs may sum a row in team order (fused multiply-adds per
+// lane, shuffle tree) instead of the reference's left-to-right order: the
+// default solve (tolerance-level parity, like its orthogonalisation). Thread-
+// local, nestable; `on == false` leaves the current state.
+struct TeamSums {
+  explicit TeamSums(bool on);
+  ~TeamSums();
+  TeamSums(const TeamSums&) = delete;
+  TeamSums& operator=(const TeamSums&) = delete;
+  static bool active();
+
+ private:
+  bool prev_;
 };
 
 // ---- primitives -----------------------------------------------------------

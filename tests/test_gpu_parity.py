@@ -776,3 +776,61 @@ def test_corrupt_transfer_negative_control(ortho):
     assert caught == 12
     with pytest.raises(mx.MgrxInvalidArgument, match="no MGR level 3"):
         H.corrupt_transfer(3, 1.01)
+
+
+@pytest.mark.parametrize("code", [0, 4, 8, 16, 32, 64 + 16, 64 + 32])
+def test_team_sum_spmv_tolerance_mode(code):
+    """Team-sum SpMV (k_spmv_vec / k_spmv_vec2: lanes share a row, fused
+    multiply-adds, a shuffle tree) is the tolerance-level kernel of the
+    DEFAULT solve only. Forced on for every team size and both variants
+    (code 0: the setup timing's own choice, MGRX_SPMV_VEC=2) over short,
+    medium and long rows:
+      * mgrx_spmv without MGRX_TEAM_SUMS stays bitwise (left-to-right sums);
+        with it, each row agrees with the exact sum to a few ulp of
+        sum |a_ij x_j| and is deterministic run to run;
+      * mgrx_apply (exact) stays bitwise equal to the oracle, the MGS-mode
+        history stays identical to the oracle's, and the default-mode solve
+        (every epilogue of the preconditioner through the team-sum kernels)
+        meets the north_star bar (history 1e-10, iterations +-1) on the 3-D
+        elasticity problem whose AMG levels have 60-200 entries per row."""
+    import subprocess
+    import sys
+    code_txt = (
+        "import sys, numpy as np; sys.path.insert(0, '.'); sys.path.insert(0, 'tests');"
+        "import paper_2101_11649_b200 as mx, refcpu;"
+        "rng = np.random.default_rng(11);\n"
+        "for n, per in ((5000, 7), (4099, 20), (3000, 45), (2500, 130)):\n"
+        "    cols = np.sort(np.stack([rng.choice(n, per, replace=False) for _ in range(n)]), axis=1).astype(np.int32)\n"
+        "    ptr = (np.arange(n + 1) * per).astype(np.int32); val = rng.uniform(-1, 1, n * per)\n"
+        "    A = mx.Matrix(ptr, cols.ravel(), val); x = rng.uniform(-1, 1, n)\n"
+        "    prod = val.reshape(n, per) * x[cols]\n"
+        "    seq = np.zeros(n)\n"
+        "    for k in range(per): seq = seq + prod[:, k]\n"
+        "    assert np.array_equal(A.spmv(x).view(np.int64), (0.0 + seq).view(np.int64)), (n, per)\n"
+        "    yt = A.spmv(x, team_sums=True)\n"
+        "    assert np.array_equal(yt.view(np.int64), A.spmv(x, team_sums=True).view(np.int64))\n"
+        "    bound = 4 * np.finfo(float).eps * np.abs(prod).sum(axis=1) * np.log2(per + 1)\n"
+        "    assert np.all(np.abs(yt - seq) <= bound), (n, per, np.max(np.abs(yt - seq) / bound))\n"
+        "    assert not np.array_equal(yt, seq)\n"
+        "P = mx.frac_problem(16); t = mx.load_strategy('frac_mgr_u_l1j')\n"
+        "H = mx.Hierarchy(mx.Matrix(P.ptr, P.col, P.val), P.partition, t, P.unknown_map)\n"
+        "R = refcpu.RefHierarchy(P.ptr, P.col, P.val, P.partition.field_order, P.partition.labels, t, P.unknown_map)\n"
+        "v = rng.uniform(-1, 1, P.n)\n"
+        "assert np.array_equal(H.apply(v).view(np.int64), R.apply(v).view(np.int64))\n"
+        "x, rep = H.solve(P.rhs, cfg=mx.KrylovConfig(restart=30, rel_tol=1e-6, ortho='mgs'))\n"
+        "xr, rr = R.solve(P.rhs, restart=30, rel_tol=1e-6)\n"
+        "assert rep.iterations == rr['iterations'] and rep.residual_history == rr['history']\n"
+        "x2, rep2 = H.solve(P.rhs, cfg=mx.KrylovConfig(restart=30, rel_tol=1e-6))\n"
+        "assert rep2.converged and abs(rep2.iterations - rr['iterations']) <= 1\n"
+        "k = min(10, len(rep2.residual_history), len(rr['history']))\n"
+        "h, hr = np.array(rep2.residual_history[:k]), np.array(rr['history'][:k])\n"
+        "assert np.all(np.abs(h - hr) <= 1e-10 * np.maximum(np.abs(hr), 1.0)), (h, hr)\n"
+        "print('ok', rep.iterations, rep2.iterations)\n")
+    root = make_golden.ROOT
+    env = {"MGRX_VERBOSE": "1", "MGRX_SPMV_VEC": "2"}
+    if code:
+        env["MGRX_SPMV_VEC_FORCE"] = str(code)
+    out = subprocess.run([sys.executable, "-c", code_txt], cwd=root, capture_output=True, text=True,
+                         env={**__import__("os").environ, **env}, timeout=900)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
+    assert "team sums (tolerance mode)" in out.stderr, out.stderr[-2000:]
