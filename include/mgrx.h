@@ -197,6 +197,28 @@ MGRX_API int mgrx_nccl_unique_id(unsigned char* out128);
 /* In-process ranks (threads on one device) for parity tests. */
 MGRX_API int mgrx_local_group_create(int size, mgrx_group** out);
 MGRX_API int mgrx_local_group_destroy(mgrx_group* g);
+/* Bring-your-own transport: the ranks are processes (one per GPU, or several
+ * sharing one GPU) connected by the caller's communicator -- MPI in the
+ * paper's setting (hypre runs MGR over MPI), gloo in this
+ * repo's tests. libmgrx stages every halo segment / all-gather operand
+ * through pinned host memory and calls these BLOCKING functions (0 = ok):
+ *   exchange: send send_count[i] doubles at send_buf[i] to rank send_peer[i]
+ *             for i < nsend and receive recv_count[j] doubles from rank
+ *             recv_peer[j] into recv_buf[j] for j < nrecv; every rank calls it
+ *             with matching lists, so it must not depend on the order of the
+ *             peers' calls (post the receives first / nonblocking sends);
+ *   allgather: out[q * count + i] = rank q's in[i].
+ * Every rank creates its own group object of the same size and passes it as
+ * `group` to mgrx_shard_create[_scatter]; destroy it with
+ * mgrx_local_group_destroy after the shard. No reference counterpart (the
+ * reference is single-process). */
+typedef struct mgrx_transport {
+  void* user;
+  int (*exchange)(void* user, int nsend, const int* send_peer, const double* const* send_buf, const int* send_count,
+                  int nrecv, const int* recv_peer, double* const* recv_buf, const int* recv_count);
+  int (*allgather)(void* user, const double* in, double* out, int count);
+} mgrx_transport;
+MGRX_API int mgrx_transport_group_create(int size, const mgrx_transport* t, mgrx_group** out);
 /* row_starts: size+1 fine-row offsets (NULL = even split). Exactly one of
  * nccl_id / group when size > 1. */
 MGRX_API int mgrx_shard_create(mgrx_hier* h, int rank, int size, const int* row_starts,

@@ -99,6 +99,7 @@ def lib() -> C.CDLL:
         L.mgrx_nccl_unique_id.argtypes = [C.c_char_p]
         L.mgrx_local_group_create.argtypes = [C.c_int, C.POINTER(vp)]
         L.mgrx_local_group_destroy.argtypes = [vp]
+        L.mgrx_transport_group_create.argtypes = [C.c_int, vp, C.POINTER(vp)]
         L.mgrx_shard_create.argtypes = [vp, C.c_int, C.c_int, vp, C.c_char_p, vp, C.POINTER(vp)]
         L.mgrx_device_memory.argtypes = [vp, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong),
                                          C.POINTER(C.c_longlong)]
@@ -415,6 +416,85 @@ class LocalGroup:
         self.size = size
         self._h = C.c_void_p()
         _check(lib().mgrx_local_group_create(size, C.byref(self._h)))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().mgrx_local_group_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_void_p), C.POINTER(C.c_int),
+                           C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_void_p), C.POINTER(C.c_int))
+_ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int)
+
+
+class _Transport(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("exchange", _EXCHANGE_FN), ("allgather", _ALLGATHER_FN)]
+
+
+def _host_array(ptr, count):
+    return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_double)), shape=(count,)) if count > 0 else np.empty(0)
+
+
+class TransportGroup:
+    """mgrx_transport_group_create: ranks are processes connected by the
+    caller's own communicator (MPI, gloo, ...), host-staged. `exchange(sends,
+    recvs)` gets lists of (peer, float64 host array) -- send each array to its
+    peer, fill each receive array from its peer -- and `allgather(src, dst)`
+    fills dst (size * len(src)) with every rank's src in rank order; both
+    block until done. Use as the `group` of a Shard in every process."""
+
+    def __init__(self, size: int, exchange, allgather):
+        self.size = size
+
+        def _xchg(_user, ns, sp, sb, sc, nr, rp, rb, rc):
+            try:
+                exchange([(sp[i], _host_array(sb[i], sc[i])) for i in range(ns)],
+                         [(rp[j], _host_array(rb[j], rc[j])) for j in range(nr)])
+                return 0
+            except Exception:  # the library reports the failure as its own error
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        def _gather(_user, src, dst, count):
+            try:
+                allgather(_host_array(src, count), _host_array(dst, count * size))
+                return 0
+            except Exception:
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        self._cb = (_EXCHANGE_FN(_xchg), _ALLGATHER_FN(_gather))  # keep the thunks alive
+        self._t = _Transport(None, self._cb[0], self._cb[1])
+        self._h = C.c_void_p()
+        _check(lib().mgrx_transport_group_create(size, C.byref(self._t), C.byref(self._h)))
+
+    @staticmethod
+    def torch_distributed(pg=None) -> "TransportGroup":
+        """Transport over an initialised torch.distributed process group
+        (gloo: host tensors; isend / irecv for the halos, all_gather)."""
+        import torch
+        import torch.distributed as dist
+        size = dist.get_world_size(pg)
+
+        def exchange(sends, recvs):
+            ops = [dist.irecv(torch.from_numpy(a), src=p, group=pg) for p, a in recvs]
+            ops += [dist.isend(torch.from_numpy(a), dst=p, group=pg) for p, a in sends]
+            for o in ops:
+                o.wait()
+
+        def allgather(src, dst):
+            dist.all_gather_into_tensor(torch.from_numpy(dst), torch.from_numpy(src), group=pg)
+
+        return TransportGroup(size, exchange, allgather)
 
     def close(self):
         if getattr(self, "_h", None):

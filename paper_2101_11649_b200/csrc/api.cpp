@@ -39,8 +39,13 @@ struct mgrx_hier {
 };
 
 struct mgrx_group {
-  std::shared_ptr<LocalHub> hub;
+  std::shared_ptr<LocalHub> hub;  // in-process ranks (threads)
   int size = 0;
+  bool host = false;              // caller-supplied host transport (one rank per process)
+  HostTransport tr;
+  std::unique_ptr<Comm> comm(int rank) const {
+    return host ? make_host_comm(tr, rank, size) : make_local_comm(hub, rank);
+  }
 };
 
 struct mgrx_shard {
@@ -690,6 +695,21 @@ int mgrx_local_group_create(int size, mgrx_group** out) {
   });
 }
 
+int mgrx_transport_group_create(int size, const mgrx_transport* t, mgrx_group** out) {
+  return guarded([&] {
+    if (size < 1 || !out || !t || !t->exchange || !t->allgather)
+      throw InvalidArgument("mgrx_transport_group_create: size >= 1 and both transport functions are required");
+    auto* g = new mgrx_group;
+    g->size = size;
+    g->host = true;
+    g->tr.user = t->user;
+    g->tr.exchange = t->exchange;
+    g->tr.allgather = t->allgather;
+    *out = g;
+    return MGRX_OK;
+  });
+}
+
 int mgrx_local_group_destroy(mgrx_group* g) {
   delete g;
   return MGRX_OK;
@@ -712,7 +732,7 @@ int mgrx_shard_create(mgrx_hier* h, int rank, int size, const int* row_starts, c
     std::unique_ptr<Comm> cm;
     if (group) {
       if (group->size != size) throw InvalidArgument("mgrx_shard_create: group size mismatch");
-      cm = make_local_comm(group->hub, rank);
+      cm = group->comm(rank);
     } else if (nccl_id) {
       cm = make_nccl_comm(nccl_id, rank, size);
     } else {
@@ -756,7 +776,7 @@ int mgrx_shard_create_scatter(mgrx_ctx* ctx, mgrx_hier* h, int rank, int size, c
     std::unique_ptr<Comm> cm;
     if (group) {
       if (group->size != size) throw InvalidArgument("mgrx_shard_create_scatter: group size mismatch");
-      cm = make_local_comm(group->hub, rank);
+      cm = group->comm(rank);
     } else if (nccl_id) {
       cm = make_nccl_comm(nccl_id, rank, size);
     } else {

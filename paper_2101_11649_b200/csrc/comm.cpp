@@ -3,6 +3,7 @@
 
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <condition_variable>
 #include <cstring>
 #include <mutex>
@@ -256,6 +257,86 @@ class LocalComm final : public Comm {
 };
 
 }  // namespace
+
+// ---------------------------------------------------------------------------
+// Host-staged transport (caller-supplied exchange / allgather)
+// ---------------------------------------------------------------------------
+namespace {
+
+class HostComm final : public Comm {
+ public:
+  HostComm(const HostTransport& t, int r, int n) : t_(t) {
+    rank = r;
+    size = n;
+    if (!t_.exchange || !t_.allgather) throw InvalidArgument("host transport: exchange and allgather are required");
+  }
+  ~HostComm() override {
+    if (sb_) cudaFreeHost(sb_);
+    if (rb_) cudaFreeHost(rb_);
+  }
+  void exchange(const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs, cudaStream_t s) override {
+    size_t ns = 0, nr = 0;
+    for (const Xfer& x : sends) ns += static_cast<size_t>(x.count);
+    for (const Xfer& x : recvs) nr += static_cast<size_t>(x.count);
+    grow(sb_, scap_, ns);
+    grow(rb_, rcap_, nr);
+    std::vector<int> sp, sc, rp, rc;
+    std::vector<const double*> sbuf;
+    std::vector<double*> rbuf;
+    size_t off = 0;
+    for (const Xfer& x : sends) {
+      MGRX_CK(cudaMemcpyAsync(sb_ + off, x.ptr, sizeof(double) * x.count, cudaMemcpyDeviceToHost, s));
+      sp.push_back(x.peer);
+      sc.push_back(x.count);
+      sbuf.push_back(sb_ + off);
+      off += static_cast<size_t>(x.count);
+    }
+    off = 0;
+    for (const Xfer& x : recvs) {
+      rp.push_back(x.peer);
+      rc.push_back(x.count);
+      rbuf.push_back(rb_ + off);
+      off += static_cast<size_t>(x.count);
+    }
+    MGRX_CK(cudaStreamSynchronize(s));
+    if (t_.exchange(t_.user, static_cast<int>(sends.size()), sp.data(), sbuf.data(), sc.data(),
+                    static_cast<int>(recvs.size()), rp.data(), rbuf.data(), rc.data()) != 0)
+      throw RuntimeError("host transport: exchange failed");
+    for (size_t j = 0; j < recvs.size(); ++j)
+      MGRX_CK(cudaMemcpyAsync(recvs[j].ptr, rbuf[j], sizeof(double) * recvs[j].count, cudaMemcpyHostToDevice, s));
+    MGRX_CK(cudaStreamSynchronize(s));  // the staging buffers are reused by the next call
+  }
+  void allgather(const double* in, double* out, int count, cudaStream_t s) override {
+    grow(sb_, scap_, static_cast<size_t>(count));
+    grow(rb_, rcap_, static_cast<size_t>(count) * size);
+    MGRX_CK(cudaMemcpyAsync(sb_, in, sizeof(double) * count, cudaMemcpyDeviceToHost, s));
+    MGRX_CK(cudaStreamSynchronize(s));
+    if (t_.allgather(t_.user, sb_, rb_, count) != 0) throw RuntimeError("host transport: allgather failed");
+    MGRX_CK(cudaMemcpyAsync(out, rb_, sizeof(double) * count * size, cudaMemcpyHostToDevice, s));
+    MGRX_CK(cudaStreamSynchronize(s));
+  }
+  bool graph_safe() const override { return false; }
+  const char* kind() const override { return "host"; }
+
+ private:
+  static void grow(double*& p, size_t& cap, size_t need) {
+    if (need <= cap) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = std::max(need, cap * 2);
+    MGRX_CK(cudaMallocHost(&p, sizeof(double) * cap));
+  }
+  HostTransport t_;
+  double* sb_ = nullptr;
+  double* rb_ = nullptr;
+  size_t scap_ = 0, rcap_ = 0;
+};
+
+}  // namespace
+
+std::unique_ptr<Comm> make_host_comm(const HostTransport& t, int rank, int size) {
+  return std::make_unique<HostComm>(t, rank, size);
+}
 
 std::shared_ptr<LocalHub> make_local_hub(int size) { return std::make_shared<LocalHub>(size); }
 

@@ -13,6 +13,7 @@
 //   local (several ranks as threads of one process on one device, for the
 //          parity tests): device-to-device copies ordered by events and host
 //          barriers. Not capturable, not a performance path.
+//   host  (caller-supplied transport, e.g. MPI or gloo; host-staged).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -56,6 +57,19 @@ constexpr int kNcclIdBytes = 128;
 void nccl_unique_id(unsigned char* out);
 // ncclCommInitRank on the current device.
 std::unique_ptr<Comm> make_nccl_comm(const unsigned char* id, int rank, int size);
+
+// Host-staged transport supplied by the caller (MPI in the paper's hypre
+// setting, gloo in the tests): segments are copied to pinned host buffers,
+// handed to the caller's blocking exchange / allgather functions, and copied
+// back. Not capturable; correctness path for stacks without NCCL and the way
+// the sharded path runs as real processes where only one GPU is available.
+struct HostTransport {
+  void* user = nullptr;
+  int (*exchange)(void* user, int nsend, const int* send_peer, const double* const* send_buf, const int* send_count,
+                  int nrecv, const int* recv_peer, double* const* recv_buf, const int* recv_count) = nullptr;
+  int (*allgather)(void* user, const double* in, double* out, int count) = nullptr;
+};
+std::unique_ptr<Comm> make_host_comm(const HostTransport& t, int rank, int size);
 
 struct LocalHub;
 std::shared_ptr<LocalHub> make_local_hub(int size);

@@ -99,3 +99,61 @@ def test_slab_ranges_are_contiguous_and_cover():
         assert all(rr[i][1] == rr[i + 1][0] for i in range(w - 1))
     flags = np.array([1, 0, 1, 1, 0, 0, 1, 0], bool)
     assert D.ranges_from_flags(flags, [(0, 4), (4, 8)]) == [(0, 3), (3, 4)]
+
+
+def _transport_worker(rank, world, port, q):
+    """The gloo closures behind mx.TransportGroup.torch_distributed (the
+    host-transport group of the multi-process sharded path), without a GPU:
+    the group object itself needs none, only Shard creation does."""
+    try:
+        import os
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+        import torch.distributed as dist
+        import paper_2101_11649_b200 as mx
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        seen = {}
+        real = mx.TransportGroup.__init__
+
+        def spy(self, size, exchange, allgather):
+            seen["exchange"], seen["allgather"] = exchange, allgather
+            real(self, size, exchange, allgather)  # the C-ABI group object (no device needed)
+
+        mx.TransportGroup.__init__ = spy
+        g = mx.TransportGroup.torch_distributed()
+        peer = 1 - rank
+        a, b = np.full(5, float(rank)), np.empty(5)
+        seen["exchange"]([(peer, a)], [(peer, b)])
+        dst = np.empty(3 * world)
+        seen["allgather"](np.array([rank, rank + 0.5, rank + 0.25]), dst)
+        # a one-sided call (scatter setup: rank 0 only sends, the others only receive)
+        c = np.empty(4)
+        if rank == 0:
+            seen["exchange"]([(1, np.arange(4.0))], [])
+        else:
+            seen["exchange"]([], [(0, c)])
+        g.close()
+        q.put((rank, b.tolist(), dst.tolist(), c.tolist() if rank else None, g.size))
+        dist.destroy_process_group()
+    except Exception:  # pragma: no cover
+        import traceback
+        q.put((rank, "error", traceback.format_exc()))
+
+
+def test_host_transport_group_over_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_transport_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(2)]
+    for p in ps:
+        p.join(timeout=60)
+    for r in res:
+        assert r[1] != "error", r[2]
+        rank, b, dst, c, size = r
+        assert size == 2
+        assert b == [float(1 - rank)] * 5
+        assert dst == [0.0, 0.5, 0.25, 1.0, 1.5, 1.25]
+        if rank:
+            assert c == [0.0, 1.0, 2.0, 3.0]
