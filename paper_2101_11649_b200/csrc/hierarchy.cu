@@ -1186,6 +1186,7 @@ void MgrHier::corrupt_transfer(int l, double factor, cudaStream_t s) {
   // plans that carry their own copy of the values would keep the clean P
   L.P.bsr = 0;
   L.P.nslice = 0;
+  L.P.tb = 0;
   L.pplan.w = 0;
   MGRX_CK(cudaStreamSynchronize(s));
   for (auto& kv : graphs_)

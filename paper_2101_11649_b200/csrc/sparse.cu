@@ -1602,9 +1602,78 @@ void launch_vec(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
   count_launch();
 }
 
+// Team-sum BSR(3) (DCsr::tb): one warp per block row; lane b takes block b
+// (its column, its nine values from the nine coalesced planes, three x
+// values), accumulates the three row sums with fused multiply-adds, and the
+// warp folds them by a shuffle tree. Tolerance-level, like k_spmv_vec.
+template <class Epi, class Xs>
+__global__ void __launch_bounds__(256) k_spmv_tbsr3(int nbr, const int* __restrict__ tptr,
+                                                    const int* __restrict__ tcol,
+                                                    const double* __restrict__ tval, Xs x, Epi epi) {
+  pdl_enter();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nw = gridDim.x * 8;
+  int R = blockIdx.x * 8 + w;
+  int p0 = 0, p1 = 0;
+  if (R < nbr) {
+    p0 = __ldg(tptr + R);
+    p1 = __ldg(tptr + R + 1);
+  }
+  for (; R < nbr; R += nw) {
+    int q0 = 0, q1 = 0;
+    if (R + nw < nbr) {
+      q0 = __ldg(tptr + R + nw);
+      q1 = __ldg(tptr + R + nw + 1);
+    }
+    const int nb = p1 - p0;
+    decltype(epi.load(0)) pre{};
+    if (lane < 3) pre = epi.load(3 * R + lane);
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    const double* v = tval + 9LL * p0;
+    for (int b = lane; b < nb; b += 32) {
+      const int c = 3 * __ldcs(tcol + p0 + b);
+      double a[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) a[k] = __ldcs(v + static_cast<long long>(k) * nb + b);
+      const double x0 = x(c), x1 = x(c + 1), x2 = x(c + 2);
+      s0 = fma(a[0], x0, s0);
+      s1 = fma(a[3], x0, s1);
+      s2 = fma(a[6], x0, s2);
+      s0 = fma(a[1], x1, s0);
+      s1 = fma(a[4], x1, s1);
+      s2 = fma(a[7], x1, s2);
+      s0 = fma(a[2], x2, s0);
+      s1 = fma(a[5], x2, s1);
+      s2 = fma(a[8], x2, s2);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if (lane < 3) epi.store(3 * R + lane, lane == 0 ? s0 : (lane == 1 ? s1 : s2), pre);
+    p0 = q0;
+    p1 = q1;
+  }
+}
+
+template <class Epi, class Xs>
+void launch_tbsr(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
+  const int nbr = A.rows / 3;
+  const int grid = std::min(blocks_for(nbr, 8), device_sms() * 8 * 4);
+  launch_pdl(k_spmv_tbsr3<Epi, Xs>, grid, 256, 0, s, nbr, A.tptr.get(), A.tcol.get(), A.tval.get(), x, epi);
+  MGRX_LAUNCH_CK();
+  count_launch();
+}
+
 template <class Epi, class Xs = XPlain>
 void launch_spmv(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
   if (A.rows == 0) return;
+  if (A.tb > 0 && TeamSums::active()) {
+    launch_tbsr(A, x, epi, s);
+    return;
+  }
   if (A.vec > 0 && TeamSums::active()) {
     launch_vec(A, x, epi, s);
     return;
@@ -2462,16 +2531,113 @@ void vec_try(DCsr& A, cudaStream_t s) {
     }
 }
 
+// Team-sum BSR(3) candidate of the tolerance-level solve (long-row matrices of
+// full aligned 3 x 3 blocks): built on the host, timed against the matrix's
+// current tolerance-mode choice (team-sum CSR or the bitwise kernel).
+// MGRX_SPMV_TBSR=0 off, 2 forced where the structure is there.
+void tbsr_try(DCsr& A, cudaStream_t s) {
+  static const int mode = [] {
+    const char* e = std::getenv("MGRX_SPMV_TBSR");
+    return e ? std::atoi(e) : 1;
+  }();
+  A.tb = 0;
+  if (!mode || A.rows < 2048 || A.rows % 3 || A.cols % 3 || A.nnz % 9) return;
+  if (mode == 1 && static_cast<long long>(A.nnz) < 24LL * A.rows) return;
+  const char* pf = std::getenv("MGRX_SPMV_PLAN_FILE");
+  int replay = -1;
+  if (pf)
+    if (FILE* f = std::fopen(pf, "r")) {
+      int r, c, z;
+      char what[16];
+      while (std::fscanf(f, "%d %d %d %15s", &r, &c, &z, what) == 4)
+        if (r == A.rows && c == A.cols && z == A.nnz) {
+          if (!std::strcmp(what, "tbsr")) replay = 1;
+          if (!std::strcmp(what, "notbsr")) replay = 0;
+        }
+      std::fclose(f);
+    }
+  if (replay == 0) return;
+  const std::vector<int> p = A.ptr.download(A.rows + 1);
+  const std::vector<int> c = A.col.download(A.nnz);
+  const int nbr = A.rows / 3;
+  std::vector<int> tptr(nbr + 1, 0), tcol;
+  tcol.reserve(A.nnz / 9);
+  for (int R = 0; R < nbr; ++R) {
+    const int r0 = 3 * R, len = p[r0 + 1] - p[r0];
+    if (len % 3 || p[r0 + 2] - p[r0 + 1] != len || p[r0 + 3] - p[r0 + 2] != len) return;
+    for (int k = 0; k < len; k += 3) {
+      const int c0 = c[p[r0] + k];
+      if (c0 % 3) return;
+      for (int r = 0; r < 3; ++r)
+        for (int q = 0; q < 3; ++q)
+          if (c[p[r0 + r] + k + q] != c0 + q) return;
+      tcol.push_back(c0 / 3);
+    }
+    tptr[R + 1] = static_cast<int>(tcol.size());
+  }
+  const std::vector<double> v = A.val.download(A.nnz);
+  std::vector<double> tv(static_cast<size_t>(tcol.size()) * 9);
+  for (int R = 0; R < nbr; ++R) {
+    const int nb = tptr[R + 1] - tptr[R];
+    double* out = tv.data() + 9 * static_cast<size_t>(tptr[R]);
+    for (int b = 0; b < nb; ++b)
+      for (int r = 0; r < 3; ++r)
+        for (int q = 0; q < 3; ++q) out[static_cast<size_t>(3 * r + q) * nb + b] = v[p[3 * R + r] + 3 * b + q];
+  }
+  A.tptr.alloc(nbr + 1, s);
+  A.tptr.upload(tptr.data(), nbr + 1);
+  A.tcol.alloc(tcol.size() > 0 ? tcol.size() : 1, s);
+  A.tcol.upload(tcol.data(), tcol.size());
+  A.tval.alloc(tv.size() > 0 ? tv.size() : 1, s);
+  A.tval.upload(tv.data(), tv.size());
+  bool keep = mode == 2 || replay == 1;
+  float tc = 0.f, tt = 0.f;
+  if (!keep) {
+    DVec<double> xs(A.cols, s), ys(A.rows, s);
+    xs.zero();
+    cudaEvent_t e0, e1;
+    MGRX_CK(cudaEventCreate(&e0));
+    MGRX_CK(cudaEventCreate(&e1));
+    tc = tt = 1e30f;
+    TeamSums on(true);
+    for (int trial = 0; trial < 3; ++trial) {
+      A.tb = 0;
+      tc = std::min(tc, tune_time(A, xs.get(), ys.get(), s, e0, e1));
+      A.tb = 3;
+      tt = std::min(tt, tune_time(A, xs.get(), ys.get(), s, e0, e1));
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    keep = tt < 0.97f * tc;
+  }
+  if (const char* e = std::getenv("MGRX_VERBOSE"); e && e[0] == '1')
+    std::fprintf(stderr, "spmv_prepare rows %d nnz %d: tolerance-mode csr %.1f us, team-sum bsr(3) %.1f us -> %s\n",
+                 A.rows, A.nnz, 100.f * tc, 100.f * tt, keep ? "team-sum bsr (tolerance mode)" : "keep");
+  A.tb = keep ? 3 : 0;
+  if (!keep) {
+    A.tptr.release();
+    A.tcol.release();
+    A.tval.release();
+  }
+  if (pf && replay < 0)
+    if (FILE* f = std::fopen(pf, "a")) {
+      std::fprintf(f, "%d %d %d %s\n", A.rows, A.cols, A.nnz, keep ? "tbsr" : "notbsr");
+      std::fclose(f);
+    }
+}
+
 void spmv_prepare(DCsr& A, cudaStream_t s) {
   A.bsr = 0;
   A.nslice = 0;
   A.xt_nblk = 0;
   A.vec = 0;
+  A.tb = 0;
   spmv_prepare_csr(A, s);
   bsr_try(A, s);
   sell_try(A, s);
   xtile_try(A, s);
   vec_try(A, s);
+  tbsr_try(A, s);
 }
 
 void spmv_prepare_csr(DCsr& A, cudaStream_t s) {

@@ -80,6 +80,15 @@ struct DCsr {
   // TeamSums scope is active (the default solve); the bitwise paths never
   // take it.
   int vec = 0;
+  // Team-sum BSR(3) copy (tolerance-level solve only; matrices whose block
+  // rows hold full aligned 3 x 3 blocks, e.g. the elasticity displacement
+  // operator): per block row the block columns (tcol) and the values as nine
+  // planes of nb doubles (value k of block b at 9 * tptr[R] + k * nb + b), so
+  // a warp reads each plane coalesced; 8.4 B per entry instead of 12.
+  // tb == 0: none.
+  int tb = 0;
+  DVec<int> tptr, tcol;
+  DVec<double> tval;
   bool empty() const { return rows == 0; }
 };
 

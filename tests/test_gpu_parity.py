@@ -781,7 +781,7 @@ def test_corrupt_transfer_negative_control(ortho):
         H.corrupt_transfer(3, 1.01)
 
 
-@pytest.mark.parametrize("code", [0, 4, 8, 16, 32, 64 + 16, 64 + 32])
+@pytest.mark.parametrize("code", [0, 4, 8, 16, 32, 64 + 16, 64 + 32, "tbsr"])
 def test_team_sum_spmv_tolerance_mode(code):
     """Team-sum SpMV (k_spmv_vec / k_spmv_vec2: lanes share a row, fused
     multiply-adds, a shuffle tree) is the tolerance-level kernel of the
@@ -815,6 +815,20 @@ def test_team_sum_spmv_tolerance_mode(code):
         "    bound = 4 * np.finfo(float).eps * np.abs(prod).sum(axis=1) * np.log2(per + 1)\n"
         "    assert np.all(np.abs(yt - seq) <= bound), (n, per, np.max(np.abs(yt - seq) / bound))\n"
         "    assert not np.array_equal(yt, seq)\n"
+        "nbr, nbk = 1200, 10\n"
+        "bc = np.sort(np.stack([rng.choice(nbr, nbk, replace=False) for _ in range(nbr)]), axis=1)\n"
+        "cols = np.repeat((3 * bc[:, None, :, None] + np.arange(3)[None, None, None, :]).reshape(nbr, 1, 3 * nbk), 3, axis=1)\n"
+        "cols = cols.reshape(3 * nbr, 3 * nbk).astype(np.int32); n, per = 3 * nbr, 3 * nbk\n"
+        "ptr = (np.arange(n + 1) * per).astype(np.int32); val = rng.uniform(-1, 1, n * per)\n"
+        "A = mx.Matrix(ptr, cols.ravel(), val); x = rng.uniform(-1, 1, n)\n"
+        "prod = val.reshape(n, per) * x[cols]\n"
+        "seq = np.zeros(n)\n"
+        "for k in range(per): seq = seq + prod[:, k]\n"
+        "assert np.array_equal(A.spmv(x).view(np.int64), (0.0 + seq).view(np.int64))\n"
+        "yt = A.spmv(x, team_sums=True)\n"
+        "assert np.array_equal(yt.view(np.int64), A.spmv(x, team_sums=True).view(np.int64))\n"
+        "assert np.all(np.abs(yt - seq) <= 4 * np.finfo(float).eps * np.abs(prod).sum(axis=1) * np.log2(per + 1))\n"
+        "assert not np.array_equal(yt, seq)\n"
         "P = mx.frac_problem(16); t = mx.load_strategy('frac_mgr_u_l1j')\n"
         "H = mx.Hierarchy(mx.Matrix(P.ptr, P.col, P.val), P.partition, t, P.unknown_map)\n"
         "R = refcpu.RefHierarchy(P.ptr, P.col, P.val, P.partition.field_order, P.partition.labels, t, P.unknown_map)\n"
@@ -831,9 +845,13 @@ def test_team_sum_spmv_tolerance_mode(code):
         "print('ok', rep.iterations, rep2.iterations)\n")
     root = make_golden.ROOT
     env = {"MGRX_VERBOSE": "1", "MGRX_SPMV_VEC": "2"}
-    if code:
+    if code == "tbsr":
+        env["MGRX_SPMV_TBSR"] = "2"  # team-sum BSR(3) wherever the 3 x 3 block structure is there
+    elif code:
         env["MGRX_SPMV_VEC_FORCE"] = str(code)
     out = subprocess.run([sys.executable, "-c", code_txt], cwd=root, capture_output=True, text=True,
                          env={**__import__("os").environ, **env}, timeout=900)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
     assert "team sums (tolerance mode)" in out.stderr, out.stderr[-2000:]
+    if code == "tbsr":
+        assert "team-sum bsr (tolerance mode)" in out.stderr, out.stderr[-2000:]
