@@ -1525,7 +1525,7 @@ __global__ void __launch_bounds__(256) k_spmv_vec(int rows, const int* __restric
 template <int kT, class Epi, class Xs>
 __global__ void __launch_bounds__(256) k_spmv_vec2(int rows, const int* __restrict__ ptr,
                                                    const int* __restrict__ col,
-                                                   const double* __restrict__ val, Xs x, Epi epi) {
+                                                   const double* __restrict__ val, Xs x, Epi epi, int keep) {
   pdl_enter();
   constexpr int kTeams = 256 / kT;
   constexpr int kU = 4;
@@ -1555,8 +1555,10 @@ __global__ void __launch_bounds__(256) k_spmv_vec2(int rows, const int* __restri
       for (int j = 0; j < kU; ++j) {
         const int qq = q + j * kT;
         const bool ok = qq < hi;
-        c[j] = ok ? __ldcs(col + qq) : -1;
-        v[j] = ok ? __ldcs(val + qq) : 0.0;
+        // keep: a small operator re-read four times per V-cycle stays in the L2
+        // (plain loads) instead of being marked evict-first
+        c[j] = ok ? (keep ? __ldg(col + qq) : __ldcs(col + qq)) : -1;
+        v[j] = ok ? (keep ? __ldg(val + qq) : __ldcs(val + qq)) : 0.0;
       }
 #pragma unroll
       for (int j = 0; j < kU; ++j) xv[j] = c[j] >= 0 ? x(c[j]) : 0.0;
@@ -1583,6 +1585,15 @@ void launch_vec(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
     const int grid = std::min(blocks_for(A.rows, teams), device_sms() * 8 * 4);
     launch_pdl(kern, grid, 256, 0, s, A.rows, A.ptr.get(), A.col.get(), A.val.get(), x, epi);
   };
+  static const long long keep_nnz = [] {  // MGRX_VEC_KEEP_NNZ: largest operator read with plain (L2-retained) loads
+    const char* e = std::getenv("MGRX_VEC_KEEP_NNZ");
+    return e ? std::atoll(e) : 0LL;  // measured no gain at cfg2 / cfg3: off
+  }();
+  const int keep = A.nnz <= keep_nnz ? 1 : 0;
+  auto go2 = [&](auto kern, int teams) {
+    const int grid = std::min(blocks_for(A.rows, teams), device_sms() * 8 * 4);
+    launch_pdl(kern, grid, 256, 0, s, A.rows, A.ptr.get(), A.col.get(), A.val.get(), x, epi, keep);
+  };
   if (A.vec & 64) {
     switch (A.vec & 63) {
       case 4: go(k_spmv_vec<4, Epi, Xs>, 64); break;
@@ -1592,10 +1603,10 @@ void launch_vec(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
     }
   } else {
     switch (A.vec & 63) {
-      case 4: go(k_spmv_vec2<4, Epi, Xs>, 64); break;
-      case 8: go(k_spmv_vec2<8, Epi, Xs>, 32); break;
-      case 16: go(k_spmv_vec2<16, Epi, Xs>, 16); break;
-      default: go(k_spmv_vec2<32, Epi, Xs>, 8); break;
+      case 4: go2(k_spmv_vec2<4, Epi, Xs>, 64); break;
+      case 8: go2(k_spmv_vec2<8, Epi, Xs>, 32); break;
+      case 16: go2(k_spmv_vec2<16, Epi, Xs>, 16); break;
+      default: go2(k_spmv_vec2<32, Epi, Xs>, 8); break;
     }
   }
   MGRX_LAUNCH_CK();
