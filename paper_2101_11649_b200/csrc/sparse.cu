@@ -1669,6 +1669,39 @@ __global__ void __launch_bounds__(256) k_spmv_tbsr3(int nbr, const int* __restri
   }
 }
 
+// Team-sum BSR(3) build: warp per block row; checks that its three rows hold
+// the same full aligned 3 x 3 blocks (bad = 1 otherwise) and writes the block
+// columns and the nine value planes.
+__global__ void __launch_bounds__(256) k_tbsr_build(int nbr, const int* __restrict__ ptr, const int* __restrict__ col,
+                                                    const double* __restrict__ val, int* __restrict__ tptr,
+                                                    int* __restrict__ tcol, double* __restrict__ tval,
+                                                    int* __restrict__ bad) {
+  const int lane = threadIdx.x & 31;
+  const int R = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (R >= nbr) return;
+  const int p0 = ptr[3 * R], p1 = ptr[3 * R + 1], p2 = ptr[3 * R + 2], p3 = ptr[3 * R + 3];
+  const int len = p1 - p0;
+  bool ok = len % 3 == 0 && p2 - p1 == len && p3 - p2 == len && p0 % 9 == 0;
+  if (lane == 0) {
+    tptr[R] = p0 / 9;
+    if (R == nbr - 1) tptr[nbr] = p3 / 9;
+  }
+  if (ok) {
+    const int nb = len / 3, t0 = p0 / 9;
+    for (int j = lane; j < len; j += 32) {
+      const int b = j / 3, q = j % 3;
+      const int c = col[p0 + j];
+      ok = ok && c - q == col[p0 + 3 * b] && (c - q) % 3 == 0 && col[p1 + j] == c && col[p2 + j] == c;
+      if (q == 0) tcol[t0 + b] = c / 3;
+      double* out = tval + 9LL * t0 + b;
+      out[static_cast<long long>(q) * nb] = val[p0 + j];
+      out[static_cast<long long>(3 + q) * nb] = val[p1 + j];
+      out[static_cast<long long>(6 + q) * nb] = val[p2 + j];
+    }
+  }
+  if (!ok) *bad = 1;
+}
+
 template <class Epi, class Xs>
 void launch_tbsr(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
   const int nbr = A.rows / 3;
@@ -2568,39 +2601,22 @@ void tbsr_try(DCsr& A, cudaStream_t s) {
       std::fclose(f);
     }
   if (replay == 0) return;
-  const std::vector<int> p = A.ptr.download(A.rows + 1);
-  const std::vector<int> c = A.col.download(A.nnz);
+  // structure check and conversion on the device (warp per block row)
   const int nbr = A.rows / 3;
-  std::vector<int> tptr(nbr + 1, 0), tcol;
-  tcol.reserve(A.nnz / 9);
-  for (int R = 0; R < nbr; ++R) {
-    const int r0 = 3 * R, len = p[r0 + 1] - p[r0];
-    if (len % 3 || p[r0 + 2] - p[r0 + 1] != len || p[r0 + 3] - p[r0 + 2] != len) return;
-    for (int k = 0; k < len; k += 3) {
-      const int c0 = c[p[r0] + k];
-      if (c0 % 3) return;
-      for (int r = 0; r < 3; ++r)
-        for (int q = 0; q < 3; ++q)
-          if (c[p[r0 + r] + k + q] != c0 + q) return;
-      tcol.push_back(c0 / 3);
-    }
-    tptr[R + 1] = static_cast<int>(tcol.size());
-  }
-  const std::vector<double> v = A.val.download(A.nnz);
-  std::vector<double> tv(static_cast<size_t>(tcol.size()) * 9);
-  for (int R = 0; R < nbr; ++R) {
-    const int nb = tptr[R + 1] - tptr[R];
-    double* out = tv.data() + 9 * static_cast<size_t>(tptr[R]);
-    for (int b = 0; b < nb; ++b)
-      for (int r = 0; r < 3; ++r)
-        for (int q = 0; q < 3; ++q) out[static_cast<size_t>(3 * r + q) * nb + b] = v[p[3 * R + r] + 3 * b + q];
-  }
+  DVec<int> bad(1, s);
+  bad.zero();
   A.tptr.alloc(nbr + 1, s);
-  A.tptr.upload(tptr.data(), nbr + 1);
-  A.tcol.alloc(tcol.size() > 0 ? tcol.size() : 1, s);
-  A.tcol.upload(tcol.data(), tcol.size());
-  A.tval.alloc(tv.size() > 0 ? tv.size() : 1, s);
-  A.tval.upload(tv.data(), tv.size());
+  A.tcol.alloc(A.nnz / 9 > 0 ? A.nnz / 9 : 1, s);
+  A.tval.alloc(A.nnz > 0 ? A.nnz : 1, s);
+  k_tbsr_build<<<blocks_for(nbr, 8), 256, 0, s>>>(nbr, A.ptr.get(), A.col.get(), A.val.get(), A.tptr.get(),
+                                                  A.tcol.get(), A.tval.get(), bad.get());
+  MGRX_LAUNCH_CK();
+  if (bad.download(1)[0] != 0) {
+    A.tptr.release();
+    A.tcol.release();
+    A.tval.release();
+    return;
+  }
   bool keep = mode == 2 || replay == 1;
   float tc = 0.f, tt = 0.f;
   if (!keep) {
