@@ -223,6 +223,10 @@ def probe_names(H):
         names += ["mgr.0.rres", "mgr.0.prolong"]
     for k in range(max(info["coarse_amg_levels"] - 1, 0)):
         names += [f"amg.{k}.resid", f"amg.{k}.pre", f"amg.{k}.post"]
+    # F-relaxation AMG hierarchies (cfg4: the unknown-based AMG on A_uu, where the time goes)
+    for l, nl in enumerate(info["frelax_amg_levels"]):
+        for k in range(min(max(nl - 1, 0), 4)):
+            names += [f"mgr.{l}.frelax.amg.{k}.resid", f"mgr.{l}.frelax.amg.{k}.pre"]
     return names
 
 

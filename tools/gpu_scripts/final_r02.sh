@@ -12,6 +12,7 @@ for c in cfg3 cfg4 cfg5; do timeout 1200 python bench.py --config $c --no-cpu-ba
 timeout 900 python bench.py --sharded --steps 3 --warmup 3 > gpurun_out/bench_sharded1.log 2>&1
 CONFIGS="cfg2 cfg3 cfg4" bash tools/gpu_scripts/launch_list_cfg.sh > gpurun_out/launch_lists.log 2>&1
 CFG=cfg2 PROBES="spmv.A cgs2dots.15 cgs2upd.15 amg.1.resid amg.0.pre amg.2.resid" bash tools/gpu_scripts/r02_ncu.sh > gpurun_out/ncu_all.log 2>&1
+CFG=cfg4 PROBES="mgr.0.frelax.amg.0.resid mgr.0.frelax.amg.1.resid" bash tools/gpu_scripts/r02_ncu.sh > gpurun_out/ncu_cfg4.log 2>&1
 rm -f gpurun_out/*.ncu-rep
 tail -4 gpurun_out/pytest_gpu_all.log; tail -2 gpurun_out/smoke.log
 for f in bench_cfg2 bench_ref bench_cfg3 bench_cfg4 bench_cfg5 bench_sharded1; do grep '^{' gpurun_out/$f.log | tail -1 | cut -c1-300; done
