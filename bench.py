@@ -6,8 +6,9 @@ pressure system with l1-Jacobi x2 AMG smoothing
 (strategies/mfd_mgr_pi_c1_l1j.json: BASELINE cfg2's "one AMG V-cycle"; the
 shipped proj/strategies/mfd_mgr_pi.json, 8 V-cycles of hybrid Gauss-Seidel,
 is measured in the same line under "variants"). Orthogonalisation: the
-default low-synchronisation lagged CGS2 (csrc/lowsync.cu); the reference's
-MGS (bitwise parity mode) is a variant.
+default low-synchronisation lagged CGS2 (csrc/lowsync.cu) with the
+tolerance-level team-sum SpMV kernels where the setup timing picks them; the
+reference's MGS (bitwise parity mode, left-to-right row sums) is a variant.
 
 A step = one complete solve from x0 = 0 with the hierarchy already built
 (setup is timed separately and reported). value = DOF * GMRES iterations /
@@ -519,11 +520,28 @@ def main():
         if "avg_ms" in probes.get(nm, {}):
             arn[kern] = {"probe": nm, "achieved": probes[nm]["GBps"], "frac": probes[nm]["GBps"] / peak,
                          "algorithmic_bytes": probes[nm]["bytes"], "avg_ms": probes[nm]["avg_ms"]}
+    # the SpMV family as a whole (k_spmv_staged and its x-window form
+    # k_spmv_xtile, the team-sum kernels): every probe of a product / sweep /
+    # residual on an operator large enough not to be launch-bound, bytes and
+    # time summed -- the time-weighted fraction of the family, next to its
+    # share of a solve's kernel time (ncu launch list, profiles/r02)
+    fam = [k for k, v in probes.items() if "GBps" in v and v["avg_ms"] >= 0.006 and
+           (k == "spmv.A" or k.endswith(".rres") or ".amg." in k or k.startswith("amg."))]
+    family = None
+    if fam:
+        fb, ft = sum(probes[k]["bytes"] for k in fam), sum(probes[k]["avg_ms"] for k in fam) * 1e-3
+        fshare = None
+        if shares:
+            fshare = round(sum(v for k, v in shares.items() if k.startswith("k_spmv") and isinstance(v, float)), 4)
+        family = {"kernels": "k_spmv_staged / k_spmv_xtile / k_spmv_vec2 / k_spmv_tbsr3 (SpMV family)",
+                  "probes": fam, "bytes": fb, "ms": ft * 1e3, "achieved": fb / ft / 1e9, "frac": fb / ft / 1e9 / peak,
+                  "share_of_solve_kernel_time": fshare}
     roof = {"bound": "hbm", "kernel": "k_spmv_staged" if dom == "spmv.A" else dom,
             "instance": "spmv.A (fine operator; GMRES SpMV)" if dom == "spmv.A" else dom,
             "achieved": d["GBps"], "peak": peak, "unit": "GB/s",
             "frac": d["GBps"] / peak, "traffic": traffic, "algorithmic_bytes": d["bytes"],
-            "peak_source": peak_kind, "launch_shares": shares, "arnoldi_low_sync": arn, "kernels": probes,
+            "peak_source": peak_kind, "launch_shares": shares, "spmv_family": family, "arnoldi_low_sync": arn,
+            "kernels": probes,
             "probe_method": "CUDA events on the library stream over 20 back-to-back launches (inputs in HBM; "
                             "the L2 may retain part of a working set near its 126 MB size)"}
 

@@ -2744,7 +2744,8 @@ void spmv_prepare_csr(DCsr& A, cudaStream_t s) {
       while (std::fscanf(f, "%d %d %d %15s", &r, &c, &z, what) == 4)
         if (r == A.rows && c == A.cols && z == A.nnz && std::strcmp(what, "bsr") && std::strcmp(what, "csr") &&
             std::strcmp(what, "sell") && std::strcmp(what, "nosell") && std::strncmp(what, "xt", 2) &&
-            std::strcmp(what, "noxtile")) {
+            std::strcmp(what, "noxtile") && std::strncmp(what, "vec", 3) && std::strcmp(what, "novec") &&
+            std::strcmp(what, "tbsr") && std::strcmp(what, "notbsr")) {
           replayed = true;
           // "wspec_staged": the specialised plan plus the staged one for the
           // products the specialised kernel does not serve
