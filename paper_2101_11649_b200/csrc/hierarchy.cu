@@ -1015,7 +1015,7 @@ void MgrHier::coarse_solve(const double* v, double* z, cudaStream_t s) {
 }
 
 void MgrHier::apply(const double* v, double* z, cudaStream_t s, bool exact) {
-  TeamSums team_sums(!exact);
+  TeamSums team_sums(!exact, exact);  // exact: bitwise kernels whatever the caller's scope
   exact_dense_ = exact;
   apply_level(0, v, z, s);
   exact_dense_ = true;

@@ -31,8 +31,9 @@ long long g_launches = 0;
 namespace {
 thread_local bool t_team_sums = false;
 }
-TeamSums::TeamSums(bool on) : prev_(t_team_sums) {
+TeamSums::TeamSums(bool on, bool off) : prev_(t_team_sums) {
   if (on) t_team_sums = true;
+  else if (off) t_team_sums = false;
 }
 TeamSums::~TeamSums() { t_team_sums = prev_; }
 bool TeamSums::active() { return t_team_sums; }

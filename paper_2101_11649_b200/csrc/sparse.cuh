@@ -97,7 +97,9 @@ struct DCsr {
 // default solve (tolerance-level parity, like its orthogonalisation). Thread-
 // local, nestable; `on == false` leaves the current state.
 struct TeamSums {
-  explicit TeamSums(bool on);
+  // on: enable for the scope; off: disable for the scope (a bitwise
+  // application inside a tolerance-level caller); neither: leave as is
+  explicit TeamSums(bool on, bool off = false);
   ~TeamSums();
   TeamSums(const TeamSums&) = delete;
   TeamSums& operator=(const TeamSums&) = delete;
