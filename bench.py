@@ -501,7 +501,7 @@ def main():
     # low-sync Arnoldi sweeps are reported beside it at the mean Krylov index
     # of a 30-step cycle (k = 15). Other strategies: the probe with the
     # largest time.
-    share = {k: v["avg_ms"] for k, v in probes.items() if "avg_ms" in v}
+    share = {k: v["avg_ms"] for k, v in probes.items() if "avg_ms" in v and "GBps" in v}
     if "l1j" in STRATEGY and "avg_ms" in probes.get("spmv.A", {}):
         dom = "spmv.A"
     else:
