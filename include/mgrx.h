@@ -13,6 +13,8 @@
  *   mgrx_solve       <- gmres(A, b, x, cfg, mgr_preconditioner(H))
  *                                                 proj/include/mgrkit/krylov.hpp:33-34,
  *                                                 proj/include/mgrkit/mgr.hpp:114
+ *   mgrx_solve_op    <- the same call with A != H's fine operator (hierarchy
+ *                       kept across Newton steps)
  *   mgrx_spmv        <- spmv(A, x)                proj/include/mgrkit/sparse.hpp:57
  *   mgrx_dump        <- MgrHierarchy / AmgHierarchy member access (levels[l].P, ...)
  *                                                 proj/include/mgrkit/mgr.hpp:79-100,
@@ -136,6 +138,18 @@ MGRX_API int mgrx_apply(mgrx_hier* h, const double* v, double* z, int on_device)
 #define MGRX_ZERO_GUESS 2
 MGRX_API int mgrx_solve(mgrx_hier* h, const double* b, double* x, const mgrx_krylov* cfg,
                mgrx_report* report, int flags);
+
+/* The same GMRES with a caller's operator A (square, as many rows as the
+ * hierarchy's fine level) and the hierarchy h as M: gmres(A, b, x, cfg,
+ * mgr_preconditioner(H)) with A != H.levels[0].A, proj/include/mgrkit/
+ * krylov.hpp:33-34 takes the two separately. This is the reuse of a
+ * hierarchy across Newton steps (the reference's Newton
+ * driver, proj/src/problems/mfd.cpp:650-677, rebuilds it every step): build
+ * A_k with mgrx_matrix_csr / mgrx_matrix_csr_device, keep h from an earlier
+ * step. Errors as the reference's: "gmres: matrix must be square",
+ * "mgr_apply: size mismatch". A and h must belong to one context. */
+MGRX_API int mgrx_solve_op(mgrx_hier* h, mgrx_mat* A, const double* b, double* x, const mgrx_krylov* cfg,
+                           mgrx_report* report, int flags);
 
 /* AmgSetupInfo of an AMG hierarchy (proj/include/mgrkit/amg.hpp:35-39):
  * which = -1 the MGR coarse solver's AMG, l >= 0 the F-relaxation AMG of MGR

@@ -196,6 +196,37 @@ int ref_solve(void* hp, const double* b, double* x, int restart, int max_iters, 
   }
 }
 
+// gmres(A', b, x, cfg, mgr_preconditioner(H)) with an operator A' other than
+// the one H was built from (proj/include/mgrkit/krylov.hpp:33-34 takes the
+// operator and the preconditioner separately).
+int ref_solve_op(void* hp, int n, const int* ptr, const int* col, const double* val, const double* b,
+                 double* x, int restart, int max_iters, double rel_tol, double abs_tol, int* converged,
+                 int* iterations, double* final_residual, double* history, int history_cap,
+                 int* history_len) {
+  try {
+    auto* h = static_cast<RefHandle*>(hp);
+    const Csr A = make_csr(n, n, ptr, col, val);
+    KrylovConfig kc;
+    kc.restart = restart;
+    kc.max_iters = max_iters;
+    kc.rel_tol = rel_tol;
+    kc.abs_tol = abs_tol;
+    const Vec bv(b, b + n);
+    Vec xv(x, x + n);
+    const SolveReport rep = gmres(A, bv, xv, kc, mgr_preconditioner(h->H));
+    std::memcpy(x, xv.data(), sizeof(double) * n);
+    *converged = rep.converged ? 1 : 0;
+    *iterations = rep.iterations;
+    *final_residual = rep.final_residual;
+    const int len = static_cast<int>(rep.residual_history.size());
+    *history_len = len;
+    for (int i = 0; i < len && i < history_cap; ++i) history[i] = rep.residual_history[i];
+    return rep.converged ? 0 : 1;
+  } catch (const std::exception& e) {
+    return fail_code(e);
+  }
+}
+
 // Two-call protocol: pass null buffers to query sizes. kind: 0 csr, 1 int list, 2 vector.
 int ref_dump(void* hp, const char* path, int* kind, int* rows, int* cols, long long* nnz, int* ptr,
              int* col, double* val) {

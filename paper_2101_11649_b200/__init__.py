@@ -88,6 +88,7 @@ def lib() -> C.CDLL:
         L.mgrx_hier_destroy.argtypes = [vp]
         L.mgrx_apply.argtypes = [vp, vp, vp, C.c_int]
         L.mgrx_solve.argtypes = [vp, vp, vp, C.POINTER(_Krylov), C.POINTER(_Report), C.c_int]
+        L.mgrx_solve_op.argtypes = [vp, vp, vp, vp, C.POINTER(_Krylov), C.POINTER(_Report), C.c_int]
         L.mgrx_dump.argtypes = [vp, C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                 C.POINTER(C.c_int), C.POINTER(C.c_longlong), vp, vp, vp]
         L.mgrx_info.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_int]
@@ -319,6 +320,24 @@ class Hierarchy:
         k = _krylov(cfg)
         _check(lib().mgrx_solve(self._h, C.c_void_p(b_ptr), C.c_void_p(x_ptr), C.byref(k), C.byref(rep), 1))
         return self._to_report(rep, hist)
+
+    def solve_op(self, A: "Matrix", b: np.ndarray, x: Optional[np.ndarray] = None,
+                 cfg: Optional[KrylovConfig] = None, history_cap: int = 4096) -> tuple:
+        """gmres(A, b, x0, cfg, mgr_preconditioner(self)) with an operator A
+        other than the one this hierarchy was built from (a hierarchy kept
+        across Newton steps; mgrx_solve_op)."""
+        cfg = cfg or KrylovConfig()
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        out = np.empty(self.n)
+        flags = 0
+        if x is None:
+            flags |= 2  # MGRX_ZERO_GUESS
+        else:
+            np.copyto(out, np.asarray(x, dtype=np.float64).reshape(-1))
+        rep, hist = self._report(history_cap)
+        k = _krylov(cfg)
+        _check(lib().mgrx_solve_op(self._h, A._h, _ptr(b), _ptr(out), C.byref(k), C.byref(rep), flags))
+        return out, self._to_report(rep, hist)
 
     @staticmethod
     def _report(cap):
@@ -632,9 +651,11 @@ def mgr_apply(H: Hierarchy, v: np.ndarray) -> np.ndarray:
 
 def gmres(A: Matrix, b: np.ndarray, x: np.ndarray, cfg: KrylovConfig, H: Hierarchy):
     """gmres(A, b, x, cfg, mgr_preconditioner(H)) — proj/include/mgrkit/krylov.hpp:33-34.
-    The hierarchy's copy of A is the operator; returns (x, SolveReport)."""
+    With the matrix H was built from, the hierarchy's copy of A is the
+    operator; any other matrix goes through mgrx_solve_op (H as a lagged
+    preconditioner). Returns (x, SolveReport)."""
     if A is not H.A:
-        raise MgrxInvalidArgument(INVALID_ARGUMENT, "gmres: hierarchy was built for a different matrix")
+        return H.solve_op(A, b, x, cfg)
     return H.solve(b, x, cfg)
 
 

@@ -429,12 +429,16 @@ int mgrx_apply(mgrx_hier* h, const double* v, double* z, int on_device) {
   });
 }
 
-int mgrx_solve(mgrx_hier* h, const double* b, double* x, const mgrx_krylov* cfg, mgrx_report* rep,
-               int flags) {
+// gmres(op, b, x, cfg, mgr_preconditioner(h->H)): op is the hierarchy's own
+// copy of A (mgrx_solve) or a caller's operator of the same size
+// (mgrx_solve_op: the hierarchy kept across Newton steps as a lagged
+// preconditioner).
+static int solve_with(mgrx_hier* h, const DCsr& op, const double* b, double* x, const mgrx_krylov* cfg,
+                      mgrx_report* rep, int flags) {
   const bool on_device = flags & MGRX_ON_DEVICE;
   const bool zero_guess = flags & MGRX_ZERO_GUESS;
-  return guarded([&] {
-    use(h->ctx);
+  const bool external = &op != &h->A;
+  {
     if (!cfg) throw InvalidArgument("mgrx_solve: null config");
     cudaStream_t s = h->ctx->stream;
     const int n = h->A.rows;
@@ -468,9 +472,12 @@ int mgrx_solve(mgrx_hier* h, const double* b, double* x, const mgrx_krylov* cfg,
       H->apply(in, out, st, exact);
     };
     EventTimer t(s);
-    GmresResult r = gmres_device(h->A, db, dx, k, prec, h->ws, s, prec_rec);
+    GmresResult r = gmres_device(op, db, dx, k, prec, h->ws, s, prec_rec);
     const double solve_s = t.stop();
     h->H.check(s);
+    // the recorded restart cycle is keyed by the operator's address: a
+    // caller's matrix may be destroyed and another created in its place
+    if (external) h->ws.ls.exec_key = LsWork::Key();
     if (!on_device) {
       MGRX_CK(cudaMemcpyAsync(x, dx, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
       MGRX_CK(cudaStreamSynchronize(s));
@@ -487,6 +494,27 @@ int mgrx_solve(mgrx_hier* h, const double* b, double* x, const mgrx_krylov* cfg,
       rep->gpu_launches = g_launches - l0;
     }
     return r.converged ? MGRX_OK : MGRX_NOT_CONVERGED;
+  }
+}
+
+int mgrx_solve(mgrx_hier* h, const double* b, double* x, const mgrx_krylov* cfg, mgrx_report* rep,
+               int flags) {
+  return guarded([&] {
+    if (!h) throw InvalidArgument("mgrx_solve: null hierarchy");
+    use(h->ctx);
+    return solve_with(h, h->A, b, x, cfg, rep, flags);
+  });
+}
+
+int mgrx_solve_op(mgrx_hier* h, mgrx_mat* A, const double* b, double* x, const mgrx_krylov* cfg,
+                  mgrx_report* rep, int flags) {
+  return guarded([&] {
+    if (!h || !A) throw InvalidArgument("mgrx_solve_op: null argument");
+    if (A->ctx != h->ctx) throw InvalidArgument("mgrx_solve_op: matrix and hierarchy belong to different contexts");
+    if (A->A.rows != A->A.cols) throw InvalidArgument("gmres: matrix must be square");
+    if (A->A.rows != h->A.rows) throw InvalidArgument("mgr_apply: size mismatch");
+    use(h->ctx);
+    return solve_with(h, A->A, b, x, cfg, rep, flags);
   });
 }
 

@@ -45,6 +45,9 @@ def lib():
         L.ref_solve.argtypes = [vp, _F64P, _F64P, C.c_int, C.c_int, C.c_double, C.c_double,
                                 C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_double), _F64P,
                                 C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_double)]
+        L.ref_solve_op.argtypes = [vp, C.c_int, _I32P, _I32P, _F64P, _F64P, _F64P, C.c_int, C.c_int,
+                                   C.c_double, C.c_double, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                   C.POINTER(C.c_double), _F64P, C.c_int, C.POINTER(C.c_int)]
         L.ref_dump.argtypes = [vp, C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                C.POINTER(C.c_int), C.POINTER(C.c_longlong), vp, vp, vp]
         L.ref_info.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_int]
@@ -120,6 +123,20 @@ class RefHierarchy:
                              C.byref(ss)))
         return x, {"converged": bool(conv.value), "iterations": it.value, "final_residual": fr.value,
                    "history": hist[:min(hl.value, cap)].tolist(), "solve_s": ss.value}
+
+    def solve_op(self, ptr, col, val, b, restart=30, max_iters=500, rel_tol=1e-6, abs_tol=0.0, x0=None,
+                 cap=4096):
+        """gmres(A', b, x, cfg, mgr_preconditioner(H)): another operator, this hierarchy as M."""
+        x = np.zeros(self.n) if x0 is None else np.array(x0, dtype=np.float64)
+        conv, it, fr, hl = C.c_int(), C.c_int(), C.c_double(), C.c_int()
+        hist = np.zeros(cap)
+        ptr = np.ascontiguousarray(ptr, np.int32)
+        _chk(lib().ref_solve_op(self._h, ptr.size - 1, ptr, np.ascontiguousarray(col, np.int32),
+                                np.ascontiguousarray(val, np.float64), np.ascontiguousarray(b, np.float64), x,
+                                restart, max_iters, rel_tol, abs_tol, C.byref(conv), C.byref(it),
+                                C.byref(fr), hist, cap, C.byref(hl)))
+        return x, {"converged": bool(conv.value), "iterations": it.value, "final_residual": fr.value,
+                   "history": hist[:min(hl.value, cap)].tolist()}
 
     def info(self):
         m, c = C.c_int(), C.c_int()

@@ -855,3 +855,67 @@ def test_team_sum_spmv_tolerance_mode(code):
     assert "team sums (tolerance mode)" in out.stderr, out.stderr[-2000:]
     if code == "tbsr":
         assert "team-sum bsr (tolerance mode)" in out.stderr, out.stderr[-2000:]
+
+
+def _newton_like_pair(seed=3):
+    """Two operators of one sparsity pattern: A0 (the hierarchy is built from
+    it) and A1 = A0 with every value scaled by 1 + 0.02 u, u ~ U(-1, 1)
+    per entry (a later Newton step's Jacobian)."""
+    P = mx.mfd_problem(8, 8, 4, "iid")
+    rng = np.random.default_rng(seed)
+    val1 = P.val * (1.0 + 0.02 * rng.uniform(-1.0, 1.0, P.val.size))
+    return P, val1
+
+
+@pytest.mark.parametrize("ortho", ["mgs", "cgs2"])
+def test_solve_op_lagged_hierarchy_matches_oracle(ortho):
+    """mgrx_solve_op: gmres(A1, b, x, cfg, mgr_preconditioner(H(A0))) — the
+    hierarchy of an earlier Newton step kept as the preconditioner of a later
+    operator (proj/include/mgrkit/krylov.hpp:33-34 takes A and M
+    separately). Oracle: the same call on refcpu."""
+    P, val1 = _newton_like_pair()
+    text = mx.load_strategy("mfd_mgr_pi_c1")
+    R = refcpu.RefHierarchy(P.ptr, P.col, P.val, P.partition.field_order, P.partition.labels, text)
+    xr, rrep = R.solve_op(P.ptr, P.col, val1, P.rhs, restart=30, rel_tol=1e-8)
+    ctx = mx.Context(0)
+    A0, A1 = mx.Matrix(P.ptr, P.col, P.val, ctx=ctx), mx.Matrix(P.ptr, P.col, val1, ctx=ctx)
+    H = mx.Hierarchy(A0, P.partition, text)
+    cfg = mx.KrylovConfig(restart=30, rel_tol=1e-8, ortho=ortho)
+    x, rep = mx.gmres(A1, P.rhs, None, cfg, H)
+    assert rep.converged and rrep["converged"]
+    assert abs(rep.iterations - rrep["iterations"]) <= 1
+    ok, detail = history_close(rep.residual_history, rrep["history"])
+    assert ok, detail
+    if ortho == "mgs":
+        assert rep.residual_history == rrep["history"]
+        assert np.array_equal(x, xr)
+    import scipy.sparse as sp
+    M1 = sp.csr_matrix((val1, P.col, P.ptr), shape=(P.n, P.n))
+    assert np.linalg.norm(P.rhs - M1 @ x) <= 1e-8 * np.linalg.norm(P.rhs) * (1 + 1e-9)
+    # the lagged hierarchy is a worse preconditioner than a fresh one, not a wrong one
+    _, rep0 = H.solve(P.rhs, cfg=cfg)
+    assert rep0.converged and rep.iterations >= rep0.iterations
+    # the hierarchy's own operator is untouched by the foreign solve, and a
+    # second foreign operator (freed / re-created matrices) re-records the cycle
+    del A1
+    A2 = mx.Matrix(P.ptr, P.col, 0.5 * (P.val + val1), ctx=ctx)
+    x2, rep2 = H.solve_op(A2, P.rhs, None, cfg)
+    _, rrep2 = R.solve_op(P.ptr, P.col, 0.5 * (P.val + val1), P.rhs, restart=30, rel_tol=1e-8)
+    assert rep2.converged and abs(rep2.iterations - rrep2["iterations"]) <= 1
+    ok, detail = history_close(rep2.residual_history, rrep2["history"])
+    assert ok, detail
+    _, rep0b = H.solve(P.rhs, cfg=cfg)
+    assert rep0b.residual_history == rep0.residual_history
+
+
+def test_solve_op_errors():
+    P, _ = _newton_like_pair()
+    text = mx.load_strategy("mfd_mgr_pi_c1")
+    ctx = mx.Context(0)
+    H = mx.Hierarchy(mx.Matrix(P.ptr, P.col, P.val, ctx=ctx), P.partition, text)
+    small = mx.Matrix(np.array([0, 1, 2], np.int32), np.array([0, 1], np.int32), np.ones(2), ctx=ctx)
+    with pytest.raises(mx.MgrxInvalidArgument, match="mgr_apply: size mismatch"):
+        H.solve_op(small, P.rhs)
+    rect = mx.Matrix(np.array([0, 1, 2], np.int32), np.array([0, 2], np.int32), np.ones(2), shape=(2, 3), ctx=ctx)
+    with pytest.raises(mx.MgrxInvalidArgument, match="gmres: matrix must be square"):
+        H.solve_op(rect, P.rhs)

@@ -86,3 +86,21 @@ def test_oracle_errors_name_rows():
         refcpu.RefHierarchy(ptr, col, val, ["a", "b"], [0, 0, 1],
                             json.dumps({"levels": [{"f_fields": ["a"]}, {"f_fields": ["a"]}]}))
     assert e.value.code == 2 and "eliminated twice" in str(e.value)
+
+
+def test_oracle_solve_op_with_own_operator_is_solve():
+    """ref_solve_op (gmres with the operator passed apart from the hierarchy,
+    proj/include/mgrkit/krylov.hpp:33-34) on the hierarchy's own A is ref_solve,
+    bit for bit; on a perturbed operator it still converges to that operator's
+    solution."""
+    P = mx.mfd_problem(6, 5, 4, "iid")
+    text = mx.load_strategy("mfd_mgr_pi_c1")
+    R = refcpu.RefHierarchy(P.ptr, P.col, P.val, P.partition.field_order, P.partition.labels, text)
+    x, rep = R.solve(P.rhs, restart=30, rel_tol=1e-8)
+    xo, repo = R.solve_op(P.ptr, P.col, P.val, P.rhs, restart=30, rel_tol=1e-8)
+    assert rep["history"] == repo["history"] and np.array_equal(x, xo)
+    val1 = P.val * (1.0 + 0.02 * np.random.default_rng(3).uniform(-1.0, 1.0, P.val.size))
+    x1, rep1 = R.solve_op(P.ptr, P.col, val1, P.rhs, restart=30, rel_tol=1e-8)
+    assert rep1["converged"] and rep1["iterations"] >= rep["iterations"]
+    y = refcpu.spmv(P.ptr, P.col, val1, x1)
+    assert np.linalg.norm(P.rhs - y) <= 1e-8 * np.linalg.norm(P.rhs) * (1 + 1e-9)
