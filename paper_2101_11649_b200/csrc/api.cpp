@@ -649,7 +649,12 @@ int mgrx_time_kernel(mgrx_hier* h, const char* which, int reps, double* avg_ms, 
     cudaStream_t s = h->ctx->stream;
     std::function<void()> fn;
     double b = 0.0;
-    const std::string w(which);
+    std::string w(which);
+    // "cold:<probe>": the launch's duration from a cold L2, measured without
+    // launch latency as the difference of two back-to-back streams of `reps`
+    // iterations, [256 MB flush read, launch] and [flush read] alone
+    const bool cold = w.rfind("cold:", 0) == 0;
+    if (cold) w = w.substr(5);
     prepare_probe(h, w, fn, b, s);
     // probes time the kernels of the default (tolerance-level) solve;
     // MGRX_PROBE_EXACT=1: the bitwise kernels
@@ -668,7 +673,32 @@ int mgrx_time_kernel(mgrx_hier* h, const char* which, int reps, double* avg_ms, 
       const char* e = std::getenv("MGRX_PROBE_FLUSH");
       return e && e[0] == '1';
     }();
-    if (!flush) {
+    if (cold) {
+      constexpr size_t kFlush = 256ull << 20;
+      if (h->flushbuf.size() < kFlush) {
+        h->flushbuf.alloc(kFlush, s);
+        h->flushbuf.zero();
+      }
+      const int n = reps > 0 ? reps : 1;
+      double best_with = 1e300, best_without = 1e300;
+      for (int round = 0; round < 3; ++round) {
+        for (int i = 0; i < 2; ++i) l2_flush_read(h->flushbuf.get(), kFlush, s);
+        {
+          EventTimer t(s);
+          for (int i = 0; i < n; ++i) l2_flush_read(h->flushbuf.get(), kFlush, s);
+          best_without = std::min(best_without, t.stop());
+        }
+        {
+          EventTimer t(s);
+          for (int i = 0; i < n; ++i) {
+            l2_flush_read(h->flushbuf.get(), kFlush, s);
+            fn();
+          }
+          best_with = std::min(best_with, t.stop());
+        }
+      }
+      *avg_ms = (best_with - best_without) * 1e3 / n;
+    } else if (!flush) {
       EventTimer t(s);
       for (int i = 0; i < reps; ++i) fn();
       *avg_ms = t.stop() * 1e3 / (reps > 0 ? reps : 1);

@@ -691,6 +691,14 @@ __global__ void __launch_bounds__(Gm::T) k_spmv_staged(int nblk, const int* __re
 // Row sums are the serial loop's (left to right), bitwise equal.
 // Geometry: kR rows (= row threads) / kE entries / kL window lines per block,
 // kS stages per CTA; one extra warp issues the copies.
+// Epilogues that declare kLate (see k_spmv_xtile's row warps).
+template <class E, class = void>
+struct epi_late : std::false_type {};
+template <class E>
+struct epi_late<E, std::void_t<decltype(E::kLate)>> : std::true_type {};
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 __constant__ int c_xt_dbg = 0;  // MGRX_XT_DBG: timing experiments (1: window as one copy)
 constexpr int kXtRuns = 32;     // runs per block: one per lane of the copy warp
 constexpr int kXtDirect = -2;   // block meta "tail" value: no window, global columns
@@ -871,14 +879,31 @@ __global__ void __launch_bounds__(Gm::T, Gm::CTAS) k_spmv_xtile(int nblk, const 
     cur = Blk{e[0], e[1], e[2], e[3], e[7]};
   }
   pdl_enter();
+  // Epilogue operands: light epilogues (one value per row) hold the next
+  // block's in registers. Heavy ones (the Jacobi sweeps: three values per
+  // row) would not fit a second set under the register bound of Gm::CTAS
+  // resident CTAs -- it spilled to local memory, which misses the small L1
+  // left beside the stages: 24 B per row through L2 on every block's critical
+  // path, 55 us instead of 20 on the cfg2 level-0 operator -- so they only
+  // prefetch the next block's lines into L2 and load their own block's
+  // operands at the top of its iteration (an L2 hit, covered by the row sum).
+  constexpr bool kLate = epi_late<Epi>::value;
   decltype(epi.load(0)) pre{};
-  if (cur.r0 + t < cur.r1) pre = epi.load(cur.r0 + t);
+  if constexpr (!kLate) {
+    if (cur.r0 + t < cur.r1) pre = epi.load(cur.r0 + t);
+  }
   int it = 0;
   for (int b = blockIdx.x; b < nblk; b += G, ++it) {
     const int s = it % kS;
     const Blk nn = load_blk(b + 2 * G);
     decltype(epi.load(0)) pre_n{};
-    if (nxt.r0 + t < nxt.r1) pre_n = epi.load(nxt.r0 + t);
+    if constexpr (kLate) {
+      if (cur.r0 + t < cur.r1) pre = epi.load(cur.r0 + t);
+      const int rn = nxt.r0 + t;
+      if (rn < nxt.r1 && (t == 0 || (rn & 15) == 0)) epi.prefetch(rn);
+    } else {
+      if (nxt.r0 + t < nxt.r1) pre_n = epi.load(nxt.r0 + t);
+    }
     const int r0 = cur.r0, r1 = cur.r1, p0 = cur.p0, tail = cur.tail;
     const int r = r0 + t;
     double xt = 0.0;  // x[xcols - 1] when xcols is odd and the block needs it (tail = its window slot)
@@ -985,7 +1010,7 @@ __global__ void __launch_bounds__(Gm::T, Gm::CTAS) k_spmv_xtile(int nblk, const 
     if (r < r1) epi.store(r, sum, pre);
     cur = nxt;
     nxt = nn;
-    pre = pre_n;
+    if constexpr (!kLate) pre = pre_n;
   }
 }
 
@@ -1189,6 +1214,12 @@ struct EpiJacobi {
   const double* dinv;
   double w;
   double* znew;
+  static constexpr bool kLate = true;
+  __device__ void prefetch(int r) const {
+    if (!brow) prefetch_l2(b + r);
+    prefetch_l2(zold + r);
+    prefetch_l2(dinv + r);
+  }
   __device__ JacPre load(int r) const { return {brow ? b[brow[r]] : b[r], zold[r], dinv[r], 0.0}; }
   __device__ void store(int r, double s, const JacPre& p) const {
     const double d = __dsub_rn(p.bv, __dadd_rn(0.0, s));
@@ -1209,6 +1240,13 @@ struct EpiJacobiEx {
   double w;
   double* znew;
   double* zacc;
+  static constexpr bool kLate = true;
+  __device__ void prefetch(int r) const {
+    if (!brow) prefetch_l2(b + r);
+    if (zold) prefetch_l2(zold + r);
+    prefetch_l2(dinv + r);
+    if (zacc) prefetch_l2(zacc + r);
+  }
   __device__ JacPre load(int r) const {
     return {brow ? b[brow[r]] : b[r], zold ? zold[r] : z0(r), dinv[r], zacc ? zacc[r] : 0.0};
   }
