@@ -29,7 +29,7 @@ for f in $O/cfg2_*_raw.csv $O/cfg4_*_raw.csv; do
   cp "$f" $P/ncu_${b}_full_raw.csv
 done
 python tools/roofline_traffic.py cfg2 $P/bench_cfg2.json $O $P/roofline_traffic.json \
-  spmv.A cgs2dots.15 cgs2upd.15 amg.1.resid amg.0.pre amg.2.resid
+  spmv.A cgs2dots.15 cgs2upd.15 amg.1.resid amg.0.pre amg.1.pre amg.2.resid
 python tools/roofline_traffic.py cfg4 $P/bench_cfg4.json $O $P/roofline_traffic.json \
   mgr.0.frelax.amg.0.resid mgr.0.frelax.amg.1.resid
 python - <<'PY'

@@ -11,7 +11,7 @@ timeout 1200 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1
 for c in cfg3 cfg4 cfg5; do timeout 1200 python bench.py --config $c --no-cpu-baseline > gpurun_out/bench_$c.log 2>&1; done
 timeout 900 python bench.py --sharded --steps 3 --warmup 3 > gpurun_out/bench_sharded1.log 2>&1
 CONFIGS="cfg2 cfg3 cfg4" bash tools/gpu_scripts/launch_list_cfg.sh > gpurun_out/launch_lists.log 2>&1
-CFG=cfg2 PROBES="spmv.A cgs2dots.15 cgs2upd.15 amg.1.resid amg.0.pre amg.2.resid" bash tools/gpu_scripts/r02_ncu.sh > gpurun_out/ncu_all.log 2>&1
+CFG=cfg2 PROBES="spmv.A cgs2dots.15 cgs2upd.15 amg.1.resid amg.0.pre amg.1.pre amg.2.resid" bash tools/gpu_scripts/r02_ncu.sh > gpurun_out/ncu_all.log 2>&1
 CFG=cfg4 PROBES="mgr.0.frelax.amg.0.resid mgr.0.frelax.amg.1.resid" bash tools/gpu_scripts/r02_ncu.sh > gpurun_out/ncu_cfg4.log 2>&1
 rm -f gpurun_out/*.ncu-rep
 tail -4 gpurun_out/pytest_gpu_all.log; tail -2 gpurun_out/smoke.log
