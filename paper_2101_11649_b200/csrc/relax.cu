@@ -744,10 +744,17 @@ __global__ void k_jacobi0(int n, double w, const double* __restrict__ dinv,
                           const double* __restrict__ r, const int* __restrict__ rrow,
                           double* __restrict__ z) {
   pdl_enter();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  // two elements per thread (i and i + 256, both coalesced): the gathered
+  // form is a chain index -> value, so the second element's loads double
+  // the requests in flight
+  const int i = blockIdx.x * 512 + threadIdx.x, j = i + 256;
   if (i >= n) return;
-  const double rv = rrow ? r[rrow[i]] : r[i];
-  z[i] = __dmul_rn(w, __dmul_rn(dinv[i], rv));
+  const bool vj = j < n;
+  const int qi = rrow ? rrow[i] : i, qj = vj ? (rrow ? rrow[j] : j) : 0;
+  const double di = dinv[i], dj = vj ? dinv[j] : 0.0;
+  const double ri = r[qi], rj = vj ? r[qj] : 0.0;
+  z[i] = __dmul_rn(w, __dmul_rn(di, ri));
+  if (vj) z[j] = __dmul_rn(w, __dmul_rn(dj, rj));
 }
 __global__ void k_vec_add(int n, const double* __restrict__ a, double* __restrict__ y) {
   pdl_enter();
@@ -1330,7 +1337,7 @@ void gs_check(GsScratch& scr, cudaStream_t s) {
 void jacobi0(int n, double w, const double* dinv, const double* r, const int* rrow, double* z,
              cudaStream_t s) {
   if (n == 0) return;
-  launch_pdl(k_jacobi0, blocks_for(n, 256), 256, 0, s, n, w, dinv, r, rrow, z);
+  launch_pdl(k_jacobi0, blocks_for(n, 512), 256, 0, s, n, w, dinv, r, rrow, z);
   MGRX_LAUNCH_CK();
   count_launch();
 }

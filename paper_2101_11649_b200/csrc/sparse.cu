@@ -373,29 +373,51 @@ __global__ void __launch_bounds__(kWarps * 32) k_spmv_wpr(int rows, const int* _
   }
 }
 
-// Thread per row for very short rows (MGR prolongation: 1-2 entries per
-// row): no staging, every thread's few loads are independent, so the warp
-// keeps many requests in flight. Same sequential row sum.
+// Thread per row for very short rows (MGR / AMG prolongations: 1-4 entries
+// per row): no staging. The kernel is bound by its chain of dependent
+// loads (row pointers -> entries -> x -> epilogue operand), so each thread
+// takes TWO rows (r and r + 256: both coalesced across the warp), loads the
+// epilogue operands up front and fetches the first four entries of both
+// rows together (predicated): twice the requests in flight and one DRAM
+// round trip less per row than the one-row form (cfg2 AMG level-0
+// prolongation 18.4 -> see DESIGN 4). Same sequential row sums.
 template <class Epi, class Xs>
 __global__ void __launch_bounds__(256) k_spmv_tpr(int rows, const int* __restrict__ ptr,
                                                   const int* __restrict__ col,
                                                   const double* __restrict__ val,
                                                   Xs x, Epi epi) {
   pdl_enter();
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= rows) return;
-  const int lo = __ldg(ptr + r), hi = __ldg(ptr + r + 1);
-  double sum = 0.0;
-  int k = lo;
-  for (; k + 4 <= hi; k += 4) {
-    const int c0 = __ldg(col + k), c1 = __ldg(col + k + 1), c2 = __ldg(col + k + 2), c3 = __ldg(col + k + 3);
-    const double a0 = __ldg(val + k), a1 = __ldg(val + k + 1), a2 = __ldg(val + k + 2), a3 = __ldg(val + k + 3);
-    const double p0 = __dmul_rn(a0, x(c0)), p1 = __dmul_rn(a1, x(c1));
-    const double p2 = __dmul_rn(a2, x(c2)), p3 = __dmul_rn(a3, x(c3));
-    sum = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(sum, p0), p1), p2), p3);
+  const int ra = blockIdx.x * 512 + threadIdx.x, rb = ra + 256;
+  const bool va = ra < rows, vb = rb < rows;
+  if (!va) return;
+  const int loa = __ldg(ptr + ra), hia = __ldg(ptr + ra + 1);
+  const int lob = vb ? __ldg(ptr + rb) : 0, hib = vb ? __ldg(ptr + rb + 1) : 0;
+  decltype(epi.load(0)) prea = epi.load(ra), preb{};
+  if (vb) preb = epi.load(rb);
+  int ca[4], cb[4];
+  double aa[4], ab[4], xa[4], xb[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    ca[u] = loa + u < hia ? __ldg(col + loa + u) : -1;
+    cb[u] = lob + u < hib ? __ldg(col + lob + u) : -1;
+    aa[u] = loa + u < hia ? __ldg(val + loa + u) : 0.0;
+    ab[u] = lob + u < hib ? __ldg(val + lob + u) : 0.0;
   }
-  for (; k < hi; ++k) sum = __dadd_rn(sum, __dmul_rn(__ldg(val + k), x(__ldg(col + k))));
-  epi(r, sum);
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    xa[u] = ca[u] >= 0 ? x(ca[u]) : 0.0;
+    xb[u] = cb[u] >= 0 ? x(cb[u]) : 0.0;
+  }
+  double suma = 0.0, sumb = 0.0;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    if (ca[u] >= 0) suma = __dadd_rn(suma, __dmul_rn(aa[u], xa[u]));
+    if (cb[u] >= 0) sumb = __dadd_rn(sumb, __dmul_rn(ab[u], xb[u]));
+  }
+  for (int k = loa + 4; k < hia; ++k) suma = __dadd_rn(suma, __dmul_rn(__ldg(val + k), x(__ldg(col + k))));
+  for (int k = lob + 4; k < hib; ++k) sumb = __dadd_rn(sumb, __dmul_rn(__ldg(val + k), x(__ldg(col + k))));
+  epi.store(ra, suma, prea);
+  if (vb) epi.store(rb, sumb, preb);
 }
 
 // ---------------------------------------------------------------------------
@@ -1797,7 +1819,7 @@ void launch_spmv(const DCsr& A, Xs x, Epi epi, cudaStream_t s) {
     return;
   }
   if (A.rows > 65536 && A.nnz <= 3LL * A.rows) {
-    launch_pdl(k_spmv_tpr<Epi, Xs>, blocks_for(A.rows, 256), 256, 0, s, A.rows, A.ptr.get(), A.col.get(), A.val.get(),
+    launch_pdl(k_spmv_tpr<Epi, Xs>, blocks_for(A.rows, 512), 256, 0, s, A.rows, A.ptr.get(), A.col.get(), A.val.get(),
                x, epi);
     MGRX_LAUNCH_CK();
     count_launch();
