@@ -512,12 +512,15 @@ def main():
     else:
         dom = max((k for k in share), key=lambda k: share[k])
     d = probes[dom]
-    traffic, shares = None, None
+    traffic, shares, captured = None, None, {}
     try:
         with open(os.path.join(ROOT, "profiles", "r02", "roofline_traffic.json")) as f:
             tr = json.load(f).get(CONFIG, {})
         traffic = tr.get("kernels", {}).get(dom, {}).get("dram_bytes_per_launch")
         shares = tr.get("launch_shares")
+        # ncu DRAM bytes over algorithmic bytes of every captured probe launch
+        captured = {k: round(v["traffic_over_algorithmic"], 3) for k, v in tr.get("kernels", {}).items()
+                    if isinstance(v, dict) and v.get("traffic_over_algorithmic") is not None}
     except Exception:
         pass
     arn = {}
@@ -564,6 +567,7 @@ def main():
                 "achieved": family["cold"]["achieved"], "peak": peak, "unit": "GB/s",
                 "frac": family["cold"]["frac"], "traffic": None,
                 "algorithmic_bytes": fb / nl, "launches_averaged": nl,
+                "traffic_over_algorithmic": {k: v for k, v in captured.items() if k in fam} or None,
                 "largest_instance": inst}
     else:
         roof = {"bound": "hbm", "kernel": "k_spmv_staged" if dom == "spmv.A" else dom,
